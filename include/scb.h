@@ -1,0 +1,178 @@
+/*
+ * scb.h -- C ABI of the B200-native single-cell hot path (libscb_b200.so).
+ *
+ * The reference (arxiv/paper_2605_13928, /root/reference) defines no compute API for
+ * this path: the pipeline is out of its scope and exists only as the
+ * Table-1 step list and the marker labels qc / norm_hvg / regress /
+ * pca / knn (pkg/tests/helpers.py:31-36).  Each entry point below replaces one
+ * Scanpy / rapids-singlecell step the paper's R script called through reticulate
+ * (PAPER.md:23,62); the Scanpy function each mirrors is named in its comment, and the
+ * Python step functions in paper_2605_13928_b200/pp.py keep Scanpy's names.
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer owned by the caller unless noted; the library
+ *     allocates only scratch held in the context;
+ *   - work is ordered on `stream` (a cudaStream_t passed as void*); no host sync
+ *     unless a function says so;
+ *   - CSR = indptr int64[n_rows+1], indices int32[nnz] (sorted within a row), data
+ *     float32[nnz];
+ *   - return 0 (SCB_OK) or a negative SCB_ERR_*; scb_last_error() gives the message
+ *     (thread-local);
+ *   - one context per GPU, used by one host thread at a time.
+ *   - "gene sums" are integer fixed-point accumulators: u64 [n_stats][2 limbs][n],
+ *     value = limb0 + limb1 * 2^32, scaled by 2^-frac_bits.  They
+ *     add exactly across shards, so multi-GPU callers all-reduce them as int64 SUM.
+ */
+#ifndef SCB_H_
+#define SCB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCB_OK 0
+#define SCB_ERR_ARG -1
+#define SCB_ERR_CUDA -2
+#define SCB_ERR_UNSUPPORTED -3
+#define SCB_ERR_DATA -4
+#define SCB_ERR_NOMEM -5
+
+#define SCB_ABI_VERSION 1
+
+/* fixed-point fractional bits of the gene-sum accumulators */
+#define SCB_FX_Y 28      /* sum of normalized counts y            */
+#define SCB_FX_Y2 24     /* sum of y^2                            */
+#define SCB_FX_L 28      /* sum of log1p values l                 */
+#define SCB_FX_L2 24     /* sum of l^2                            */
+
+#if defined(__GNUC__)
+#define SCB_API __attribute__((visibility("default")))
+#else
+#define SCB_API
+#endif
+
+typedef struct scb_ctx scb_ctx;
+
+SCB_API int scb_abi_version(void);
+SCB_API const char* scb_last_error(void);
+SCB_API int scb_ctx_create(int device, scb_ctx** out);
+SCB_API int scb_ctx_destroy(scb_ctx* ctx);
+
+/* ---- a1: sc.pp.calculate_qc_metrics(qc_vars=["mt"], percent_top=None, log1p=False)
+ * Per cell: n_genes_by_counts, total_counts, total_counts_mt, pct_counts_mt.
+ * Per gene: n_cells_by_counts, total_counts (exact; counts must be non-negative
+ * integers < 2^24 stored as float32, otherwise SCB_ERR_DATA). */
+SCB_API int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* data,
+                   int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
+                   int32_t* n_genes_by_counts, double* total_counts, double* total_counts_mt,
+                   double* pct_counts_mt, int32_t* n_cells_by_counts, double* gene_total_counts,
+                   void* stream);
+
+/* ---- a2: sc.pp.filter_cells(min_genes, max_genes) + pct_counts_mt < max_pct_mt, and
+ * sc.pp.filter_genes(min_cells).  max_genes < 0 disables the upper bound.
+ * n_kept (device int64[2]) receives {kept cells, kept genes}. */
+SCB_API int scb_filter_masks(scb_ctx* ctx, const int32_t* n_genes_by_counts, const double* pct_counts_mt,
+                     int64_t n_rows, const int32_t* n_cells_by_counts, int32_t n_cols,
+                     int32_t min_genes, int32_t max_genes, double max_pct_mt, int32_t min_cells,
+                     uint8_t* cell_mask, uint8_t* gene_mask, int64_t* n_kept, void* stream);
+
+/* ---- a2: adata[cell_mask, gene_mask] -- pass 1.  Builds gene_remap (new column or -1),
+ * new_indptr (int64[n_kept_cells+1]; new_indptr[n_kept] = kept nnz) and, if
+ * row_scale != NULL, the per-KEPT-row normalize_total factor float32(target_sum/total)
+ * (fused count pass of the pipeline; target_sum ignored when row_scale == NULL).
+ * If row_scale_orig != NULL it also receives the factor per ORIGINAL row (0 = dropped). */
+SCB_API int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* data,
+                     int64_t n_rows, int32_t n_cols, const uint8_t* cell_mask,
+                     const uint8_t* gene_mask, int32_t* gene_remap, int64_t* new_indptr,
+                     double target_sum, float* row_scale, float* row_scale_orig, void* stream);
+
+/* ---- a2 pass 2: writes the compacted CSR.  If row_scale != NULL the values written are
+ * log1p(x * row_scale[kept_row]) (fused normalize_total + log1p), else raw x. */
+SCB_API int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* data,
+                    int64_t n_rows, const uint8_t* cell_mask, const int32_t* gene_remap,
+                    const int64_t* new_indptr, const float* row_scale, int32_t* new_indices,
+                    float* new_data, void* stream);
+
+/* ---- a3+a4: sc.pp.normalize_total(target_sum) + sc.pp.log1p, out of place (out may
+ * alias data).  row_scale receives float32(target_sum / row total) (1 for empty rows). */
+SCB_API int scb_normalize_log1p(scb_ctx* ctx, const int64_t* indptr, const float* data, int64_t n_rows,
+                        double target_sum, float* out, float* row_scale, void* stream);
+
+/* ---- a5 partial: per-gene fixed-point sums of y = x*row_scale[r] and y^2 over rows with
+ * row_scale != 0, accumulated (+=) into sums u64[2][2][n_out_cols] (stat, limb, gene).
+ * gene_remap (optional) maps input columns to output columns (-1 = skip). */
+SCB_API int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* data,
+                      const float* row_scale, int64_t n_rows, int32_t n_cols,
+                      const int32_t* gene_remap, int32_t n_out_cols, uint64_t* sums, void* stream);
+
+/* ---- a5: sc.pp.highly_variable_genes(flavor="seurat", n_top_genes, n_bins) from the
+ * (all-reduced) gene sums.  Outputs per gene: means, variances, dispersions (log),
+ * dispersions_norm, mean_bin; hvg_mask; hvg_index = sorted selected genes (int32[n_top]).
+ * n_selected (device int32) = min(n_top, #genes with finite dispersions_norm). */
+SCB_API int scb_hvg_select(scb_ctx* ctx, const uint64_t* sums, int32_t n_cols, int64_t n_cells,
+                   int32_t n_top, int32_t n_bins, double* means, double* variances,
+                   double* dispersions, double* dispersions_norm, int32_t* mean_bin,
+                   uint8_t* hvg_mask, int32_t* hvg_index, int32_t* n_selected, void* stream);
+
+/* ---- a6 partial: fixed-point sums of l and l^2 for the selected genes
+ * (gene_slot[g] = HVG slot or -1), accumulated into sums u64[2][2][n_slots]. */
+SCB_API int scb_scale_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                        const float* logdata, int64_t n_rows, int32_t n_cols,
+                        const int32_t* gene_slot, int32_t n_slots, uint64_t* sums, void* stream);
+
+/* ---- a6: mean / inverse std (ddof=1, std==0 -> 1) from the all-reduced sums. */
+SCB_API int scb_scale_finalize(scb_ctx* ctx, const uint64_t* sums, int32_t n_slots, int64_t n_cells,
+                       double* mean, double* inv_std, void* stream);
+
+/* ---- a6: sc.pp.scale(max_value) of the HVG columns into a dense row-major float32
+ * matrix Z[n_rows][ldz]: column j < n_slots = min((l - mean)*inv_std, max_value);
+ * column ones_col (if >= 0) = 1.0; other columns up to ldz = 0. */
+SCB_API int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                    const float* logdata, int64_t n_rows, int32_t n_cols, const int32_t* gene_slot,
+                    int32_t n_slots, const double* mean, const double* inv_std, double max_value,
+                    float* Z, int64_t ldz, int32_t ones_col, void* stream);
+
+/* ---- a7: partial Gram matrix C = Z^T Z (float32 [hp][hp], full symmetric) on the
+ * 5th-gen tensor cores (tcgen05, TF32 inputs, FP32 accumulate in TMEM, operands staged by
+ * TMA).  hp = ldz must be a multiple of 128; n_rows any. */
+SCB_API int scb_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp, float* C, void* stream);
+
+/* ---- a8: top-n_comps eigenpairs of the centred covariance
+ * Cov = (C[:h,:h] - N m m^T)/(N-1), m = C[ones_col, :h]/N (column means of Z).
+ * Outputs eigenvalues (desc, float64), components_t float32[n_comps_pad][hp] (row j =
+ * component j, sign-canonical: largest |loading| positive, zero-padded), col_mean
+ * float32[hp] and trace (float64, total variance).  Subspace iteration in float64. */
+SCB_API int scb_pca_eig(scb_ctx* ctx, const float* C, int32_t h, int32_t hp, int32_t ones_col,
+                int64_t n_cells, int32_t n_comps, int32_t n_comps_pad, double* eigenvalues,
+                float* components_t, float* col_mean, double* trace, void* stream);
+
+/* ---- a8: X_pca = (Z - m) V, float32 [n_rows][ld_out] (columns >= n_comps zeroed). */
+SCB_API int scb_project(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp,
+                const float* components_t, const float* col_mean, int32_t n_comps,
+                int32_t n_comps_pad, float* X_pca, int32_t ld_out, void* stream);
+
+/* ---- a9: sc.pp.neighbors(n_neighbors=k, method exact, metric euclidean): for each query
+ * row, the k nearest key rows (self included) ordered by (distance, index).  Candidate
+ * distances on tcgen05 (TF32) with a fused per-row top-k_cand, then exact FP32 re-rank.
+ * queries/keys float32 [n][ld] (ld = 64, columns >= d zero); key_offset = global index of
+ * keys[0] is added to the reported indices' base for sharded queries (0 single GPU). */
+SCB_API int scb_knn(scb_ctx* ctx, const float* queries, int64_t n_queries, const float* keys,
+            int64_t n_keys, int32_t d, int32_t ld, int32_t k, int32_t k_cand,
+            int32_t* knn_index, float* knn_dist, void* stream);
+
+/* ---- synthetic negative-binomial counts (oracle/synth.py specification), on device.
+ * Pass 1 counts nnz per row into row_nnz (int64[n_rows]); pass 2 fills a CSR whose
+ * indptr the caller built from row_nnz.  Tables: log_mu f64[G], A f64[T][G],
+ * B f64[R][G], cum f64[T]. */
+SCB_API int scb_synth_rows(scb_ctx* ctx, uint64_t seed, int64_t row0, int64_t n_rows, int32_t n_genes,
+                   const double* log_mu, const double* A, int32_t n_types, const double* B,
+                   int32_t n_factors, const double* cum, const int64_t* indptr, int64_t* row_nnz,
+                   int32_t* indices, float* data, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCB_H_ */

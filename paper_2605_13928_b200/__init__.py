@@ -1,0 +1,11 @@
+"""B200-native (sm_100a) single-cell hot path: QC -> normalize -> log1p -> HVG -> scale -> PCA -> kNN.
+
+Scanpy-shaped step functions (``pp``) over hand-written CUDA kernels behind a C ABI
+(``include/scb.h``, ``libscb_b200.so``); see DESIGN.md.  No CPU fallback.
+"""
+from . import _lib  # noqa: F401
+from .pp import (DeviceCSR, calculate_qc_metrics, filter_masks, subset, normalize_log1p,  # noqa: F401
+                 highly_variable_genes, scale, Scaled)
+
+__all__ = ["DeviceCSR", "calculate_qc_metrics", "filter_masks", "subset", "normalize_log1p",
+           "highly_variable_genes", "scale", "Scaled"]

@@ -1,0 +1,113 @@
+"""ctypes binding of libscb_b200.so (the C ABI declared in include/scb.h).
+
+There is no fallback: if the shared library is missing or no B200 is visible, every
+step function raises.  The library is built in-tree by ``__graft_entry__.build()``
+(``make -C paper_2605_13928_b200/csrc``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libscb_b200.so")
+
+c_i32, c_i64, c_u64, c_dbl, c_ptr = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
+
+# name -> argtypes (all functions return int status unless listed in _RESTYPE)
+SIGNATURES = {
+    "scb_abi_version": [],
+    "scb_last_error": [],
+    "scb_ctx_create": [ctypes.c_int, ctypes.POINTER(c_ptr)],
+    "scb_ctx_destroy": [c_ptr],
+    "scb_qc_metrics": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+    "scb_filter_masks": [c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_i32, c_i32, c_i32, c_dbl, c_i32, c_ptr, c_ptr, c_ptr, c_ptr],
+    "scb_subset_count": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr],
+    "scb_subset_fill": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+    "scb_normalize_log1p": [c_ptr, c_ptr, c_ptr, c_i64, c_dbl, c_ptr, c_ptr, c_ptr],
+    "scb_hvg_gene_sums": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr],
+    "scb_hvg_select": [c_ptr, c_ptr, c_i32, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+    "scb_scale_gene_sums": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr],
+    "scb_scale_finalize": [c_ptr, c_ptr, c_i32, c_i64, c_ptr, c_ptr, c_ptr],
+    "scb_scale_dense": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_dbl, c_ptr, c_i64, c_i32, c_ptr],
+    "scb_gram": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
+    "scb_pca_eig": [c_ptr, c_ptr, c_i32, c_i32, c_i32, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+    "scb_project": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_i32, c_ptr],
+    "scb_knn": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_i32, c_i32, c_i32, c_ptr, c_ptr, c_ptr],
+    "scb_synth_rows": [c_ptr, c_u64, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+}
+_RESTYPE = {"scb_last_error": ctypes.c_char_p}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class ScbError(RuntimeError):
+    """Raised when a C-ABI call returns a non-zero status (message from scb_last_error)."""
+
+    def __init__(self, fn, code, msg):
+        super().__init__(f"{fn} failed ({code}): {msg}")
+        self.code = code
+
+
+def load(path: str = LIB_PATH):
+    """Load the shared library and bind every symbol in SIGNATURES (raises if any is missing)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                              " (or `make -C paper_2605_13928_b200/csrc`); there is no CPU fallback")
+        lib = ctypes.CDLL(path)
+        for name, argtypes in SIGNATURES.items():
+            fn = getattr(lib, name)  # AttributeError if not exported
+            fn.argtypes = argtypes
+            fn.restype = _RESTYPE.get(name, ctypes.c_int)
+        _lib = lib
+        return lib
+
+
+def call(name, *args):
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.scb_last_error()
+        raise ScbError(name, rc, msg.decode() if msg else "")
+    return rc
+
+
+_ctx = {}
+
+
+def context(device: int):
+    """Per-device scb_ctx (created lazily, destroyed at interpreter exit)."""
+    with _lock:
+        c = _ctx.get(device)
+    if c is None:
+        lib = load()
+        p = c_ptr()
+        rc = lib.scb_ctx_create(device, ctypes.byref(p))
+        if rc != 0:
+            raise ScbError("scb_ctx_create", rc, lib.scb_last_error().decode())
+        with _lock:
+            _ctx[device] = p.value
+        c = p.value
+    return c
+
+
+def _destroy_all():
+    if _lib is None:
+        return
+    for c in list(_ctx.values()):
+        try:
+            _lib.scb_ctx_destroy(c)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+    _ctx.clear()
+
+
+import atexit  # noqa: E402
+
+atexit.register(_destroy_all)

@@ -1,0 +1,852 @@
+// CSR count-matrix stages: QC metrics, filter masks, subset, normalize_total+log1p,
+// HVG gene sums + seurat selection, scale (sums, finalize, dense gather).
+//
+// All are HBM-bound streaming passes over (indices, data).  Row-local work is
+// warp-per-row with coalesced loads; column (per-gene) reductions are privatised in
+// shared memory per CTA using NATIVE 32-bit shared atomics (ATOMS.ADD) on integer
+// fixed-point words -- shared fp32/fp64/u64 atomicAdd compile to CAS loops on sm_100a,
+// and global fp64 REDs sustain only ~146 G/s (scratch/mb_atomics.cu, profiles/).
+// Integer sums are exact and order independent, so results are deterministic and
+// identical across 1/2/4/8-way cell sharding.
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace scb {
+
+constexpr int kRowThreads = 512;          // threads per CTA of the row-streaming kernels
+constexpr size_t kSmemLimit = 227 * 1024;  // opt-in dynamic shared memory per CTA
+
+static int grid_for(scb_ctx* ctx, int ctas_per_sm) { return ctx->num_sms * ctas_per_sm; }
+
+// ============================================================================ QC
+// smem: n_cells u32[W], total_lo u32[W] for a gene tile [g0, g0+W), mt bitmask.
+__global__ void __launch_bounds__(kRowThreads)
+qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+          const float* __restrict__ data, int64_t n_rows, int32_t n_cols,
+          const uint8_t* __restrict__ mt_mask, int32_t tile_w,
+          int32_t* __restrict__ n_genes, double* __restrict__ total, double* __restrict__ total_mt,
+          double* __restrict__ pct, uint32_t* __restrict__ g_cells, unsigned long long* __restrict__ g_total,
+          int* __restrict__ flag) {
+  extern __shared__ uint32_t sm[];
+  const int tile = blockIdx.y;
+  const int g0 = tile * tile_w;
+  const int w = min(tile_w, n_cols - g0);
+  uint32_t* s_cells = sm;
+  uint32_t* s_tot = sm + tile_w;
+  uint32_t* s_mt = sm + 2 * tile_w;  // bitmask over ALL genes
+  const int mt_words = (n_cols + 31) >> 5;
+  for (int i = threadIdx.x; i < 2 * tile_w; i += blockDim.x) sm[i] = 0;
+  for (int i = threadIdx.x; i < mt_words; i += blockDim.x) {
+    uint32_t m = 0;
+    for (int b = 0; b < 32; ++b) {
+      int g = i * 32 + b;
+      if (g < n_cols && mt_mask[g]) m |= 1u << b;
+    }
+    s_mt[i] = m;
+  }
+  __syncthreads();
+  const bool row_owner = (tile == 0);  // tile 0 also writes the per-cell metrics
+  const int lane = lane_id();
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  bool bad = false;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    int cnt = 0;
+    double sum = 0.0, summt = 0.0;
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int g = ldg_stream(indices + p);
+      const float x = ldg_stream(data + p);
+      bad |= !(x >= 0.0f && x == rintf(x) && x < 16777216.0f) || g < 0 || g >= n_cols;
+      if (x > 0.0f) {
+        cnt += 1;
+        sum += (double)x;
+        if ((s_mt[g >> 5] >> (g & 31)) & 1u) summt += (double)x;
+        const int gl = g - g0;
+        if (gl >= 0 && gl < w) {
+          atomicAdd(&s_cells[gl], 1u);
+          const uint32_t xv = (uint32_t)x;
+          const uint32_t old = atomicAdd(&s_tot[gl], xv);
+          if (old > 0xffffffffu - xv) atomicAdd(&g_total[g], 1ull << 32);  // rare carry
+        }
+      }
+    }
+    if (row_owner) {
+      cnt = warp_sum(cnt);
+      sum = warp_sum(sum);
+      summt = warp_sum(summt);
+      if (lane == 0) {
+        n_genes[r] = cnt;
+        total[r] = sum;
+        total_mt[r] = summt;
+        pct[r] = __ddiv_rn(__dmul_rn(100.0, summt), sum);
+      }
+    }
+  }
+  if (bad) atomicOr(flag, 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < w; i += blockDim.x) {
+    if (s_cells[i]) atomicAdd(&g_cells[g0 + i], s_cells[i]);
+    if (s_tot[i]) atomicAdd(&g_total[g0 + i], (unsigned long long)s_tot[i]);
+  }
+}
+
+__global__ void qc_finalize(const uint32_t* g_cells, const unsigned long long* g_total, int32_t n,
+                            int32_t* n_cells, double* gene_total) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    n_cells[i] = (int32_t)g_cells[i];
+    gene_total[i] = (double)g_total[i];
+  }
+}
+
+// ============================================================================ masks
+__global__ void cell_mask_kernel(const int32_t* ng, const double* pct, int64_t n, int32_t min_genes,
+                                 int32_t max_genes, double max_pct, uint8_t* mask,
+                                 unsigned long long* kept) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool k = false;
+  if (i < n) {
+    k = ng[i] >= min_genes && (max_genes < 0 || ng[i] <= max_genes) && (pct[i] < max_pct);
+    mask[i] = k ? 1 : 0;
+  }
+  unsigned c = __popc(__ballot_sync(0xffffffffu, k));
+  if (lane_id() == 0 && c) atomicAdd(kept, (unsigned long long)c);
+}
+
+__global__ void gene_mask_kernel(const int32_t* nc, int32_t n, int32_t min_cells, uint8_t* mask,
+                                 unsigned long long* kept) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool k = false;
+  if (i < n) {
+    k = nc[i] >= min_cells;
+    mask[i] = k ? 1 : 0;
+  }
+  unsigned c = __popc(__ballot_sync(0xffffffffu, k));
+  if (lane_id() == 0 && c) atomicAdd(kept + 1, (unsigned long long)c);
+}
+
+// ============================================================================ subset
+// gene_remap = exclusive scan of gene_mask (or -1), computed by one CTA.
+__global__ void gene_remap_kernel(const uint8_t* gmask, int32_t n, int32_t* remap) {
+  __shared__ int32_t carry;
+  __shared__ int32_t wsum[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    int i = base + threadIdx.x;
+    int v = (i < n && gmask[i]) ? 1 : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane_id() >= o) incl += t;
+    }
+    if (lane_id() == 31) wsum[warp_id()] = incl;
+    __syncthreads();
+    if (warp_id() == 0) {
+      int s = (lane_id() < (int)(blockDim.x >> 5)) ? wsum[lane_id()] : 0;
+      int si = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, si, o);
+        if (lane_id() >= o) si += t;
+      }
+      wsum[lane_id()] = si - s;
+    }
+    __syncthreads();
+    int excl = carry + wsum[warp_id()] + incl - v;
+    if (i < n) remap[i] = v ? excl : -1;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+}
+
+// Count kept entries (and kept total) per original row; writes counts into
+// cnt[kept_row] where kept_row = row_pos[r] (exclusive scan of cell_mask).
+__global__ void __launch_bounds__(kRowThreads)
+subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                    const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
+                    const int32_t* __restrict__ remap, const int64_t* __restrict__ row_pos,
+                    int64_t* __restrict__ cnt, double target_sum, float* __restrict__ row_scale,
+                    float* __restrict__ row_scale_orig) {
+  const int lane = lane_id();
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+    if (!cmask[r]) {
+      if (lane == 0 && row_scale_orig) row_scale_orig[r] = 0.0f;
+      continue;
+    }
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    int c = 0;
+    double sum = 0.0;
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int g = ldg_stream(indices + p);
+      if (remap[g] >= 0) {
+        ++c;
+        if (row_scale) sum += (double)ldg_stream(data + p);
+      }
+    }
+    c = warp_sum(c);
+    if (row_scale) sum = warp_sum(sum);
+    if (lane == 0) {
+      const int64_t kr = row_pos[r];
+      cnt[kr] = c;
+      if (row_scale) {
+        const float s = (sum > 0.0) ? (float)__ddiv_rn(target_sum, sum) : 1.0f;
+        row_scale[kr] = s;
+        if (row_scale_orig) row_scale_orig[r] = s;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRowThreads)
+subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                   const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
+                   const int32_t* __restrict__ remap, const int64_t* __restrict__ row_pos,
+                   const int64_t* __restrict__ new_indptr, const float* __restrict__ row_scale,
+                   int32_t* __restrict__ out_idx, float* __restrict__ out_val) {
+  const int lane = lane_id();
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+    if (!cmask[r]) continue;
+    const int64_t kr = row_pos[r];
+    const float s = row_scale ? row_scale[kr] : 1.0f;
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    int64_t o = new_indptr[kr];
+    for (int64_t p0 = b; p0 < e; p0 += 32) {
+      const int64_t p = p0 + lane;
+      int ng = -1;
+      float x = 0.0f;
+      if (p < e) {
+        ng = remap[ldg_stream(indices + p)];
+        x = ldg_stream(data + p);
+      }
+      const unsigned keep = __ballot_sync(0xffffffffu, ng >= 0);
+      if (ng >= 0) {
+        const int64_t q = o + __popc(keep & lt);
+        out_idx[q] = ng;
+        out_val[q] = row_scale ? log1pf(__fmul_rn(x, s)) : x;
+      }
+      o += __popc(keep);
+    }
+  }
+}
+
+// ============================================================================ normalize + log1p
+__global__ void __launch_bounds__(kRowThreads)
+normalize_log1p_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ data,
+                       int64_t n_rows, double target_sum, float* __restrict__ out,
+                       float* __restrict__ row_scale) {
+  const int lane = lane_id();
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    double sum = 0.0;
+    for (int64_t p = b + lane; p < e; p += 32) sum += (double)data[p];
+    sum = warp_sum(sum);
+    const float s = (sum > 0.0) ? (float)__ddiv_rn(target_sum, sum) : 1.0f;
+    if (lane == 0) row_scale[r] = s;
+    for (int64_t p = b + lane; p < e; p += 32) out[p] = log1pf(__fmul_rn(data[p], s));
+  }
+}
+
+// ============================================================================ HVG gene sums
+// Tiled column reduction: CTA (row block, gene tile); smem holds 4 u32 words per gene of
+// the tile (sum y lo/hi, sum y^2 lo/hi).  Adjacent CTAs (same rows, other tiles) re-read
+// the rows from L2.
+__device__ __forceinline__ uint64_t fx_round(double v) { return (uint64_t)__double2ull_rn(v); }
+
+__global__ void __launch_bounds__(kRowThreads)
+hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                const float* __restrict__ data, const float* __restrict__ row_scale, int64_t n_rows,
+                int32_t n_cols, const int32_t* __restrict__ remap, int32_t n_out, int32_t tile_w,
+                int32_t n_tiles, int64_t rows_per_block, unsigned long long* __restrict__ sums) {
+  extern __shared__ uint32_t sm[];
+  const int tile = blockIdx.x % n_tiles;
+  const int64_t rblk = blockIdx.x / n_tiles;
+  const int g0 = tile * tile_w;
+  const int w = min(tile_w, n_out - g0);
+  uint32_t* s1lo = sm;
+  uint32_t* s1hi = sm + tile_w;
+  uint32_t* s2lo = sm + 2 * tile_w;
+  uint32_t* s2hi = sm + 3 * tile_w;
+  for (int i = threadIdx.x; i < 4 * tile_w; i += blockDim.x) sm[i] = 0;
+  __syncthreads();
+  const int lane = lane_id();
+  const int64_t r0 = rblk * rows_per_block;
+  const int64_t r1 = min(n_rows, r0 + rows_per_block);
+  for (int64_t r = r0 + warp_id(); r < r1; r += (blockDim.x >> 5)) {
+    const float s = row_scale[r];
+    if (s == 0.0f) continue;
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    for (int64_t p = b + lane; p < e; p += 32) {
+      int g = ldg_stream(indices + p);
+      if (remap) g = remap[g];
+      const int gl = g - g0;
+      if (g >= 0 && gl >= 0 && gl < w) {
+        const float y = __fmul_rn(ldg_stream(data + p), s);   // float32 normalized count
+        const double yd = (double)y;
+        fx_add(&s1lo[gl], &s1hi[gl], fx_round(yd * 268435456.0));          // y * 2^28
+        fx_add(&s2lo[gl], &s2hi[gl], fx_round((yd * yd) * 16777216.0));     // y^2 * 2^24
+      }
+    }
+  }
+  __syncthreads();
+  unsigned long long* l0 = sums;               // stat 0 limb 0
+  unsigned long long* l1 = sums + n_out;       // stat 0 limb 1
+  unsigned long long* m0 = sums + 2 * n_out;   // stat 1 limb 0
+  unsigned long long* m1 = sums + 3 * n_out;   // stat 1 limb 1
+  for (int i = threadIdx.x; i < w; i += blockDim.x) {
+    if (s1lo[i]) atomicAdd(&l0[g0 + i], (unsigned long long)s1lo[i]);
+    if (s1hi[i]) atomicAdd(&l1[g0 + i], (unsigned long long)s1hi[i]);
+    if (s2lo[i]) atomicAdd(&m0[g0 + i], (unsigned long long)s2lo[i]);
+    if (s2hi[i]) atomicAdd(&m1[g0 + i], (unsigned long long)s2hi[i]);
+  }
+}
+
+// ============================================================================ HVG select
+// Single CTA.  All float64 arithmetic uses explicit _rn intrinsics (no FMA contraction)
+// so that the oracle (numpy, IEEE double) reproduces it bit for bit.
+constexpr int kSelThreads = 1024;
+constexpr int kChunks = 64;
+constexpr int kMaxBins = 32;
+
+// Canonical value of a limb pair (limb0 + limb1 * 2^32, as an exact integer) rounded once
+// to float64 -- independent of how the total was split into limbs across CTAs/ranks.
+__device__ __forceinline__ double limbs_to_double(unsigned long long l0, unsigned long long l1) {
+  const unsigned long long lo = l0 + (l1 << 32);
+  const unsigned long long hi = (l1 >> 32) + (lo < l0 ? 1ull : 0ull);
+  if (hi == 0ull) return __ull2double_rn(lo);
+  return __dadd_rn(__dmul_rn(__ull2double_rn(hi), 18446744073709551616.0), __ull2double_rn(lo));
+}
+
+__device__ __forceinline__ unsigned long long order_key(double d) {
+  if (isnan(d)) return 0ull;
+  unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+template <typename T>
+__device__ T block_reduce(T v, T (*op)(T, T), T* sbuf) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane_id() == 0) sbuf[warp_id()] = v;
+  __syncthreads();
+  if (warp_id() == 0) {
+    v = (lane_id() < (int)(blockDim.x >> 5)) ? sbuf[lane_id()] : sbuf[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane_id() == 0) sbuf[0] = v;
+  }
+  __syncthreads();
+  T r = sbuf[0];
+  __syncthreads();
+  return r;
+}
+__device__ double dmin(double a, double b) { return fmin(a, b); }
+__device__ double dmax(double a, double b) { return fmax(a, b); }
+__device__ int iadd(int a, int b) { return a + b; }
+
+__global__ void __launch_bounds__(kSelThreads)
+hvg_select_kernel(const unsigned long long* __restrict__ sums, int32_t G, int64_t N, int32_t n_top,
+                  int32_t n_bins, double* __restrict__ means, double* __restrict__ vars,
+                  double* __restrict__ disp, double* __restrict__ dnorm, int32_t* __restrict__ mbin,
+                  uint8_t* __restrict__ mask, int32_t* __restrict__ hvg_index,
+                  int32_t* __restrict__ n_selected, double* __restrict__ mean_log) {
+  __shared__ double sred[32];
+  __shared__ int ired[32];
+  __shared__ double edges[kMaxBins + 1];
+  __shared__ double part[kMaxBins][kChunks];
+  __shared__ int npart[kMaxBins][kChunks];
+  __shared__ double bmean[kMaxBins], bstd[kMaxBins];
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_need;
+  const double Nd = (double)N;
+  // ---- 1. per-gene moments
+  double lmin = INFINITY, lmax = -INFINITY;
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    const double s1 = __dmul_rn(limbs_to_double(sums[g], sums[G + g]), 3.725290298461914e-09);   // 2^-28
+    const double s2 = __dmul_rn(limbs_to_double(sums[2 * G + g], sums[3 * G + g]), 5.960464477539063e-08);  // 2^-24
+    double mean = __ddiv_rn(s1, Nd);
+    const double msq = __ddiv_rn(s2, Nd);
+    const double var = __dmul_rn(__dsub_rn(msq, __dmul_rn(mean, mean)), __ddiv_rn(Nd, __dsub_rn(Nd, 1.0)));
+    vars[g] = var;
+    if (mean == 0.0) mean = 1e-12;
+    means[g] = mean;
+    double d = __ddiv_rn(var, mean);
+    d = (d == 0.0) ? CUDART_NAN : log(d);
+    disp[g] = d;
+    const double ml = log1p(mean);
+    mean_log[g] = ml;
+    lmin = fmin(lmin, ml);
+    lmax = fmax(lmax, ml);
+  }
+  lmin = block_reduce<double>(lmin, dmin, sred);
+  lmax = block_reduce<double>(lmax, dmax, sred);
+  // ---- 2. pandas.cut edges
+  if (threadIdx.x == 0) {
+    if (lmin == lmax) {
+      const double adj = (lmin != 0.0) ? __dmul_rn(0.001, fabs(lmin)) : 0.001;
+      const double lo = __dsub_rn(lmin, adj), hi = __dadd_rn(lmax, adj);
+      const double step = __ddiv_rn(__dsub_rn(hi, lo), (double)n_bins);
+      for (int i = 0; i < n_bins; ++i) edges[i] = __dadd_rn(__dmul_rn((double)i, step), lo);
+      edges[n_bins] = hi;
+    } else {
+      const double range = __dsub_rn(lmax, lmin);
+      const double step = __ddiv_rn(range, (double)n_bins);
+      for (int i = 0; i < n_bins; ++i) edges[i] = __dadd_rn(__dmul_rn((double)i, step), lmin);
+      edges[n_bins] = lmax;
+      edges[0] = __dsub_rn(edges[0], __dmul_rn(range, 0.001));
+    }
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    const double x = mean_log[g];
+    int c = 0;
+    for (int i = 0; i <= n_bins; ++i) c += (edges[i] < x) ? 1 : 0;  // searchsorted(left)
+    int b = c - 1;
+    b = b < 0 ? 0 : (b > n_bins - 1 ? n_bins - 1 : b);
+    mbin[g] = b;
+  }
+  __syncthreads();
+  // ---- 3. per-bin mean and std (ddof=1), fixed chunked order
+  const int chunk = (G + kChunks - 1) / kChunks;
+  for (int t = threadIdx.x; t < n_bins * kChunks; t += blockDim.x) {
+    const int b = t / kChunks, c = t % kChunks;
+    double acc = 0.0;
+    int n = 0;
+    for (int g = c * chunk; g < min(G, (c + 1) * chunk); ++g) {
+      const double d = disp[g];
+      if (mbin[g] == b && !isnan(d)) { acc = __dadd_rn(acc, d); ++n; }
+    }
+    part[b][c] = acc;
+    npart[b][c] = n;
+  }
+  __syncthreads();
+  if (threadIdx.x < n_bins) {
+    const int b = threadIdx.x;
+    double acc = 0.0;
+    int n = 0;
+    for (int c = 0; c < kChunks; ++c) { acc = __dadd_rn(acc, part[b][c]); n += npart[b][c]; }
+    bmean[b] = (n > 0) ? __ddiv_rn(acc, (double)n) : CUDART_NAN;
+    npart[b][0] = n;  // stash count (chunk 0 slot no longer needed after this point)
+  }
+  __syncthreads();
+  __shared__ int bcount[kMaxBins];
+  if (threadIdx.x < n_bins) bcount[threadIdx.x] = npart[threadIdx.x][0];
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_bins * kChunks; t += blockDim.x) {
+    const int b = t / kChunks, c = t % kChunks;
+    const double m = bmean[b];
+    double acc = 0.0;
+    for (int g = c * chunk; g < min(G, (c + 1) * chunk); ++g) {
+      const double d = disp[g];
+      if (mbin[g] == b && !isnan(d)) {
+        const double dd = __dsub_rn(d, m);
+        acc = __dadd_rn(acc, __dmul_rn(dd, dd));
+      }
+    }
+    part[b][c] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < n_bins) {
+    const int b = threadIdx.x;
+    const int n = bcount[b];
+    double acc = 0.0;
+    for (int c = 0; c < kChunks; ++c) acc = __dadd_rn(acc, part[b][c]);
+    double sd = (n >= 2) ? sqrt(__ddiv_rn(acc, (double)(n - 1))) : CUDART_NAN;
+    double mn = bmean[b];
+    if (isnan(sd) && !isnan(mn)) { sd = mn; mn = 0.0; }  // one gene in the bin
+    bstd[b] = sd;
+    bmean[b] = mn;
+  }
+  __syncthreads();
+  int valid = 0;
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    const int b = mbin[g];
+    const double dn = __ddiv_rn(__dsub_rn(disp[g], bmean[b]), bstd[b]);
+    dnorm[g] = dn;
+    valid += isnan(dn) ? 0 : 1;
+  }
+  valid = block_reduce<int>(valid, iadd, ired);
+  const int need_total = min(n_top, valid);
+  // ---- 4. radix select of the need_total-th largest key
+  if (threadIdx.x == 0) { s_prefix = 0ull; s_need = need_total; }
+  __syncthreads();
+  unsigned long long prefix_mask = 0ull;
+  for (int shift = 56; shift >= 0 && need_total > 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned long long pfx = s_prefix;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+      const unsigned long long k = order_key(dnorm[g]);
+      if (k != 0ull && (k & prefix_mask) == pfx) atomicAdd(&hist[(k >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int need = s_need;
+      int dgt = 255;
+      for (; dgt >= 0; --dgt) {
+        if ((int)hist[dgt] >= need) break;
+        need -= hist[dgt];
+      }
+      if (dgt < 0) dgt = 0;
+      s_prefix = pfx | ((unsigned long long)dgt << shift);
+      s_need = need;  // how many to take among keys with the extended prefix
+    }
+    prefix_mask |= 0xffull << shift;
+    __syncthreads();
+  }
+  const unsigned long long thr = s_prefix;
+  // ties (key == thr) are taken in gene-index order: s_need of them
+  const int take_ties = s_need;
+  __shared__ int tie_carry;
+  __shared__ int wtie[32];
+  if (threadIdx.x == 0) tie_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < G; base += blockDim.x) {
+    const int g = base + threadIdx.x;
+    unsigned long long k = 0ull;
+    if (g < G) k = order_key(dnorm[g]);
+    const bool tie = (need_total > 0) && g < G && k == thr;
+    const unsigned bal = __ballot_sync(0xffffffffu, tie);
+    if (lane_id() == 0) wtie[warp_id()] = __popc(bal);
+    __syncthreads();
+    int before = tie_carry;
+    for (int w2 = 0; w2 < warp_id(); ++w2) before += wtie[w2];
+    before += __popc(bal & ((1u << lane_id()) - 1u));
+    bool sel = (need_total > 0) && g < G && k != 0ull && (k > thr || (tie && before < take_ties));
+    if (g < G) mask[g] = sel ? 1 : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) tot += wtie[w2];
+      tie_carry += tot;
+    }
+    __syncthreads();
+  }
+  // ---- 5. sorted index list
+  __shared__ int sel_carry;
+  if (threadIdx.x == 0) sel_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < G; base += blockDim.x) {
+    const int g = base + threadIdx.x;
+    const bool s = g < G && mask[g];
+    const unsigned bal = __ballot_sync(0xffffffffu, s);
+    if (lane_id() == 0) wtie[warp_id()] = __popc(bal);
+    __syncthreads();
+    int before = sel_carry;
+    for (int w2 = 0; w2 < warp_id(); ++w2) before += wtie[w2];
+    before += __popc(bal & ((1u << lane_id()) - 1u));
+    if (s) hvg_index[before] = g;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) tot += wtie[w2];
+      sel_carry += tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_selected = need_total;
+}
+
+// ============================================================================ scale
+__global__ void __launch_bounds__(kRowThreads)
+scale_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                  const float* __restrict__ ldata, int64_t n_rows, int32_t n_cols,
+                  const int32_t* __restrict__ slot, int32_t n_slots, unsigned long long* __restrict__ sums) {
+  extern __shared__ uint32_t sm[];
+  int16_t* s_slot = reinterpret_cast<int16_t*>(sm + 4 * n_slots);
+  for (int i = threadIdx.x; i < 4 * n_slots; i += blockDim.x) sm[i] = 0;
+  for (int i = threadIdx.x; i < n_cols; i += blockDim.x) s_slot[i] = (int16_t)slot[i];
+  __syncthreads();
+  uint32_t* s1lo = sm;
+  uint32_t* s1hi = sm + n_slots;
+  uint32_t* s2lo = sm + 2 * n_slots;
+  uint32_t* s2hi = sm + 3 * n_slots;
+  const int lane = lane_id();
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int j = s_slot[ldg_stream(indices + p)];
+      if (j >= 0) {
+        const double l = (double)ldg_stream(ldata + p);
+        fx_add(&s1lo[j], &s1hi[j], fx_round(l * 268435456.0));        // l * 2^28
+        fx_add(&s2lo[j], &s2hi[j], fx_round((l * l) * 16777216.0));    // l^2 * 2^24
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_slots; i += blockDim.x) {
+    if (s1lo[i]) atomicAdd(&sums[i], (unsigned long long)s1lo[i]);
+    if (s1hi[i]) atomicAdd(&sums[n_slots + i], (unsigned long long)s1hi[i]);
+    if (s2lo[i]) atomicAdd(&sums[2 * n_slots + i], (unsigned long long)s2lo[i]);
+    if (s2hi[i]) atomicAdd(&sums[3 * n_slots + i], (unsigned long long)s2hi[i]);
+  }
+}
+
+__global__ void scale_finalize_kernel(const unsigned long long* __restrict__ sums, int32_t H, int64_t N,
+                                      double* __restrict__ mean, double* __restrict__ inv_std) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= H) return;
+  const double Nd = (double)N;
+  const double s1 = __dmul_rn(limbs_to_double(sums[j], sums[H + j]), 3.725290298461914e-09);
+  const double s2 = __dmul_rn(limbs_to_double(sums[2 * H + j], sums[3 * H + j]), 5.960464477539063e-08);
+  const double m = __ddiv_rn(s1, Nd);
+  const double msq = __ddiv_rn(s2, Nd);
+  const double var = __dmul_rn(__dsub_rn(msq, __dmul_rn(m, m)), __ddiv_rn(Nd, __dsub_rn(Nd, 1.0)));
+  double sd = sqrt(var);
+  if (sd == 0.0 || isnan(sd)) sd = 1.0;  // var < 0 by rounding -> NaN -> 1 (documented)
+  mean[j] = m;
+  inv_std[j] = __ddiv_rn(1.0, sd);
+}
+
+// Dense gather: one warp per row.  Background row (z0, ones column, zero padding) is
+// written with 16-byte stores, then (after __syncwarp, which orders the warp's global
+// stores) the row's HVG entries are scattered on top.
+__global__ void __launch_bounds__(kRowThreads)
+scale_dense_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                   const float* __restrict__ ldata, int64_t n_rows, int32_t n_cols,
+                   const int32_t* __restrict__ slot, int32_t H, const double* __restrict__ mean,
+                   const double* __restrict__ inv, double max_value, float* __restrict__ Z, int64_t ldz,
+                   int32_t ones_col) {
+  extern __shared__ float zsm[];                        // background row [ldz]
+  int16_t* s_slot = reinterpret_cast<int16_t*>(zsm + ldz);
+  for (int j = threadIdx.x; j < ldz; j += blockDim.x) {
+    float v = 0.0f;
+    if (j < H) v = (float)fmin(__dmul_rn(__dsub_rn(0.0, mean[j]), inv[j]), max_value);
+    else if (j == ones_col) v = 1.0f;
+    zsm[j] = v;
+  }
+  for (int i = threadIdx.x; i < n_cols; i += blockDim.x) s_slot[i] = (int16_t)slot[i];
+  __syncthreads();
+  const int lane = lane_id();
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const float4* bg = reinterpret_cast<const float4*>(zsm);
+  const int n4 = (int)(ldz >> 2);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+    float* zr = Z + r * ldz;
+    float4* zr4 = reinterpret_cast<float4*>(zr);
+    for (int j = lane; j < n4; j += 32) zr4[j] = bg[j];
+    __syncwarp();
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int j = s_slot[ldg_stream(indices + p)];
+      if (j >= 0) {
+        const double l = (double)ldg_stream(ldata + p);
+        zr[j] = (float)fmin(__dmul_rn(__dsub_rn(l, mean[j]), inv[j]), max_value);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace scb
+
+// ============================================================================ C ABI
+using namespace scb;
+
+extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                              const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
+                              int32_t* n_genes, double* total, double* total_mt, double* pct,
+                              int32_t* n_cells, double* gene_total, void* stream) {
+  SCB_REQUIRE(ctx && indptr && mt_mask && n_genes && total && total_mt && pct && n_cells && gene_total,
+              SCB_ERR_ARG, "scb_qc_metrics: null argument");
+  SCB_REQUIRE(n_rows >= 0 && n_cols > 0, SCB_ERR_ARG, "scb_qc_metrics: bad shape");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int mt_words = (n_cols + 31) / 32;
+  const int max_w = (int)((kSmemLimit - mt_words * 4) / 8);
+  const int n_tiles = ceil_div(n_cols, max_w);
+  const int tile_w = ceil_div(n_cols, n_tiles);
+  void* ws;
+  const size_t ws_bytes = (size_t)n_cols * 4 + (size_t)n_cols * 8;
+  SCB_TRY(ws_get(ctx, 0, ws_bytes, &ws, s));
+  uint32_t* g_cells = (uint32_t*)ws;
+  unsigned long long* g_total = (unsigned long long*)((char*)ws + ((size_t)n_cols * 4 + 7) / 8 * 8);
+  SCB_CUDA(cudaMemsetAsync(ws, 0, ws_bytes + 8, s));
+  SCB_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), s));
+  const size_t smem = (size_t)tile_w * 8 + (size_t)mt_words * 4;
+  SCB_CUDA(cudaFuncSetAttribute(qc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (n_rows > 0) {
+    dim3 grid(grid_for(ctx, 1), n_tiles);
+    qc_kernel<<<grid, kRowThreads, smem, s>>>(indptr, indices, data, n_rows, n_cols, mt_mask, tile_w,
+                                              n_genes, total, total_mt, pct, g_cells, g_total, ctx->d_flag);
+    SCB_LAUNCH_CHECK();
+  }
+  qc_finalize<<<ceil_div(n_cols, 256), 256, 0, s>>>(g_cells, g_total, n_cols, n_cells, gene_total);
+  SCB_LAUNCH_CHECK();
+  int flag = 0;
+  SCB_CUDA(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SCB_CUDA(cudaStreamSynchronize(s));
+  SCB_REQUIRE(flag == 0, SCB_ERR_DATA,
+              "scb_qc_metrics: counts must be non-negative integers < 2^24 with column indices in range");
+  return SCB_OK;
+}
+
+extern "C" int scb_filter_masks(scb_ctx* ctx, const int32_t* ng, const double* pct, int64_t n_rows,
+                                const int32_t* nc, int32_t n_cols, int32_t min_genes, int32_t max_genes,
+                                double max_pct, int32_t min_cells, uint8_t* cmask, uint8_t* gmask,
+                                int64_t* n_kept, void* stream) {
+  SCB_REQUIRE(ctx && ng && pct && nc && cmask && gmask && n_kept, SCB_ERR_ARG, "scb_filter_masks: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  SCB_CUDA(cudaMemsetAsync(n_kept, 0, 2 * sizeof(int64_t), s));
+  if (n_rows > 0) {
+    cell_mask_kernel<<<ceil_div(n_rows, 256), 256, 0, s>>>(ng, pct, n_rows, min_genes, max_genes, max_pct,
+                                                           cmask, (unsigned long long*)n_kept);
+    SCB_LAUNCH_CHECK();
+  }
+  gene_mask_kernel<<<ceil_div(n_cols, 256), 256, 0, s>>>(nc, n_cols, min_cells, gmask,
+                                                         (unsigned long long*)n_kept);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
+extern "C" int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                                const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+                                const uint8_t* gmask, int32_t* remap, int64_t* new_indptr,
+                                double target_sum, float* row_scale, float* row_scale_orig, void* stream) {
+  SCB_REQUIRE(ctx && indptr && indices && cmask && gmask && remap && new_indptr, SCB_ERR_ARG,
+              "scb_subset_count: null argument");
+  SCB_REQUIRE(!row_scale || data, SCB_ERR_ARG, "scb_subset_count: row_scale needs data");
+  cudaStream_t s = (cudaStream_t)stream;
+  gene_remap_kernel<<<1, 1024, 0, s>>>(gmask, n_cols, remap);
+  SCB_LAUNCH_CHECK();
+  // row_pos = exclusive scan of cell_mask (int64), cnt[kept] then scanned into new_indptr
+  void* ws;
+  SCB_TRY(ws_get(ctx, 1, (size_t)(n_rows + 1) * 8 * 2, &ws, s));
+  int64_t* row_pos = (int64_t*)ws;
+  int64_t* cnt = row_pos + (n_rows + 1);
+  SCB_TRY(scan_u8_to_i64(ctx, cmask, n_rows, row_pos, s));
+  if (n_rows > 0) {
+    subset_count_kernel<<<grid_for(ctx, 4), kRowThreads, 0, s>>>(indptr, indices, data, n_rows, cmask, remap,
+                                                                 row_pos, cnt, target_sum, row_scale,
+                                                                 row_scale_orig);
+    SCB_LAUNCH_CHECK();
+  }
+  // number of kept rows is row_pos[n_rows]; scan cnt[0..kept) -> new_indptr (device-side length)
+  SCB_TRY(scan_i64_dev_len(ctx, cnt, row_pos + n_rows, n_rows, new_indptr, s));
+  return SCB_OK;
+}
+
+extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                               const float* data, int64_t n_rows, const uint8_t* cmask,
+                               const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
+                               int32_t* new_indices, float* new_data, void* stream) {
+  SCB_REQUIRE(ctx && indptr && indices && data && cmask && remap && new_indptr && new_indices && new_data,
+              SCB_ERR_ARG, "scb_subset_fill: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  void* ws;
+  SCB_TRY(ws_get(ctx, 1, (size_t)(n_rows + 1) * 8 * 2, &ws, s));
+  int64_t* row_pos = (int64_t*)ws;
+  SCB_TRY(scan_u8_to_i64(ctx, cmask, n_rows, row_pos, s));
+  if (n_rows > 0) {
+    subset_fill_kernel<<<grid_for(ctx, 4), kRowThreads, 0, s>>>(indptr, indices, data, n_rows, cmask, remap,
+                                                                row_pos, new_indptr, row_scale, new_indices,
+                                                                new_data);
+    SCB_LAUNCH_CHECK();
+  }
+  return SCB_OK;
+}
+
+extern "C" int scb_normalize_log1p(scb_ctx* ctx, const int64_t* indptr, const float* data, int64_t n_rows,
+                                   double target_sum, float* out, float* row_scale, void* stream) {
+  SCB_REQUIRE(ctx && indptr && data && out && row_scale, SCB_ERR_ARG, "scb_normalize_log1p: null argument");
+  SCB_REQUIRE(target_sum > 0, SCB_ERR_ARG, "scb_normalize_log1p: target_sum must be > 0");
+  if (n_rows == 0) return SCB_OK;
+  normalize_log1p_kernel<<<grid_for(ctx, 4), kRowThreads, 0, (cudaStream_t)stream>>>(indptr, data, n_rows,
+                                                                                     target_sum, out, row_scale);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
+extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                                 const float* data, const float* row_scale, int64_t n_rows, int32_t n_cols,
+                                 const int32_t* remap, int32_t n_out, uint64_t* sums, void* stream) {
+  SCB_REQUIRE(ctx && indptr && indices && data && row_scale && sums, SCB_ERR_ARG,
+              "scb_hvg_gene_sums: null argument");
+  SCB_REQUIRE(n_out > 0, SCB_ERR_ARG, "scb_hvg_gene_sums: n_out must be > 0");
+  if (n_rows == 0) return SCB_OK;
+  const int max_w = (int)(kSmemLimit / 16);
+  const int n_tiles = ceil_div(n_out, max_w);
+  const int tile_w = ceil_div(n_out, n_tiles);
+  const size_t smem = (size_t)tile_w * 16;
+  // row blocks: keep per-CTA hi words far from overflow (<= 4096 rows) and give >= 2 waves
+  int64_t rows_per_block = std::max<int64_t>(64, std::min<int64_t>(4096, n_rows / (2 * ctx->num_sms) + 1));
+  const int64_t n_blocks = (n_rows + rows_per_block - 1) / rows_per_block;
+  SCB_CUDA(cudaFuncSetAttribute(hvg_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kRowThreads, smem, (cudaStream_t)stream>>>(
+      indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, tile_w, n_tiles, rows_per_block,
+      (unsigned long long*)sums);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
+extern "C" int scb_hvg_select(scb_ctx* ctx, const uint64_t* sums, int32_t n_cols, int64_t n_cells,
+                              int32_t n_top, int32_t n_bins, double* means, double* vars, double* disp,
+                              double* dnorm, int32_t* mbin, uint8_t* mask, int32_t* hvg_index,
+                              int32_t* n_selected, void* stream) {
+  SCB_REQUIRE(ctx && sums && means && vars && disp && dnorm && mbin && mask && hvg_index && n_selected,
+              SCB_ERR_ARG, "scb_hvg_select: null argument");
+  SCB_REQUIRE(n_bins >= 1 && n_bins <= kMaxBins, SCB_ERR_ARG, "scb_hvg_select: n_bins must be in [1, %d]",
+              kMaxBins);
+  SCB_REQUIRE(n_cells >= 2 && n_cols >= 1 && n_top >= 0, SCB_ERR_ARG, "scb_hvg_select: bad sizes");
+  cudaStream_t s = (cudaStream_t)stream;
+  void* ws;
+  SCB_TRY(ws_get(ctx, 2, (size_t)n_cols * 8, &ws, s));
+  hvg_select_kernel<<<1, kSelThreads, 0, s>>>((const unsigned long long*)sums, n_cols, n_cells, n_top, n_bins,
+                                              means, vars, disp, dnorm, mbin, mask, hvg_index, n_selected,
+                                              (double*)ws);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
+extern "C" int scb_scale_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                                   const float* ldata, int64_t n_rows, int32_t n_cols, const int32_t* slot,
+                                   int32_t n_slots, uint64_t* sums, void* stream) {
+  SCB_REQUIRE(ctx && indptr && indices && ldata && slot && sums, SCB_ERR_ARG, "scb_scale_gene_sums: null argument");
+  SCB_REQUIRE(n_slots > 0 && n_slots < 32768, SCB_ERR_UNSUPPORTED, "scb_scale_gene_sums: n_slots must be in [1, 32767]");
+  const size_t smem = (size_t)n_slots * 16 + (size_t)n_cols * 2;
+  SCB_REQUIRE(smem <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_scale_gene_sums: too many genes for one CTA");
+  if (n_rows == 0) return SCB_OK;
+  SCB_CUDA(cudaFuncSetAttribute(scale_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int per_sm = std::max(1, std::min(4, (int)(kSmemLimit / (smem + 1024))));
+  scale_sums_kernel<<<grid_for(ctx, per_sm), kRowThreads, smem, (cudaStream_t)stream>>>(
+      indptr, indices, ldata, n_rows, n_cols, slot, n_slots, (unsigned long long*)sums);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
+extern "C" int scb_scale_finalize(scb_ctx* ctx, const uint64_t* sums, int32_t n_slots, int64_t n_cells,
+                                  double* mean, double* inv_std, void* stream) {
+  SCB_REQUIRE(ctx && sums && mean && inv_std, SCB_ERR_ARG, "scb_scale_finalize: null argument");
+  SCB_REQUIRE(n_cells >= 2, SCB_ERR_ARG, "scb_scale_finalize: need >= 2 cells");
+  scale_finalize_kernel<<<ceil_div(n_slots, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const unsigned long long*)sums, n_slots, n_cells, mean, inv_std);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
+extern "C" int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                               const float* ldata, int64_t n_rows, int32_t n_cols, const int32_t* slot,
+                               int32_t n_slots, const double* mean, const double* inv_std, double max_value,
+                               float* Z, int64_t ldz, int32_t ones_col, void* stream) {
+  SCB_REQUIRE(ctx && indptr && indices && ldata && slot && mean && inv_std && Z, SCB_ERR_ARG,
+              "scb_scale_dense: null argument");
+  SCB_REQUIRE(ldz % 4 == 0 && ldz >= n_slots && ones_col < ldz, SCB_ERR_ARG,
+              "scb_scale_dense: ldz must be a multiple of 4 and >= n_slots");
+  SCB_REQUIRE(((uintptr_t)Z & 15) == 0, SCB_ERR_ARG, "scb_scale_dense: Z must be 16-byte aligned");
+  const size_t smem = (size_t)ldz * 4 + (size_t)n_cols * 2;
+  SCB_REQUIRE(smem <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_scale_dense: too many genes");
+  if (n_rows == 0) return SCB_OK;
+  SCB_CUDA(cudaFuncSetAttribute(scale_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int per_sm = std::max(1, std::min(4, (int)(kSmemLimit / (smem + 1024))));
+  scale_dense_kernel<<<grid_for(ctx, per_sm), kRowThreads, smem, (cudaStream_t)stream>>>(
+      indptr, indices, ldata, n_rows, n_cols, slot, n_slots, mean, inv_std, max_value, Z, ldz, ones_col);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}

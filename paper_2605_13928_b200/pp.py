@@ -1,0 +1,249 @@
+"""Scanpy-shaped step functions backed by the sm_100a kernels of libscb_b200.so.
+
+Each function is a thin host wrapper around one or more C-ABI calls (include/scb.h);
+device memory, streams and collectives are PyTorch plumbing.  Semantics are fixed in
+oracle/pipeline.py (the CPU restatement used as the parity checker) and DESIGN.md.
+
+Reference anchor: the paper's Table 1 steps (reference PAPER.md:84-89) and the marker
+labels the reference's tests use for them (pkg/tests/helpers.py:31-36): ``qc`` ->
+calculate_qc_metrics / filter / subset, ``norm_hvg`` -> normalize_total + log1p +
+highly_variable_genes, ``regress`` -> scale, ``pca`` -> pca, ``knn`` -> neighbors.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import torch
+
+from . import _lib
+
+ONES_PAD = 128  # dense scaled matrix row stride multiple (tcgen05 tile size)
+
+
+def _p(t):
+    return 0 if t is None else t.data_ptr()
+
+
+def _stream(device=None):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ctx(t: torch.Tensor):
+    if not t.is_cuda:
+        raise ValueError("step functions take CUDA tensors (no CPU fallback)")
+    return _lib.context(t.device.index if t.device.index is not None else torch.cuda.current_device())
+
+
+@dataclasses.dataclass
+class DeviceCSR:
+    """CSR count matrix resident in HBM: indptr int64[N+1], indices int32[nnz], data float32[nnz]."""
+
+    indptr: torch.Tensor
+    indices: torch.Tensor
+    data: torch.Tensor
+    n_cols: int
+    # set by normalize_log1p: (raw counts data, per-row scale) of the same sparsity pattern
+    counts: Optional[torch.Tensor] = None
+    row_scale: Optional[torch.Tensor] = None
+
+    @property
+    def n_rows(self) -> int:
+        return self.indptr.numel() - 1
+
+    @property
+    def nnz(self) -> int:
+        return self.indices.numel()
+
+    @property
+    def device(self):
+        return self.data.device
+
+    @staticmethod
+    def from_host(indptr, indices, data, n_cols, device="cuda"):
+        def t(a, dt):
+            return torch.as_tensor(a).to(dtype=dt).to(device, non_blocking=False)
+        return DeviceCSR(t(indptr, torch.int64), t(indices, torch.int32), t(data, torch.float32), int(n_cols))
+
+    def to_host(self):
+        return (self.indptr.cpu().numpy(), self.indices.cpu().numpy(), self.data.cpu().numpy(), self.n_cols)
+
+
+# ----------------------------------------------------------------------------- qc
+def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor):
+    """sc.pp.calculate_qc_metrics(qc_vars=['mt'], percent_top=None, log1p=False)."""
+    dev = X.device
+    N, G = X.n_rows, X.n_cols
+    out = dict(
+        n_genes_by_counts=torch.empty(N, dtype=torch.int32, device=dev),
+        total_counts=torch.empty(N, dtype=torch.float64, device=dev),
+        total_counts_mt=torch.empty(N, dtype=torch.float64, device=dev),
+        pct_counts_mt=torch.empty(N, dtype=torch.float64, device=dev),
+        n_cells_by_counts=torch.empty(G, dtype=torch.int32, device=dev),
+        gene_total_counts=torch.empty(G, dtype=torch.float64, device=dev),
+    )
+    mt = mt_mask.to(device=dev, dtype=torch.uint8).contiguous()
+    _lib.call("scb_qc_metrics", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), N, G, _p(mt),
+              _p(out["n_genes_by_counts"]), _p(out["total_counts"]), _p(out["total_counts_mt"]),
+              _p(out["pct_counts_mt"]), _p(out["n_cells_by_counts"]), _p(out["gene_total_counts"]),
+              _stream(dev))
+    return out
+
+
+def filter_masks(qc, min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3):
+    """sc.pp.filter_cells(min_genes, max_genes) & pct_counts_mt < max_pct_mt; sc.pp.filter_genes(min_cells).
+    Returns (cell_mask u8[N], gene_mask u8[G], (n_kept_cells, n_kept_genes))."""
+    ng = qc["n_genes_by_counts"]
+    dev = ng.device
+    N, G = ng.numel(), qc["n_cells_by_counts"].numel()
+    cm = torch.empty(N, dtype=torch.uint8, device=dev)
+    gm = torch.empty(G, dtype=torch.uint8, device=dev)
+    kept = torch.empty(2, dtype=torch.int64, device=dev)
+    _lib.call("scb_filter_masks", _ctx(ng), _p(ng), _p(qc["pct_counts_mt"]), N, _p(qc["n_cells_by_counts"]), G,
+              int(min_genes), -1 if max_genes is None else int(max_genes), float(max_pct_mt), int(min_cells),
+              _p(cm), _p(gm), _p(kept), _stream(dev))
+    k = kept.cpu().tolist()
+    return cm, gm, (int(k[0]), int(k[1]))
+
+
+def subset(X: DeviceCSR, cell_mask, gene_mask, n_kept=None, target_sum=None):
+    """adata[cell_mask, gene_mask] (rows/columns kept in order, columns renumbered).
+
+    With ``target_sum`` set, the values are normalize_total + log1p'd in the same pass
+    (fused pipeline form) and the returned matrix carries ``counts``=None and
+    ``row_scale`` (per kept row)."""
+    dev = X.device
+    if n_kept is None:
+        n_kept = (int(cell_mask.sum().item()), int(gene_mask.sum().item()))
+    nk, gk = n_kept
+    remap = torch.empty(X.n_cols, dtype=torch.int32, device=dev)
+    new_indptr = torch.empty(nk + 1, dtype=torch.int64, device=dev)
+    row_scale = torch.empty(nk, dtype=torch.float32, device=dev) if target_sum is not None else None
+    ctx, s = _ctx(X.data), _stream(dev)
+    _lib.call("scb_subset_count", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols,
+              _p(cell_mask), _p(gene_mask), _p(remap), _p(new_indptr), float(target_sum or 0.0),
+              _p(row_scale), 0, s)
+    nnz = int(new_indptr[nk].item())
+    ind = torch.empty(nnz, dtype=torch.int32, device=dev)
+    dat = torch.empty(nnz, dtype=torch.float32, device=dev)
+    _lib.call("scb_subset_fill", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, _p(cell_mask),
+              _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(dat), s)
+    out = DeviceCSR(new_indptr, ind, dat, gk)
+    out.row_scale = row_scale
+    return out
+
+
+# ----------------------------------------------------------------------------- norm_hvg
+def normalize_log1p(X: DeviceCSR, target_sum: float = 1e4) -> DeviceCSR:
+    """sc.pp.normalize_total(target_sum) followed by sc.pp.log1p (out of place).  The result
+    keeps a reference to the raw counts and the per-row factor for highly_variable_genes."""
+    dev = X.device
+    out = torch.empty_like(X.data)
+    scale = torch.empty(X.n_rows, dtype=torch.float32, device=dev)
+    _lib.call("scb_normalize_log1p", _ctx(X.data), _p(X.indptr), _p(X.data), X.n_rows, float(target_sum),
+              _p(out), _p(scale), _stream(dev))
+    return DeviceCSR(X.indptr, X.indices, out, X.n_cols, counts=X.data, row_scale=scale)
+
+
+def hvg_gene_sums(X: DeviceCSR, counts=None, row_scale=None, gene_remap=None, n_out=None, sums=None):
+    """Fixed-point per-gene sums of the normalized counts (u64[2][2][G]); additive across shards."""
+    counts = X.counts if counts is None else counts
+    row_scale = X.row_scale if row_scale is None else row_scale
+    if counts is None or row_scale is None:
+        raise ValueError("highly_variable_genes needs the output of normalize_log1p (raw counts + row scale)")
+    n_out = X.n_cols if n_out is None else n_out
+    if sums is None:
+        sums = torch.zeros((2, 2, n_out), dtype=torch.int64, device=X.device)
+    _lib.call("scb_hvg_gene_sums", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(counts), _p(row_scale),
+              X.n_rows, X.n_cols, _p(gene_remap), n_out, _p(sums), _stream(X.device))
+    return sums
+
+
+def hvg_select(sums, n_cells: int, n_top_genes: int, n_bins: int = 20):
+    dev = sums.device
+    G = sums.shape[-1]
+    st = dict(means=torch.empty(G, dtype=torch.float64, device=dev),
+              variances=torch.empty(G, dtype=torch.float64, device=dev),
+              dispersions=torch.empty(G, dtype=torch.float64, device=dev),
+              dispersions_norm=torch.empty(G, dtype=torch.float64, device=dev),
+              mean_bin=torch.empty(G, dtype=torch.int32, device=dev))
+    mask = torch.empty(G, dtype=torch.uint8, device=dev)
+    index = torch.empty(max(1, n_top_genes), dtype=torch.int32, device=dev)
+    nsel = torch.empty(1, dtype=torch.int32, device=dev)
+    _lib.call("scb_hvg_select", _ctx(sums), _p(sums), G, int(n_cells), int(n_top_genes), int(n_bins),
+              _p(st["means"]), _p(st["variances"]), _p(st["dispersions"]), _p(st["dispersions_norm"]),
+              _p(st["mean_bin"]), _p(mask), _p(index), _p(nsel), _stream(dev))
+    n = int(nsel.item())
+    st["n_selected"] = n
+    return mask, index[:n], st
+
+
+def highly_variable_genes(X_log: DeviceCSR, n_top_genes: int = 2000, n_bins: int = 20):
+    """sc.pp.highly_variable_genes(flavor='seurat', n_top_genes, n_bins) on normalize_log1p output.
+    Returns (hvg_mask u8[G], hvg_index i32[H] sorted, stats dict)."""
+    sums = hvg_gene_sums(X_log)
+    return hvg_select(sums, X_log.n_rows, n_top_genes, n_bins)
+
+
+# ----------------------------------------------------------------------------- regress (scale)
+@dataclasses.dataclass
+class Scaled:
+    """Dense scaled HVG matrix Z[N][ld] (float32, row-major): columns [0, H) are the HVGs,
+    column ``ones_col`` = 1 (gives the column sums in the Gram), the rest zero."""
+    Z: torch.Tensor
+    H: int
+    ones_col: int
+    mean: torch.Tensor
+    inv_std: torch.Tensor
+
+    @property
+    def ld(self):
+        return self.Z.shape[1]
+
+    def values(self):
+        return self.Z[:, : self.H]
+
+
+def padded_width(H: int) -> int:
+    return ((H + 1 + ONES_PAD - 1) // ONES_PAD) * ONES_PAD
+
+
+def gene_slots(hvg_index: torch.Tensor, n_cols: int):
+    slot = torch.full((n_cols,), -1, dtype=torch.int32, device=hvg_index.device)
+    slot[hvg_index.long()] = torch.arange(hvg_index.numel(), dtype=torch.int32, device=hvg_index.device)
+    return slot
+
+
+def scale_gene_sums(X_log: DeviceCSR, slot, H, sums=None):
+    if sums is None:
+        sums = torch.zeros((2, 2, H), dtype=torch.int64, device=X_log.device)
+    _lib.call("scb_scale_gene_sums", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
+              X_log.n_rows, X_log.n_cols, _p(slot), H, _p(sums), _stream(X_log.device))
+    return sums
+
+
+def scale_finalize(sums, n_cells: int):
+    H = sums.shape[-1]
+    dev = sums.device
+    mean = torch.empty(H, dtype=torch.float64, device=dev)
+    inv = torch.empty(H, dtype=torch.float64, device=dev)
+    _lib.call("scb_scale_finalize", _ctx(sums), _p(sums), H, int(n_cells), _p(mean), _p(inv), _stream(dev))
+    return mean, inv
+
+
+def scale_dense(X_log: DeviceCSR, slot, H, mean, inv, max_value=10.0, out=None) -> Scaled:
+    ld = padded_width(H)
+    Z = out if out is not None else torch.empty((X_log.n_rows, ld), dtype=torch.float32, device=X_log.device)
+    _lib.call("scb_scale_dense", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
+              X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value), _p(Z), ld, H,
+              _stream(X_log.device))
+    return Scaled(Z, H, H, mean, inv)
+
+
+def scale(X_log: DeviceCSR, hvg_index: torch.Tensor, max_value: float = 10.0) -> Scaled:
+    """sc.pp.scale(adata[:, hvg], max_value) -> dense float32 (zero-centred, unit variance, clipped)."""
+    H = int(hvg_index.numel())
+    slot = gene_slots(hvg_index, X_log.n_cols)
+    sums = scale_gene_sums(X_log, slot, H)
+    mean, inv = scale_finalize(sums, X_log.n_rows)
+    return scale_dense(X_log, slot, H, mean, inv, max_value)

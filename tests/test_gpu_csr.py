@@ -1,0 +1,85 @@
+"""GPU parity of the CSR stages (QC, masks, subset, normalize+log1p, HVG, scale) vs the oracle."""
+import numpy as np
+import pytest
+
+from tests.gpu_fixtures import C1, c1_inputs, c1_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev_state():
+    import torch
+    import paper_2605_13928_b200 as scb
+    from paper_2605_13928_b200 import pp
+    X, mt = c1_inputs()
+    p = C1["params"]
+    Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, X.n_cols)
+    qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
+    cm, gm, kept = scb.filter_masks(qc, p.min_genes, p.max_genes, p.max_pct_mt, p.min_cells)
+    Xs = scb.subset(Xd, cm, gm, kept)
+    Xl = scb.normalize_log1p(Xs, p.target_sum)
+    hvg_mask, hvg_index, st = scb.highly_variable_genes(Xl, p.n_top_genes, p.n_bins)
+    sc = scb.scale(Xl, hvg_index, p.max_value)
+    torch.cuda.synchronize()
+    return dict(qc=qc, cm=cm, gm=gm, Xs=Xs, Xl=Xl, hvg=hvg_mask, hvg_index=hvg_index, st=st, sc=sc)
+
+
+def test_qc_bit_exact(dev_state):
+    o = c1_oracle(False)["qc"]
+    qc = dev_state["qc"]
+    for k in ["n_genes_by_counts", "total_counts", "total_counts_mt", "n_cells_by_counts", "gene_total_counts"]:
+        np.testing.assert_array_equal(qc[k].cpu().numpy(), o[k], err_msg=k)
+    np.testing.assert_array_equal(qc["pct_counts_mt"].cpu().numpy(), o["pct_counts_mt"])
+
+
+def test_masks_bit_exact(dev_state):
+    o = c1_oracle(False)
+    np.testing.assert_array_equal(dev_state["cm"].cpu().numpy(), o["cell_mask"])
+    np.testing.assert_array_equal(dev_state["gm"].cpu().numpy(), o["gene_mask"])
+
+
+def test_subset_bit_exact(dev_state):
+    o = c1_oracle(False)["X_sub"]
+    ip, ix, d, g = dev_state["Xs"].to_host()
+    assert g == o.n_cols
+    np.testing.assert_array_equal(ip, o.indptr)
+    np.testing.assert_array_equal(ix, o.indices)
+    np.testing.assert_array_equal(d, o.data)
+
+
+def test_normalize_log1p(dev_state):
+    o = c1_oracle(False)
+    Xl = dev_state["Xl"]
+    np.testing.assert_array_equal(Xl.row_scale.cpu().numpy(), o["row_scale"])
+    got = Xl.data.cpu().numpy()
+    ref = o["X_log"].data
+    np.testing.assert_allclose(got, ref, rtol=1e-5, atol=0)
+
+
+def test_hvg_set_bit_exact(dev_state):
+    o = c1_oracle(False)
+    np.testing.assert_array_equal(dev_state["hvg"].cpu().numpy(), o["hvg_mask"])
+    st, ost = dev_state["st"], o["hvg_stats"]
+    np.testing.assert_array_equal(st["means"].cpu().numpy(), ost["means"])
+    np.testing.assert_array_equal(st["variances"].cpu().numpy(), ost["variances"])
+    np.testing.assert_array_equal(st["mean_bin"].cpu().numpy(), ost["mean_bin"])
+    np.testing.assert_allclose(st["dispersions_norm"].cpu().numpy(), ost["dispersions_norm"], rtol=1e-12, atol=1e-12)
+
+
+def test_scale(dev_state):
+    o = c1_oracle(False)
+    sc = dev_state["sc"]
+    Z = sc.values().cpu().numpy()
+    ref = o["Z"]
+    assert Z.shape == ref.shape
+    # relative error w.r.t. the magnitude before centring: log1p differs from numpy's by
+    # <= 1 ulp, and (l - mean) cancels when l ~ mean, so |ref| alone is not a fair scale.
+    mag = np.maximum(np.abs(ref), np.abs(o["scale_mean"] * o["scale_inv_std"])[None, :])
+    err = np.abs(Z - ref) / np.maximum(mag, 1e-30)
+    assert err.max() < 1e-5, err.max()
+    np.testing.assert_allclose(sc.mean.cpu().numpy(), o["scale_mean"], rtol=1e-7)
+    np.testing.assert_allclose(sc.inv_std.cpu().numpy(), o["scale_inv_std"], rtol=1e-7)
+    full = sc.Z.cpu().numpy()
+    assert np.all(full[:, sc.ones_col] == 1.0)
+    assert np.all(full[:, sc.H + 1:] == 0.0)
