@@ -134,17 +134,18 @@ SCB_API int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* 
                     int32_t n_slots, const double* mean, const double* inv_std, double max_value,
                     float* Z, int64_t ldz, int32_t ones_col, void* stream);
 
-/* ---- a7: partial Gram matrix C = Z^T Z (float32 [hp][hp], full symmetric) on the
- * 5th-gen tensor cores (tcgen05, TF32 inputs, FP32 accumulate in TMEM, operands staged by
- * TMA).  hp = ldz must be a multiple of 128; n_rows any. */
-SCB_API int scb_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp, float* C, void* stream);
+/* ---- a7: partial Gram matrix C = Z^T Z (float64 [hp][hp], full symmetric) on the
+ * 5th-gen tensor cores (tcgen05, 3xTF32 split products, FP32 accumulate in TMEM per
+ * <=64k-cell K-slice, slices summed in float64; operands staged by TMA).  hp = ldz must
+ * be a multiple of 128; n_rows any. */
+SCB_API int scb_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp, double* C, void* stream);
 
 /* ---- a8: top-n_comps eigenpairs of the centred covariance
  * Cov = (C[:h,:h] - N m m^T)/(N-1), m = C[ones_col, :h]/N (column means of Z).
  * Outputs eigenvalues (desc, float64), components_t float32[n_comps_pad][hp] (row j =
  * component j, sign-canonical: largest |loading| positive, zero-padded), col_mean
  * float32[hp] and trace (float64, total variance).  Subspace iteration in float64. */
-SCB_API int scb_pca_eig(scb_ctx* ctx, const float* C, int32_t h, int32_t hp, int32_t ones_col,
+SCB_API int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, int32_t ones_col,
                 int64_t n_cells, int32_t n_comps, int32_t n_comps_pad, double* eigenvalues,
                 float* components_t, float* col_mean, double* trace, void* stream);
 

@@ -1,0 +1,435 @@
+// Top-k eigenpairs of the (small, dense) PCA covariance, on the device, in float64.
+//
+// Cov = (C[:h,:h] - N m m^T)/(N-1) with m = C[ones_col, :h]/N (column means of Z, exposed
+// by the ones column of the scaled matrix).  Block subspace iteration with block size
+// b = 96 (>= n_comps + oversampling): Y = Cov^q Q, Cholesky-QR (twice), repeated; then
+// Rayleigh-Ritz T = Q^T Cov Q solved by a one-CTA cyclic Jacobi, and V = Q W.  The
+// residual max_j ||Cov v_j - l_j v_j|| / l_1 is checked on the device and iterations
+// continue until it falls below 1e-10 (or an iteration cap).  Sign rule: the
+// largest-|loading| entry of every component is positive (first index on ties).
+#include "common.cuh"
+
+namespace scb {
+
+constexpr int kB = 96;   // subspace block size (n_comps + oversampling)
+constexpr int kLd = kB + 1;
+
+// ------------------------------------------------------------------ small fp64 GEMM
+// Cm[M][N] (ldc) = alpha * op(A) * op(B) + beta * Cm ; row-major operands.
+// opA: 0 -> A[M][K] (lda), 1 -> A^T where A is [K][M]; opB: 0 -> B[K][N], 1 -> B^T ([N][K]).
+// 64x64 tiles, 256 threads, 4x4 per thread, K chunk 16; split-K over blockIdx.z with
+// atomicAdd when gridDim.z > 1 (caller zeroes Cm and passes beta = 0).
+__global__ void __launch_bounds__(256) dgemm_kernel(int M, int N, int K, double alpha, const double* __restrict__ A,
+                                                    int lda, int opA, const double* __restrict__ B, int ldb, int opB,
+                                                    double beta, double* __restrict__ Cm, int ldc) {
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int kchunk = (K + gridDim.z - 1) / gridDim.z;
+  const int kb = blockIdx.z * kchunk, ke = min(K, kb + kchunk);
+  double acc[4][4] = {};
+  for (int k0 = kb; k0 < ke; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int kk = e / 64, mm = e % 64;
+      const int gk = k0 + kk;
+      double a = 0.0, b = 0.0;
+      if (gk < ke) {
+        const int gm = m0 + mm, gn = n0 + mm;
+        if (gm < M) a = opA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk];
+        if (gn < N) b = opB ? B[(size_t)gn * ldb + gk] : B[(size_t)gk * ldb + gn];
+      }
+      As[kk][mm] = a;
+      Bs[kk][mm] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gm = m0 + ty * 4 + i, gn = n0 + tx * 4 + j;
+      if (gm < M && gn < N) {
+        double* c = Cm + (size_t)gm * ldc + gn;
+        if (gridDim.z > 1) atomicAdd(c, alpha * acc[i][j]);
+        else *c = alpha * acc[i][j] + (beta != 0.0 ? beta * *c : 0.0);
+      }
+    }
+}
+
+static int dgemm(int M, int N, int K, const double* A, int lda, int opA, const double* B, int ldb, int opB, double* Cm,
+                 int ldc, cudaStream_t s, int splitk = 1) {
+  dim3 g((N + 63) / 64, (M + 63) / 64, splitk);
+  if (splitk > 1) SCB_CUDA(cudaMemsetAsync(Cm, 0, sizeof(double) * (size_t)M * ldc, s));
+  dgemm_kernel<<<g, 256, 0, s>>>(M, N, K, 1.0, A, lda, opA, B, ldb, opB, 0.0, Cm, ldc);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
+// ------------------------------------------------------------------ covariance
+__global__ void cov_build_kernel(const double* __restrict__ Cg, int hp, int h, int ones_col, int64_t n,
+                                 double* __restrict__ cov, double* __restrict__ mean) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= h) return;
+  const double N = (double)n;
+  const double mi = Cg[(size_t)ones_col * hp + i] / N;
+  const double mj = Cg[(size_t)ones_col * hp + j] / N;
+  cov[(size_t)i * h + j] = (Cg[(size_t)i * hp + j] - N * mi * mj) / (N - 1.0);
+  if (i == 0) mean[j] = mj;
+}
+
+__global__ void trace_kernel(const double* __restrict__ cov, int h, double* __restrict__ tr) {
+  __shared__ double sb[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < h; i += blockDim.x) s += cov[(size_t)i * h + i];
+  s = warp_sum(s);
+  if (lane_id() == 0) sb[warp_id()] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sb[w];
+    *tr = t;
+  }
+}
+
+// deterministic start block: Q0[i][j] = hash-based uniform in [-1, 1)
+__global__ void init_block_kernel(double* __restrict__ Q, int h) {
+  const int i = blockIdx.x, j = threadIdx.x;
+  uint64_t z = ((uint64_t)i << 32) ^ (uint64_t)j ^ 0x5DEECE66Dull;
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  Q[(size_t)i * kB + j] = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+// ------------------------------------------------------------------ Cholesky QR
+// In place Cholesky of the kB x kB Gram S = Q^T Q (one CTA), S -> R (upper, row-major).
+__global__ void __launch_bounds__(1024) chol_kernel(double* __restrict__ S, int* __restrict__ fail) {
+  extern __shared__ double dyn[];
+  double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
+  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) a[e / kB][e % kB] = S[e];
+  __syncthreads();
+  for (int k = 0; k < kB; ++k) {
+    if (threadIdx.x == 0) {
+      double d = a[k][k];
+      if (!(d > 0.0)) { *fail = 1; d = 1e-300; }
+      a[k][k] = sqrt(d);
+    }
+    __syncthreads();
+    const double inv = 1.0 / a[k][k];
+    for (int j = k + 1 + threadIdx.x; j < kB; j += blockDim.x) a[k][j] *= inv;  // row k of R
+    __syncthreads();
+    for (int e = threadIdx.x; e < (kB - k - 1) * (kB - k - 1); e += blockDim.x) {
+      const int i = k + 1 + e / (kB - k - 1), j = k + 1 + e % (kB - k - 1);
+      if (j >= i) a[i][j] -= a[k][i] * a[k][j];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
+    const int i = e / kB, j = e % kB;
+    S[e] = (j >= i) ? a[i][j] : 0.0;
+  }
+}
+
+// Q[h][kB] := Q R^{-1}  (row-wise forward substitution x R = q)
+__global__ void trsm_kernel(double* __restrict__ Q, const double* __restrict__ R, int h) {
+  extern __shared__ double dyn[];
+  double (*r)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
+  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) r[e / kB][e % kB] = R[e];
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= h) return;
+  double x[kB];
+  double* q = Q + (size_t)i * kB;
+#pragma unroll 8
+  for (int j = 0; j < kB; ++j) x[j] = q[j];
+  for (int j = 0; j < kB; ++j) {
+    double v = x[j];
+    for (int l = 0; l < j; ++l) v -= x[l] * r[l][j];
+    x[j] = v / r[j][j];
+  }
+#pragma unroll 8
+  for (int j = 0; j < kB; ++j) q[j] = x[j];
+}
+
+// ------------------------------------------------------------------ Jacobi (one CTA)
+// Cyclic two-sided Jacobi on the symmetric kB x kB matrix T; W accumulates rotations.
+// Round-robin ordering: kB/2 disjoint (p, q) pairs per round, kB-1 rounds per sweep.
+__global__ void __launch_bounds__(1024) jacobi_kernel(double* __restrict__ T, double* __restrict__ W, int sweeps) {
+  extern __shared__ double dyn[];
+  double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
+  double (*w)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn + kB * kLd);
+  __shared__ double cs[kB / 2], sn[kB / 2];
+  __shared__ int pp[kB / 2], qq[kB / 2];
+  __shared__ int ring[kB];
+  __shared__ double off_s, dia_s;
+  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
+    a[e / kB][e % kB] = T[e];
+    w[e / kB][e % kB] = (e / kB == e % kB) ? 1.0 : 0.0;
+  }
+  if (threadIdx.x < kB) ring[threadIdx.x] = threadIdx.x;
+  __syncthreads();
+  for (int sw = 0; sw < sweeps; ++sw) {
+    for (int rd = 0; rd < kB - 1; ++rd) {
+      if (threadIdx.x < kB / 2) {
+        int p = ring[threadIdx.x], q = ring[kB - 1 - threadIdx.x];
+        if (p > q) { int t = p; p = q; q = t; }
+        pp[threadIdx.x] = p;
+        qq[threadIdx.x] = q;
+        const double apq = a[p][q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0) {
+          const double tau = (a[q][q] - a[p][p]) / (2.0 * apq);
+          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+        }
+        cs[threadIdx.x] = c;
+        sn[threadIdx.x] = s;
+      }
+      __syncthreads();
+      // rows: A := J^T A
+      for (int e = threadIdx.x; e < (kB / 2) * kB; e += blockDim.x) {
+        const int k = e / kB, j = e % kB;
+        const int p = pp[k], q = qq[k];
+        const double c = cs[k], s = sn[k];
+        const double ap = a[p][j], aq = a[q][j];
+        a[p][j] = c * ap - s * aq;
+        a[q][j] = s * ap + c * aq;
+      }
+      __syncthreads();
+      // columns: A := A J ; W := W J
+      for (int e = threadIdx.x; e < (kB / 2) * kB; e += blockDim.x) {
+        const int k = e / kB, i = e % kB;
+        const int p = pp[k], q = qq[k];
+        const double c = cs[k], s = sn[k];
+        const double ap = a[i][p], aq = a[i][q];
+        a[i][p] = c * ap - s * aq;
+        a[i][q] = s * ap + c * aq;
+        const double wp = w[i][p], wq = w[i][q];
+        w[i][p] = c * wp - s * wq;
+        w[i][q] = s * wp + c * wq;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {  // rotate the ring (element 0 fixed)
+        const int last = ring[kB - 1];
+        for (int i = kB - 1; i > 1; --i) ring[i] = ring[i - 1];
+        ring[1] = last;
+      }
+      __syncthreads();
+    }
+    // convergence: off-diagonal Frobenius norm relative to the diagonal
+    if (threadIdx.x == 0) { off_s = 0.0; dia_s = 0.0; }
+    __syncthreads();
+    double off = 0.0, dia = 0.0;
+    for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
+      const int i = e / kB, j = e % kB;
+      if (i != j) off += a[i][j] * a[i][j];
+      else dia += a[i][j] * a[i][j];
+    }
+    off = warp_sum(off);
+    dia = warp_sum(dia);
+    if (lane_id() == 0) { atomicAdd(&off_s, off); atomicAdd(&dia_s, dia); }
+    __syncthreads();
+    const bool conv = off_s <= 1e-30 * dia_s;
+    __syncthreads();
+    if (conv) break;
+  }
+  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
+    T[e] = a[e / kB][e % kB];
+    W[e] = w[e / kB][e % kB];
+  }
+}
+
+// order eigenpairs by eigenvalue (desc), top k; eigenvalues from diag(T)
+__global__ void select_kernel(const double* __restrict__ T, int k, int* __restrict__ order, double* __restrict__ lam) {
+  __shared__ double d[kB];
+  if (threadIdx.x < kB) d[threadIdx.x] = T[threadIdx.x * kB + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < kB) {
+    const int i = threadIdx.x;
+    int rank = 0;
+    for (int j = 0; j < kB; ++j) rank += (d[j] > d[i] || (d[j] == d[i] && j < i)) ? 1 : 0;
+    if (rank < k) {
+      order[rank] = i;
+      lam[rank] = d[i];
+    }
+  }
+}
+
+// V[h][k] = Q[h][kB] * W[:, order]
+__global__ void gather_cols_kernel(const double* __restrict__ W, const int* __restrict__ order, int k,
+                                   double* __restrict__ Wk) {
+  const int i = blockIdx.x, j = threadIdx.x;
+  if (j < k) Wk[(size_t)i * k + j] = W[(size_t)i * kB + order[j]];
+}
+
+// residual r_j = ||Cov v_j - l_j v_j||, components sign fix and output
+__global__ void residual_kernel(const double* __restrict__ CV, const double* __restrict__ V, const double* __restrict__ lam,
+                                int h, int k, double* __restrict__ res) {
+  const int j = blockIdx.x;
+  __shared__ double sb[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < h; i += blockDim.x) {
+    const double d = CV[(size_t)i * k + j] - lam[j] * V[(size_t)i * k + j];
+    s += d * d;
+  }
+  s = warp_sum(s);
+  if (lane_id() == 0) sb[warp_id()] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sb[w];
+    res[j] = sqrt(t);
+  }
+}
+
+__global__ void finalize_components_kernel(const double* __restrict__ V, int h, int k, int hp, int kpad,
+                                           float* __restrict__ comp_t) {
+  const int j = blockIdx.x;  // component
+  __shared__ double best;
+  __shared__ int besti;
+  if (threadIdx.x == 0) {
+    best = -1.0;
+    besti = 0;
+    for (int i = 0; i < h; ++i) {
+      const double a = fabs(V[(size_t)i * k + j]);
+      if (a > best) { best = a; besti = i; }
+    }
+  }
+  __syncthreads();
+  const double sgn = (V[(size_t)besti * k + j] < 0.0) ? -1.0 : 1.0;
+  for (int i = threadIdx.x; i < hp; i += blockDim.x)
+    comp_t[(size_t)j * hp + i] = (i < h) ? (float)(sgn * V[(size_t)i * k + j]) : 0.0f;
+  (void)kpad;
+}
+
+__global__ void fill_zero_rows(float* __restrict__ comp_t, int k, int kpad, int hp) {
+  const int j = k + blockIdx.x;
+  if (j < kpad)
+    for (int i = threadIdx.x; i < hp; i += blockDim.x) comp_t[(size_t)j * hp + i] = 0.0f;
+}
+
+__global__ void mean_out_kernel(const double* __restrict__ m, int h, int hp, float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < hp) out[i] = (i < h) ? (float)m[i] : 0.0f;
+}
+
+}  // namespace scb
+
+using namespace scb;
+
+extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, int32_t ones_col, int64_t n_cells,
+                           int32_t n_comps, int32_t n_comps_pad, double* eigenvalues, float* components_t,
+                           float* col_mean, double* trace, void* stream) {
+  SCB_REQUIRE(ctx && C && eigenvalues && components_t && col_mean && trace, SCB_ERR_ARG, "scb_pca_eig: null argument");
+  SCB_REQUIRE(n_comps >= 1 && n_comps <= kB - 16 && n_comps <= h && n_comps_pad >= n_comps, SCB_ERR_ARG,
+              "scb_pca_eig: need 1 <= n_comps <= %d and <= h", kB - 16);
+  SCB_REQUIRE(h >= kB && ones_col >= 0 && ones_col < hp && h <= hp, SCB_ERR_ARG,
+              "scb_pca_eig: need h >= %d (block size) and a ones column", kB);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int kSmemKB = kB * kLd * 8;
+  SCB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemKB));
+  SCB_CUDA(cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemKB));
+  SCB_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSmemKB));
+  // workspace: cov h*h, Q h*kB, Y h*kB, S kB*kB, W kB*kB, Wk kB*n, V h*n, CV h*n, mean h, misc
+  const size_t nd = (size_t)h * h + 2 * (size_t)h * kB + 2 * kB * kB + (size_t)kB * n_comps + 2 * (size_t)h * n_comps +
+                    h + 4 * kB + 64;
+  void* ws;
+  SCB_TRY(ws_get(ctx, 2, nd * 8 + 4096, &ws, s));
+  double* cov = (double*)ws;
+  double* Q = cov + (size_t)h * h;
+  double* Y = Q + (size_t)h * kB;
+  double* S = Y + (size_t)h * kB;
+  double* W = S + kB * kB;
+  double* Wk = W + kB * kB;
+  double* V = Wk + (size_t)kB * n_comps;
+  double* CV = V + (size_t)h * n_comps;
+  double* mean = CV + (size_t)h * n_comps;
+  double* res = mean + h;
+  double* lam_all = res + kB;
+  int* order = (int*)(lam_all + kB);
+  int* fail = order + kB;
+
+  dim3 gc((h + 255) / 256, h);
+  cov_build_kernel<<<gc, 256, 0, s>>>(C, hp, h, ones_col, n_cells, cov, mean);
+  SCB_LAUNCH_CHECK();
+  trace_kernel<<<1, 1024, 0, s>>>(cov, h, trace);
+  SCB_LAUNCH_CHECK();
+  init_block_kernel<<<h, kB, 0, s>>>(Q, h);
+  SCB_LAUNCH_CHECK();
+  SCB_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
+  const int splitk = std::max(1, std::min(16, h / 128));
+  auto orth = [&](double* M) -> int {
+    for (int rep = 0; rep < 2; ++rep) {  // CholQR2
+      SCB_TRY(dgemm(kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s, splitk));
+      chol_kernel<<<1, 1024, kSmemKB, s>>>(S, fail);
+      SCB_LAUNCH_CHECK();
+      trsm_kernel<<<(h + 127) / 128, 128, kSmemKB, s>>>(M, S, h);
+      SCB_LAUNCH_CHECK();
+    }
+    return SCB_OK;
+  };
+  SCB_TRY(orth(Q));
+  const int kPower = 4, kMaxOuter = 60;
+  double host_res[kB];
+  int outer = 0;
+  for (; outer < kMaxOuter; ++outer) {
+    for (int p = 0; p < kPower; ++p) {
+      SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s));
+      std::swap(Q, Y);
+      if (p == 1) SCB_TRY(orth(Q));  // keep the block well conditioned
+    }
+    SCB_TRY(orth(Q));
+    if ((outer + 1) % 5 != 0) continue;
+    // Rayleigh-Ritz + residual check
+    SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s));       // Y = Cov Q
+    SCB_TRY(dgemm(kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s, splitk));  // T = Q^T Y
+    jacobi_kernel<<<1, 1024, 2 * kSmemKB, s>>>(S, W, 30);
+    SCB_LAUNCH_CHECK();
+    select_kernel<<<1, kB, 0, s>>>(S, n_comps, order, lam_all);
+    SCB_LAUNCH_CHECK();
+    gather_cols_kernel<<<kB, kB, 0, s>>>(W, order, n_comps, Wk);
+    SCB_LAUNCH_CHECK();
+    SCB_TRY(dgemm(h, n_comps, kB, Q, kB, 0, Wk, n_comps, 0, V, n_comps, s));     // V = Q Wk
+    SCB_TRY(dgemm(h, n_comps, h, cov, h, 0, V, n_comps, 0, CV, n_comps, s));     // Cov V
+    residual_kernel<<<n_comps, 256, 0, s>>>(CV, V, lam_all, h, n_comps, res);
+    SCB_LAUNCH_CHECK();
+    double lam0 = 0.0;
+    SCB_CUDA(cudaMemcpyAsync(host_res, res, sizeof(double) * n_comps, cudaMemcpyDeviceToHost, s));
+    SCB_CUDA(cudaMemcpyAsync(&lam0, lam_all, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SCB_CUDA(cudaStreamSynchronize(s));
+    double worst = 0.0;
+    for (int j = 0; j < n_comps; ++j) worst = std::max(worst, host_res[j]);
+    if (worst <= 1e-10 * std::max(lam0, 1e-300)) break;
+  }
+  int hfail = 0;
+  SCB_CUDA(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SCB_CUDA(cudaStreamSynchronize(s));
+  SCB_REQUIRE(hfail == 0, SCB_ERR_DATA, "scb_pca_eig: Cholesky-QR breakdown (rank-deficient subspace)");
+  SCB_CUDA(cudaMemcpyAsync(eigenvalues, lam_all, sizeof(double) * n_comps, cudaMemcpyDeviceToDevice, s));
+  finalize_components_kernel<<<n_comps, 256, 0, s>>>(V, h, n_comps, hp, n_comps_pad, components_t);
+  SCB_LAUNCH_CHECK();
+  if (n_comps_pad > n_comps) {
+    fill_zero_rows<<<n_comps_pad - n_comps, 256, 0, s>>>(components_t, n_comps, n_comps_pad, hp);
+    SCB_LAUNCH_CHECK();
+  }
+  mean_out_kernel<<<(hp + 255) / 256, 256, 0, s>>>(mean, h, hp, col_mean);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}

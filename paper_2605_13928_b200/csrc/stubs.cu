@@ -1,8 +1,8 @@
 // Entry points not implemented yet in this build (return SCB_ERR_UNSUPPORTED).
 #include "common.cuh"
 #define STUB(name, ...) extern "C" int name(__VA_ARGS__) { scb::set_error(#name ": not implemented"); return SCB_ERR_UNSUPPORTED; }
-STUB(scb_gram, scb_ctx*, const float*, int64_t, int32_t, float*, void*)
-STUB(scb_pca_eig, scb_ctx*, const float*, int32_t, int32_t, int32_t, int64_t, int32_t, int32_t, double*, float*, float*, double*, void*)
-STUB(scb_project, scb_ctx*, const float*, int64_t, int32_t, const float*, const float*, int32_t, int32_t, float*, int32_t, void*)
+
+
+
 STUB(scb_knn, scb_ctx*, const float*, int64_t, const float*, int64_t, int32_t, int32_t, int32_t, int32_t, int32_t*, float*, void*)
 STUB(scb_synth_rows, scb_ctx*, uint64_t, int64_t, int64_t, int32_t, const double*, const double*, int32_t, const double*, int32_t, const double*, const int64_t*, int64_t*, int32_t*, float*, void*)

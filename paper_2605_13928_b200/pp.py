@@ -247,3 +247,54 @@ def scale(X_log: DeviceCSR, hvg_index: torch.Tensor, max_value: float = 10.0) ->
     sums = scale_gene_sums(X_log, slot, H)
     mean, inv = scale_finalize(sums, X_log.n_rows)
     return scale_dense(X_log, slot, H, mean, inv, max_value)
+
+
+# ----------------------------------------------------------------------------- pca
+@dataclasses.dataclass
+class PCAResult:
+    X_pca: torch.Tensor           # float32 [N][ld] (first n_comps columns valid, rest 0)
+    components: torch.Tensor      # float32 [n_comps][H] (row j = component j, sign-canonical)
+    variance: torch.Tensor        # float64 [n_comps]
+    variance_ratio: torch.Tensor  # float64 [n_comps]
+    col_mean: torch.Tensor        # float32 [ld_z] column means of Z (centring)
+    n_comps: int
+
+
+def gram(sc: Scaled, out=None):
+    """Partial (local) Gram matrix Z^T Z, float64 [ld][ld] (tcgen05, 3xTF32)."""
+    ld = sc.ld
+    C = out if out is not None else torch.empty((ld, ld), dtype=torch.float64, device=sc.Z.device)
+    _lib.call("scb_gram", _ctx(sc.Z), _p(sc.Z), sc.Z.shape[0], ld, _p(C), _stream(sc.Z.device))
+    return C
+
+
+def pca_from_gram(sc: Scaled, C, n_cells: int, n_comps: int = 50):
+    dev = sc.Z.device
+    ld = sc.ld
+    npad = 64 if n_comps <= 64 else 128
+    lam = torch.empty(n_comps, dtype=torch.float64, device=dev)
+    comp_t = torch.empty((npad, ld), dtype=torch.float32, device=dev)
+    mean = torch.empty(ld, dtype=torch.float32, device=dev)
+    tr = torch.empty(1, dtype=torch.float64, device=dev)
+    _lib.call("scb_pca_eig", _ctx(C), _p(C), sc.H, ld, sc.ones_col, int(n_cells), n_comps, npad, _p(lam), _p(comp_t),
+              _p(mean), _p(tr), _stream(dev))
+    return lam, comp_t, mean, tr
+
+
+def project(sc: Scaled, comp_t, mean, n_comps: int, ld_out: int = 64):
+    dev = sc.Z.device
+    npad = comp_t.shape[0]
+    X = torch.empty((sc.Z.shape[0], max(ld_out, npad)), dtype=torch.float32, device=dev)
+    _lib.call("scb_project", _ctx(sc.Z), _p(sc.Z), sc.Z.shape[0], sc.ld, _p(comp_t), _p(mean), n_comps, npad, _p(X),
+              X.shape[1], _stream(dev))
+    return X
+
+
+def pca(sc: Scaled, n_comps: int = 50) -> PCAResult:
+    """sc.tl.pca(n_comps, zero_center=True) on the scaled matrix: tcgen05 Gram, float64
+    subspace-iteration eigensolve, tcgen05 projection."""
+    C = gram(sc)
+    N = sc.Z.shape[0]
+    lam, comp_t, mean, tr = pca_from_gram(sc, C, N, n_comps)
+    X = project(sc, comp_t, mean, n_comps)
+    return PCAResult(X, comp_t[:n_comps, : sc.H], lam, lam / tr, mean, n_comps)

@@ -1,0 +1,70 @@
+"""GPU parity of PCA: tcgen05 Gram (3xTF32), float64 eigensolve, tcgen05 projection."""
+import numpy as np
+import pytest
+
+from oracle import pipeline as op
+from tests.gpu_fixtures import C1, c1_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _scaled_from_host(Z, H):
+    import torch
+    from paper_2605_13928_b200 import pp
+    ld = pp.padded_width(H)
+    Zp = np.zeros((Z.shape[0], ld), dtype=np.float32)
+    Zp[:, :H] = Z
+    Zp[:, H] = 1.0
+    return pp.Scaled(torch.as_tensor(Zp).cuda(), H, H, None, None)
+
+
+@pytest.mark.parametrize("n,h", [(1000, 200), (4099, 1000), (70001, 300)])
+def test_gram_matches_fp64(n, h):
+    import torch
+    from paper_2605_13928_b200 import pp
+    rng = np.random.default_rng(n)
+    Z = rng.standard_normal((n, h)).astype(np.float32)
+    sc = _scaled_from_host(Z, h)
+    C = pp.gram(sc).cpu().numpy()
+    Zp = sc.Z.cpu().numpy().astype(np.float64)
+    ref = Zp.T @ Zp
+    scale = np.sqrt(np.outer(np.diag(ref), np.diag(ref)))
+    err = np.abs(C - ref) / np.maximum(scale, 1e-30)
+    # tcgen05 FP32 accumulation rounds toward zero: a systematic ~1e-8-per-cell relative bias
+    # on monotone sums (the diagonal) within one K-slice; slices are <= 64k cells.
+    assert err.max() < 1e-3, err.max()
+    off = err.copy()
+    np.fill_diagonal(off, 0)
+    assert off.max() < 2e-6, off.max()
+    np.testing.assert_array_equal(C, C.T)
+
+
+def test_pca_matches_oracle():
+    from paper_2605_13928_b200 import pp
+    o = c1_oracle(False)
+    Z = o["Z"]
+    H = Z.shape[1]
+    sc = _scaled_from_host(Z, H)
+    r = pp.pca(sc, C1["params"].n_comps)
+    V = r.components.cpu().numpy().T.astype(np.float64)   # [H][k]
+    Vo = o["components"]
+    ang = op.subspace_angle(V, Vo)
+    assert ang < 1e-3, ang
+    lam = r.variance.cpu().numpy()
+    np.testing.assert_allclose(lam, o["variance"], rtol=1e-4)
+    np.testing.assert_allclose(r.variance_ratio.cpu().numpy(), o["variance_ratio"], rtol=1e-4)
+    # per-component agreement (sign-canonical) where the eigen-gap is not tiny
+    spec = o["spectrum"]
+    k = V.shape[1]
+    gaps = np.minimum(np.abs(spec[:k] - np.r_[np.inf, spec[:k - 1]]), np.abs(spec[:k] - spec[1:k + 1])) / spec[:k]
+    for j in range(k):
+        if gaps[j] > 1e-2:
+            c = abs(float(V[:, j] @ Vo[:, j]))
+            assert c > 1 - 1e-6, (j, c, gaps[j])
+            np.testing.assert_allclose(V[:, j], Vo[:, j], atol=1e-4)
+    X = r.X_pca.cpu().numpy()[:, :k]
+    # embedding in the oracle's basis (rotation within near-degenerate pairs allowed)
+    Xo = o["X_pca"].astype(np.float64)
+    resid = X - Xo @ (Vo.T @ V)
+    assert np.abs(resid).max() < 1e-3 * np.abs(Xo).max(), np.abs(resid).max()
+    assert np.all(r.X_pca.cpu().numpy()[:, k:] == 0)
