@@ -4,5 +4,5 @@
 
 
 
-STUB(scb_knn, scb_ctx*, const float*, int64_t, const float*, int64_t, int32_t, int32_t, int32_t, int32_t, int32_t*, float*, void*)
+
 STUB(scb_synth_rows, scb_ctx*, uint64_t, int64_t, int64_t, int32_t, const double*, const double*, int32_t, const double*, int32_t, const double*, const int64_t*, int64_t*, int32_t*, float*, void*)

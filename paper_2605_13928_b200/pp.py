@@ -298,3 +298,22 @@ def pca(sc: Scaled, n_comps: int = 50) -> PCAResult:
     lam, comp_t, mean, tr = pca_from_gram(sc, C, N, n_comps)
     X = project(sc, comp_t, mean, n_comps)
     return PCAResult(X, comp_t[:n_comps, : sc.H], lam, lam / tr, mean, n_comps)
+
+
+# ----------------------------------------------------------------------------- knn
+def neighbors(X_pca: torch.Tensor, n_neighbors: int = 15, n_comps: Optional[int] = None, keys: Optional[torch.Tensor] = None):
+    """sc.pp.neighbors(n_neighbors, method='exact' brute force, metric='euclidean'):
+    (indices int32 [Nq][k], distances float32 [Nq][k]) ordered by (distance, index), self
+    included.  ``keys`` (default: X_pca itself) is the full embedding when the queries are a
+    shard (multi-GPU); returned indices index ``keys``."""
+    keys = X_pca if keys is None else keys
+    d = X_pca.shape[1] if n_comps is None else n_comps
+    dev = X_pca.device
+    nq = X_pca.shape[0]
+    k = int(n_neighbors)
+    kc = 32 if k <= 16 else 64
+    idx = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    _lib.call("scb_knn", _ctx(X_pca), _p(X_pca), nq, _p(keys), keys.shape[0], d, X_pca.stride(0), k, kc, _p(idx),
+              _p(dist), _stream(dev))
+    return idx, dist
