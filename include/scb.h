@@ -57,6 +57,8 @@ typedef struct scb_ctx scb_ctx;
 
 SCB_API int scb_abi_version(void);
 SCB_API const char* scb_last_error(void);
+/* number of kernels this library has launched in the process (for launch accounting) */
+SCB_API unsigned long long scb_launch_count(void);
 SCB_API int scb_ctx_create(int device, scb_ctx** out);
 SCB_API int scb_ctx_destroy(scb_ctx* ctx);
 
@@ -163,14 +165,28 @@ SCB_API int scb_knn(scb_ctx* ctx, const float* queries, int64_t n_queries, const
             int64_t n_keys, int32_t d, int32_t ld, int32_t k, int32_t k_cand,
             int32_t* knn_index, float* knn_dist, void* stream);
 
+/* ---- a9 in pieces (what scb_knn runs): prep writes the 64-column augmented query
+ * (is_key = 0: [q, 1, 1, 0..]) or key (is_key = 1: [-2x, hi|x|^2, lo|x|^2, 0..]) rows;
+ * candidates writes k_cand (32 | 64) candidate key indices per query (tcgen05 kernel);
+ * rerank computes exact FP32 distances of the candidates and keeps the k best. */
+SCB_API int scb_knn_prep(scb_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t ld, int32_t is_key, float* out,
+                         void* stream);
+SCB_API int scb_knn_candidates(scb_ctx* ctx, const float* Qa, int64_t n_q, const float* Ka, int64_t n_k,
+                               int32_t k_cand, int32_t* cand, void* stream);
+SCB_API int scb_knn_rerank(scb_ctx* ctx, const float* queries, int64_t n_q, const float* keys, int32_t d, int32_t ld,
+                           const int32_t* cand, int32_t k_cand, int32_t k, int32_t* knn_index, float* knn_dist,
+                           void* stream);
+
 /* ---- synthetic negative-binomial counts (oracle/synth.py specification), on device.
- * Pass 1 counts nnz per row into row_nnz (int64[n_rows]); pass 2 fills a CSR whose
- * indptr the caller built from row_nnz.  Tables: log_mu f64[G], A f64[T][G],
- * B f64[R][G], cum f64[T]. */
+ * Rows [row0, row0+n_rows) of the matrix.  log mean of entry (c, g) =
+ * log_s[c] + log_mu[g] + A[cell_type[c]][g] + Lf[c][g] where Lf = U B is the low-rank
+ * factor term (float32 [n_rows][n_genes], computed by the caller).  Pass 1 (indptr ==
+ * NULL) writes nnz per row into row_nnz; pass 2 fills indices/data of a CSR whose indptr
+ * (absolute offsets for these rows) the caller built from row_nnz. */
 SCB_API int scb_synth_rows(scb_ctx* ctx, uint64_t seed, int64_t row0, int64_t n_rows, int32_t n_genes,
-                   const double* log_mu, const double* A, int32_t n_types, const double* B,
-                   int32_t n_factors, const double* cum, const int64_t* indptr, int64_t* row_nnz,
-                   int32_t* indices, float* data, void* stream);
+                           const double* log_mu, const double* A, const int32_t* cell_type, const double* log_s,
+                           const float* Lf, const int64_t* indptr, int64_t* row_nnz, int32_t* indices, float* data,
+                           void* stream);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,7 @@ c_i32, c_i64, c_u64, c_dbl, c_ptr = ctypes.c_int32, ctypes.c_int64, ctypes.c_uin
 SIGNATURES = {
     "scb_abi_version": [],
     "scb_last_error": [],
+    "scb_launch_count": [],
     "scb_ctx_create": [ctypes.c_int, ctypes.POINTER(c_ptr)],
     "scb_ctx_destroy": [c_ptr],
     "scb_qc_metrics": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
@@ -35,9 +36,12 @@ SIGNATURES = {
     "scb_pca_eig": [c_ptr, c_ptr, c_i32, c_i32, c_i32, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_project": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_i32, c_ptr],
     "scb_knn": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_i32, c_i32, c_i32, c_ptr, c_ptr, c_ptr],
-    "scb_synth_rows": [c_ptr, c_u64, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+    "scb_knn_prep": [c_ptr, c_ptr, c_i64, c_i32, c_i32, c_i32, c_ptr, c_ptr],
+    "scb_knn_candidates": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
+    "scb_knn_rerank": [c_ptr, c_ptr, c_i64, c_ptr, c_i32, c_i32, c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr],
+    "scb_synth_rows": [c_ptr, c_u64, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
 }
-_RESTYPE = {"scb_last_error": ctypes.c_char_p}
+_RESTYPE = {"scb_last_error": ctypes.c_char_p, "scb_launch_count": ctypes.c_ulonglong}
 
 _lib = None
 _lock = threading.Lock()
@@ -76,6 +80,11 @@ def call(name, *args):
         msg = lib.scb_last_error()
         raise ScbError(name, rc, msg.decode() if msg else "")
     return rc
+
+
+def launch_count() -> int:
+    """Kernels launched by libscb_b200.so so far in this process."""
+    return int(load().scb_launch_count())
 
 
 _ctx = {}

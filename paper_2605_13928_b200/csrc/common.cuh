@@ -22,6 +22,7 @@ constexpr int kWarp = 32;
 // ------------------------------------------------------------------ error plumbing
 void set_error(const char* fmt, ...);
 const char* last_error();
+void count_launch();  // every kernel launch of the library bumps a process-wide counter
 
 #define SCB_CUDA(call)                                                              \
   do {                                                                              \
@@ -35,6 +36,7 @@ const char* last_error();
 
 #define SCB_LAUNCH_CHECK()                                                          \
   do {                                                                              \
+    ::scb::count_launch();                                                          \
     cudaError_t _e = cudaGetLastError();                                            \
     if (_e != cudaSuccess) {                                                        \
       ::scb::set_error("%s:%d launch: %s", __FILE__, __LINE__,                      \

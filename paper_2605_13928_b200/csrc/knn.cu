@@ -318,20 +318,9 @@ __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __re
 }
 
 template <int KC>
-static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* Kx, int64_t n_k, int d, int ld, int k,
-                      int* out_i, float* out_d, cudaStream_t s) {
+static int launch_candidates(scb_ctx* ctx, const float* Qa, int64_t n_q, const float* Ka, int64_t n_k, int* cand,
+                             cudaStream_t s) {
   using Cfg = KnnCfg<KC>;
-  void* ws;
-  const size_t qa_bytes = (size_t)n_q * kD * 4, ka_bytes = (size_t)n_k * kD * 4, cb = (size_t)n_q * KC * 4;
-  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  SCB_TRY(ws_get(ctx, 0, up(qa_bytes) + up(ka_bytes) + up(cb), &ws, s));
-  float* Qa = (float*)ws;
-  float* Ka = (float*)((char*)ws + up(qa_bytes));
-  int* cand = (int*)((char*)Ka + up(ka_bytes));
-  knn_prep_kernel<<<ceil_div(n_q, 8), 256, 0, s>>>(Qx, n_q, d, ld, 0, Qa);
-  SCB_LAUNCH_CHECK();
-  knn_prep_kernel<<<ceil_div(n_k, 8), 256, 0, s>>>(Kx, n_k, d, ld, 1, Ka);
-  SCB_LAUNCH_CHECK();
   CUtensorMap tq, tk;
   SCB_TRY(make_tmap_2d_f32(&tq, Qa, (uint64_t)n_q, kD, kD, 32, Cfg::BM));
   SCB_TRY(make_tmap_2d_f32(&tk, Ka, (uint64_t)n_k, kD, kD, 32, Cfg::BN));
@@ -340,14 +329,49 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   const int n_pairs = (int)((n_q + 2 * Cfg::BM - 1) / (2 * Cfg::BM));
   kern<<<std::min(n_pairs, ctx->num_sms), kKnnThreads, Cfg::SMEM, s>>>(tq, tk, n_q, n_k, cand);
   SCB_LAUNCH_CHECK();
-  knn_rerank_kernel<KC><<<ceil_div(n_q, 8), 256, 0, s>>>(Qx, Kx, n_q, d, ld, cand, k, out_i, out_d);
-  SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
 
 }  // namespace scb
 
 using namespace scb;
+
+extern "C" int scb_knn_prep(scb_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t ld, int32_t is_key, float* out,
+                            void* stream) {
+  SCB_REQUIRE(ctx && X && out, SCB_ERR_ARG, "scb_knn_prep: null argument");
+  SCB_REQUIRE(d >= 1 && d <= kD - 2 && ld >= d, SCB_ERR_ARG, "scb_knn_prep: need 1 <= d <= %d and ld >= d", kD - 2);
+  SCB_REQUIRE(((uintptr_t)out & 15) == 0, SCB_ERR_ARG, "scb_knn_prep: out must be 16-byte aligned");
+  if (n == 0) return SCB_OK;
+  knn_prep_kernel<<<ceil_div(n, 8), 256, 0, (cudaStream_t)stream>>>(X, n, d, ld, is_key ? 1 : 0, out);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
+extern "C" int scb_knn_candidates(scb_ctx* ctx, const float* Qa, int64_t n_q, const float* Ka, int64_t n_k,
+                                  int32_t k_cand, int32_t* cand, void* stream) {
+  SCB_REQUIRE(ctx && Qa && Ka && cand, SCB_ERR_ARG, "scb_knn_candidates: null argument");
+  SCB_REQUIRE(k_cand == 32 || k_cand == 64, SCB_ERR_ARG, "scb_knn_candidates: k_cand must be 32 or 64");
+  SCB_REQUIRE(n_k < (1ll << 31) && n_q < (1ll << 31), SCB_ERR_ARG, "scb_knn_candidates: too many rows");
+  if (n_q == 0) return SCB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  return k_cand == 32 ? launch_candidates<32>(ctx, Qa, n_q, Ka, n_k, cand, s)
+                      : launch_candidates<64>(ctx, Qa, n_q, Ka, n_k, cand, s);
+}
+
+extern "C" int scb_knn_rerank(scb_ctx* ctx, const float* queries, int64_t n_q, const float* keys, int32_t d, int32_t ld,
+                              const int32_t* cand, int32_t k_cand, int32_t k, int32_t* knn_index, float* knn_dist,
+                              void* stream) {
+  SCB_REQUIRE(ctx && queries && keys && cand && knn_index && knn_dist, SCB_ERR_ARG, "scb_knn_rerank: null argument");
+  SCB_REQUIRE(k >= 1 && k <= k_cand && (k_cand == 32 || k_cand == 64), SCB_ERR_ARG, "scb_knn_rerank: bad k / k_cand");
+  if (n_q == 0) return SCB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (k_cand == 32)
+    knn_rerank_kernel<32><<<ceil_div(n_q, 8), 256, 0, s>>>(queries, keys, n_q, d, ld, cand, k, knn_index, knn_dist);
+  else
+    knn_rerank_kernel<64><<<ceil_div(n_q, 8), 256, 0, s>>>(queries, keys, n_q, d, ld, cand, k, knn_index, knn_dist);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
 
 extern "C" int scb_knn(scb_ctx* ctx, const float* queries, int64_t n_queries, const float* keys, int64_t n_keys,
                        int32_t d, int32_t ld, int32_t k, int32_t k_cand, int32_t* knn_index, float* knn_dist,
@@ -358,7 +382,15 @@ extern "C" int scb_knn(scb_ctx* ctx, const float* queries, int64_t n_queries, co
   SCB_REQUIRE(k_cand >= k && (k_cand == 32 || k_cand == 64), SCB_ERR_ARG, "scb_knn: k_cand must be 32 or 64 and >= k");
   SCB_REQUIRE(n_keys < (1ll << 31) && n_queries < (1ll << 31), SCB_ERR_ARG, "scb_knn: too many rows");
   if (n_queries == 0) return SCB_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (k_cand == 32) return launch_knn<32>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s);
-  return launch_knn<64>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s);
+  void* ws;
+  const size_t qa = (size_t)n_queries * kD * 4, ka = (size_t)n_keys * kD * 4, cb = (size_t)n_queries * k_cand * 4;
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  SCB_TRY(ws_get(ctx, 0, up(qa) + up(ka) + up(cb), &ws, (cudaStream_t)stream));
+  float* Qa = (float*)ws;
+  float* Ka = (float*)((char*)ws + up(qa));
+  int* cand = (int*)((char*)Ka + up(ka));
+  SCB_TRY(scb_knn_prep(ctx, queries, n_queries, d, ld, 0, Qa, stream));
+  SCB_TRY(scb_knn_prep(ctx, keys, n_keys, d, ld, 1, Ka, stream));
+  SCB_TRY(scb_knn_candidates(ctx, Qa, n_queries, Ka, n_keys, k_cand, cand, stream));
+  return scb_knn_rerank(ctx, queries, n_queries, keys, d, ld, cand, k_cand, k, knn_index, knn_dist, stream);
 }

@@ -1,10 +1,13 @@
 // Context, scratch arena and error reporting behind the C ABI.
 #include "common.cuh"
 #include <algorithm>
+#include <atomic>
 
 namespace scb {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -40,6 +43,7 @@ int ws_get(scb_ctx* ctx, int slot, size_t bytes, void** out, cudaStream_t s) {
 
 extern "C" int scb_abi_version(void) { return SCB_ABI_VERSION; }
 extern "C" const char* scb_last_error(void) { return scb::last_error(); }
+extern "C" unsigned long long scb_launch_count(void) { return scb::g_launches.load(); }
 
 extern "C" int scb_ctx_create(int device, scb_ctx** out) {
   SCB_REQUIRE(out, SCB_ERR_ARG, "scb_ctx_create: null out");

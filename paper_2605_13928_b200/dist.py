@@ -1,0 +1,71 @@
+"""Cell-sharded multi-GPU plumbing over torch.distributed (NCCL on B200s, gloo in CPU tests).
+
+Rows (cells) are split into contiguous blocks; every collective of the path is one of
+(SURVEY.md §8(e)): SUM all-reduce of per-gene integer sums / counts and of the partial
+Gram matrix, a broadcast of the rank-0 eigenvectors, and a row all-gather of the PCA
+embedding for the kNN keys.  Integer fixed-point gene sums make the HVG set and the scale
+statistics bit-identical for any world size.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as td
+
+
+def shard_rows(n: int, rank: int, world: int):
+    """Contiguous, balanced [begin, end) row range of ``rank``."""
+    base, rem = divmod(n, world)
+    b = rank * base + min(rank, rem)
+    return b, b + base + (1 if rank < rem else 0)
+
+
+class Comm:
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = td.get_rank(group)
+        self.world = td.get_world_size(group)
+        self.cpu_only = td.get_backend(group) == "gloo"
+
+    def _dev(self, t):
+        return t.cpu() if (self.cpu_only and t.is_cuda) else t
+
+    def allreduce_(self, t: torch.Tensor, op=td.ReduceOp.SUM):
+        x = self._dev(t)
+        td.all_reduce(x, op=op, group=self.group)
+        if x is not t:
+            t.copy_(x)
+        return t
+
+    def allreduce_int(self, v: int) -> int:
+        dev = "cpu" if self.cpu_only else torch.device("cuda", torch.cuda.current_device())
+        t = torch.tensor([int(v)], dtype=torch.int64, device=dev)
+        td.all_reduce(t, group=self.group)
+        return int(t.item())
+
+    def allreduce_max(self, v: float) -> float:
+        dev = "cpu" if self.cpu_only else torch.device("cuda", torch.cuda.current_device())
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        td.all_reduce(t, op=td.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def broadcast_(self, t: torch.Tensor, src: int = 0):
+        x = self._dev(t)
+        td.broadcast(x, src, group=self.group)
+        if x is not t:
+            t.copy_(x)
+        return t
+
+    def allgather_rows(self, X: torch.Tensor) -> torch.Tensor:
+        """Concatenate every rank's rows (possibly unequal counts) in rank order."""
+        x = self._dev(X.contiguous())
+        n = torch.tensor([x.shape[0]], dtype=torch.int64, device=x.device)
+        ns = [torch.zeros_like(n) for _ in range(self.world)]
+        td.all_gather(ns, n, group=self.group)
+        ns = [int(v.item()) for v in ns]
+        m = max(ns)
+        pad = torch.zeros((m,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        pad[: x.shape[0]] = x
+        outs = [torch.empty_like(pad) for _ in range(self.world)]
+        td.all_gather(outs, pad, group=self.group)
+        full = torch.cat([o[:k] for o, k in zip(outs, ns)], 0)
+        return full.to(X.device) if full.device != X.device else full

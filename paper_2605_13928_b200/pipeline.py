@@ -1,0 +1,152 @@
+"""Fused QC -> normalize -> log1p -> HVG -> scale -> PCA -> kNN pipeline (one call per step).
+
+This is what the paper's pipeline script runs between its CudaMon markers
+(reference PAPER.md:44-52 cm_timestamp; marker labels ``qc, norm_hvg, regress, pca, knn``
+as in the reference fixtures pkg/tests/helpers.py:31-36).  Each step is a short sequence of
+C-ABI calls on one CUDA stream; per-step device time comes from CUDA events (the
+reference's 1 ms marker resolution and zero-length-step drop, trace.py:270-274, cannot
+resolve B200 stage times), and an optional ``mark(label)`` callback -- e.g. a gputrace
+``SamplerHandle.mark`` or ``paper_2605_13928_b200.trace`` handle -- is invoked at each
+step boundary so NVML samples are attributed to steps exactly as in the reference.
+
+Multi-GPU: cells (rows) are sharded across ranks; the only collectives are the
+all-reduces of per-gene integer sums / gene counts and of the partial Gram matrix, a
+broadcast of the eigenvectors, and the all-gather of the embedding for kNN
+(SURVEY.md §8(e)).  ``comm`` is any object with the small interface of ``dist.Comm``.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Callable, Optional
+
+import torch
+
+from . import pp
+
+STEPS = ("qc", "norm_hvg", "regress", "pca", "knn")
+
+
+@dataclasses.dataclass(frozen=True)
+class Params:
+    min_genes: int = 200
+    max_genes: Optional[int] = None
+    max_pct_mt: float = 20.0
+    min_cells: int = 3
+    target_sum: float = 1e4
+    n_top_genes: int = 2000
+    n_bins: int = 20
+    max_value: float = 10.0
+    n_comps: int = 50
+    n_neighbors: int = 15
+
+
+@dataclasses.dataclass
+class Result:
+    qc: dict
+    cell_mask: torch.Tensor
+    gene_mask: torch.Tensor
+    X_log: pp.DeviceCSR
+    hvg_mask: torch.Tensor
+    hvg_index: torch.Tensor
+    hvg_stats: dict
+    scaled: pp.Scaled
+    pca: pp.PCAResult
+    knn_index: torch.Tensor
+    knn_dist: torch.Tensor
+    n_cells_total: int
+    step_ms: dict
+
+
+class _Timer:
+    def __init__(self, enabled: bool, mark: Optional[Callable[[str], None]]):
+        self.enabled = enabled
+        self.mark = mark
+        self.events = []
+
+    def step(self, label: str):
+        if self.mark is not None:
+            if self.enabled:
+                torch.cuda.current_stream().synchronize()  # align host markers with device work
+            self.mark(label)
+        if self.enabled:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.events.append((label, ev))
+
+    def finish(self):
+        if not self.enabled:
+            return {}
+        end = torch.cuda.Event(enable_timing=True)
+        end.record()
+        end.synchronize()
+        out = {}
+        evs = self.events + [("end", end)]
+        for (lab, a), (_, b) in zip(evs[:-1], evs[1:]):
+            out[lab] = a.elapsed_time(b)
+        return out
+
+
+def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, comm=None,
+        mark: Optional[Callable[[str], None]] = None, timing: bool = True, with_knn: bool = True,
+        knn_timer=None) -> Result:
+    """Run the whole hot path on the device-resident count matrix ``X`` (this rank's rows)."""
+    p = params
+    tm = _Timer(timing, mark)
+    dev = X.device
+
+    # ------------------------------------------------------------------ qc
+    tm.step("qc")
+    qc = pp.calculate_qc_metrics(X, mt_mask)
+    if comm is not None:
+        comm.allreduce_(qc["n_cells_by_counts"])
+        comm.allreduce_(qc["gene_total_counts"])
+    cm, gm, (nk_local, gk) = pp.filter_masks(qc, p.min_genes, p.max_genes, p.max_pct_mt, p.min_cells)
+    n_total = nk_local if comm is None else comm.allreduce_int(nk_local)
+
+    # ------------------------------------------------------------------ norm_hvg
+    tm.step("norm_hvg")
+    X_log, remap, row_scale_orig = pp.subset_normalize(X, cm, gm, (nk_local, gk), p.target_sum)
+    # HVG statistics of the normalized counts straight from the raw matrix (remapped genes)
+    sums = pp.hvg_gene_sums(X, counts=X.data, row_scale=row_scale_orig, gene_remap=remap, n_out=gk)
+    if comm is not None:
+        comm.allreduce_(sums)
+    hvg_mask, hvg_index, st = pp.hvg_select(sums, n_total, p.n_top_genes, p.n_bins)
+
+    # ------------------------------------------------------------------ regress (scale)
+    tm.step("regress")
+    H = int(hvg_index.numel())
+    slot = pp.gene_slots(hvg_index, gk)
+    ssum = pp.scale_gene_sums(X_log, slot, H)
+    if comm is not None:
+        comm.allreduce_(ssum)
+    mean, inv = pp.scale_finalize(ssum, n_total)
+    sc = pp.scale_dense(X_log, slot, H, mean, inv, p.max_value)
+
+    # ------------------------------------------------------------------ pca
+    tm.step("pca")
+    C = pp.gram(sc)
+    if comm is not None:
+        comm.allreduce_(C)
+    npad = 64 if p.n_comps <= 64 else 128
+    if comm is None or comm.rank == 0:
+        lam, comp_t, cmean, tr = pp.pca_from_gram(sc, C, n_total, p.n_comps)
+    else:
+        lam = torch.empty(p.n_comps, dtype=torch.float64, device=dev)
+        comp_t = torch.empty((npad, sc.ld), dtype=torch.float32, device=dev)
+        cmean = torch.empty(sc.ld, dtype=torch.float32, device=dev)
+        tr = torch.empty(1, dtype=torch.float64, device=dev)
+    if comm is not None:
+        for t in (lam, comp_t, cmean, tr):
+            comm.broadcast_(t, 0)
+    Xp = pp.project(sc, comp_t, cmean, p.n_comps)
+    res_pca = pp.PCAResult(Xp, comp_t[: p.n_comps, :H], lam, lam / tr, cmean, p.n_comps)
+
+    # ------------------------------------------------------------------ knn
+    tm.step("knn")
+    if with_knn:
+        keys = Xp if comm is None else comm.allgather_rows(Xp)
+        ki, kd = pp.neighbors(Xp, p.n_neighbors, n_comps=p.n_comps, keys=keys, timer=knn_timer)
+    else:
+        ki = kd = None
+    ms = tm.finish()
+    return Result(qc, cm, gm, X_log, hvg_mask, hvg_index, st, sc, res_pca, ki, kd, n_total, ms)

@@ -133,6 +133,27 @@ def subset(X: DeviceCSR, cell_mask, gene_mask, n_kept=None, target_sum=None):
     return out
 
 
+def subset_normalize(X: DeviceCSR, cell_mask, gene_mask, n_kept, target_sum: float = 1e4):
+    """Fused subset + normalize_total + log1p (two streaming passes over X).  Returns the
+    log-normalized kept matrix, the gene remap (new column or -1) and the per-ORIGINAL-row
+    normalization factor (0 for dropped rows) used by hvg_gene_sums on X itself."""
+    dev = X.device
+    nk, gk = n_kept
+    remap = torch.empty(X.n_cols, dtype=torch.int32, device=dev)
+    new_indptr = torch.empty(nk + 1, dtype=torch.int64, device=dev)
+    row_scale = torch.empty(nk, dtype=torch.float32, device=dev)
+    row_scale_orig = torch.empty(X.n_rows, dtype=torch.float32, device=dev)
+    ctx, s = _ctx(X.data), _stream(dev)
+    _lib.call("scb_subset_count", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols, _p(cell_mask),
+              _p(gene_mask), _p(remap), _p(new_indptr), float(target_sum), _p(row_scale), _p(row_scale_orig), s)
+    nnz = int(new_indptr[nk].item())
+    ind = torch.empty(nnz, dtype=torch.int32, device=dev)
+    logv = torch.empty(nnz, dtype=torch.float32, device=dev)
+    _lib.call("scb_subset_fill", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, _p(cell_mask), _p(remap),
+              _p(new_indptr), _p(row_scale), _p(ind), _p(logv), s)
+    return DeviceCSR(new_indptr, ind, logv, gk, row_scale=row_scale), remap, row_scale_orig
+
+
 # ----------------------------------------------------------------------------- norm_hvg
 def normalize_log1p(X: DeviceCSR, target_sum: float = 1e4) -> DeviceCSR:
     """sc.pp.normalize_total(target_sum) followed by sc.pp.log1p (out of place).  The result
@@ -301,19 +322,31 @@ def pca(sc: Scaled, n_comps: int = 50) -> PCAResult:
 
 
 # ----------------------------------------------------------------------------- knn
-def neighbors(X_pca: torch.Tensor, n_neighbors: int = 15, n_comps: Optional[int] = None, keys: Optional[torch.Tensor] = None):
+def neighbors(X_pca: torch.Tensor, n_neighbors: int = 15, n_comps: Optional[int] = None,
+              keys: Optional[torch.Tensor] = None, timer=None):
     """sc.pp.neighbors(n_neighbors, method='exact' brute force, metric='euclidean'):
     (indices int32 [Nq][k], distances float32 [Nq][k]) ordered by (distance, index), self
     included.  ``keys`` (default: X_pca itself) is the full embedding when the queries are a
-    shard (multi-GPU); returned indices index ``keys``."""
+    shard (multi-GPU); returned indices index ``keys``.  ``timer`` = (start, end) CUDA events
+    recorded around the tensor-core candidate kernel (bench roofline)."""
     keys = X_pca if keys is None else keys
     d = X_pca.shape[1] if n_comps is None else n_comps
     dev = X_pca.device
-    nq = X_pca.shape[0]
+    nq, nk = X_pca.shape[0], keys.shape[0]
     k = int(n_neighbors)
     kc = 32 if k <= 16 else 64
+    ctx, s = _ctx(X_pca), _stream(dev)
+    Qa = torch.empty((nq, 64), dtype=torch.float32, device=dev)
+    Ka = torch.empty((nk, 64), dtype=torch.float32, device=dev)
+    cand = torch.empty((nq, kc), dtype=torch.int32, device=dev)
     idx = torch.empty((nq, k), dtype=torch.int32, device=dev)
     dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
-    _lib.call("scb_knn", _ctx(X_pca), _p(X_pca), nq, _p(keys), keys.shape[0], d, X_pca.stride(0), k, kc, _p(idx),
-              _p(dist), _stream(dev))
+    _lib.call("scb_knn_prep", ctx, _p(X_pca), nq, d, X_pca.stride(0), 0, _p(Qa), s)
+    _lib.call("scb_knn_prep", ctx, _p(keys), nk, d, keys.stride(0), 1, _p(Ka), s)
+    if timer is not None:
+        timer[0].record()
+    _lib.call("scb_knn_candidates", ctx, _p(Qa), nq, _p(Ka), nk, kc, _p(cand), s)
+    if timer is not None:
+        timer[1].record()
+    _lib.call("scb_knn_rerank", ctx, _p(X_pca), nq, _p(keys), d, X_pca.stride(0), _p(cand), kc, k, _p(idx), _p(dist), s)
     return idx, dist
