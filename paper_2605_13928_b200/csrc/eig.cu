@@ -7,6 +7,7 @@
 // residual max_j ||Cov v_j - l_j v_j|| / l_1 is checked on the device and iterations
 // continue until it falls below 1e-10 (or an iteration cap).  Sign rule: the
 // largest-|loading| entry of every component is positive (first index on ties).
+#include <cstdlib>
 #include "common.cuh"
 
 namespace scb {
@@ -146,25 +147,22 @@ __global__ void __launch_bounds__(1024) chol_kernel(double* __restrict__ S, int*
   }
 }
 
-// Q[h][kB] := Q R^{-1}  (row-wise forward substitution x R = q)
-__global__ void trsm_kernel(double* __restrict__ Q, const double* __restrict__ R, int h) {
+// Rinv = R^{-1} for the upper-triangular kB x kB R (one CTA; column j solved by thread j:
+// R x = e_j by back substitution over the smem copy of R).
+__global__ void __launch_bounds__(kB) triinv_kernel(const double* __restrict__ R, double* __restrict__ Rinv) {
   extern __shared__ double dyn[];
   double (*r)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
+  double (*x)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn + kB * kLd);
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) r[e / kB][e % kB] = R[e];
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= h) return;
-  double x[kB];
-  double* q = Q + (size_t)i * kB;
-#pragma unroll 8
-  for (int j = 0; j < kB; ++j) x[j] = q[j];
-  for (int j = 0; j < kB; ++j) {
-    double v = x[j];
-    for (int l = 0; l < j; ++l) v -= x[l] * r[l][j];
-    x[j] = v / r[j][j];
+  const int j = threadIdx.x;
+  for (int i = kB - 1; i >= 0; --i) {
+    double v = (i == j) ? 1.0 : 0.0;
+    for (int l = i + 1; l <= j; ++l) v -= r[i][l] * x[l][j];
+    x[i][j] = (i <= j) ? v / r[i][i] : 0.0;
   }
-#pragma unroll 8
-  for (int j = 0; j < kB; ++j) q[j] = x[j];
+  __syncthreads();
+  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) Rinv[e] = x[e / kB][e % kB];
 }
 
 // ------------------------------------------------------------------ Jacobi (one CTA)
@@ -281,7 +279,7 @@ __global__ void gather_cols_kernel(const double* __restrict__ W, const int* __re
 
 // residual r_j = ||Cov v_j - l_j v_j||, components sign fix and output
 __global__ void residual_kernel(const double* __restrict__ CV, const double* __restrict__ V, const double* __restrict__ lam,
-                                int h, int k, double* __restrict__ res) {
+                                int h, int k, double* __restrict__ res) {  // k = leading dimension of CV / V
   const int j = blockIdx.x;
   __shared__ double sb[32];
   double s = 0.0;
@@ -319,6 +317,11 @@ __global__ void finalize_components_kernel(const double* __restrict__ V, int h, 
   (void)kpad;
 }
 
+__global__ void gather_first_cols_kernel(const double* __restrict__ Q, int ld, int k, double* __restrict__ V) {
+  const int i = blockIdx.x, j = threadIdx.x;
+  if (j < k) V[(size_t)i * k + j] = Q[(size_t)i * ld + j];
+}
+
 __global__ void fill_zero_rows(float* __restrict__ comp_t, int k, int kpad, int hp) {
   const int j = k + blockIdx.x;
   if (j < kpad)
@@ -345,10 +348,10 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   cudaStream_t s = (cudaStream_t)stream;
   const int kSmemKB = kB * kLd * 8;
   SCB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemKB));
-  SCB_CUDA(cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemKB));
   SCB_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSmemKB));
+  SCB_CUDA(cudaFuncSetAttribute(triinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSmemKB));
   // workspace: cov h*h, Q h*kB, Y h*kB, S kB*kB, W kB*kB, Wk kB*n, V h*n, CV h*n, mean h, misc
-  const size_t nd = (size_t)h * h + 2 * (size_t)h * kB + 2 * kB * kB + (size_t)kB * n_comps + 2 * (size_t)h * n_comps +
+  const size_t nd = (size_t)h * h + 2 * (size_t)h * kB + 3 * kB * kB + (size_t)kB * kB + 2 * (size_t)h * kB +
                     h + 4 * kB + 64;
   void* ws;
   SCB_TRY(ws_get(ctx, 2, nd * 8 + 4096, &ws, s));
@@ -356,11 +359,11 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   double* Q = cov + (size_t)h * h;
   double* Y = Q + (size_t)h * kB;
   double* S = Y + (size_t)h * kB;
-  double* W = S + kB * kB;
+  double* W = S + 2 * kB * kB;  // S, Rinv
   double* Wk = W + kB * kB;
-  double* V = Wk + (size_t)kB * n_comps;
-  double* CV = V + (size_t)h * n_comps;
-  double* mean = CV + (size_t)h * n_comps;
+  double* V = Wk + (size_t)kB * kB;
+  double* CV = V + (size_t)h * kB;
+  double* mean = CV + (size_t)h * kB;
   double* res = mean + h;
   double* lam_all = res + kB;
   int* order = (int*)(lam_all + kB);
@@ -375,40 +378,50 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   SCB_LAUNCH_CHECK();
   SCB_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
   const int splitk = std::max(1, std::min(16, h / 128));
-  auto orth = [&](double* M) -> int {
-    for (int rep = 0; rep < 2; ++rep) {  // CholQR2
+  double* Rinv = S + kB * kB;  // scratch: W is only needed inside rayleigh_ritz
+  double* Q2 = CV;             // h x kB scratch (CV region sized h * n_comps <= h * kB? ensured below)
+  auto orth = [&](double*& M) -> int {
+    for (int rep = 0; rep < 2; ++rep) {  // CholQR2: M := M R^{-1}
       SCB_TRY(dgemm(kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s, splitk));
       chol_kernel<<<1, 1024, kSmemKB, s>>>(S, fail);
       SCB_LAUNCH_CHECK();
-      trsm_kernel<<<(h + 127) / 128, 128, kSmemKB, s>>>(M, S, h);
+      triinv_kernel<<<1, kB, 2 * kSmemKB, s>>>(S, Rinv);
       SCB_LAUNCH_CHECK();
+      SCB_TRY(dgemm(h, kB, kB, M, kB, 0, Rinv, kB, 0, Y, kB, s));
+      std::swap(M, Y);
     }
     return SCB_OK;
   };
   SCB_TRY(orth(Q));
-  const int kPower = 4, kMaxOuter = 60;
+  const int kPower = 2, kMaxOuter = 100;
   double host_res[kB];
   int outer = 0;
+  const bool verbose = getenv("SCB_EIG_VERBOSE") != nullptr;
+  cudaEvent_t ev0, ev1;
+  if (verbose) {
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
+    cudaEventRecord(ev0, s);
+  }
   for (; outer < kMaxOuter; ++outer) {
-    for (int p = 0; p < kPower; ++p) {
-      SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s));
+    for (int pw = 0; pw < kPower; ++pw) {
+      SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, 3));
       std::swap(Q, Y);
-      if (p == 1) SCB_TRY(orth(Q));  // keep the block well conditioned
     }
     SCB_TRY(orth(Q));
-    if ((outer + 1) % 5 != 0) continue;
-    // Rayleigh-Ritz + residual check
-    SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s));       // Y = Cov Q
-    SCB_TRY(dgemm(kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s, splitk));  // T = Q^T Y
+    // Rayleigh-Ritz: T = Q^T Cov Q, T = W diag W^T; rotate Q := Q W (sorted descending)
+    SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, 3));        // Y = Cov Q
+    SCB_TRY(dgemm(kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s, splitk));   // T = Q^T Y
     jacobi_kernel<<<1, 1024, 2 * kSmemKB, s>>>(S, W, 30);
     SCB_LAUNCH_CHECK();
-    select_kernel<<<1, kB, 0, s>>>(S, n_comps, order, lam_all);
+    select_kernel<<<1, kB, 0, s>>>(S, kB, order, lam_all);
     SCB_LAUNCH_CHECK();
-    gather_cols_kernel<<<kB, kB, 0, s>>>(W, order, n_comps, Wk);
+    gather_cols_kernel<<<kB, kB, 0, s>>>(W, order, kB, Wk);
     SCB_LAUNCH_CHECK();
-    SCB_TRY(dgemm(h, n_comps, kB, Q, kB, 0, Wk, n_comps, 0, V, n_comps, s));     // V = Q Wk
-    SCB_TRY(dgemm(h, n_comps, h, cov, h, 0, V, n_comps, 0, CV, n_comps, s));     // Cov V
-    residual_kernel<<<n_comps, 256, 0, s>>>(CV, V, lam_all, h, n_comps, res);
+    SCB_TRY(dgemm(h, kB, kB, Q, kB, 0, Wk, kB, 0, Q2, kB, s));          // Ritz vectors
+    SCB_TRY(dgemm(h, kB, kB, Y, kB, 0, Wk, kB, 0, V, kB, s));           // Cov * Ritz vectors
+    std::swap(Q, Q2);
+    residual_kernel<<<n_comps, 256, 0, s>>>(V, Q, lam_all, h, kB, res);
     SCB_LAUNCH_CHECK();
     double lam0 = 0.0;
     SCB_CUDA(cudaMemcpyAsync(host_res, res, sizeof(double) * n_comps, cudaMemcpyDeviceToHost, s));
@@ -416,8 +429,18 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     SCB_CUDA(cudaStreamSynchronize(s));
     double worst = 0.0;
     for (int j = 0; j < n_comps; ++j) worst = std::max(worst, host_res[j]);
-    if (worst <= 1e-10 * std::max(lam0, 1e-300)) break;
+    if (verbose) {
+      cudaEventRecord(ev1, s);
+      cudaEventSynchronize(ev1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev0, ev1);
+      fprintf(stderr, "[scb_pca_eig] outer %d residual %.3e (lam0 %.4e) elapsed %.2f ms\n", outer + 1, worst, lam0, ms);
+    }
+    if (worst <= 1e-9 * std::max(lam0, 1e-300)) break;
   }
+  // V := the n_comps leading Ritz vectors (columns 0..n_comps-1 of Q, already sorted)
+  gather_first_cols_kernel<<<h, kB, 0, s>>>(Q, kB, n_comps, V);
+  SCB_LAUNCH_CHECK();
   int hfail = 0;
   SCB_CUDA(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
   SCB_CUDA(cudaStreamSynchronize(s));

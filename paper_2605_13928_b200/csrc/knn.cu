@@ -22,11 +22,12 @@ constexpr int kD = 64;            // padded embedding width (two 128-byte K atom
 
 template <int KC>
 struct KnnCfg {
-  static constexpr int BM = 128, BN = 128, STAGES = 4;
+  static constexpr int BM = 128, BN = 128, STAGES = 3;
   static constexpr int HALF = BM * 32 * 4;             // 16 KB: 128 rows x 32 fp32 (one K atom column)
   static constexpr int A_BYTES = 2 * 2 * HALF;          // 2 query tiles x 2 K halves = 64 KB
   static constexpr int B_BYTES = 2 * HALF;              // 128 keys x 64 = 32 KB per stage
-  static constexpr int SMEM = A_BYTES + STAGES * B_BYTES + 1024 + 256;
+  static constexpr int SPILL = 8 * 32 * 32 * 4;          // per-epilogue-warp chunk staging (32 KB)
+  static constexpr int SMEM = A_BYTES + STAGES * B_BYTES + SPILL + 1024 + 256;
   static constexpr uint32_t IDESC = tc::idesc_tf32(BM, BN, false, false);
 };
 
@@ -79,7 +80,8 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* a_base = smem;                          // [qtile][khalf][128 rows x 128 B]
   uint8_t* b_base = smem + C::A_BYTES;             // [stage][khalf][128 rows x 128 B]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(b_base + C::STAGES * C::B_BYTES);
+  float* spill = reinterpret_cast<float*>(b_base + C::STAGES * C::B_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(b_base + C::STAGES * C::B_BYTES + C::SPILL);
   uint64_t* a_full = bar;
   uint64_t* a_empty = bar + 1;
   uint64_t* b_full = bar + 2;
@@ -201,13 +203,21 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
 #pragma unroll
           for (int j = 1; j < 32; ++j) m = fminf(m, v[j]);
           if (__any_sync(0xffffffffu, m < L[KC - 1])) {
+            // rare path: stage the chunk (transposed: conflict-free) and walk it with ONE
+            // rolled loop around a single inlined insertion (keeps the I-cache footprint small)
+            float* sp = spill + e * 32 * 32;
 #pragma unroll
+            for (int j = 0; j < 32; ++j) sp[j * 32 + lane] = v[j];
+            __syncwarp();
+#pragma unroll 1
             for (int j = 0; j < 32; ++j) {
-              const bool ins = v[j] < L[KC - 1];
+              const float x = sp[j * 32 + lane];
+              const bool ins = x < L[KC - 1];
               if (__any_sync(0xffffffffu, ins)) {
-                if (ins) list_insert<KC>(L, I, v[j], key0 + c * 32 + j);
+                if (ins) list_insert<KC>(L, I, x, key0 + c * 32 + j);
               }
             }
+            __syncwarp();
           }
         }
         tc::tc_fence_before();
