@@ -165,17 +165,11 @@ SCB_API int scb_knn(scb_ctx* ctx, const float* queries, int64_t n_queries, const
             int64_t n_keys, int32_t d, int32_t ld, int32_t k, int32_t k_cand,
             int32_t* knn_index, float* knn_dist, void* stream);
 
-/* ---- a9 in pieces (what scb_knn runs): prep writes the 64-column augmented query
- * (is_key = 0: [q, 1, 1, 0..]) or key (is_key = 1: [-2x, hi|x|^2, lo|x|^2, 0..]) rows;
- * candidates writes k_cand (32 | 64) candidate key indices per query (tcgen05 kernel);
- * rerank computes exact FP32 distances of the candidates and keeps the k best. */
-SCB_API int scb_knn_prep(scb_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t ld, int32_t is_key, float* out,
-                         void* stream);
-SCB_API int scb_knn_candidates(scb_ctx* ctx, const float* Qa, int64_t n_q, const float* Ka, int64_t n_k,
-                               int32_t k_cand, int32_t* cand, void* stream);
-SCB_API int scb_knn_rerank(scb_ctx* ctx, const float* queries, int64_t n_q, const float* keys, int32_t d, int32_t ld,
-                           const int32_t* cand, int32_t k_cand, int32_t k, int32_t* knn_index, float* knn_dist,
-                           void* stream);
+/* ---- a9 with device timing: as scb_knn, and if ev_start / ev_end (cudaEvent_t) are
+ * non-NULL they are recorded on `stream` immediately around the tcgen05 candidate kernel. */
+SCB_API int scb_knn_timed(scb_ctx* ctx, const float* queries, int64_t n_queries, const float* keys, int64_t n_keys,
+                          int32_t d, int32_t ld, int32_t k, int32_t k_cand, int32_t* knn_index, float* knn_dist,
+                          void* stream, void* ev_start, void* ev_end);
 
 /* ---- synthetic negative-binomial counts (oracle/synth.py specification), on device.
  * Rows [row0, row0+n_rows) of the matrix.  log mean of entry (c, g) =

@@ -36,9 +36,7 @@ SIGNATURES = {
     "scb_pca_eig": [c_ptr, c_ptr, c_i32, c_i32, c_i32, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_project": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_i32, c_ptr],
     "scb_knn": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_i32, c_i32, c_i32, c_ptr, c_ptr, c_ptr],
-    "scb_knn_prep": [c_ptr, c_ptr, c_i64, c_i32, c_i32, c_i32, c_ptr, c_ptr],
-    "scb_knn_candidates": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
-    "scb_knn_rerank": [c_ptr, c_ptr, c_i64, c_ptr, c_i32, c_i32, c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr],
+    "scb_knn_timed": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_i32, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_synth_rows": [c_ptr, c_u64, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
 }
 _RESTYPE = {"scb_last_error": ctypes.c_char_p, "scb_launch_count": ctypes.c_ulonglong}

@@ -1,59 +1,220 @@
 // Exact brute-force kNN graph on the PCA embedding (sc.pp.neighbors, method exact).
 //
-// 1. prep: queries Qa = [q, 1, 1, 0...] and keys Ka = [-2x, hi(|x|^2), lo(|x|^2), 0...]
-//    (64 columns), so one K=64 dot product gives the query-invariant score
-//    s_ij = |x_j|^2 - 2 q_i.x_j = d^2_ij - |q_i|^2.
-// 2. candidates (tcgen05): each persistent CTA owns a PAIR of 128-query tiles (M = 2 x 128,
-//    resident in smem) and streams every 128-key tile through a 4-stage TMA pipeline; one
-//    thread issues 2 x 8 tcgen05.mma.kind::tf32 (128x128x8) per key tile into a double-
-//    buffered TMEM accumulator (4 x 128 of the 512 columns).  Eight epilogue warps own one
-//    query row each and keep a register-resident sorted top-KC list; a 32-wide min filter
-//    against the list's current worst score skips almost every chunk, so the epilogue
-//    stays under the tensor time.
-// 3. rerank: one warp per query recomputes exact FP32 squared distances of the KC
-//    candidates, sorts by (distance, index) and keeps k (self included).
+// 1. order: rows are bucket-sorted along a 3-D Morton (Z-order) curve over their leading
+//    principal components PC1..PC3, and every query pair scans the key tiles OUTWARD from its
+//    own curve position (spatially nearest first).  The scan still visits every key (exact
+//    brute force); the order only makes each row's running top-K threshold tight after a few
+//    tiles and keeps the 32 queries of a warp spatially coherent, so the insert path is rare.
+// 2. prep: FP16 rows of width 64 (one 128-byte swizzle row):
+//    queries Qa = [q/s, 1, 1, 0..], keys Ka = [-2x/s, hi(|x|^2/s^2), lo(|x|^2/s^2), 0..]
+//    with s = max|X|/16 so everything fits FP16; one K=64 dot product gives the
+//    query-invariant score (d^2 - |q|^2)/s^2 with the 11-bit significands of TF32.
+// 3. candidates (tcgen05.mma.kind::f16, FP32 accumulate in TMEM): a persistent CTA owns a
+//    PAIR of 128-query tiles (smem-resident) and streams 128-key tiles through a 6-stage
+//    TMA pipeline; one thread issues 2 x 4 MMAs (128x128x16) per key tile into a double-
+//    buffered accumulator (512 TMEM columns).  Eight epilogue warps own one query row each
+//    and keep a register-resident sorted top-KC list behind a 32-wide min filter.
+// 4. rerank: one warp per query recomputes exact FP32 squared distances of the KC
+//    candidates, sorts by (distance, original index) and keeps k (self included).
+#include <cstdlib>
 #include <vector>
+#include <cuda_fp16.h>
 #include "tc_common.cuh"
 
 namespace scb {
 
 constexpr int kKnnThreads = 320;  // warp0 TMA, warp1 MMA, warps 2..9 epilogue
-constexpr int kD = 64;            // padded embedding width (two 128-byte K atoms)
+constexpr int kD = 64;            // padded augmented width (one 128-byte FP16 row)
+constexpr int kBuckets = 1 << 16; // PC1 counting-sort buckets
 
 template <int KC>
 struct KnnCfg {
-  static constexpr int BM = 128, BN = 128, STAGES = 3;
-  static constexpr int HALF = BM * 32 * 4;             // 16 KB: 128 rows x 32 fp32 (one K atom column)
-  static constexpr int A_BYTES = 2 * 2 * HALF;          // 2 query tiles x 2 K halves = 64 KB
-  static constexpr int B_BYTES = 2 * HALF;              // 128 keys x 64 = 32 KB per stage
-  static constexpr int SPILL = 8 * 32 * 32 * 4;          // per-epilogue-warp chunk staging (32 KB)
+  static constexpr int BM = 128, BN = 128, STAGES = 6;
+  static constexpr int TILE = BM * kD * 2;              // 16 KB: 128 rows x 64 fp16
+  static constexpr int A_BYTES = 2 * TILE;              // 2 query tiles
+  static constexpr int B_BYTES = TILE;                  // 128 keys
+  static constexpr int SPILL = 8 * 32 * 32 * 4;         // per-epilogue-warp chunk staging
   static constexpr int SMEM = A_BYTES + STAGES * B_BYTES + SPILL + 1024 + 256;
-  static constexpr uint32_t IDESC = tc::idesc_tf32(BM, BN, false, false);
+  // kind::f16: c_format F32 (1) [4,6), a/b format F16 (0), K-major, N>>3 [17,23), M>>4 [24,29)
+  static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 };
 
-// queries: [q, 1, 1, 0...]; keys: [-2x, hi(|x|^2), lo(|x|^2), 0...]  (64 columns, fp32)
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+// ------------------------------------------------------------------ ordering by PC1
+// ordered-int encoding for float min/max via integer atomics
+__device__ __forceinline__ int f2o(float f) { const int i = __float_as_int(f); return i >= 0 ? i : i ^ 0x7fffffff; }
+__device__ __forceinline__ float o2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+constexpr int kOrderDims = 3;  // Morton curve over PC1..PC3
+
+__global__ void range_kernel(const float* __restrict__ X, int64_t n, int d, int ld, unsigned* __restrict__ amax,
+                             int* __restrict__ omin, int* __restrict__ omax) {
+  float m = 0.0f, lo[kOrderDims], hi[kOrderDims];
+#pragma unroll
+  for (int c = 0; c < kOrderDims; ++c) { lo[c] = INFINITY; hi[c] = -INFINITY; }
+  const int dims = min(d, kOrderDims);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const float* x = X + r * ld;
+    for (int j = 0; j < d; ++j) m = fmaxf(m, fabsf(x[j]));
+#pragma unroll
+    for (int c = 0; c < kOrderDims; ++c)
+      if (c < dims) { lo[c] = fminf(lo[c], x[c]); hi[c] = fmaxf(hi[c], x[c]); }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+#pragma unroll
+    for (int c = 0; c < kOrderDims; ++c) {
+      lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmaxf(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  }
+  if (lane_id() == 0) {
+    atomicMax(amax, __float_as_uint(m));  // non-negative floats order like unsigned ints
+#pragma unroll
+    for (int c = 0; c < kOrderDims; ++c) {
+      atomicMin(omin + c, f2o(lo[c]));
+      atomicMax(omax + c, f2o(hi[c]));
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> every third bit
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+// 16-bit bucket = top bits of the 30-bit Morton code of (PC1, PC2, PC3) quantised to 10 bits
+__device__ __forceinline__ int order_bucket(const float* x, int d, const int* omin, const int* omax) {
+  uint32_t code = 0;
+#pragma unroll
+  for (int c = 0; c < kOrderDims; ++c) {
+    uint32_t qv = 0;
+    if (c < d) {
+      const float lo = o2f(omin[c]), hi = o2f(omax[c]);
+      const float w = hi - lo;
+      int qi = (w > 0.0f) ? (int)((x[c] - lo) / w * 1024.0f) : 0;
+      qv = (uint32_t)(qi < 0 ? 0 : (qi > 1023 ? 1023 : qi));
+    }
+    code |= spread3(qv) << (2 - c);
+  }
+  return (int)(code >> 14);  // 30 -> 16 bits
+}
+
+__global__ void bucket_hist_kernel(const float* __restrict__ X, int64_t n, int d, int ld, const int* omin,
+                                   const int* omax, int* __restrict__ hist) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&hist[order_bucket(X + r * ld, d, omin, omax)], 1);
+}
+
+// single CTA exclusive scan of the bucket histogram (in place)
+__global__ void bucket_scan_kernel(int* __restrict__ hist) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < kBuckets; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int v = hist[i];
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane_id() >= o) incl += t;
+    }
+    if (lane_id() == 31) wsum[warp_id()] = incl;
+    __syncthreads();
+    if (warp_id() == 0) {
+      const int sv = (lane_id() < (int)(blockDim.x >> 5)) ? wsum[lane_id()] : 0;
+      int si = sv;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, si, o);
+        if (lane_id() >= o) si += t;
+      }
+      wsum[lane_id()] = si - sv;
+    }
+    __syncthreads();
+    const int ex = carry + wsum[warp_id()] + incl - v;
+    hist[i] = ex;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = ex + v;
+    __syncthreads();
+  }
+}
+
+// scatter rows into curve order; key_sorted[pos] = bucket id (non-decreasing, for start search)
+__global__ void bucket_scatter_kernel(const float* __restrict__ X, int64_t n, int d, int ld, const int* omin,
+                                      const int* omax, int* __restrict__ cursor, int* __restrict__ perm,
+                                      float* __restrict__ key_sorted) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int b = order_bucket(X + r * ld, d, omin, omax);
+    const int pos = atomicAdd(&cursor[b], 1);
+    perm[pos] = (int)r;
+    key_sorted[pos] = (float)b;
+  }
+}
+
+// queries: [q/s, 1, 1, 0...]; keys: [-2x/s, hi(|x|^2/s^2), lo(|x|^2/s^2), 0...]  (fp16, sorted order)
 __global__ void knn_prep_kernel(const float* __restrict__ X, int64_t n, int d, int ld, int is_key,
-                                float* __restrict__ out) {
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
-  if (r >= n) return;
+                                const int* __restrict__ perm, const unsigned* __restrict__ amax, __half* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (i >= n) return;
   const int l = lane_id();
+  const float s = fmaxf(__uint_as_float(*amax), 1e-30f) * (1.0f / 16.0f);
+  const float inv = 1.0f / s;
+  const int64_t r = perm ? perm[i] : i;
   const float* x = X + r * ld;
-  const float a = (l < d) ? x[l] : 0.0f;
-  const float b = (l + 32 < d) ? x[l + 32] : 0.0f;
-  float* o = out + r * kD;
+  const float a = (l < d) ? x[l] * inv : 0.0f;
+  const float b = (l + 32 < d) ? x[l + 32] * inv : 0.0f;
+  __half* o = out + i * kD;
   if (!is_key) {
     auto val = [&](int col, float xv) { return col < d ? xv : ((col == d || col == d + 1) ? 1.0f : 0.0f); };
-    o[l] = val(l, a);
-    o[l + 32] = val(l + 32, b);
+    o[l] = __float2half_rn(val(l, a));
+    o[l + 32] = __float2half_rn(val(l + 32, b));
   } else {
-    const double nrm = warp_sum((double)a * a + (double)b * b);
-    float hi, lo;
-    tc::split_tf32((float)nrm, hi, lo);
-    lo = (float)(nrm - (double)hi);
-    auto val = [&](int col, float xv) { return col < d ? -2.0f * xv : (col == d ? hi : (col == d + 1 ? lo : 0.0f)); };
+    const float nrm = warp_sum(a * a + b * b);
+    const __half hh = __float2half_rn(nrm);
+    const __half hl = __float2half_rn(nrm - __half2float(hh));
+    auto val = [&](int col, float xv) -> __half {
+      return col < d ? __float2half_rn(-2.0f * xv) : (col == d ? hh : (col == d + 1 ? hl : __float2half_rn(0.0f)));
+    };
     o[l] = val(l, a);
     o[l + 32] = val(l + 32, b);
   }
+}
+
+// start key tile of each query pair: PC1 of the pair's middle query, located in the sorted keys
+__global__ void start_tile_kernel(const float* __restrict__ q_pc1_sorted, int64_t n_q, const float* __restrict__ k_pc1_sorted,
+                                  int64_t n_k, int bm, int bn, int* __restrict__ start) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_pairs = (n_q + 2 * bm - 1) / (2 * bm);
+  if (p >= n_pairs) return;
+  const int64_t mid = min(n_q - 1, (int64_t)p * 2 * bm + bm);
+  const float v = q_pc1_sorted[mid];
+  int64_t lo = 0, hi = n_k;  // first position with key pc1 >= v
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (k_pc1_sorted[m] < v) lo = m + 1; else hi = m;
+  }
+  const int64_t n_kt = (n_k + bn - 1) / bn;
+  const int64_t t = min(lo, n_k - 1) / bn;
+  start[p] = (int)min(t, n_kt - 1);
+}
+
+// i-th key tile of the outward scan from `start` (start, start+1, start-1, start+2, ...);
+// -1 for positions that fall off either end (the 2*n_kt sequence covers every tile once).
+__device__ __forceinline__ int outward_tile(int start, int i, int n_kt) {
+  const int dd = (i + 1) >> 1;
+  const int t = (i & 1) ? start + dd : start - dd;
+  return (t >= 0 && t < n_kt) ? t : -1;
 }
 
 template <int KC>
@@ -71,28 +232,55 @@ __device__ __forceinline__ void list_insert(float (&L)[KC], int (&I)[KC], float 
   }
 }
 
+constexpr int kQ = 4;  // per-lane pending queue in front of the sorted list
+
+// merge the pending queue into the sorted list (executed by the whole warp at once, so the
+// O(KC) insertions of different lanes share the same issue slots)
+template <int KC>
+__device__ __forceinline__ void queue_merge(float (&L)[KC], int (&I)[KC], float (&Qv)[kQ], int (&Qi)[kQ], int& qn) {
+#pragma unroll
+  for (int s = 0; s < kQ; ++s)
+    if (s < qn) list_insert<KC>(L, I, Qv[s], Qi[s]);
+  qn = 0;
+}
+
+// min of 32 values as a 3-ary tree (sm_100a FMNMX3)
+__device__ __forceinline__ float min32(const float (&v)[32]) {
+  float a[11];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) a[j] = fminf(fminf(v[3 * j], v[3 * j + 1]), v[3 * j + 2]);
+  a[10] = fminf(v[30], v[31]);
+  const float b0 = fminf(fminf(a[0], a[1]), a[2]);
+  const float b1 = fminf(fminf(a[3], a[4]), a[5]);
+  const float b2 = fminf(fminf(a[6], a[7]), a[8]);
+  const float b3 = fminf(a[9], a[10]);
+  return fminf(fminf(b0, b1), fminf(b2, b3));
+}
+
 template <int KC>
 __global__ void __launch_bounds__(kKnnThreads, 1)
 knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, int64_t n_q,
-                      int64_t n_k, int* __restrict__ cand) {
+                      int64_t n_k, const int* __restrict__ start_tile, int* __restrict__ cand, int dbg_mode) {
   using C = KnnCfg<KC>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* a_base = smem;                          // [qtile][khalf][128 rows x 128 B]
-  uint8_t* b_base = smem + C::A_BYTES;             // [stage][khalf][128 rows x 128 B]
-  float* spill = reinterpret_cast<float*>(b_base + C::STAGES * C::B_BYTES);
+  uint8_t* a_base = smem;                          // [qtile][128 rows x 128 B]
+  uint8_t* b_base = smem + C::A_BYTES;             // [stage][128 rows x 128 B]
+  // staging buffer addressed from the __shared__ symbol itself (keeps LDS/STS, not generic LD)
+  float* spill = reinterpret_cast<float*>(smem_raw + ((smem - smem_raw) + C::A_BYTES + C::STAGES * C::B_BYTES));
   uint64_t* bar = reinterpret_cast<uint64_t*>(b_base + C::STAGES * C::B_BYTES + C::SPILL);
   uint64_t* a_full = bar;
   uint64_t* a_empty = bar + 1;
   uint64_t* b_full = bar + 2;
   uint64_t* b_empty = b_full + C::STAGES;
-  uint64_t* t_full = b_empty + C::STAGES;
-  uint64_t* t_empty = t_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+  uint64_t* t_full = b_empty + C::STAGES;   // [buf][qtile]
+  uint64_t* t_empty = t_full + 4;           // [buf][qtile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 4);
 
   const int warp = warp_id(), lane = lane_id();
   const int n_pairs = (int)((n_q + 2 * C::BM - 1) / (2 * C::BM));
   const int n_kt = (int)((n_k + C::BN - 1) / C::BN);
+  const int n_seq = 2 * n_kt;  // outward sequence length (positions off the ends are skipped)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -104,9 +292,9 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         tc::mbar_init(&b_full[s], 1);
         tc::mbar_init(&b_empty[s], 1);
       }
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < 4; ++b) {
         tc::mbar_init(&t_full[b], 1);
-        tc::mbar_init(&t_empty[b], 8);
+        tc::mbar_init(&t_empty[b], 4);
       }
       tc::fence_barrier_init();
     }
@@ -122,18 +310,18 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
     if (lane == 0) {
       int it = 0, pc = 0;
       for (int pair = blockIdx.x; pair < n_pairs; pair += gridDim.x, ++pc) {
+        const int st = start_tile[pair];
         tc::mbar_wait(a_empty, (pc & 1) ^ 1);
         tc::mbar_arrive_expect_tx(a_full, C::A_BYTES);
-        for (int t = 0; t < 2; ++t)
-          for (int h = 0; h < 2; ++h)
-            tc::tma_load_2d(a_base + (t * 2 + h) * C::HALF, &tq, a_full, h * 32, (pair * 2 + t) * C::BM);
-        for (int kt = 0; kt < n_kt; ++kt, ++it) {
+        for (int t = 0; t < 2; ++t) tc::tma_load_2d(a_base + t * C::TILE, &tq, a_full, 0, (pair * 2 + t) * C::BM);
+        for (int i = 0; i < n_seq; ++i) {
+          const int kt = outward_tile(st, i, n_kt);
+          if (kt < 0) continue;
           const int s = it % C::STAGES;
           tc::mbar_wait(&b_empty[s], ((it / C::STAGES) & 1) ^ 1);
           tc::mbar_arrive_expect_tx(&b_full[s], C::B_BYTES);
-          uint8_t* b = b_base + s * C::B_BYTES;
-          tc::tma_load_2d(b, &tk, &b_full[s], 0, kt * C::BN);
-          tc::tma_load_2d(b + C::HALF, &tk, &b_full[s], 32, kt * C::BN);
+          tc::tma_load_2d(b_base + s * C::B_BYTES, &tk, &b_full[s], 0, kt * C::BN);
+          ++it;
         }
       }
     }
@@ -142,26 +330,24 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       int it = 0, pc = 0;
       for (int pair = blockIdx.x; pair < n_pairs; pair += gridDim.x, ++pc) {
         tc::mbar_wait(a_full, pc & 1);
-        for (int kt = 0; kt < n_kt; ++kt, ++it) {
+        for (int i = 0; i < n_kt; ++i, ++it) {
           const int s = it % C::STAGES;
           const int buf = it & 1;
-          tc::mbar_wait(&t_empty[buf], ((it >> 1) & 1) ^ 1);
           tc::mbar_wait(&b_full[s], (it / C::STAGES) & 1);
-          tc::tc_fence_after();
           const uint32_t bb = tc::smem_u32(b_base + s * C::B_BYTES);
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
-            const uint32_t ab = tc::smem_u32(a_base + t * 2 * C::HALF);
+            tc::mbar_wait(&t_empty[buf * 2 + t], ((it >> 1) & 1) ^ 1);
+            tc::tc_fence_after();
+            const uint32_t ab = tc::smem_u32(a_base + t * C::TILE);
             const uint32_t d = tmem + buf * 256 + t * 128;
 #pragma unroll
-            for (int kk = 0; kk < kD / 8; ++kk) {
-              const uint32_t off = (kk >> 2) * C::HALF + (kk & 3) * 32;
-              tc::mma_tf32(d, tc::smem_desc_sw128(ab + off, 16, 1024), tc::smem_desc_sw128(bb + off, 16, 1024),
-                           C::IDESC, kk > 0 ? 1u : 0u);
-            }
+            for (int kk = 0; kk < kD / 16; ++kk)  // K = 16 fp16 = 32 bytes per MMA
+              mma_f16(d, tc::smem_desc_sw128(ab + kk * 32, 16, 1024), tc::smem_desc_sw128(bb + kk * 32, 16, 1024),
+                      C::IDESC, kk > 0 ? 1u : 0u);
+            tc::mma_commit(&t_full[buf * 2 + t]);
           }
           tc::mma_commit(&b_empty[s]);
-          tc::mma_commit(&t_full[buf]);
         }
         tc::mma_commit(a_empty);
       }
@@ -172,58 +358,106 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
     const int t = e >> 2;         // query tile of the pair
     int it = 0;
     for (int pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+      const int st = start_tile[pair];
       float L[KC];
       int I[KC];
+      float Qv[kQ];
+      int Qi[kQ];
+      int qn = 0;
 #pragma unroll
       for (int j = 0; j < KC; ++j) {
         L[j] = INFINITY;
         I[j] = -1;
       }
+#pragma unroll
+      for (int j = 0; j < kQ; ++j) {
+        Qv[j] = INFINITY;
+        Qi[j] = -1;
+      }
       const int64_t row = (int64_t)(pair * 2 + t) * C::BM + 32 * q + lane;
-      for (int kt = 0; kt < n_kt; ++kt, ++it) {
+      for (int i = 0; i < n_seq; ++i) {
+        const int kt = outward_tile(st, i, n_kt);
+        if (kt < 0) continue;
         const int buf = it & 1;
-        tc::mbar_wait(&t_full[buf], (it >> 1) & 1);
+        tc::mbar_wait(&t_full[buf * 2 + t], (it >> 1) & 1);
         tc::tc_fence_after();
         const int key0 = kt * C::BN;
         const bool tail = key0 + C::BN > n_k;
+        if (dbg_mode == 2) {  // debug: no TMEM traffic at all
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&t_empty[buf * 2 + t]);
+          ++it;
+          continue;
+        }
 #pragma unroll 1
-        for (int c = 0; c < C::BN / 32; ++c) {
-          uint32_t r[32];
-          tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + buf * 256 + t * 128 + c * 32, r);
+        for (int c2 = 0; c2 < C::BN / 64; ++c2) {
+          // two 32-column TMEM loads in flight per wait (hides the tcgen05.ld latency)
+          uint32_t r0[32], r1[32];
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + buf * 256 + t * 128 + c2 * 64;
+          tc::tmem_ld32(ta, r0);
+          tc::tmem_ld32(ta + 32, r1);
           tc::tmem_ld_wait();
-          float v[32];
+          if (dbg_mode == 1) {  // debug: TMEM loads only
+            uint32_t x = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          if (tail) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (key0 + c * 32 + j >= n_k) v[j] = INFINITY;
+            for (int j = 0; j < 32; ++j) x ^= r0[j] ^ r1[j];
+            if (x == 0x12345678u) I[0] = (int)x;
+            continue;
           }
-          float m = v[0];
 #pragma unroll
-          for (int j = 1; j < 32; ++j) m = fminf(m, v[j]);
-          if (__any_sync(0xffffffffu, m < L[KC - 1])) {
-            // rare path: stage the chunk (transposed: conflict-free) and walk it with ONE
-            // rolled loop around a single inlined insertion (keeps the I-cache footprint small)
-            float* sp = spill + e * 32 * 32;
+          for (int h = 0; h < 2; ++h) {
+            const int c = c2 * 2 + h;
+            float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) sp[j * 32 + lane] = v[j];
-            __syncwarp();
-#pragma unroll 1
-            for (int j = 0; j < 32; ++j) {
-              const float x = sp[j * 32 + lane];
-              const bool ins = x < L[KC - 1];
-              if (__any_sync(0xffffffffu, ins)) {
-                if (ins) list_insert<KC>(L, I, x, key0 + c * 32 + j);
-              }
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(h ? r1[j] : r0[j]);
+            if (tail) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (key0 + c * 32 + j >= n_k) v[j] = INFINITY;
             }
-            __syncwarp();
+            const float m = min32(v);
+            if (__any_sync(0xffffffffu, m < L[KC - 1])) {
+              // rare path: bitmask of this lane's passing scores, staged chunk (transposed,
+              // conflict-free) and a loop over set bits; passing scores go to the lane's small
+              // queue, and a full queue on ANY lane merges every lane's queue at once.
+              float* sp = spill + e * 32 * 32;
+              const float thr = L[KC - 1];
+              uint32_t mask = 0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                sp[j * 32 + lane] = v[j];
+                mask |= (v[j] < thr) ? (1u << j) : 0u;
+              }
+              __syncwarp();
+              while (__any_sync(0xffffffffu, mask != 0)) {
+                if (__any_sync(0xffffffffu, qn == kQ)) queue_merge<KC>(L, I, Qv, Qi, qn);
+                if (mask) {
+                  const int j = __ffs(mask) - 1;
+                  mask &= mask - 1;
+                  const float x = sp[j * 32 + lane];
+                  if (x < L[KC - 1]) {
+                    const int id = key0 + c * 32 + j;
+#pragma unroll
+                    for (int q2 = 0; q2 < kQ; ++q2)
+                      if (q2 == qn) {
+                        Qv[q2] = x;
+                        Qi[q2] = id;
+                      }
+                    ++qn;
+                  }
+                }
+              }
+              __syncwarp();
+            }
           }
         }
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&t_empty[buf]);
+        if (lane == 0) tc::mbar_arrive(&t_empty[buf * 2 + t]);
+        ++it;
       }
+      queue_merge<KC>(L, I, Qv, Qi, qn);
       if (row < n_q) {
         int* o = cand + row * KC;
 #pragma unroll
@@ -236,15 +470,18 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
-// one warp per query: exact fp32 distances of the candidates, bitonic sort by (d2, idx)
+// one warp per (sorted) query: exact fp32 distances of the candidates (sorted key positions
+// mapped back through perm_k), bitonic sort by (d2, original index), keep k; the output row
+// is the query's original row perm_q[i].
 template <int KC>
 __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __restrict__ Kx, int64_t n_q, int d,
-                                  int ld, const int* __restrict__ cand, int k, int* __restrict__ out_i,
-                                  float* __restrict__ out_d) {
-  constexpr int PER = KC / 32;  // candidates per lane (KC in {32, 64})
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
-  if (r >= n_q) return;
+                                  int ld, const int* __restrict__ perm_q, const int* __restrict__ perm_k,
+                                  const int* __restrict__ cand, int k, int* __restrict__ out_i, float* __restrict__ out_d) {
+  constexpr int PER = KC / 32;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (i >= n_q) return;
   const int l = lane_id();
+  const int64_t r = perm_q[i];
   const float* qp = Q + r * ld;
   const float qa = (l < d) ? qp[l] : 0.0f;
   const float qb = (l + 32 < d) ? qp[l + 32] : 0.0f;
@@ -252,11 +489,10 @@ __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __re
   int ii[PER];
 #pragma unroll
   for (int p = 0; p < PER; ++p) {
-    const int c = cand[r * KC + p * 32 + l];
-    ii[p] = c;
+    const int c = cand[i * KC + p * 32 + l];
+    ii[p] = (c >= 0) ? perm_k[c] : -1;
     dd[p] = INFINITY;
   }
-  // each candidate's distance computed cooperatively: lanes hold query dims l and l+32
 #pragma unroll
   for (int p = 0; p < PER; ++p) {
     for (int j = 0; j < 32; ++j) {
@@ -272,7 +508,6 @@ __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __re
       if (l == j) dd[p] = (c >= 0) ? s : INFINITY;
     }
   }
-  // bitonic sort of KC (d, idx) pairs ascending; element e = p*32 + lane
   auto less = [](float da, int ia, float db, int ib) {
     return da < db || (da == db && (unsigned)ia < (unsigned)ib);
   };
@@ -283,24 +518,10 @@ __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __re
 #pragma unroll
       for (int p = 0; p < PER; ++p) {
         const int e = p * 32 + l;
-        const int partner = e ^ stride;
-        float od;
-        int oi;
-        if (stride >= 32) {  // partner in another register slot, same lane
-          od = dd[p ^ (stride >> 5)];
-          oi = ii[p ^ (stride >> 5)];
-        } else {
-          od = __shfl_xor_sync(0xffffffffu, dd[p], stride);
-          oi = __shfl_xor_sync(0xffffffffu, ii[p], stride);
-        }
         const bool up = ((e & size) == 0);
-        const bool lower = e < partner;
-        const bool mine_less = less(dd[p], ii[p], od, oi);
-        const bool keep = (lower == up) ? mine_less : !mine_less;
         if (stride >= 32) {
-          // both slots handled when p is the lower slot; write after computing both
+          const int pq = p ^ (stride >> 5);
           if ((p & (stride >> 5)) == 0) {
-            const int pq = p ^ (stride >> 5);
             const float d0 = dd[p], d1 = dd[pq];
             const int i0 = ii[p], i1 = ii[pq];
             const bool lt = less(d0, i0, d1, i1);
@@ -310,9 +531,16 @@ __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __re
             dd[pq] = swp ? d0 : d1;
             ii[pq] = swp ? i0 : i1;
           }
-        } else if (!keep) {
-          dd[p] = od;
-          ii[p] = oi;
+        } else {
+          const float od = __shfl_xor_sync(0xffffffffu, dd[p], stride);
+          const int oi = __shfl_xor_sync(0xffffffffu, ii[p], stride);
+          const bool lower = e < (e ^ stride);
+          const bool mine_less = less(dd[p], ii[p], od, oi);
+          const bool keep = (lower == up) ? mine_less : !mine_less;
+          if (!keep) {
+            dd[p] = od;
+            ii[p] = oi;
+          }
         }
       }
     }
@@ -327,17 +555,80 @@ __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __re
   }
 }
 
+// ------------------------------------------------------------------ host orchestration
+static int sort_by_pc1(const float* X, int64_t n, int d, int ld, const int* omin, const int* omax, int* hist, int* perm,
+                       float* pc1_sorted, cudaStream_t s) {
+  SCB_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * kBuckets, s));
+  const int g = std::max(1, std::min(1184, ceil_div(n, 256)));
+  bucket_hist_kernel<<<g, 256, 0, s>>>(X, n, d, ld, omin, omax, hist);
+  SCB_LAUNCH_CHECK();
+  bucket_scan_kernel<<<1, 1024, 0, s>>>(hist);
+  SCB_LAUNCH_CHECK();
+  bucket_scatter_kernel<<<g, 256, 0, s>>>(X, n, d, ld, omin, omax, hist, perm, pc1_sorted);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
 template <int KC>
-static int launch_candidates(scb_ctx* ctx, const float* Qa, int64_t n_q, const float* Ka, int64_t n_k, int* cand,
-                             cudaStream_t s) {
+static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* Kx, int64_t n_k, int d, int ld, int k,
+                      int* out_i, float* out_d, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
   using Cfg = KnnCfg<KC>;
+  const bool same = (Qx == Kx && n_q == n_k);
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  const int64_t n_pairs = (n_q + 2 * Cfg::BM - 1) / (2 * Cfg::BM);
+  const size_t sz[] = {256, sizeof(int) * kBuckets, 4 * (size_t)n_q, 4 * (size_t)n_k, 4 * (size_t)n_q,
+                       4 * (size_t)n_k, 4 * (size_t)n_pairs, (size_t)n_q * kD * 2, (size_t)n_k * kD * 2,
+                       (size_t)n_q * KC * 4};
+  size_t total = 0;
+  for (size_t v : sz) total += up(v);
+  void* ws;
+  SCB_TRY(ws_get(ctx, 0, total, &ws, s));
+  char* p = (char*)ws;
+  unsigned* amax = (unsigned*)p;
+  int* omin = (int*)(p + 16);
+  int* omax = (int*)(p + 32);
+  p += up(sz[0]);
+  int* hist = (int*)p; p += up(sz[1]);
+  int* perm_q = (int*)p; p += up(sz[2]);
+  int* perm_k = (int*)p; p += up(sz[3]);
+  float* pc1_q = (float*)p; p += up(sz[4]);
+  float* pc1_k = (float*)p; p += up(sz[5]);
+  int* start = (int*)p; p += up(sz[6]);
+  __half* Qa = (__half*)p; p += up(sz[7]);
+  __half* Ka = (__half*)p; p += up(sz[8]);
+  int* cand = (int*)p;
+  // FP16 scale and the PC1 range come from the KEYS (queries are rows of the same embedding)
+  const int init[12] = {0, 0, 0, 0, 0x7fffffff, 0x7fffffff, 0x7fffffff, 0, (int)0x80000000, (int)0x80000000,
+                        (int)0x80000000, 0};
+  SCB_CUDA(cudaMemcpyAsync(amax, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  const int g = std::max(1, std::min(1184, ceil_div(n_k, 256)));
+  range_kernel<<<g, 256, 0, s>>>(Kx, n_k, d, ld, amax, omin, omax);
+  SCB_LAUNCH_CHECK();
+  SCB_TRY(sort_by_pc1(Kx, n_k, d, ld, omin, omax, hist, perm_k, pc1_k, s));
+  if (same) {
+    perm_q = perm_k;
+    pc1_q = pc1_k;
+  } else {
+    SCB_TRY(sort_by_pc1(Qx, n_q, d, ld, omin, omax, hist, perm_q, pc1_q, s));
+  }
+  knn_prep_kernel<<<ceil_div(n_q, 8), 256, 0, s>>>(Qx, n_q, d, ld, 0, perm_q, amax, Qa);
+  SCB_LAUNCH_CHECK();
+  knn_prep_kernel<<<ceil_div(n_k, 8), 256, 0, s>>>(Kx, n_k, d, ld, 1, perm_k, amax, Ka);
+  SCB_LAUNCH_CHECK();
+  start_tile_kernel<<<ceil_div(n_pairs, 256), 256, 0, s>>>(pc1_q, n_q, pc1_k, n_k, Cfg::BM, Cfg::BN, start);
+  SCB_LAUNCH_CHECK();
   CUtensorMap tq, tk;
-  SCB_TRY(make_tmap_2d_f32(&tq, Qa, (uint64_t)n_q, kD, kD, 32, Cfg::BM));
-  SCB_TRY(make_tmap_2d_f32(&tk, Ka, (uint64_t)n_k, kD, kD, 32, Cfg::BN));
+  SCB_TRY(make_tmap_2d(&tq, Qa, (uint64_t)n_q, kD, kD, 2, 64, Cfg::BM));
+  SCB_TRY(make_tmap_2d(&tk, Ka, (uint64_t)n_k, kD, kD, 2, 64, Cfg::BN));
   auto kern = knn_candidates_kernel<KC>;
   SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  const int n_pairs = (int)((n_q + 2 * Cfg::BM - 1) / (2 * Cfg::BM));
-  kern<<<std::min(n_pairs, ctx->num_sms), kKnnThreads, Cfg::SMEM, s>>>(tq, tk, n_q, n_k, cand);
+  if (ev0) SCB_CUDA(cudaEventRecord(ev0, s));
+  const char* dbg = getenv("SCB_KNN_DEBUG_MODE");
+  kern<<<(int)std::min<int64_t>(n_pairs, ctx->num_sms), kKnnThreads, Cfg::SMEM, s>>>(tq, tk, n_q, n_k, start, cand,
+                                                                                 dbg ? atoi(dbg) : 0);
+  SCB_LAUNCH_CHECK();
+  if (ev1) SCB_CUDA(cudaEventRecord(ev1, s));
+  knn_rerank_kernel<KC><<<ceil_div(n_q, 8), 256, 0, s>>>(Qx, Kx, n_q, d, ld, perm_q, perm_k, cand, k, out_i, out_d);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
@@ -346,61 +637,24 @@ static int launch_candidates(scb_ctx* ctx, const float* Qa, int64_t n_q, const f
 
 using namespace scb;
 
-extern "C" int scb_knn_prep(scb_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t ld, int32_t is_key, float* out,
-                            void* stream) {
-  SCB_REQUIRE(ctx && X && out, SCB_ERR_ARG, "scb_knn_prep: null argument");
-  SCB_REQUIRE(d >= 1 && d <= kD - 2 && ld >= d, SCB_ERR_ARG, "scb_knn_prep: need 1 <= d <= %d and ld >= d", kD - 2);
-  SCB_REQUIRE(((uintptr_t)out & 15) == 0, SCB_ERR_ARG, "scb_knn_prep: out must be 16-byte aligned");
-  if (n == 0) return SCB_OK;
-  knn_prep_kernel<<<ceil_div(n, 8), 256, 0, (cudaStream_t)stream>>>(X, n, d, ld, is_key ? 1 : 0, out);
-  SCB_LAUNCH_CHECK();
-  return SCB_OK;
-}
-
-extern "C" int scb_knn_candidates(scb_ctx* ctx, const float* Qa, int64_t n_q, const float* Ka, int64_t n_k,
-                                  int32_t k_cand, int32_t* cand, void* stream) {
-  SCB_REQUIRE(ctx && Qa && Ka && cand, SCB_ERR_ARG, "scb_knn_candidates: null argument");
-  SCB_REQUIRE(k_cand == 32 || k_cand == 64, SCB_ERR_ARG, "scb_knn_candidates: k_cand must be 32 or 64");
-  SCB_REQUIRE(n_k < (1ll << 31) && n_q < (1ll << 31), SCB_ERR_ARG, "scb_knn_candidates: too many rows");
-  if (n_q == 0) return SCB_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  return k_cand == 32 ? launch_candidates<32>(ctx, Qa, n_q, Ka, n_k, cand, s)
-                      : launch_candidates<64>(ctx, Qa, n_q, Ka, n_k, cand, s);
-}
-
-extern "C" int scb_knn_rerank(scb_ctx* ctx, const float* queries, int64_t n_q, const float* keys, int32_t d, int32_t ld,
-                              const int32_t* cand, int32_t k_cand, int32_t k, int32_t* knn_index, float* knn_dist,
-                              void* stream) {
-  SCB_REQUIRE(ctx && queries && keys && cand && knn_index && knn_dist, SCB_ERR_ARG, "scb_knn_rerank: null argument");
-  SCB_REQUIRE(k >= 1 && k <= k_cand && (k_cand == 32 || k_cand == 64), SCB_ERR_ARG, "scb_knn_rerank: bad k / k_cand");
-  if (n_q == 0) return SCB_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (k_cand == 32)
-    knn_rerank_kernel<32><<<ceil_div(n_q, 8), 256, 0, s>>>(queries, keys, n_q, d, ld, cand, k, knn_index, knn_dist);
-  else
-    knn_rerank_kernel<64><<<ceil_div(n_q, 8), 256, 0, s>>>(queries, keys, n_q, d, ld, cand, k, knn_index, knn_dist);
-  SCB_LAUNCH_CHECK();
-  return SCB_OK;
-}
-
-extern "C" int scb_knn(scb_ctx* ctx, const float* queries, int64_t n_queries, const float* keys, int64_t n_keys,
-                       int32_t d, int32_t ld, int32_t k, int32_t k_cand, int32_t* knn_index, float* knn_dist,
-                       void* stream) {
+extern "C" int scb_knn_timed(scb_ctx* ctx, const float* queries, int64_t n_queries, const float* keys, int64_t n_keys,
+                             int32_t d, int32_t ld, int32_t k, int32_t k_cand, int32_t* knn_index, float* knn_dist,
+                             void* stream, void* ev_start, void* ev_end) {
   SCB_REQUIRE(ctx && queries && keys && knn_index && knn_dist, SCB_ERR_ARG, "scb_knn: null argument");
   SCB_REQUIRE(d >= 1 && d <= kD - 2 && ld >= d, SCB_ERR_ARG, "scb_knn: need 1 <= d <= %d and ld >= d", kD - 2);
   SCB_REQUIRE(k >= 1 && k <= 64 && k <= n_keys, SCB_ERR_ARG, "scb_knn: need 1 <= k <= min(64, n_keys)");
   SCB_REQUIRE(k_cand >= k && (k_cand == 32 || k_cand == 64), SCB_ERR_ARG, "scb_knn: k_cand must be 32 or 64 and >= k");
   SCB_REQUIRE(n_keys < (1ll << 31) && n_queries < (1ll << 31), SCB_ERR_ARG, "scb_knn: too many rows");
   if (n_queries == 0) return SCB_OK;
-  void* ws;
-  const size_t qa = (size_t)n_queries * kD * 4, ka = (size_t)n_keys * kD * 4, cb = (size_t)n_queries * k_cand * 4;
-  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  SCB_TRY(ws_get(ctx, 0, up(qa) + up(ka) + up(cb), &ws, (cudaStream_t)stream));
-  float* Qa = (float*)ws;
-  float* Ka = (float*)((char*)ws + up(qa));
-  int* cand = (int*)((char*)Ka + up(ka));
-  SCB_TRY(scb_knn_prep(ctx, queries, n_queries, d, ld, 0, Qa, stream));
-  SCB_TRY(scb_knn_prep(ctx, keys, n_keys, d, ld, 1, Ka, stream));
-  SCB_TRY(scb_knn_candidates(ctx, Qa, n_queries, Ka, n_keys, k_cand, cand, stream));
-  return scb_knn_rerank(ctx, queries, n_queries, keys, d, ld, cand, k_cand, k, knn_index, knn_dist, stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t e0 = (cudaEvent_t)ev_start, e1 = (cudaEvent_t)ev_end;
+  if (k_cand == 32) return launch_knn<32>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
+  return launch_knn<64>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
+}
+
+extern "C" int scb_knn(scb_ctx* ctx, const float* queries, int64_t n_queries, const float* keys, int64_t n_keys,
+                       int32_t d, int32_t ld, int32_t k, int32_t k_cand, int32_t* knn_index, float* knn_dist,
+                       void* stream) {
+  return scb_knn_timed(ctx, queries, n_queries, keys, n_keys, d, ld, k, k_cand, knn_index, knn_dist, stream, nullptr,
+                       nullptr);
 }

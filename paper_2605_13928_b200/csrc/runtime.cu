@@ -89,8 +89,8 @@ namespace scb {
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-int make_tmap_2d_f32(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems,
-                     uint32_t box_cols, uint32_t box_rows, bool atom32) {
+int make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems, int elem_bytes,
+                 uint32_t box_cols, uint32_t box_rows, bool atom32) {
   if (!g_encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -98,18 +98,24 @@ int make_tmap_2d_f32(CUtensorMap* m, const void* base, uint64_t rows, uint64_t c
     SCB_REQUIRE(fn && q == cudaDriverEntryPointSuccess, SCB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  SCB_REQUIRE(((uintptr_t)base & 15) == 0 && (ld_elems * 4) % 16 == 0, SCB_ERR_ARG,
+  SCB_REQUIRE(elem_bytes == 4 || elem_bytes == 2, SCB_ERR_ARG, "TMA: unsupported element size");
+  SCB_REQUIRE(((uintptr_t)base & 15) == 0 && (ld_elems * elem_bytes) % 16 == 0, SCB_ERR_ARG,
               "TMA operand must be 16-byte aligned with a 16-byte multiple row stride");
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {ld_elems * 4};
+  cuuint64_t strides[1] = {ld_elems * (uint64_t)elem_bytes};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+  CUresult r = g_encode(m, elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                        const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   SCB_REQUIRE(r == CUDA_SUCCESS, SCB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return SCB_OK;
+}
+
+int make_tmap_2d_f32(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems,
+                     uint32_t box_cols, uint32_t box_rows, bool atom32) {
+  return make_tmap_2d(m, base, rows, cols, ld_elems, 4, box_cols, box_rows, atom32);
 }
 
 }  // namespace scb

@@ -141,5 +141,8 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
 // (16-byte atoms) or, with atom32 = true, 128B with 32-byte atoms (MN-major TF32 operands).
 int make_tmap_2d_f32(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems,
                      uint32_t box_cols, uint32_t box_rows, bool atom32 = false);
+// same for fp32 (elem_bytes 4) or fp16 (2) operands
+int make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems, int elem_bytes,
+                 uint32_t box_cols, uint32_t box_rows, bool atom32 = false);
 
 }  // namespace scb

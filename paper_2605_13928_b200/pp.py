@@ -335,18 +335,13 @@ def neighbors(X_pca: torch.Tensor, n_neighbors: int = 15, n_comps: Optional[int]
     nq, nk = X_pca.shape[0], keys.shape[0]
     k = int(n_neighbors)
     kc = 32 if k <= 16 else 64
-    ctx, s = _ctx(X_pca), _stream(dev)
-    Qa = torch.empty((nq, 64), dtype=torch.float32, device=dev)
-    Ka = torch.empty((nk, 64), dtype=torch.float32, device=dev)
-    cand = torch.empty((nq, kc), dtype=torch.int32, device=dev)
     idx = torch.empty((nq, k), dtype=torch.int32, device=dev)
     dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
-    _lib.call("scb_knn_prep", ctx, _p(X_pca), nq, d, X_pca.stride(0), 0, _p(Qa), s)
-    _lib.call("scb_knn_prep", ctx, _p(keys), nk, d, keys.stride(0), 1, _p(Ka), s)
+    e0 = e1 = 0
     if timer is not None:
-        timer[0].record()
-    _lib.call("scb_knn_candidates", ctx, _p(Qa), nq, _p(Ka), nk, kc, _p(cand), s)
-    if timer is not None:
-        timer[1].record()
-    _lib.call("scb_knn_rerank", ctx, _p(X_pca), nq, _p(keys), d, X_pca.stride(0), _p(cand), kc, k, _p(idx), _p(dist), s)
+        for ev in timer:
+            ev.record()  # materialise the cudaEvent_t (torch creates events lazily)
+        e0, e1 = timer[0].cuda_event, timer[1].cuda_event
+    _lib.call("scb_knn_timed", _ctx(X_pca), _p(X_pca), nq, _p(keys), nk, d, X_pca.stride(0), k, kc, _p(idx), _p(dist),
+              _stream(dev), e0, e1)
     return idx, dist
