@@ -70,7 +70,14 @@ SCB_API int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
                    int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
                    int32_t* n_genes_by_counts, double* total_counts, double* total_counts_mt,
                    double* pct_counts_mt, int32_t* n_cells_by_counts, double* gene_total_counts,
-                   void* stream);
+                   int32_t* hvg_row_splits, void* stream);
+
+/* Number of gene tiles T the HVG column pass uses for n_cols genes.  If T > 1, passing
+ * hvg_row_splits (int32 [n_rows][T-1]) to scb_qc_metrics records, per row, how many entries
+ * have a gene index below each tile boundary; scb_hvg_gene_sums then streams every nonzero
+ * exactly once (otherwise each tile re-reads whole rows).  indices/data arrays of every CSR
+ * entry point must be 16-byte aligned. */
+SCB_API int32_t scb_hvg_tiles(int32_t n_cols);
 
 /* ---- a2: sc.pp.filter_cells(min_genes, max_genes) + pct_counts_mt < max_pct_mt, and
  * sc.pp.filter_genes(min_cells).  max_genes < 0 disables the upper bound.
@@ -107,7 +114,8 @@ SCB_API int scb_normalize_log1p(scb_ctx* ctx, const int64_t* indptr, const float
  * gene_remap (optional) maps input columns to output columns (-1 = skip). */
 SCB_API int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* data,
                       const float* row_scale, int64_t n_rows, int32_t n_cols,
-                      const int32_t* gene_remap, int32_t n_out_cols, uint64_t* sums, void* stream);
+                      const int32_t* gene_remap, int32_t n_out_cols, const int32_t* hvg_row_splits,
+                      uint64_t* sums, void* stream);
 
 /* ---- a5: sc.pp.highly_variable_genes(flavor="seurat", n_top_genes, n_bins) from the
  * (all-reduced) gene sums.  Outputs per gene: means, variances, dispersions (log),

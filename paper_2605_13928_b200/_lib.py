@@ -22,12 +22,14 @@ SIGNATURES = {
     "scb_launch_count": [],
     "scb_ctx_create": [ctypes.c_int, ctypes.POINTER(c_ptr)],
     "scb_ctx_destroy": [c_ptr],
-    "scb_qc_metrics": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+    "scb_qc_metrics": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+                       c_ptr],
+    "scb_hvg_tiles": [c_i32],
     "scb_filter_masks": [c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_i32, c_i32, c_i32, c_dbl, c_i32, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_subset_count": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr],
     "scb_subset_fill": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_normalize_log1p": [c_ptr, c_ptr, c_ptr, c_i64, c_dbl, c_ptr, c_ptr, c_ptr],
-    "scb_hvg_gene_sums": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr],
+    "scb_hvg_gene_sums": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr],
     "scb_hvg_select": [c_ptr, c_ptr, c_i32, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_scale_gene_sums": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr],
     "scb_scale_finalize": [c_ptr, c_ptr, c_i32, c_i64, c_ptr, c_ptr, c_ptr],
@@ -39,7 +41,7 @@ SIGNATURES = {
     "scb_knn_timed": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_i32, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_synth_rows": [c_ptr, c_u64, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
 }
-_RESTYPE = {"scb_last_error": ctypes.c_char_p, "scb_launch_count": ctypes.c_ulonglong}
+_RESTYPE = {"scb_last_error": ctypes.c_char_p, "scb_launch_count": ctypes.c_ulonglong, "scb_hvg_tiles": ctypes.c_int32}
 
 _lib = None
 _lock = threading.Lock()
@@ -74,6 +76,8 @@ def load(path: str = LIB_PATH):
 def call(name, *args):
     lib = load()
     rc = getattr(lib, name)(*args)
+    if name in _RESTYPE:
+        return rc
     if rc != 0:
         msg = lib.scb_last_error()
         raise ScbError(name, rc, msg.decode() if msg else "")

@@ -10,23 +10,31 @@
 // identical across 1/2/4/8-way cell sharding.
 #include "common.cuh"
 #include "scan.cuh"
+#include "stream.cuh"
 
 namespace scb {
 
 constexpr int kRowThreads = 512;          // threads per CTA of the row-streaming kernels
+constexpr int kQcThreads = 1024;          // QC: one CTA per SM (gene histogram fills smem)
+constexpr int kMaxSplit = 3;              // gene tiles of the HVG pass: up to 4 (G <= ~58k)
+constexpr int kHvgTileW = (int)(227 * 1024 / 16);  // genes per HVG tile (4 u32 words each)
 constexpr size_t kSmemLimit = 227 * 1024;  // opt-in dynamic shared memory per CTA
 
 static int grid_for(scb_ctx* ctx, int ctas_per_sm) { return ctx->num_sms * ctas_per_sm; }
 
 // ============================================================================ QC
-// smem: n_cells u32[W], total_lo u32[W] for a gene tile [g0, g0+W), mt bitmask.
-__global__ void __launch_bounds__(kRowThreads)
+// smem: n_cells u32[W], total_lo u32[W] for a gene tile [g0, g0+W), mt bitmask.  The tile-0
+// CTAs also write the per-cell metrics and, for the HVG pass, the per-row positions where
+// the original gene index crosses each HVG tile boundary (splits[r][t-1] = #entries with
+// gene < t*split_w, relative to the row start).
+__global__ void __launch_bounds__(kQcThreads)
 qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
           const float* __restrict__ data, int64_t n_rows, int32_t n_cols,
-          const uint8_t* __restrict__ mt_mask, int32_t tile_w,
-          int32_t* __restrict__ n_genes, double* __restrict__ total, double* __restrict__ total_mt,
-          double* __restrict__ pct, uint32_t* __restrict__ g_cells, unsigned long long* __restrict__ g_total,
-          int* __restrict__ flag) {
+          const uint8_t* __restrict__ mt_mask, int32_t tile_w, int32_t n_split, int32_t split_w,
+          int32_t* __restrict__ splits, int32_t* __restrict__ n_genes, double* __restrict__ total,
+          double* __restrict__ total_mt, double* __restrict__ pct, uint32_t* __restrict__ g_cells,
+          unsigned long long* __restrict__ g_total, int* __restrict__ flag) {
+  const int64_t nnz = indptr[n_rows];
   extern __shared__ uint32_t sm[];
   const int tile = blockIdx.y;
   const int g0 = tile * tile_w;
@@ -38,47 +46,58 @@ qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indice
   for (int i = threadIdx.x; i < 2 * tile_w; i += blockDim.x) sm[i] = 0;
   for (int i = threadIdx.x; i < mt_words; i += blockDim.x) {
     uint32_t m = 0;
-    for (int b = 0; b < 32; ++b) {
-      int g = i * 32 + b;
-      if (g < n_cols && mt_mask[g]) m |= 1u << b;
+    for (int bb = 0; bb < 32; ++bb) {
+      const int g = i * 32 + bb;
+      if (g < n_cols && mt_mask[g]) m |= 1u << bb;
     }
     s_mt[i] = m;
   }
   __syncthreads();
-  const bool row_owner = (tile == 0);  // tile 0 also writes the per-cell metrics
+  const bool row_owner = (tile == 0);
   const int lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   bool bad = false;
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
     const int64_t b = indptr[r], e = indptr[r + 1];
-    int cnt = 0;
-    double sum = 0.0, summt = 0.0;
-    for (int64_t p = b + lane; p < e; p += 32) {
-      const int g = ldg_stream(indices + p);
-      const float x = ldg_stream(data + p);
-      bad |= !(x >= 0.0f && x == rintf(x) && x < 16777216.0f) || g < 0 || g >= n_cols;
-      if (x > 0.0f) {
-        cnt += 1;
-        sum += (double)x;
-        if ((s_mt[g >> 5] >> (g & 31)) & 1u) summt += (double)x;
-        const int gl = g - g0;
-        if (gl >= 0 && gl < w) {
-          atomicAdd(&s_cells[gl], 1u);
+    uint32_t cnt = 0;
+    unsigned long long sum = 0, summt = 0;
+    int sc[kMaxSplit] = {0, 0, 0};
+    stream_row<2>(indices, data, b, e, nnz, [&](const Quad& q) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!((q.valid >> k) & 1u)) continue;
+        const int g = q.g[k];
+        const float x = q.x[k];
+        bad |= !(x >= 0.0f && x == rintf(x) && x < 16777216.0f) || g < 0 || g >= n_cols;
+#pragma unroll
+        for (int t = 0; t < kMaxSplit; ++t) sc[t] += (t < n_split && g < (t + 1) * split_w) ? 1 : 0;
+        if (x > 0.0f && !bad) {
           const uint32_t xv = (uint32_t)x;
-          const uint32_t old = atomicAdd(&s_tot[gl], xv);
-          if (old > 0xffffffffu - xv) atomicAdd(&g_total[g], 1ull << 32);  // rare carry
+          cnt += 1;
+          sum += xv;
+          if ((s_mt[g >> 5] >> (g & 31)) & 1u) summt += xv;
+          const int gl = g - g0;
+          if (gl >= 0 && gl < w) {
+            atomicAdd(&s_cells[gl], 1u);
+            const uint32_t old = atomicAdd(&s_tot[gl], xv);
+            if (old > 0xffffffffu - xv) atomicAdd(&g_total[g], 1ull << 32);  // rare carry
+          }
         }
       }
-    }
+    });
     if (row_owner) {
       cnt = warp_sum(cnt);
       sum = warp_sum(sum);
       summt = warp_sum(summt);
+#pragma unroll
+      for (int t = 0; t < kMaxSplit; ++t) sc[t] = warp_sum(sc[t]);
       if (lane == 0) {
-        n_genes[r] = cnt;
-        total[r] = sum;
-        total_mt[r] = summt;
-        pct[r] = __ddiv_rn(__dmul_rn(100.0, summt), sum);
+        n_genes[r] = (int32_t)cnt;
+        const double sd = (double)sum, md = (double)summt;
+        total[r] = sd;
+        total_mt[r] = md;
+        pct[r] = __ddiv_rn(__dmul_rn(100.0, md), sd);
+        for (int t = 0; t < n_split; ++t) splits[r * n_split + t] = sc[t];
       }
     }
   }
@@ -170,6 +189,7 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
                     const int32_t* __restrict__ remap, const int64_t* __restrict__ row_pos,
                     int64_t* __restrict__ cnt, double target_sum, float* __restrict__ row_scale,
                     float* __restrict__ row_scale_orig) {
+  const int64_t nnz = indptr[n_rows];
   const int lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
@@ -180,13 +200,14 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
     const int64_t b = indptr[r], e = indptr[r + 1];
     int c = 0;
     double sum = 0.0;
-    for (int64_t p = b + lane; p < e; p += 32) {
-      const int g = ldg_stream(indices + p);
-      if (remap[g] >= 0) {
-        ++c;
-        if (row_scale) sum += (double)ldg_stream(data + p);
-      }
-    }
+    stream_row<2>(indices, row_scale ? data : nullptr, b, e, nnz, [&](const Quad& q) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (((q.valid >> k) & 1u) && remap[q.g[k]] >= 0) {
+          ++c;
+          sum += (double)q.x[k];
+        }
+    });
     c = warp_sum(c);
     if (row_scale) sum = warp_sum(sum);
     if (lane == 0) {
@@ -201,45 +222,54 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
   }
 }
 
+// Compacting copy: each lane's 4-element quad contributes its kept count to a warp-wide
+// exclusive scan so the output stays in row order.
 __global__ void __launch_bounds__(kRowThreads)
 subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                    const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
                    const int32_t* __restrict__ remap, const int64_t* __restrict__ row_pos,
                    const int64_t* __restrict__ new_indptr, const float* __restrict__ row_scale,
                    int32_t* __restrict__ out_idx, float* __restrict__ out_val) {
+  const int64_t nnz = indptr[n_rows];
   const int lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const unsigned lt = (1u << lane) - 1u;
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
     if (!cmask[r]) continue;
     const int64_t kr = row_pos[r];
     const float s = row_scale ? row_scale[kr] : 1.0f;
     const int64_t b = indptr[r], e = indptr[r + 1];
     int64_t o = new_indptr[kr];
-    for (int64_t p0 = b; p0 < e; p0 += 32) {
-      const int64_t p = p0 + lane;
-      int ng = -1;
-      float x = 0.0f;
-      if (p < e) {
-        ng = remap[ldg_stream(indices + p)];
-        x = ldg_stream(data + p);
+    stream_row<2>(indices, data, b, e, nnz, [&](const Quad& q) {
+      int ng[4];
+      int kc = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        ng[k] = ((q.valid >> k) & 1u) ? remap[q.g[k]] : -1;
+        kc += ng[k] >= 0 ? 1 : 0;
       }
-      const unsigned keep = __ballot_sync(0xffffffffu, ng >= 0);
-      if (ng >= 0) {
-        const int64_t q = o + __popc(keep & lt);
-        out_idx[q] = ng;
-        out_val[q] = row_scale ? log1pf(__fmul_rn(x, s)) : x;
+      int incl = kc;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
       }
-      o += __popc(keep);
-    }
+      int64_t pos = o + incl - kc;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (ng[k] >= 0) {
+          out_idx[pos] = ng[k];
+          out_val[pos] = row_scale ? log1pf(__fmul_rn(q.x[k], s)) : q.x[k];
+          ++pos;
+        }
+      o += __shfl_sync(0xffffffffu, incl, 31);
+    });
   }
 }
 
 // ============================================================================ normalize + log1p
 __global__ void __launch_bounds__(kRowThreads)
-normalize_log1p_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ data,
-                       int64_t n_rows, double target_sum, float* __restrict__ out,
-                       float* __restrict__ row_scale) {
+normalize_log1p_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ data, int64_t n_rows,
+                       double target_sum, float* __restrict__ out, float* __restrict__ row_scale) {
   const int lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
@@ -254,45 +284,54 @@ normalize_log1p_kernel(const int64_t* __restrict__ indptr, const float* __restri
 }
 
 // ============================================================================ HVG gene sums
-// Tiled column reduction: CTA (row block, gene tile); smem holds 4 u32 words per gene of
-// the tile (sum y lo/hi, sum y^2 lo/hi).  Adjacent CTAs (same rows, other tiles) re-read
-// the rows from L2.
+// Tiled column reduction over ORIGINAL gene ranges [t*tile_w, (t+1)*tile_w): CTA (row block,
+// tile) keeps 4 u32 fixed-point words per gene of its tile (sum y lo/hi, sum y^2 lo/hi) in
+// smem.  With row splits (from QC) each CTA streams only its tile's sub-range of every row,
+// so each nonzero is read exactly once; without them every tile CTA filters whole rows.
 __device__ __forceinline__ uint64_t fx_round(double v) { return (uint64_t)__double2ull_rn(v); }
 
 __global__ void __launch_bounds__(kRowThreads)
 hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                 const float* __restrict__ data, const float* __restrict__ row_scale, int64_t n_rows,
                 int32_t n_cols, const int32_t* __restrict__ remap, int32_t n_out, int32_t tile_w,
-                int32_t n_tiles, int64_t rows_per_block, unsigned long long* __restrict__ sums) {
+                int32_t n_tiles, const int32_t* __restrict__ splits, int64_t rows_per_block,
+                unsigned long long* __restrict__ sums) {
+  const int64_t nnz = indptr[n_rows];
   extern __shared__ uint32_t sm[];
   const int tile = blockIdx.x % n_tiles;
   const int64_t rblk = blockIdx.x / n_tiles;
   const int g0 = tile * tile_w;
-  const int w = min(tile_w, n_out - g0);
+  const int w = min(tile_w, n_cols - g0);
   uint32_t* s1lo = sm;
   uint32_t* s1hi = sm + tile_w;
   uint32_t* s2lo = sm + 2 * tile_w;
   uint32_t* s2hi = sm + 3 * tile_w;
   for (int i = threadIdx.x; i < 4 * tile_w; i += blockDim.x) sm[i] = 0;
   __syncthreads();
-  const int lane = lane_id();
   const int64_t r0 = rblk * rows_per_block;
   const int64_t r1 = min(n_rows, r0 + rows_per_block);
+  const int ns = n_tiles - 1;
   for (int64_t r = r0 + warp_id(); r < r1; r += (blockDim.x >> 5)) {
     const float s = row_scale[r];
     if (s == 0.0f) continue;
-    const int64_t b = indptr[r], e = indptr[r + 1];
-    for (int64_t p = b + lane; p < e; p += 32) {
-      int g = ldg_stream(indices + p);
-      if (remap) g = remap[g];
-      const int gl = g - g0;
-      if (g >= 0 && gl >= 0 && gl < w) {
-        const float y = __fmul_rn(ldg_stream(data + p), s);   // float32 normalized count
-        const double yd = (double)y;
-        fx_add(&s1lo[gl], &s1hi[gl], fx_round(yd * 268435456.0));          // y * 2^28
-        fx_add(&s2lo[gl], &s2hi[gl], fx_round((yd * yd) * 16777216.0));     // y^2 * 2^24
-      }
+    int64_t b = indptr[r], e = indptr[r + 1];
+    if (splits && ns > 0) {
+      const int64_t rb = b;
+      if (tile > 0) b = rb + splits[r * ns + tile - 1];
+      if (tile < ns) e = rb + splits[r * ns + tile];
     }
+    stream_row<2>(indices, data, b, e, nnz, [&](const Quad& q) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int gl = q.g[k] - g0;
+        if (((q.valid >> k) & 1u) && gl >= 0 && gl < w && (!remap || remap[q.g[k]] >= 0)) {
+          const float y = __fmul_rn(q.x[k], s);   // float32 normalized count
+          const double yd = (double)y;
+          fx_add(&s1lo[gl], &s1hi[gl], fx_round(yd * 268435456.0));          // y * 2^28
+          fx_add(&s2lo[gl], &s2hi[gl], fx_round((yd * yd) * 16777216.0));     // y^2 * 2^24
+        }
+      }
+    });
   }
   __syncthreads();
   unsigned long long* l0 = sums;               // stat 0 limb 0
@@ -300,10 +339,12 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
   unsigned long long* m0 = sums + 2 * n_out;   // stat 1 limb 0
   unsigned long long* m1 = sums + 3 * n_out;   // stat 1 limb 1
   for (int i = threadIdx.x; i < w; i += blockDim.x) {
-    if (s1lo[i]) atomicAdd(&l0[g0 + i], (unsigned long long)s1lo[i]);
-    if (s1hi[i]) atomicAdd(&l1[g0 + i], (unsigned long long)s1hi[i]);
-    if (s2lo[i]) atomicAdd(&m0[g0 + i], (unsigned long long)s2lo[i]);
-    if (s2hi[i]) atomicAdd(&m1[g0 + i], (unsigned long long)s2hi[i]);
+    const int go = remap ? remap[g0 + i] : g0 + i;
+    if (go < 0) continue;
+    if (s1lo[i]) atomicAdd(&l0[go], (unsigned long long)s1lo[i]);
+    if (s1hi[i]) atomicAdd(&l1[go], (unsigned long long)s1hi[i]);
+    if (s2lo[i]) atomicAdd(&m0[go], (unsigned long long)s2lo[i]);
+    if (s2hi[i]) atomicAdd(&m1[go], (unsigned long long)s2hi[i]);
   }
 }
 
@@ -559,6 +600,7 @@ __global__ void __launch_bounds__(kRowThreads)
 scale_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                   const float* __restrict__ ldata, int64_t n_rows, int32_t n_cols,
                   const int32_t* __restrict__ slot, int32_t n_slots, unsigned long long* __restrict__ sums) {
+  const int64_t nnz = indptr[n_rows];
   extern __shared__ uint32_t sm[];
   int16_t* s_slot = reinterpret_cast<int16_t*>(sm + 4 * n_slots);
   for (int i = threadIdx.x; i < 4 * n_slots; i += blockDim.x) sm[i] = 0;
@@ -568,18 +610,20 @@ scale_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
   uint32_t* s1hi = sm + n_slots;
   uint32_t* s2lo = sm + 2 * n_slots;
   uint32_t* s2hi = sm + 3 * n_slots;
-  const int lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
-    const int64_t b = indptr[r], e = indptr[r + 1];
-    for (int64_t p = b + lane; p < e; p += 32) {
-      const int j = s_slot[ldg_stream(indices + p)];
-      if (j >= 0) {
-        const double l = (double)ldg_stream(ldata + p);
-        fx_add(&s1lo[j], &s1hi[j], fx_round(l * 268435456.0));        // l * 2^28
-        fx_add(&s2lo[j], &s2hi[j], fx_round((l * l) * 16777216.0));    // l^2 * 2^24
+    stream_row<2>(indices, ldata, indptr[r], indptr[r + 1], nnz, [&](const Quad& q) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!((q.valid >> k) & 1u)) continue;
+        const int j = s_slot[q.g[k]];
+        if (j >= 0) {
+          const double l = (double)q.x[k];
+          fx_add(&s1lo[j], &s1hi[j], fx_round(l * 268435456.0));        // l * 2^28
+          fx_add(&s2lo[j], &s2hi[j], fx_round((l * l) * 16777216.0));    // l^2 * 2^24
+        }
       }
-    }
+    });
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n_slots; i += blockDim.x) {
@@ -615,8 +659,11 @@ scale_dense_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
                    const int32_t* __restrict__ slot, int32_t H, const double* __restrict__ mean,
                    const double* __restrict__ inv, double max_value, float* __restrict__ Z, int64_t ldz,
                    int32_t ones_col) {
+  const int64_t nnz = indptr[n_rows];
   extern __shared__ float zsm[];                        // background row [ldz]
   int16_t* s_slot = reinterpret_cast<int16_t*>(zsm + ldz);
+  double* s_mean = reinterpret_cast<double*>(s_slot + ((n_cols + 3) & ~3));
+  double* s_inv = s_mean + H;
   for (int j = threadIdx.x; j < ldz; j += blockDim.x) {
     float v = 0.0f;
     if (j < H) v = (float)fmin(__dmul_rn(__dsub_rn(0.0, mean[j]), inv[j]), max_value);
@@ -624,6 +671,10 @@ scale_dense_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
     zsm[j] = v;
   }
   for (int i = threadIdx.x; i < n_cols; i += blockDim.x) s_slot[i] = (int16_t)slot[i];
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    s_mean[j] = mean[j];
+    s_inv[j] = inv[j];
+  }
   __syncthreads();
   const int lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -633,15 +684,16 @@ scale_dense_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
     float* zr = Z + r * ldz;
     float4* zr4 = reinterpret_cast<float4*>(zr);
     for (int j = lane; j < n4; j += 32) zr4[j] = bg[j];
-    __syncwarp();
-    const int64_t b = indptr[r], e = indptr[r + 1];
-    for (int64_t p = b + lane; p < e; p += 32) {
-      const int j = s_slot[ldg_stream(indices + p)];
-      if (j >= 0) {
-        const double l = (double)ldg_stream(ldata + p);
-        zr[j] = (float)fmin(__dmul_rn(__dsub_rn(l, mean[j]), inv[j]), max_value);
+    __syncwarp();  // orders this warp's background stores before the scattered overwrites
+    stream_row<2>(indices, ldata, indptr[r], indptr[r + 1], nnz, [&](const Quad& q) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!((q.valid >> k) & 1u)) continue;
+        const int j = s_slot[q.g[k]];
+        if (j >= 0)
+          zr[j] = (float)fmin(__dmul_rn(__dsub_rn((double)q.x[k], s_mean[j]), s_inv[j]), max_value);
       }
-    }
+    });
     __syncwarp();
   }
 }
@@ -651,13 +703,21 @@ scale_dense_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
 // ============================================================================ C ABI
 using namespace scb;
 
+extern "C" int32_t scb_hvg_tiles(int32_t n_cols) { return n_cols <= 0 ? 1 : (n_cols + kHvgTileW - 1) / kHvgTileW; }
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
                               const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
                               int32_t* n_genes, double* total, double* total_mt, double* pct,
-                              int32_t* n_cells, double* gene_total, void* stream) {
+                              int32_t* n_cells, double* gene_total, int32_t* hvg_row_splits, void* stream) {
   SCB_REQUIRE(ctx && indptr && mt_mask && n_genes && total && total_mt && pct && n_cells && gene_total,
               SCB_ERR_ARG, "scb_qc_metrics: null argument");
   SCB_REQUIRE(n_rows >= 0 && n_cols > 0, SCB_ERR_ARG, "scb_qc_metrics: bad shape");
+  SCB_REQUIRE(aligned16(indices) && aligned16(data), SCB_ERR_ARG, "scb_qc_metrics: indices/data must be 16-byte aligned");
+  const int n_tiles_hvg = scb_hvg_tiles(n_cols);
+  SCB_REQUIRE(n_tiles_hvg - 1 <= kMaxSplit, SCB_ERR_UNSUPPORTED, "scb_qc_metrics: too many genes (max %d)",
+              (kMaxSplit + 1) * kHvgTileW);
   cudaStream_t s = (cudaStream_t)stream;
   const int mt_words = (n_cols + 31) / 32;
   const int max_w = (int)((kSmemLimit - mt_words * 4) / 8);
@@ -665,17 +725,19 @@ extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t
   const int tile_w = ceil_div(n_cols, n_tiles);
   void* ws;
   const size_t ws_bytes = (size_t)n_cols * 4 + (size_t)n_cols * 8;
-  SCB_TRY(ws_get(ctx, 0, ws_bytes, &ws, s));
+  SCB_TRY(ws_get(ctx, 0, ws_bytes + 16, &ws, s));
   uint32_t* g_cells = (uint32_t*)ws;
   unsigned long long* g_total = (unsigned long long*)((char*)ws + ((size_t)n_cols * 4 + 7) / 8 * 8);
   SCB_CUDA(cudaMemsetAsync(ws, 0, ws_bytes + 8, s));
   SCB_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), s));
   const size_t smem = (size_t)tile_w * 8 + (size_t)mt_words * 4;
   SCB_CUDA(cudaFuncSetAttribute(qc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int n_split = hvg_row_splits ? n_tiles_hvg - 1 : 0;
   if (n_rows > 0) {
     dim3 grid(grid_for(ctx, 1), n_tiles);
-    qc_kernel<<<grid, kRowThreads, smem, s>>>(indptr, indices, data, n_rows, n_cols, mt_mask, tile_w,
-                                              n_genes, total, total_mt, pct, g_cells, g_total, ctx->d_flag);
+    qc_kernel<<<grid, kQcThreads, smem, s>>>(indptr, indices, data, n_rows, n_cols, mt_mask, tile_w, n_split,
+                                             kHvgTileW, hvg_row_splits, n_genes, total, total_mt, pct, g_cells,
+                                             g_total, ctx->d_flag);
     SCB_LAUNCH_CHECK();
   }
   qc_finalize<<<ceil_div(n_cols, 256), 256, 0, s>>>(g_cells, g_total, n_cols, n_cells, gene_total);
@@ -713,6 +775,7 @@ extern "C" int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32
   SCB_REQUIRE(ctx && indptr && indices && cmask && gmask && remap && new_indptr, SCB_ERR_ARG,
               "scb_subset_count: null argument");
   SCB_REQUIRE(!row_scale || data, SCB_ERR_ARG, "scb_subset_count: row_scale needs data");
+  SCB_REQUIRE(aligned16(indices) && (!data || aligned16(data)), SCB_ERR_ARG, "scb_subset_count: 16-byte alignment");
   cudaStream_t s = (cudaStream_t)stream;
   gene_remap_kernel<<<1, 1024, 0, s>>>(gmask, n_cols, remap);
   SCB_LAUNCH_CHECK();
@@ -739,6 +802,7 @@ extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_
                                int32_t* new_indices, float* new_data, void* stream) {
   SCB_REQUIRE(ctx && indptr && indices && data && cmask && remap && new_indptr && new_indices && new_data,
               SCB_ERR_ARG, "scb_subset_fill: null argument");
+  SCB_REQUIRE(aligned16(indices) && aligned16(data), SCB_ERR_ARG, "scb_subset_fill: 16-byte alignment");
   cudaStream_t s = (cudaStream_t)stream;
   void* ws;
   SCB_TRY(ws_get(ctx, 1, (size_t)(n_rows + 1) * 8 * 2, &ws, s));
@@ -766,22 +830,23 @@ extern "C" int scb_normalize_log1p(scb_ctx* ctx, const int64_t* indptr, const fl
 
 extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
                                  const float* data, const float* row_scale, int64_t n_rows, int32_t n_cols,
-                                 const int32_t* remap, int32_t n_out, uint64_t* sums, void* stream) {
+                                 const int32_t* remap, int32_t n_out, const int32_t* row_splits, uint64_t* sums,
+                                 void* stream) {
   SCB_REQUIRE(ctx && indptr && indices && data && row_scale && sums, SCB_ERR_ARG,
               "scb_hvg_gene_sums: null argument");
   SCB_REQUIRE(n_out > 0, SCB_ERR_ARG, "scb_hvg_gene_sums: n_out must be > 0");
+  SCB_REQUIRE(aligned16(indices) && aligned16(data), SCB_ERR_ARG, "scb_hvg_gene_sums: 16-byte alignment");
   if (n_rows == 0) return SCB_OK;
-  const int max_w = (int)(kSmemLimit / 16);
-  const int n_tiles = ceil_div(n_out, max_w);
-  const int tile_w = ceil_div(n_out, n_tiles);
-  const size_t smem = (size_t)tile_w * 16;
+  const int n_tiles = scb_hvg_tiles(n_cols);
+  const int tile_w = kHvgTileW;
+  const size_t smem = (size_t)std::min(tile_w, n_cols) * 16;
   // row blocks: keep per-CTA hi words far from overflow (<= 4096 rows) and give >= 2 waves
   int64_t rows_per_block = std::max<int64_t>(64, std::min<int64_t>(4096, n_rows / (2 * ctx->num_sms) + 1));
   const int64_t n_blocks = (n_rows + rows_per_block - 1) / rows_per_block;
   SCB_CUDA(cudaFuncSetAttribute(hvg_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kRowThreads, smem, (cudaStream_t)stream>>>(
-      indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, tile_w, n_tiles, rows_per_block,
-      (unsigned long long*)sums);
+      indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles,
+      row_splits, rows_per_block, (unsigned long long*)sums);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
@@ -810,6 +875,7 @@ extern "C" int scb_scale_gene_sums(scb_ctx* ctx, const int64_t* indptr, const in
                                    int32_t n_slots, uint64_t* sums, void* stream) {
   SCB_REQUIRE(ctx && indptr && indices && ldata && slot && sums, SCB_ERR_ARG, "scb_scale_gene_sums: null argument");
   SCB_REQUIRE(n_slots > 0 && n_slots < 32768, SCB_ERR_UNSUPPORTED, "scb_scale_gene_sums: n_slots must be in [1, 32767]");
+  SCB_REQUIRE(aligned16(indices) && aligned16(ldata), SCB_ERR_ARG, "scb_scale_gene_sums: 16-byte alignment");
   const size_t smem = (size_t)n_slots * 16 + (size_t)n_cols * 2;
   SCB_REQUIRE(smem <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_scale_gene_sums: too many genes for one CTA");
   if (n_rows == 0) return SCB_OK;
@@ -840,7 +906,8 @@ extern "C" int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_
   SCB_REQUIRE(ldz % 4 == 0 && ldz >= n_slots && ones_col < ldz, SCB_ERR_ARG,
               "scb_scale_dense: ldz must be a multiple of 4 and >= n_slots");
   SCB_REQUIRE(((uintptr_t)Z & 15) == 0, SCB_ERR_ARG, "scb_scale_dense: Z must be 16-byte aligned");
-  const size_t smem = (size_t)ldz * 4 + (size_t)n_cols * 2;
+  SCB_REQUIRE(aligned16(indices) && aligned16(ldata), SCB_ERR_ARG, "scb_scale_dense: 16-byte alignment");
+  const size_t smem = (size_t)ldz * 4 + (size_t)((n_cols + 3) & ~3) * 2 + (size_t)n_slots * 16;
   SCB_REQUIRE(smem <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_scale_dense: too many genes");
   if (n_rows == 0) return SCB_OK;
   SCB_CUDA(cudaFuncSetAttribute(scale_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -120,7 +120,7 @@ __global__ void init_block_kernel(double* __restrict__ Q, int h) {
 
 // ------------------------------------------------------------------ Cholesky QR
 // In place Cholesky of the kB x kB Gram S = Q^T Q (one CTA), S -> R (upper, row-major).
-__global__ void __launch_bounds__(1024) chol_kernel(double* __restrict__ S, int* __restrict__ fail) {
+__global__ void __launch_bounds__(256) chol_kernel(double* __restrict__ S, int* __restrict__ fail) {
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) a[e / kB][e % kB] = S[e];
@@ -167,42 +167,46 @@ __global__ void __launch_bounds__(kB) triinv_kernel(const double* __restrict__ R
 
 // ------------------------------------------------------------------ Jacobi (one CTA)
 // Cyclic two-sided Jacobi on the symmetric kB x kB matrix T; W accumulates rotations.
-// Round-robin ordering: kB/2 disjoint (p, q) pairs per round, kB-1 rounds per sweep.
-__global__ void __launch_bounds__(1024) jacobi_kernel(double* __restrict__ T, double* __restrict__ W, int sweeps) {
+// Round-robin tournament ordering in closed form: in round r, pair 0 = (kB-1, r) and pair
+// i >= 1 = ((r+i) mod (kB-1), (r-i) mod (kB-1)): kB/2 disjoint pairs, every pair once per
+// sweep.  Sweeps stop when the off-diagonal Frobenius norm is <= 1e-13 of the diagonal's.
+constexpr int kJacThreads = 256;
+__global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict__ T, double* __restrict__ W, int sweeps) {
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
   double (*w)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn + kB * kLd);
   __shared__ double cs[kB / 2], sn[kB / 2];
   __shared__ int pp[kB / 2], qq[kB / 2];
-  __shared__ int ring[kB];
-  __shared__ double off_s, dia_s;
+  __shared__ double red[2][kJacThreads / 32];
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
     a[e / kB][e % kB] = T[e];
     w[e / kB][e % kB] = (e / kB == e % kB) ? 1.0 : 0.0;
   }
-  if (threadIdx.x < kB) ring[threadIdx.x] = threadIdx.x;
   __syncthreads();
+  constexpr int M = kB - 1;
   for (int sw = 0; sw < sweeps; ++sw) {
-    for (int rd = 0; rd < kB - 1; ++rd) {
+    for (int rd = 0; rd < M; ++rd) {
       if (threadIdx.x < kB / 2) {
-        int p = ring[threadIdx.x], q = ring[kB - 1 - threadIdx.x];
-        if (p > q) { int t = p; p = q; q = t; }
-        pp[threadIdx.x] = p;
-        qq[threadIdx.x] = q;
+        const int i = threadIdx.x;
+        int p, q;
+        if (i == 0) { p = rd; q = M; }
+        else { p = (rd + i) % M; q = (rd - i + M) % M; }
+        if (p > q) { const int t = p; p = q; q = t; }
+        pp[i] = p;
+        qq[i] = q;
         const double apq = a[p][q];
         double c = 1.0, s = 0.0;
         if (apq != 0.0) {
           const double tau = (a[q][q] - a[p][p]) / (2.0 * apq);
           const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + t * t);
+          c = rsqrt(1.0 + t * t);
           s = t * c;
         }
-        cs[threadIdx.x] = c;
-        sn[threadIdx.x] = s;
+        cs[i] = c;
+        sn[i] = s;
       }
       __syncthreads();
-      // rows: A := J^T A
-      for (int e = threadIdx.x; e < (kB / 2) * kB; e += blockDim.x) {
+      for (int e = threadIdx.x; e < (kB / 2) * kB; e += blockDim.x) {  // rows: A := J^T A
         const int k = e / kB, j = e % kB;
         const int p = pp[k], q = qq[k];
         const double c = cs[k], s = sn[k];
@@ -211,8 +215,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(double* __restrict__ T, do
         a[q][j] = s * ap + c * aq;
       }
       __syncthreads();
-      // columns: A := A J ; W := W J
-      for (int e = threadIdx.x; e < (kB / 2) * kB; e += blockDim.x) {
+      for (int e = threadIdx.x; e < (kB / 2) * kB; e += blockDim.x) {  // columns: A := A J, W := W J
         const int k = e / kB, i = e % kB;
         const int p = pp[k], q = qq[k];
         const double c = cs[k], s = sn[k];
@@ -224,29 +227,21 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(double* __restrict__ T, do
         w[i][q] = s * wp + c * wq;
       }
       __syncthreads();
-      if (threadIdx.x == 0) {  // rotate the ring (element 0 fixed)
-        const int last = ring[kB - 1];
-        for (int i = kB - 1; i > 1; --i) ring[i] = ring[i - 1];
-        ring[1] = last;
-      }
-      __syncthreads();
     }
-    // convergence: off-diagonal Frobenius norm relative to the diagonal
-    if (threadIdx.x == 0) { off_s = 0.0; dia_s = 0.0; }
-    __syncthreads();
     double off = 0.0, dia = 0.0;
     for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
       const int i = e / kB, j = e % kB;
-      if (i != j) off += a[i][j] * a[i][j];
-      else dia += a[i][j] * a[i][j];
+      const double v = a[i][j] * a[i][j];
+      if (i != j) off += v; else dia += v;
     }
     off = warp_sum(off);
     dia = warp_sum(dia);
-    if (lane_id() == 0) { atomicAdd(&off_s, off); atomicAdd(&dia_s, dia); }
+    if (lane_id() == 0) { red[0][warp_id()] = off; red[1][warp_id()] = dia; }
     __syncthreads();
-    const bool conv = off_s <= 1e-30 * dia_s;
+    double o = 0.0, d = 0.0;
+    for (int w2 = 0; w2 < kJacThreads / 32; ++w2) { o += red[0][w2]; d += red[1][w2]; }
     __syncthreads();
-    if (conv) break;
+    if (o <= 1e-26 * d) break;
   }
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
     T[e] = a[e / kB][e % kB];
@@ -383,7 +378,7 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   auto orth = [&](double*& M) -> int {
     for (int rep = 0; rep < 2; ++rep) {  // CholQR2: M := M R^{-1}
       SCB_TRY(dgemm(kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s, splitk));
-      chol_kernel<<<1, 1024, kSmemKB, s>>>(S, fail);
+      chol_kernel<<<1, 256, kSmemKB, s>>>(S, fail);
       SCB_LAUNCH_CHECK();
       triinv_kernel<<<1, kB, 2 * kSmemKB, s>>>(S, Rinv);
       SCB_LAUNCH_CHECK();
@@ -393,7 +388,7 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     return SCB_OK;
   };
   SCB_TRY(orth(Q));
-  const int kPower = 2, kMaxOuter = 100;
+  const int kPower = 3, kMaxOuter = 60;
   double host_res[kB];
   int outer = 0;
   const bool verbose = getenv("SCB_EIG_VERBOSE") != nullptr;
@@ -409,10 +404,11 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
       std::swap(Q, Y);
     }
     SCB_TRY(orth(Q));
+    if (outer % 2 == 0 && outer + 1 < kMaxOuter) continue;  // Rayleigh-Ritz every other outer step
     // Rayleigh-Ritz: T = Q^T Cov Q, T = W diag W^T; rotate Q := Q W (sorted descending)
     SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, 3));        // Y = Cov Q
     SCB_TRY(dgemm(kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s, splitk));   // T = Q^T Y
-    jacobi_kernel<<<1, 1024, 2 * kSmemKB, s>>>(S, W, 30);
+    jacobi_kernel<<<1, kJacThreads, 2 * kSmemKB, s>>>(S, W, 30);
     SCB_LAUNCH_CHECK();
     select_kernel<<<1, kB, 0, s>>>(S, kB, order, lam_all);
     SCB_LAUNCH_CHECK();

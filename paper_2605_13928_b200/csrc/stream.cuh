@@ -1,0 +1,75 @@
+// Warp-per-row streaming of CSR rows with 16-byte vector loads.
+//
+// A warp walks the row [b, e) in windows of 128 elements: lane l owns the 4 consecutive
+// elements at base + 128*u + 4*l (u < U windows in flight), loaded with one 16-byte
+// ld.global.nc per array, so every warp keeps U x 1 KB of index+value bytes in flight.
+// Elements outside [b, e) are masked (the vector start is rounded down to a multiple of 4;
+// the arrays must be 16-byte aligned).  The tail vector that would cross the end of the
+// arrays is read with scalar loads.
+#pragma once
+#include "common.cuh"
+
+namespace scb {
+
+__device__ __forceinline__ int4 ld_nc_v4(const int* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 ld_nc_v4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+struct Quad {
+  int64_t p;   // position of element 0
+  int g[4];    // column indices
+  float x[4];  // values (0 when no value array)
+  unsigned valid;  // bit k: element p+k inside [b, e)
+};
+
+template <int U, typename F>
+__device__ __forceinline__ void stream_row(const int* __restrict__ idx, const float* __restrict__ val, int64_t b,
+                                           int64_t e, int64_t nnz, F&& f) {
+  const int lane = lane_id();
+  for (int64_t base = b & ~int64_t(3); base < e; base += 128 * U) {
+    Quad q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = base + 128 * u + 4 * lane;
+      q[u].p = p;
+      q[u].valid = 0;
+      if (p < e) {
+        if (p + 4 <= nnz) {
+          const int4 iv = ld_nc_v4(idx + p);
+          q[u].g[0] = iv.x; q[u].g[1] = iv.y; q[u].g[2] = iv.z; q[u].g[3] = iv.w;
+          if (val) {
+            const float4 dv = ld_nc_v4(val + p);
+            q[u].x[0] = dv.x; q[u].x[1] = dv.y; q[u].x[2] = dv.z; q[u].x[3] = dv.w;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            q[u].g[k] = (p + k < nnz) ? idx[p + k] : 0;
+            if (val) q[u].x[k] = (p + k < nnz) ? val[p + k] : 0.0f;
+          }
+        }
+        if (!val) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) q[u].x[k] = 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[u].valid |= (p + k >= b && p + k < e) ? (1u << k) : 0u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) f(q[u]);
+  }
+}
+
+}  // namespace scb

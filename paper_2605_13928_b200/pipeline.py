@@ -96,7 +96,7 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
 
     # ------------------------------------------------------------------ qc
     tm.step("qc")
-    qc = pp.calculate_qc_metrics(X, mt_mask)
+    qc = pp.calculate_qc_metrics(X, mt_mask, row_splits=True)
     if comm is not None:
         comm.allreduce_(qc["n_cells_by_counts"])
         comm.allreduce_(qc["gene_total_counts"])
@@ -107,7 +107,8 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
     tm.step("norm_hvg")
     X_log, remap, row_scale_orig = pp.subset_normalize(X, cm, gm, (nk_local, gk), p.target_sum)
     # HVG statistics of the normalized counts straight from the raw matrix (remapped genes)
-    sums = pp.hvg_gene_sums(X, counts=X.data, row_scale=row_scale_orig, gene_remap=remap, n_out=gk)
+    sums = pp.hvg_gene_sums(X, counts=X.data, row_scale=row_scale_orig, gene_remap=remap, n_out=gk,
+                            row_splits=qc["hvg_row_splits"])
     if comm is not None:
         comm.allreduce_(sums)
     hvg_mask, hvg_index, st = pp.hvg_select(sums, n_total, p.n_top_genes, p.n_bins)

@@ -70,8 +70,11 @@ class DeviceCSR:
 
 
 # ----------------------------------------------------------------------------- qc
-def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor):
-    """sc.pp.calculate_qc_metrics(qc_vars=['mt'], percent_top=None, log1p=False)."""
+def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor, row_splits: bool = False):
+    """sc.pp.calculate_qc_metrics(qc_vars=['mt'], percent_top=None, log1p=False).
+
+    With ``row_splits`` the result also holds ``hvg_row_splits`` (per-row gene-tile split
+    counts that let the HVG column pass read every nonzero exactly once)."""
     dev = X.device
     N, G = X.n_rows, X.n_cols
     out = dict(
@@ -83,10 +86,16 @@ def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor):
         gene_total_counts=torch.empty(G, dtype=torch.float64, device=dev),
     )
     mt = mt_mask.to(device=dev, dtype=torch.uint8).contiguous()
+    splits = None
+    if row_splits:
+        T = int(_lib.call("scb_hvg_tiles", G))
+        if T > 1:
+            splits = torch.empty((N, T - 1), dtype=torch.int32, device=dev)
     _lib.call("scb_qc_metrics", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), N, G, _p(mt),
               _p(out["n_genes_by_counts"]), _p(out["total_counts"]), _p(out["total_counts_mt"]),
               _p(out["pct_counts_mt"]), _p(out["n_cells_by_counts"]), _p(out["gene_total_counts"]),
-              _stream(dev))
+              _p(splits), _stream(dev))
+    out["hvg_row_splits"] = splits
     return out
 
 
@@ -166,7 +175,8 @@ def normalize_log1p(X: DeviceCSR, target_sum: float = 1e4) -> DeviceCSR:
     return DeviceCSR(X.indptr, X.indices, out, X.n_cols, counts=X.data, row_scale=scale)
 
 
-def hvg_gene_sums(X: DeviceCSR, counts=None, row_scale=None, gene_remap=None, n_out=None, sums=None):
+def hvg_gene_sums(X: DeviceCSR, counts=None, row_scale=None, gene_remap=None, n_out=None, sums=None,
+                  row_splits=None):
     """Fixed-point per-gene sums of the normalized counts (u64[2][2][G]); additive across shards."""
     counts = X.counts if counts is None else counts
     row_scale = X.row_scale if row_scale is None else row_scale
@@ -176,7 +186,7 @@ def hvg_gene_sums(X: DeviceCSR, counts=None, row_scale=None, gene_remap=None, n_
     if sums is None:
         sums = torch.zeros((2, 2, n_out), dtype=torch.int64, device=X.device)
     _lib.call("scb_hvg_gene_sums", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(counts), _p(row_scale),
-              X.n_rows, X.n_cols, _p(gene_remap), n_out, _p(sums), _stream(X.device))
+              X.n_rows, X.n_cols, _p(gene_remap), n_out, _p(row_splits), _p(sums), _stream(X.device))
     return sums
 
 
