@@ -29,10 +29,10 @@ constexpr int kBuckets = 1 << 16; // PC1 counting-sort buckets
 
 template <int KC>
 struct KnnCfg {
-  static constexpr int BM = 128, BN = 128, STAGES = 6;
+  static constexpr int BM = 128, BN = 128, STAGES = 6, NBUF = 2;  // TMEM ring: 2 bufs x 2 qtiles x 128 = 512 cols
   static constexpr int TILE = BM * kD * 2;              // 16 KB: 128 rows x 64 fp16
   static constexpr int A_BYTES = 2 * TILE;              // 2 query tiles
-  static constexpr int B_BYTES = TILE;                  // 128 keys
+  static constexpr int B_BYTES = BN * kD * 2;           // 128 keys (16 KB)
   static constexpr int SPILL = 8 * 32 * 32 * 4;         // per-epilogue-warp chunk staging
   static constexpr int SMEM = A_BYTES + STAGES * B_BYTES + SPILL + 1024 + 256;
   // kind::f16: c_format F32 (1) [4,6), a/b format F16 (0), K-major, N>>3 [17,23), M>>4 [24,29)
@@ -233,6 +233,7 @@ __device__ __forceinline__ void list_insert(float (&L)[KC], int (&I)[KC], float 
 }
 
 constexpr int kQ = 4;  // per-lane pending queue in front of the sorted list
+__device__ unsigned long long g_knn_stats[4];  // debug counters (dbg_mode 3)
 
 // merge the pending queue into the sorted list (executed by the whole warp at once, so the
 // O(KC) insertions of different lanes share the same issue slots)
@@ -274,8 +275,8 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   uint64_t* b_full = bar + 2;
   uint64_t* b_empty = b_full + C::STAGES;
   uint64_t* t_full = b_empty + C::STAGES;   // [buf][qtile]
-  uint64_t* t_empty = t_full + 4;           // [buf][qtile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 4);
+  uint64_t* t_empty = t_full + 2 * C::NBUF; // [buf][qtile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2 * C::NBUF);
 
   const int warp = warp_id(), lane = lane_id();
   const int n_pairs = (int)((n_q + 2 * C::BM - 1) / (2 * C::BM));
@@ -292,7 +293,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         tc::mbar_init(&b_full[s], 1);
         tc::mbar_init(&b_empty[s], 1);
       }
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < 2 * C::NBUF; ++b) {
         tc::mbar_init(&t_full[b], 1);
         tc::mbar_init(&t_empty[b], 4);
       }
@@ -332,15 +333,15 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         tc::mbar_wait(a_full, pc & 1);
         for (int i = 0; i < n_kt; ++i, ++it) {
           const int s = it % C::STAGES;
-          const int buf = it & 1;
+          const int buf = it % C::NBUF;
           tc::mbar_wait(&b_full[s], (it / C::STAGES) & 1);
           const uint32_t bb = tc::smem_u32(b_base + s * C::B_BYTES);
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
-            tc::mbar_wait(&t_empty[buf * 2 + t], ((it >> 1) & 1) ^ 1);
+            tc::mbar_wait(&t_empty[buf * 2 + t], ((it / C::NBUF) & 1) ^ 1);
             tc::tc_fence_after();
             const uint32_t ab = tc::smem_u32(a_base + t * C::TILE);
-            const uint32_t d = tmem + buf * 256 + t * 128;
+            const uint32_t d = tmem + buf * (2 * C::BN) + t * C::BN;
 #pragma unroll
             for (int kk = 0; kk < kD / 16; ++kk)  // K = 16 fp16 = 32 bytes per MMA
               mma_f16(d, tc::smem_desc_sw128(ab + kk * 32, 16, 1024), tc::smem_desc_sw128(bb + kk * 32, 16, 1024),
@@ -378,8 +379,8 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       for (int i = 0; i < n_seq; ++i) {
         const int kt = outward_tile(st, i, n_kt);
         if (kt < 0) continue;
-        const int buf = it & 1;
-        tc::mbar_wait(&t_full[buf * 2 + t], (it >> 1) & 1);
+        const int buf = it % C::NBUF;
+        tc::mbar_wait(&t_full[buf * 2 + t], (it / C::NBUF) & 1);
         tc::tc_fence_after();
         const int key0 = kt * C::BN;
         const bool tail = key0 + C::BN > n_k;
@@ -394,7 +395,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         for (int c2 = 0; c2 < C::BN / 64; ++c2) {
           // two 32-column TMEM loads in flight per wait (hides the tcgen05.ld latency)
           uint32_t r0[32], r1[32];
-          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + buf * 256 + t * 128 + c2 * 64;
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + buf * (2 * C::BN) + t * C::BN + c2 * 64;
           tc::tmem_ld32(ta, r0);
           tc::tmem_ld32(ta + 32, r1);
           tc::tmem_ld_wait();
@@ -417,7 +418,9 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
                 if (key0 + c * 32 + j >= n_k) v[j] = INFINITY;
             }
             const float m = min32(v);
+            if (dbg_mode == 3 && lane == 0) atomicAdd(&g_knn_stats[0], 1ull);
             if (__any_sync(0xffffffffu, m < L[KC - 1])) {
+              if (dbg_mode == 3 && lane == 0) atomicAdd(&g_knn_stats[1], 1ull);
               // rare path: bitmask of this lane's passing scores, staged chunk (transposed,
               // conflict-free) and a loop over set bits; passing scores go to the lane's small
               // queue, and a full queue on ANY lane merges every lane's queue at once.
@@ -431,7 +434,11 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
               }
               __syncwarp();
               while (__any_sync(0xffffffffu, mask != 0)) {
-                if (__any_sync(0xffffffffu, qn == kQ)) queue_merge<KC>(L, I, Qv, Qi, qn);
+                if (__any_sync(0xffffffffu, qn == kQ)) {
+                  if (dbg_mode == 3 && lane == 0) atomicAdd(&g_knn_stats[3], 1ull);
+                  queue_merge<KC>(L, I, Qv, Qi, qn);
+                }
+                if (dbg_mode == 3 && lane == 0) atomicAdd(&g_knn_stats[2], 1ull);
                 if (mask) {
                   const int j = __ffs(mask) - 1;
                   mask &= mask - 1;
@@ -628,6 +635,15 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
                                                                                  dbg ? atoi(dbg) : 0);
   SCB_LAUNCH_CHECK();
   if (ev1) SCB_CUDA(cudaEventRecord(ev1, s));
+  if (dbg && atoi(dbg) == 3) {
+    unsigned long long st[4];
+    SCB_CUDA(cudaMemcpyFromSymbolAsync(st, g_knn_stats, sizeof(st), 0, cudaMemcpyDeviceToHost, s));
+    SCB_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "[knn stats] warp-chunks %llu slow %llu (%.2f%%) bit-iterations %llu merges %llu\n", st[0], st[1],
+            100.0 * st[1] / (double)(st[0] ? st[0] : 1), st[2], st[3]);
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    SCB_CUDA(cudaMemcpyToSymbolAsync(g_knn_stats, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
+  }
   knn_rerank_kernel<KC><<<ceil_div(n_q, 8), 256, 0, s>>>(Qx, Kx, n_q, d, ld, perm_q, perm_k, cand, k, out_i, out_d);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
