@@ -1,0 +1,218 @@
+"""CPU tests of the oracle (oracle/): hand known-answer tests, the committed golden fixtures,
+and cross-checks against independent restatements (scipy.sparse, pandas -- the library Scanpy's
+seurat-flavour HVG code is written in --, sklearn PCA / NearestNeighbors).  No GPU needed."""
+import numpy as np
+import pandas as pd
+import pytest
+import scipy.sparse as sp
+
+from oracle import pipeline as op
+from oracle.synth import SynthSpec, generate_csr, mt_mask
+from tests.golden import make_golden as mg
+
+GOLDEN = "tests/golden/g600x300.npz"
+
+
+# ----------------------------------------------------------------------------- known answers
+def micro():
+    # 4 cells x 5 genes, gene 0 mitochondrial; row 1 has an explicit zero, row 2 is empty
+    indptr = np.array([0, 3, 5, 5, 10], dtype=np.int64)
+    indices = np.array([0, 2, 3, 1, 4, 0, 1, 2, 3, 4], dtype=np.int32)
+    data = np.array([1, 2, 3, 5, 0, 1, 1, 1, 1, 6], dtype=np.float32)
+    return op.CSR(indptr, indices, data, 5), np.array([1, 0, 0, 0, 0], dtype=np.uint8)
+
+
+def test_qc_known_answers():
+    X, mt = micro()
+    q = op.qc_metrics(X, mt)
+    np.testing.assert_array_equal(q["n_genes_by_counts"], [3, 1, 0, 5])
+    np.testing.assert_array_equal(q["total_counts"], [6, 5, 0, 10])
+    np.testing.assert_array_equal(q["total_counts_mt"], [1, 0, 0, 1])
+    np.testing.assert_allclose(q["pct_counts_mt"][[0, 1, 3]], [100 / 6, 0, 10])
+    assert np.isnan(q["pct_counts_mt"][2])
+    np.testing.assert_array_equal(q["n_cells_by_counts"], [2, 2, 2, 2, 1])
+    np.testing.assert_array_equal(q["gene_total_counts"], [2, 6, 3, 4, 6])
+
+
+def test_filter_and_subset_known_answers():
+    X, mt = micro()
+    q = op.qc_metrics(X, mt)
+    cm, gm = op.filter_masks(q, op.Params(min_genes=1, max_genes=None, max_pct_mt=20.0, min_cells=2))
+    np.testing.assert_array_equal(cm, [1, 1, 0, 1])        # row 2 empty (NaN pct fails)
+    np.testing.assert_array_equal(gm, [1, 1, 1, 1, 0])     # gene 4 in one cell only
+    S = op.subset(X, cm, gm)
+    np.testing.assert_array_equal(S.indptr, [0, 3, 4, 8])
+    np.testing.assert_array_equal(S.indices, [0, 2, 3, 1, 0, 1, 2, 3])
+    np.testing.assert_array_equal(S.data, [1, 2, 3, 5, 1, 1, 1, 1])
+    assert S.n_cols == 4
+
+
+def test_filter_mask_max_genes():
+    X, mt = micro()
+    q = op.qc_metrics(X, mt)
+    cm, _ = op.filter_masks(q, op.Params(min_genes=1, max_genes=4, max_pct_mt=50.0, min_cells=2))
+    # row0: 3 genes, 16.7% mt -> kept; row1 kept; row2 empty; row3 has 5 genes > 4
+    np.testing.assert_array_equal(cm, [1, 1, 0, 0])
+
+
+def test_normalize_log1p_known_answers():
+    X, mt = micro()
+    Xl, y32, s = op.normalize_log1p(X, target_sum=10.0)
+    np.testing.assert_array_equal(s, np.array([10 / 6, 10 / 5, 1.0, 1.0], dtype=np.float32))
+    np.testing.assert_array_equal(y32[:3], (np.array([1, 2, 3], np.float32) * np.float32(10 / 6)))
+    np.testing.assert_allclose(Xl.data[:3], np.log1p(np.array([1, 2, 3]) * 10 / 6), rtol=1e-6)
+    assert Xl.data[4] == 0.0  # explicit zero stays zero
+
+
+def test_fixed_point_sums_match_float64():
+    rng = np.random.default_rng(0)
+    idx = rng.integers(0, 50, 20000).astype(np.int32)
+    v = (rng.integers(1, 30, 20000) * rng.uniform(0.1, 5, 20000)).astype(np.float32)
+    s1, s2 = op.fx_gene_sums(idx, v, 50)
+    r1, r2 = op.gene_sums(idx, v.astype(np.float64), 50)
+    np.testing.assert_allclose(s1, r1, rtol=1e-12)
+    np.testing.assert_allclose(s2, r2, rtol=1e-9)
+    # order independence: any permutation gives the identical (integer) result
+    perm = rng.permutation(len(idx))
+    t1, t2 = op.fx_gene_sums(idx[perm], v[perm], 50)
+    np.testing.assert_array_equal(s1, t1)
+    np.testing.assert_array_equal(s2, t2)
+
+
+def test_scale_constant_gene_std_one():
+    # a gene with the same log value in every cell (incl. zeros?) -> std 0 -> 1, z = l - mean
+    indptr = np.array([0, 2, 4, 6], np.int64)
+    indices = np.array([0, 1, 0, 1, 0, 1], np.int32)
+    data = np.array([2.0, 1.0, 2.0, 3.0, 2.0, 5.0], np.float32)
+    X = op.CSR(indptr, indices, data, 2)
+    Z, mean, inv = op.scale(X, np.array([1, 1], np.uint8), max_value=10.0)
+    assert inv[0] == 1.0
+    np.testing.assert_allclose(Z[:, 0], 0.0, atol=1e-6)
+
+
+def test_scale_clip_upper_only():
+    rng = np.random.default_rng(1)
+    n = 400
+    rows = np.arange(n)
+    data = np.zeros(n, np.float32)
+    data[0] = 50.0   # one huge outlier, everything else zero -> z0 slightly negative, outlier clipped to 10
+    X = op.CSR(np.arange(n + 1, dtype=np.int64), np.zeros(n, np.int32), np.maximum(data, 1e-3).astype(np.float32), 1)
+    Z, _, _ = op.scale(X, np.array([1], np.uint8), max_value=10.0)
+    assert Z.max() == 10.0 and Z.min() > -10.0
+    del rows, rng
+
+
+# ----------------------------------------------------------------------------- golden fixtures
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(GOLDEN)
+
+
+def test_generator_reproduces_golden_input(golden):
+    ip, ix, d = generate_csr(mg.SPEC)
+    np.testing.assert_array_equal(ip, golden["indptr"])
+    np.testing.assert_array_equal(ix, golden["indices"])
+    np.testing.assert_array_equal(d, golden["data"])
+
+
+def test_generator_chunking_independent():
+    spec = SynthSpec(300, 120, seed=3)
+    a = generate_csr(spec, chunk_cells=64)
+    b = generate_csr(spec, chunk_cells=1000)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_oracle_reproduces_golden(golden):
+    out = mg.compute()
+    for k in golden.files:
+        a, b = out[k], golden[k]
+        if a.dtype.kind in "iub":
+            np.testing.assert_array_equal(a, b, err_msg=k)
+        else:
+            np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-12, equal_nan=True, err_msg=k)
+
+
+# ----------------------------------------------------------------------------- cross-checks
+def _sp(X):
+    return sp.csr_matrix((X.data.astype(np.float64), X.indices, X.indptr), shape=(X.n_rows, X.n_cols))
+
+
+def test_qc_vs_scipy(golden):
+    X = op.CSR(golden["indptr"], golden["indices"], golden["data"], 300)
+    q = op.qc_metrics(X, golden["mt_mask"])
+    A = _sp(X)
+    np.testing.assert_array_equal(q["total_counts"], np.asarray(A.sum(1)).ravel())
+    np.testing.assert_array_equal(q["gene_total_counts"], np.asarray(A.sum(0)).ravel())
+    np.testing.assert_array_equal(q["n_genes_by_counts"], np.asarray((A > 0).sum(1)).ravel())
+    np.testing.assert_array_equal(q["n_cells_by_counts"], np.asarray((A > 0).sum(0)).ravel())
+
+
+def scanpy_seurat_pandas(mean, var, n_top, n_bins=20):
+    """Transcription of Scanpy's seurat-flavour normalised dispersion (pandas cut/groupby)."""
+    mean = mean.copy()
+    mean[mean == 0] = 1e-12
+    disp = var / mean
+    disp[disp == 0] = np.nan
+    disp = np.log(disp)
+    mean = np.log1p(mean)
+    df = pd.DataFrame({"means": mean, "dispersions": disp})
+    df["mean_bin"] = pd.cut(df["means"], bins=n_bins)
+    g = df.groupby("mean_bin", observed=False)["dispersions"]
+    bmean, bstd = g.mean(), g.std(ddof=1)
+    one = bstd.isnull()
+    bstd[one.values] = bmean[one.values].values
+    bmean[one.values] = 0
+    dn = (df["dispersions"].values - bmean[df["mean_bin"]].values) / bstd[df["mean_bin"]].values
+    srt = np.sort(dn[~np.isnan(dn)])[::-1]
+    cut = srt[n_top - 1]
+    return np.nan_to_num(dn) >= cut, dn
+
+
+def test_hvg_vs_pandas_scanpy_transcription(golden):
+    sub = op.CSR(golden["sub_indptr"], golden["sub_indices"], golden["sub_data"], int(golden["gene_mask"].sum()))
+    Xl, y32, _ = op.normalize_log1p(sub, 1e4)
+    s1, s2 = op.fx_gene_sums(Xl.indices, y32, Xl.n_cols)
+    mean, var = op.mean_var(s1, s2, float(sub.n_rows))
+    sel_pd, dn_pd = scanpy_seurat_pandas(mean, var, 100)
+    mask, st = op.hvg_seurat_from_sums(s1, s2, sub.n_rows, 100)
+    np.testing.assert_allclose(st["dispersions_norm"], dn_pd, rtol=1e-10, atol=1e-12, equal_nan=True)
+    assert sel_pd.sum() == 100  # no ties at the cutoff here, so Scanpy's >= rule picks exactly n
+    np.testing.assert_array_equal(mask.astype(bool), sel_pd)
+
+
+def test_pandas_cut_edges_match_pandas():
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=1000)
+    e = op.pandas_cut_edges(float(x.min()), float(x.max()), 20)
+    _, bins = pd.cut(x, 20, retbins=True)
+    np.testing.assert_array_equal(e, bins)
+
+
+def test_pca_vs_sklearn(golden):
+    from sklearn.decomposition import PCA
+    Z = golden["Z"].astype(np.float64)
+    k = golden["components"].shape[1]
+    skp = PCA(n_components=k, svd_solver="full").fit(Z)
+    assert op.subspace_angle(skp.components_.T, golden["components"]) < 1e-6  # arccos resolution ~1e-8
+    np.testing.assert_allclose(skp.explained_variance_, golden["variance"], rtol=1e-9)
+    np.testing.assert_allclose(skp.explained_variance_ratio_, golden["variance_ratio"], rtol=1e-9)
+
+
+def test_knn_vs_sklearn(golden):
+    from sklearn.neighbors import NearestNeighbors
+    X = golden["X_pca"].astype(np.float64)
+    k = golden["knn_idx"].shape[1]
+    d, i = NearestNeighbors(n_neighbors=k, algorithm="brute").fit(X).kneighbors(X)
+    np.testing.assert_allclose(golden["knn_dist"], d, rtol=1e-5, atol=1e-5)
+    assert op.knn_recall(golden["knn_idx"], i) > 0.999
+    assert np.all(golden["knn_idx"][:, 0] == np.arange(len(X)))  # self first
+
+
+def test_knn_tie_order_by_index():
+    X = np.array([[0.0, 0.0], [1.0, 0.0], [-1.0, 0.0], [0.0, 1.0], [0.0, -1.0], [1.0, 0.0]])
+    i, d = op.knn(X, 6)
+    # all four unit-distance points (and the duplicate of point 1) tie: ascending index order
+    np.testing.assert_array_equal(i[0], [0, 1, 2, 3, 4, 5])
+    np.testing.assert_array_equal(i[1], [1, 5, 0, 3, 4, 2])
+    np.testing.assert_allclose(d[1][:2], [0.0, 0.0])
