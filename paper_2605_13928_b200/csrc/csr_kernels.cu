@@ -327,8 +327,21 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
         if (((q.valid >> k) & 1u) && gl >= 0 && gl < w && (!remap || remap[q.g[k]] >= 0)) {
           const float y = __fmul_rn(q.x[k], s);   // float32 normalized count
           const double yd = (double)y;
-          fx_add(&s1lo[gl], &s1hi[gl], fx_round(yd * 268435456.0));          // y * 2^28
-          fx_add(&s2lo[gl], &s2hi[gl], fx_round((yd * yd) * 16777216.0));     // y^2 * 2^24
+          // carry-free split: low 22 bits + high part; with <= 1024 rows per CTA neither u32
+          // word can overflow, so both adds are fire-and-forget (no returned value needed)
+          const uint64_t v1 = fx_round(yd * 268435456.0);        // y * 2^28   (< 2^42)
+          const uint64_t v2 = fx_round((yd * yd) * 16777216.0);   // y^2 * 2^24
+          atomicAdd(&s1lo[gl], (uint32_t)(v1 & 0x3FFFFFu));
+          atomicAdd(&s1hi[gl], (uint32_t)(v1 >> 22));
+          atomicAdd(&s2lo[gl], (uint32_t)(v2 & 0x3FFFFFu));
+          const uint64_t h2 = v2 >> 22;
+          if (h2 < (1ull << 21)) {
+            atomicAdd(&s2hi[gl], (uint32_t)h2);
+          } else {  // rare huge y^2 (y > ~724): straight into the global limbs
+            const int go = remap ? remap[q.g[k]] : q.g[k];
+            atomicAdd(&sums[2 * n_out + go], (unsigned long long)(h2 & 1023u) << 22);
+            atomicAdd(&sums[3 * n_out + go], (unsigned long long)(h2 >> 10));
+          }
         }
       }
     });
@@ -338,13 +351,16 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
   unsigned long long* l1 = sums + n_out;       // stat 0 limb 1
   unsigned long long* m0 = sums + 2 * n_out;   // stat 1 limb 0
   unsigned long long* m1 = sums + 3 * n_out;   // stat 1 limb 1
+  // words hold (lo, hi) with value lo + hi * 2^22 = lo + (hi mod 1024) * 2^22 + (hi / 1024) * 2^32
   for (int i = threadIdx.x; i < w; i += blockDim.x) {
     const int go = remap ? remap[g0 + i] : g0 + i;
     if (go < 0) continue;
-    if (s1lo[i]) atomicAdd(&l0[go], (unsigned long long)s1lo[i]);
-    if (s1hi[i]) atomicAdd(&l1[go], (unsigned long long)s1hi[i]);
-    if (s2lo[i]) atomicAdd(&m0[go], (unsigned long long)s2lo[i]);
-    if (s2hi[i]) atomicAdd(&m1[go], (unsigned long long)s2hi[i]);
+    const unsigned long long a0 = (unsigned long long)s1lo[i] + ((unsigned long long)(s1hi[i] & 1023u) << 22);
+    const unsigned long long b0 = (unsigned long long)s2lo[i] + ((unsigned long long)(s2hi[i] & 1023u) << 22);
+    if (a0) atomicAdd(&l0[go], a0);
+    if (s1hi[i] >> 10) atomicAdd(&l1[go], (unsigned long long)(s1hi[i] >> 10));
+    if (b0) atomicAdd(&m0[go], b0);
+    if (s2hi[i] >> 10) atomicAdd(&m1[go], (unsigned long long)(s2hi[i] >> 10));
   }
 }
 
@@ -840,8 +856,8 @@ extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int3
   const int n_tiles = scb_hvg_tiles(n_cols);
   const int tile_w = kHvgTileW;
   const size_t smem = (size_t)std::min(tile_w, n_cols) * 16;
-  // row blocks: keep per-CTA hi words far from overflow (<= 4096 rows) and give >= 2 waves
-  int64_t rows_per_block = std::max<int64_t>(64, std::min<int64_t>(4096, n_rows / (2 * ctx->num_sms) + 1));
+  // row blocks of <= 1024 rows: the 22-bit low words cannot overflow (1024 * 2^22 = 2^32)
+  int64_t rows_per_block = std::max<int64_t>(64, std::min<int64_t>(1024, n_rows / (2 * ctx->num_sms) + 1));
   const int64_t n_blocks = (n_rows + rows_per_block - 1) / rows_per_block;
   SCB_CUDA(cudaFuncSetAttribute(hvg_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kRowThreads, smem, (cudaStream_t)stream>>>(

@@ -171,6 +171,8 @@ __global__ void __launch_bounds__(kB) triinv_kernel(const double* __restrict__ R
 // i >= 1 = ((r+i) mod (kB-1), (r-i) mod (kB-1)): kB/2 disjoint pairs, every pair once per
 // sweep.  Sweeps stop when the off-diagonal Frobenius norm is <= 1e-13 of the diagonal's.
 constexpr int kJacThreads = 256;
+__device__ int g_jacobi_sweeps;  // debug: sweeps used by the last call
+
 __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict__ T, double* __restrict__ W, int sweeps) {
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
     double o = 0.0, d = 0.0;
     for (int w2 = 0; w2 < kJacThreads / 32; ++w2) { o += red[0][w2]; d += red[1][w2]; }
     __syncthreads();
+    if (threadIdx.x == 0) g_jacobi_sweeps = sw + 1;
     if (o <= 1e-26 * d) break;
   }
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
@@ -317,6 +320,14 @@ __global__ void gather_first_cols_kernel(const double* __restrict__ Q, int ld, i
   if (j < k) V[(size_t)i * k + j] = Q[(size_t)i * ld + j];
 }
 
+// Chebyshev three-term step: out = alpha * CY + beta * Y + gamma * Yold (element-wise)
+__global__ void cheb_combine_kernel(const double* __restrict__ CY, const double* __restrict__ Y,
+                                    const double* __restrict__ Yold, int64_t n, double alpha, double beta, double gamma,
+                                    double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = alpha * CY[i] + beta * Y[i] + (Yold ? gamma * Yold[i] : 0.0);
+}
+
 __global__ void fill_zero_rows(float* __restrict__ comp_t, int k, int kpad, int hp) {
   const int j = k + blockIdx.x;
   if (j < kpad)
@@ -374,9 +385,8 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   SCB_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
   const int splitk = std::max(1, std::min(16, h / 128));
   double* Rinv = S + kB * kB;  // scratch: W is only needed inside rayleigh_ritz
-  double* Q2 = CV;             // h x kB scratch (CV region sized h * n_comps <= h * kB? ensured below)
-  auto orth = [&](double*& M) -> int {
-    for (int rep = 0; rep < 2; ++rep) {  // CholQR2: M := M R^{-1}
+  auto orth = [&](double*& M, int reps) -> int {
+    for (int rep = 0; rep < reps; ++rep) {  // CholQR(reps): M := M R^{-1}
       SCB_TRY(dgemm(kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s, splitk));
       chol_kernel<<<1, 256, kSmemKB, s>>>(S, fail);
       SCB_LAUNCH_CHECK();
@@ -387,7 +397,7 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     }
     return SCB_OK;
   };
-  SCB_TRY(orth(Q));
+  SCB_TRY(orth(Q, 2));
   const int kPower = 3, kMaxOuter = 60;
   double host_res[kB];
   int outer = 0;
@@ -398,13 +408,35 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     cudaEventCreate(&ev1);
     cudaEventRecord(ev0, s);
   }
+  double cheb_b = 0.0;  // top of the damped interval [0, b] (smallest Ritz value of the block)
+  double* Yold = CV;      // h x kB scratch for the three-term recurrence (CV reused below)
   for (; outer < kMaxOuter; ++outer) {
-    for (int pw = 0; pw < kPower; ++pw) {
-      SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, 3));
-      std::swap(Q, Y);
+    if (cheb_b <= 0.0) {
+      // plain power steps until Ritz values are known
+      for (int pw = 0; pw < kPower; ++pw) {
+        SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, 3));
+        std::swap(Q, Y);
+      }
+    } else {
+      // Chebyshev filter T_kPower(sigma), sigma = (2/b) Cov - I: damps [0, b], amplifies > b
+      const int64_t nel = (int64_t)h * kB;
+      const int eb = (int)((nel + 255) / 256);
+      const double a2 = 2.0 / cheb_b;
+      // Y1 = sigma Q  -> stored in Y
+      SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, V, kB, s, 3));
+      cheb_combine_kernel<<<eb, 256, 0, s>>>(V, Q, nullptr, nel, a2, -1.0, 0.0, Y);
+      SCB_LAUNCH_CHECK();
+      std::swap(Q, Yold);  // Yold = Y0
+      for (int k = 1; k < kPower; ++k) {  // Y_{k+1} = 2 sigma Y_k - Y_{k-1}
+        SCB_TRY(dgemm(h, kB, h, cov, h, 0, Y, kB, 0, V, kB, s, 3));
+        cheb_combine_kernel<<<eb, 256, 0, s>>>(V, Y, Yold, nel, 2.0 * a2, -2.0, -1.0, Q);
+        SCB_LAUNCH_CHECK();
+        std::swap(Yold, Y);  // Yold = Y_k
+        std::swap(Y, Q);     // Y = Y_{k+1}
+      }
+      std::swap(Q, Y);  // Q = last iterate
     }
-    SCB_TRY(orth(Q));
-    if (outer % 2 == 0 && outer + 1 < kMaxOuter) continue;  // Rayleigh-Ritz every other outer step
+    SCB_TRY(orth(Q, 2));
     // Rayleigh-Ritz: T = Q^T Cov Q, T = W diag W^T; rotate Q := Q W (sorted descending)
     SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, 3));        // Y = Cov Q
     SCB_TRY(dgemm(kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s, splitk));   // T = Q^T Y
@@ -414,15 +446,17 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     SCB_LAUNCH_CHECK();
     gather_cols_kernel<<<kB, kB, 0, s>>>(W, order, kB, Wk);
     SCB_LAUNCH_CHECK();
-    SCB_TRY(dgemm(h, kB, kB, Q, kB, 0, Wk, kB, 0, Q2, kB, s));          // Ritz vectors
+    SCB_TRY(dgemm(h, kB, kB, Q, kB, 0, Wk, kB, 0, Yold, kB, s));        // Ritz vectors (spare buffer)
     SCB_TRY(dgemm(h, kB, kB, Y, kB, 0, Wk, kB, 0, V, kB, s));           // Cov * Ritz vectors
-    std::swap(Q, Q2);
+    std::swap(Q, Yold);
     residual_kernel<<<n_comps, 256, 0, s>>>(V, Q, lam_all, h, kB, res);
     SCB_LAUNCH_CHECK();
-    double lam0 = 0.0;
+    double lam0 = 0.0, lamb = 0.0;
     SCB_CUDA(cudaMemcpyAsync(host_res, res, sizeof(double) * n_comps, cudaMemcpyDeviceToHost, s));
     SCB_CUDA(cudaMemcpyAsync(&lam0, lam_all, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SCB_CUDA(cudaMemcpyAsync(&lamb, lam_all + kB - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
     SCB_CUDA(cudaStreamSynchronize(s));
+    cheb_b = std::max(lamb, 1e-12 * lam0);
     double worst = 0.0;
     for (int j = 0; j < n_comps; ++j) worst = std::max(worst, host_res[j]);
     if (verbose) {
@@ -430,7 +464,10 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
       cudaEventSynchronize(ev1);
       float ms = 0;
       cudaEventElapsedTime(&ms, ev0, ev1);
-      fprintf(stderr, "[scb_pca_eig] outer %d residual %.3e (lam0 %.4e) elapsed %.2f ms\n", outer + 1, worst, lam0, ms);
+      int sweeps = 0;
+      cudaMemcpyFromSymbol(&sweeps, g_jacobi_sweeps, sizeof(int));
+      fprintf(stderr, "[scb_pca_eig] outer %d residual %.3e (lam0 %.4e) jacobi sweeps %d elapsed %.2f ms\n", outer + 1,
+              worst, lam0, sweeps, ms);
     }
     if (worst <= 1e-9 * std::max(lam0, 1e-300)) break;
   }

@@ -19,10 +19,11 @@ constexpr int kGemmThreads = 192;  // warp0 TMA, warp1 MMA, warps 2..5 convert +
 template <int BN, int STAGES>
 struct GramCfg {
   static constexpr int BM = 128;
-  static constexpr int KB = 32;                       // cells per stage
+  static constexpr int KB = 16;                       // cells per stage (4-stage ring fits smem)
   static constexpr int A_BYTES = BM * KB * 4;         // 16 KB
   static constexpr int B_BYTES = BN * KB * 4;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BOX = KB * 128;                // one [KB cells x 32 genes] TMA box = MN chunk stride (LBO)
   static constexpr int SMEM = 2 * STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t IDESC = tc::idesc_tf32(BM, BN, true, true);
 };
@@ -81,9 +82,9 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
         const int k0 = (int)(k_begin + (int64_t)it * C::KB);
         tc::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
 #pragma unroll
-        for (int c = 0; c < C::BM / 32; ++c) tc::tma_load_2d(a + c * 4096, &tmap, &full[s], i0 + 32 * c, k0);
+        for (int c = 0; c < C::BM / 32; ++c) tc::tma_load_2d(a + c * C::BOX, &tmap, &full[s], i0 + 32 * c, k0);
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) tc::tma_load_2d(b + c * 4096, &tmap, &full[s], j0 + 32 * c, k0);
+        for (int c = 0; c < BN / 32; ++c) tc::tma_load_2d(b + c * C::BOX, &tmap, &full[s], j0 + 32 * c, k0);
       }
     }
   } else if (warp == 1) {
@@ -101,10 +102,10 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
         for (int k = 0; k < C::KB / 8; ++k) {
           // MN-major TF32: 128B_BASE32B layout, 4-cell atoms (SBO 512), 32-gene chunks 4 KB apart
           const uint32_t off = k * 1024;  // next 8 cells
-          const uint64_t dah = tc::smem_desc_sw128_b32(ah + off, 4096, 512);
-          const uint64_t dbh = tc::smem_desc_sw128_b32(bh + off, 4096, 512);
-          const uint64_t dal = tc::smem_desc_sw128_b32(al + off, 4096, 512);
-          const uint64_t dbl = tc::smem_desc_sw128_b32(bl + off, 4096, 512);
+          const uint64_t dah = tc::smem_desc_sw128_b32(ah + off, C::BOX, 512);
+          const uint64_t dbh = tc::smem_desc_sw128_b32(bh + off, C::BOX, 512);
+          const uint64_t dal = tc::smem_desc_sw128_b32(al + off, C::BOX, 512);
+          const uint64_t dbl = tc::smem_desc_sw128_b32(bl + off, C::BOX, 512);
           const uint32_t acc0 = (it > 0 || k > 0) ? 1u : 0u;
           tc::mma_tf32(tmem, dah, dbh, C::IDESC, acc0);
           tc::mma_tf32(tmem, dah, dbl, C::IDESC, 1u);
@@ -179,7 +180,7 @@ template <int BN, int STAGES>
 static int launch_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int hp, double* C, cudaStream_t s) {
   using Cfg = GramCfg<BN, STAGES>;
   CUtensorMap tmap;
-  SCB_TRY(make_tmap_2d_f32(&tmap, Z, (uint64_t)std::max<int64_t>(n_rows, 1), hp, hp, 32, 32, /*atom32=*/true));
+  SCB_TRY(make_tmap_2d_f32(&tmap, Z, (uint64_t)std::max<int64_t>(n_rows, 1), hp, hp, 32, Cfg::KB, /*atom32=*/true));
   // upper-triangle tile list
   std::vector<int2> tl;
   for (int bi = 0; bi < hp / Cfg::BM; ++bi)
@@ -218,6 +219,6 @@ extern "C" int scb_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp
   SCB_REQUIRE(hp > 0 && hp % 128 == 0, SCB_ERR_ARG, "scb_gram: hp must be a multiple of 128");
   SCB_REQUIRE(n_rows >= 0 && n_rows < (1ll << 31), SCB_ERR_ARG, "scb_gram: n_rows out of range");
   cudaStream_t s = (cudaStream_t)stream;
-  if (hp % 256 == 0) return launch_gram<256, 2>(ctx, Z, n_rows, hp, C, s);
-  return launch_gram<128, 3>(ctx, Z, n_rows, hp, C, s);
+  if (hp % 256 == 0) return launch_gram<256, 4>(ctx, Z, n_rows, hp, C, s);
+  return launch_gram<128, 6>(ctx, Z, n_rows, hp, C, s);
 }
