@@ -10,11 +10,18 @@
 //    with s = max|X|/16 so everything fits FP16; one K=64 dot product gives the
 //    query-invariant score (d^2 - |q|^2)/s^2 with the 11-bit significands of TF32.
 // 3. candidates (tcgen05.mma.kind::f16, FP32 accumulate in TMEM): a persistent CTA owns a
-//    PAIR of 128-query tiles (smem-resident) and streams 128-key tiles through a 6-stage
-//    TMA pipeline; one thread issues 2 x 4 MMAs (128x128x16) per key tile into a double-
-//    buffered accumulator (512 TMEM columns).  Eight epilogue warps own one query row each
-//    and keep a register-resident sorted top-KC list behind a 32-wide min filter.
-// 4. rerank: one warp per query recomputes exact FP32 squared distances of the KC
+//    PAIR of 128-query tiles (smem-resident) and streams 128-key tiles through an 8-stage TMA
+//    pipeline.  Two MMA-issuing threads alternate key tiles (a tcgen05.commit stalls its
+//    issuer until the pipe drains, so one issuer leaves the tensor pipe idle ~45% of the
+//    time); each issues 2 x 4 MMAs (128x128x16) per key tile into its own half of a
+//    double-buffered accumulator (512 TMEM columns).  Epilogue warps own one query row per
+//    lane and COLS = 128/HALVES key columns of every tile, keep a register-resident sorted
+//    top-KC list behind a 32-wide min filter, and re-read the few passing columns straight
+//    from TMEM (tcgen05.ld x1) instead of staging scores through shared memory.  With
+//    HALVES = 2 (k_cand 32) sixteen epilogue warps, four per SM sub-partition, hide the
+//    TMEM-load and vote latencies; the two half-lists of a row are concatenated (the top-k
+//    of the union is contained in the union of the per-half top-KC for k <= KC).
+// 4. rerank: one warp per query recomputes exact FP32 squared distances of the k_cand
 //    candidates, sorts by (distance, original index) and keeps k (self included).
 #include <cstdlib>
 #include <vector>
@@ -23,20 +30,25 @@
 
 namespace scb {
 
-constexpr int kKnnThreads = 320;  // warp0 TMA, warp1 MMA, warps 2..9 epilogue
 constexpr int kD = 64;            // padded augmented width (one 128-byte FP16 row)
 constexpr int kBuckets = 1 << 16; // PC1 counting-sort buckets
 
-template <int KC>
+// KC = per-warp list length, HALVES = epilogue warps per (query tile, TMEM lane quarter)
+template <int KC, int HALVES>
 struct KnnCfg {
-  static constexpr int BM = 128, BN = 128, STAGES = 6, NBUF = 2;  // TMEM ring: 2 bufs x 2 qtiles x 128 = 512 cols
+  static constexpr int BM = 128, BN = 128, STAGES = 8, NBUF = 2;  // TMEM: 2 bufs x 2 qtiles x 128 = 512 cols
   static constexpr int TILE = BM * kD * 2;              // 16 KB: 128 rows x 64 fp16
   static constexpr int A_BYTES = 2 * TILE;              // 2 query tiles
   static constexpr int B_BYTES = BN * kD * 2;           // 128 keys (16 KB)
-  static constexpr int SPILL = 8 * 32 * 32 * 4;         // per-epilogue-warp chunk staging
-  static constexpr int SMEM = A_BYTES + STAGES * B_BYTES + SPILL + 1024 + 256;
+  static constexpr int COLS = BN / HALVES;              // key columns per epilogue warp per tile
+  static constexpr int KCT = KC * HALVES;               // candidates per query row (k_cand)
+  static constexpr int EPI_WARPS = 8 * HALVES;
+  static constexpr int THREADS = 32 * (3 + EPI_WARPS);  // warp0 TMA, warps 1-2 MMA, then epilogue
+  static constexpr int SMEM = A_BYTES + STAGES * B_BYTES + 1024 + 256;
   // kind::f16: c_format F32 (1) [4,6), a/b format F16 (0), K-major, N>>3 [17,23), M>>4 [24,29)
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  static_assert(NBUF == 2 && STAGES % 2 == 0, "MMA issuer p owns units of parity p: buffer p, even/odd stages");
+  static_assert(COLS % 32 == 0, "epilogue chunks are 32 columns");
 };
 
 __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
@@ -233,7 +245,6 @@ __device__ __forceinline__ void list_insert(float (&L)[KC], int (&I)[KC], float 
 }
 
 constexpr int kQ = 4;  // per-lane pending queue in front of the sorted list
-__device__ unsigned long long g_knn_stats[4];  // debug counters (dbg_mode 3)
 
 // merge the pending queue into the sorted list (executed by the whole warp at once, so the
 // O(KC) insertions of different lanes share the same issue slots)
@@ -258,18 +269,22 @@ __device__ __forceinline__ float min32(const float (&v)[32]) {
   return fminf(fminf(b0, b1), fminf(b2, b3));
 }
 
-template <int KC>
-__global__ void __launch_bounds__(kKnnThreads, 1)
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  return r;
+}
+
+template <int KC, int HALVES>
+__global__ void __launch_bounds__(KnnCfg<KC, HALVES>::THREADS, 1)
 knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, int64_t n_q,
-                      int64_t n_k, const int* __restrict__ start_tile, int* __restrict__ cand, int dbg_mode) {
-  using C = KnnCfg<KC>;
+                      int64_t n_k, const int* __restrict__ start_tile, int* __restrict__ cand) {
+  using C = KnnCfg<KC, HALVES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* a_base = smem;                          // [qtile][128 rows x 128 B]
   uint8_t* b_base = smem + C::A_BYTES;             // [stage][128 rows x 128 B]
-  // staging buffer addressed from the __shared__ symbol itself (keeps LDS/STS, not generic LD)
-  float* spill = reinterpret_cast<float*>(smem_raw + ((smem - smem_raw) + C::A_BYTES + C::STAGES * C::B_BYTES));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(b_base + C::STAGES * C::B_BYTES + C::SPILL);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(b_base + C::STAGES * C::B_BYTES);
   uint64_t* a_full = bar;
   uint64_t* a_empty = bar + 1;
   uint64_t* b_full = bar + 2;
@@ -288,14 +303,14 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       tc::tma_prefetch(&tq);
       tc::tma_prefetch(&tk);
       tc::mbar_init(a_full, 1);
-      tc::mbar_init(a_empty, 1);
+      tc::mbar_init(a_empty, 2);  // one commit per MMA issuer
       for (int s = 0; s < C::STAGES; ++s) {
         tc::mbar_init(&b_full[s], 1);
         tc::mbar_init(&b_empty[s], 1);
       }
       for (int b = 0; b < 2 * C::NBUF; ++b) {
         tc::mbar_init(&t_full[b], 1);
-        tc::mbar_init(&t_empty[b], 4);
+        tc::mbar_init(&t_empty[b], 4 * HALVES);
       }
       tc::fence_barrier_init();
     }
@@ -326,12 +341,16 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp <= 2) {
+    // Issuer p handles the key tiles of parity p.  Units of one parity always use the same
+    // TMEM buffer and stage parity (NBUF = 2, STAGES even): the issuers never share state.
+    const int p = warp - 1;
     if (lane == 0) {
       int it = 0, pc = 0;
       for (int pair = blockIdx.x; pair < n_pairs; pair += gridDim.x, ++pc) {
         tc::mbar_wait(a_full, pc & 1);
         for (int i = 0; i < n_kt; ++i, ++it) {
+          if ((it & 1) != p) continue;
           const int s = it % C::STAGES;
           const int buf = it % C::NBUF;
           tc::mbar_wait(&b_full[s], (it / C::STAGES) & 1);
@@ -354,9 +373,11 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       }
     }
   } else {
-    const int e = warp - 2;       // 0..7
-    const int q = warp & 3;       // TMEM lane quarter
-    const int t = e >> 2;         // query tile of the pair
+    const int e = warp - 3;            // 0 .. EPI_WARPS-1
+    const int q = warp & 3;            // TMEM lane quarter this warp may access
+    const int t = (e >> 2) & 1;        // query tile of the pair
+    const int hf = e >> 3;             // key-column slice of each tile (HALVES == 2)
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + t * C::BN + hf * C::COLS;
     int it = 0;
     for (int pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
       const int st = start_tile[pair];
@@ -382,80 +403,48 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         const int buf = it % C::NBUF;
         tc::mbar_wait(&t_full[buf * 2 + t], (it / C::NBUF) & 1);
         tc::tc_fence_after();
-        const int key0 = kt * C::BN;
-        const bool tail = key0 + C::BN > n_k;
-        if (dbg_mode == 2) {  // debug: no TMEM traffic at all
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&t_empty[buf * 2 + t]);
-          ++it;
-          continue;
-        }
+        const int key0 = kt * C::BN + hf * C::COLS;
+        const int valid = (int)(n_k - key0 < C::COLS ? n_k - key0 : (int64_t)C::COLS);  // keys of the last tile may be padding
 #pragma unroll 1
-        for (int c2 = 0; c2 < C::BN / 64; ++c2) {
-          // two 32-column TMEM loads in flight per wait (hides the tcgen05.ld latency)
-          uint32_t r0[32], r1[32];
-          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + buf * (2 * C::BN) + t * C::BN + c2 * 64;
-          tc::tmem_ld32(ta, r0);
-          tc::tmem_ld32(ta + 32, r1);
+        for (int c = 0; c < C::COLS / 32; ++c) {
+          const uint32_t ta = tl + buf * (2 * C::BN) + c * 32;
+          uint32_t r[32];
+          tc::tmem_ld32(ta, r);
           tc::tmem_ld_wait();
-          if (dbg_mode == 1) {  // debug: TMEM loads only
-            uint32_t x = 0;
+          float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) x ^= r0[j] ^ r1[j];
-            if (x == 0x12345678u) I[0] = (int)x;
-            continue;
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          const int lim = valid - c * 32;
+          if (lim < 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j >= lim) v[j] = INFINITY;
           }
+          const float thr = L[KC - 1];
+          if (__any_sync(0xffffffffu, min32(v) < thr)) {
+            // rare path: columns where any lane passes; each is re-read from TMEM (one
+            // column per lane) and goes to the lane's small queue; a full queue on ANY lane
+            // merges every lane's queue at once.
+            uint32_t mask = 0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = c2 * 2 + h;
-            float v[32];
+            for (int j = 0; j < 32; ++j) mask |= (v[j] < thr) ? (1u << j) : 0u;
+            uint32_t cm = __reduce_or_sync(0xffffffffu, mask);
+            while (cm) {
+              const int j = __ffs(cm) - 1;
+              cm &= cm - 1;
+              if (__any_sync(0xffffffffu, qn == kQ)) queue_merge<KC>(L, I, Qv, Qi, qn);
+              const float x = __uint_as_float(tmem_ld1(ta + j));
+              tc::tmem_ld_wait();
+              if (((mask >> j) & 1u) && x < L[KC - 1]) {
+                const int id = key0 + c * 32 + j;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(h ? r1[j] : r0[j]);
-            if (tail) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (key0 + c * 32 + j >= n_k) v[j] = INFINITY;
-            }
-            const float m = min32(v);
-            if (dbg_mode == 3 && lane == 0) atomicAdd(&g_knn_stats[0], 1ull);
-            if (__any_sync(0xffffffffu, m < L[KC - 1])) {
-              if (dbg_mode == 3 && lane == 0) atomicAdd(&g_knn_stats[1], 1ull);
-              // rare path: bitmask of this lane's passing scores, staged chunk (transposed,
-              // conflict-free) and a loop over set bits; passing scores go to the lane's small
-              // queue, and a full queue on ANY lane merges every lane's queue at once.
-              float* sp = spill + e * 32 * 32;
-              const float thr = L[KC - 1];
-              uint32_t mask = 0;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                sp[j * 32 + lane] = v[j];
-                mask |= (v[j] < thr) ? (1u << j) : 0u;
-              }
-              __syncwarp();
-              while (__any_sync(0xffffffffu, mask != 0)) {
-                if (__any_sync(0xffffffffu, qn == kQ)) {
-                  if (dbg_mode == 3 && lane == 0) atomicAdd(&g_knn_stats[3], 1ull);
-                  queue_merge<KC>(L, I, Qv, Qi, qn);
-                }
-                if (dbg_mode == 3 && lane == 0) atomicAdd(&g_knn_stats[2], 1ull);
-                if (mask) {
-                  const int j = __ffs(mask) - 1;
-                  mask &= mask - 1;
-                  const float x = sp[j * 32 + lane];
-                  if (x < L[KC - 1]) {
-                    const int id = key0 + c * 32 + j;
-#pragma unroll
-                    for (int q2 = 0; q2 < kQ; ++q2)
-                      if (q2 == qn) {
-                        Qv[q2] = x;
-                        Qi[q2] = id;
-                      }
-                    ++qn;
+                for (int q2 = 0; q2 < kQ; ++q2)
+                  if (q2 == qn) {
+                    Qv[q2] = x;
+                    Qi[q2] = id;
                   }
-                }
+                ++qn;
               }
-              __syncwarp();
             }
           }
         }
@@ -466,7 +455,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       }
       queue_merge<KC>(L, I, Qv, Qi, qn);
       if (row < n_q) {
-        int* o = cand + row * KC;
+        int* o = cand + row * C::KCT + hf * KC;
 #pragma unroll
         for (int j = 0; j < KC; ++j) o[j] = I[j];
       }
@@ -477,9 +466,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
-// one warp per (sorted) query: exact fp32 distances of the candidates (sorted key positions
-// mapped back through perm_k), bitonic sort by (d2, original index), keep k; the output row
-// is the query's original row perm_q[i].
+// ------------------------------------------------------------------ rerank
 template <int KC>
 __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __restrict__ Kx, int64_t n_q, int d,
                                   int ld, const int* __restrict__ perm_q, const int* __restrict__ perm_k,
@@ -576,16 +563,17 @@ static int sort_by_pc1(const float* X, int64_t n, int d, int ld, const int* omin
   return SCB_OK;
 }
 
-template <int KC>
+template <int KC, int HALVES>
 static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* Kx, int64_t n_k, int d, int ld, int k,
                       int* out_i, float* out_d, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
-  using Cfg = KnnCfg<KC>;
+  using Cfg = KnnCfg<KC, HALVES>;
+  constexpr int KCT = Cfg::KCT;
   const bool same = (Qx == Kx && n_q == n_k);
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
   const int64_t n_pairs = (n_q + 2 * Cfg::BM - 1) / (2 * Cfg::BM);
   const size_t sz[] = {256, sizeof(int) * kBuckets, 4 * (size_t)n_q, 4 * (size_t)n_k, 4 * (size_t)n_q,
                        4 * (size_t)n_k, 4 * (size_t)n_pairs, (size_t)n_q * kD * 2, (size_t)n_k * kD * 2,
-                       (size_t)n_q * KC * 4};
+                       (size_t)n_q * KCT * 4};
   size_t total = 0;
   for (size_t v : sz) total += up(v);
   void* ws;
@@ -627,24 +615,13 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   CUtensorMap tq, tk;
   SCB_TRY(make_tmap_2d(&tq, Qa, (uint64_t)n_q, kD, kD, 2, 64, Cfg::BM));
   SCB_TRY(make_tmap_2d(&tk, Ka, (uint64_t)n_k, kD, kD, 2, 64, Cfg::BN));
-  auto kern = knn_candidates_kernel<KC>;
+  auto kern = knn_candidates_kernel<KC, HALVES>;
   SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   if (ev0) SCB_CUDA(cudaEventRecord(ev0, s));
-  const char* dbg = getenv("SCB_KNN_DEBUG_MODE");
-  kern<<<(int)std::min<int64_t>(n_pairs, ctx->num_sms), kKnnThreads, Cfg::SMEM, s>>>(tq, tk, n_q, n_k, start, cand,
-                                                                                 dbg ? atoi(dbg) : 0);
+  kern<<<(int)std::min<int64_t>(n_pairs, ctx->num_sms), Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, n_q, n_k, start, cand);
   SCB_LAUNCH_CHECK();
   if (ev1) SCB_CUDA(cudaEventRecord(ev1, s));
-  if (dbg && atoi(dbg) == 3) {
-    unsigned long long st[4];
-    SCB_CUDA(cudaMemcpyFromSymbolAsync(st, g_knn_stats, sizeof(st), 0, cudaMemcpyDeviceToHost, s));
-    SCB_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[knn stats] warp-chunks %llu slow %llu (%.2f%%) bit-iterations %llu merges %llu\n", st[0], st[1],
-            100.0 * st[1] / (double)(st[0] ? st[0] : 1), st[2], st[3]);
-    const unsigned long long z[4] = {0, 0, 0, 0};
-    SCB_CUDA(cudaMemcpyToSymbolAsync(g_knn_stats, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
-  }
-  knn_rerank_kernel<KC><<<ceil_div(n_q, 8), 256, 0, s>>>(Qx, Kx, n_q, d, ld, perm_q, perm_k, cand, k, out_i, out_d);
+  knn_rerank_kernel<KCT><<<ceil_div(n_q, 8), 256, 0, s>>>(Qx, Kx, n_q, d, ld, perm_q, perm_k, cand, k, out_i, out_d);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
@@ -664,8 +641,8 @@ extern "C" int scb_knn_timed(scb_ctx* ctx, const float* queries, int64_t n_queri
   if (n_queries == 0) return SCB_OK;
   cudaStream_t s = (cudaStream_t)stream;
   cudaEvent_t e0 = (cudaEvent_t)ev_start, e1 = (cudaEvent_t)ev_end;
-  if (k_cand == 32) return launch_knn<32>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
-  return launch_knn<64>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
+  if (k_cand == 32) return launch_knn<16, 2>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
+  return launch_knn<64, 1>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
 }
 
 extern "C" int scb_knn(scb_ctx* ctx, const float* queries, int64_t n_queries, const float* keys, int64_t n_keys,
