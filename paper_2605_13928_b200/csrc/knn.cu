@@ -47,7 +47,7 @@ struct KnnCfg {
   static constexpr int SMEM = A_BYTES + STAGES * B_BYTES + 1024 + 256;
   // kind::f16: c_format F32 (1) [4,6), a/b format F16 (0), K-major, N>>3 [17,23), M>>4 [24,29)
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-  static_assert(NBUF == 2 && STAGES % 2 == 0, "MMA issuer p owns units of parity p: buffer p, even/odd stages");
+  static_assert(NBUF == 2, "TMEM: 2 buffers x 2 query tiles x 128 columns");
   static_assert(COLS % 32 == 0, "epilogue chunks are 32 columns");
 };
 
@@ -221,12 +221,16 @@ __global__ void start_tile_kernel(const float* __restrict__ q_pc1_sorted, int64_
   start[p] = (int)min(t, n_kt - 1);
 }
 
-// i-th key tile of the outward scan from `start` (start, start+1, start-1, start+2, ...);
-// -1 for positions that fall off either end (the 2*n_kt sequence covers every tile once).
-__device__ __forceinline__ int outward_tile(int start, int i, int n_kt) {
-  const int dd = (i + 1) >> 1;
-  const int t = (i & 1) ? start + dd : start - dd;
-  return (t >= 0 && t < n_kt) ? t : -1;
+// j-th key tile (0 <= j < n_kt) of the outward scan from `start`: start, start+1, start-1,
+// start+2, start-2, ... and, once one end is reached, the rest of the other side in order.
+__device__ __forceinline__ int outward_tile(int start, int j, int n_kt) {
+  const int below = start, above = n_kt - 1 - start;
+  const int m = min(below, above);
+  if (j <= 2 * m) {
+    const int dd = (j + 1) >> 1;
+    return (j & 1) ? start + dd : start - dd;
+  }
+  return above > below ? start + (j - below) : start - (j - above);
 }
 
 template <int KC>
@@ -269,6 +273,22 @@ __device__ __forceinline__ float min32(const float (&v)[32]) {
   return fminf(fminf(b0, b1), fminf(b2, b3));
 }
 
+#ifdef SCB_KNN_PROF
+__device__ unsigned long long g_knn_prof[8];  // [0] epi t_full wait, [1] epi total, [2] mma t_empty wait, [3] mma b_full wait, [4] mma total
+#define PROF_T0(v) const long long v = clock64()
+#define PROF_ADD(i, v) prof_acc[i] += clock64() - (v)
+#define PROF_DECL long long prof_acc[7] = {0, 0, 0, 0, 0, 0, 0}
+#define PROF_FLUSH                                                                              \
+  do {                                                                                        \
+    if (lane_id() == 0)                                                                       \
+      for (int i_ = 0; i_ < 7; ++i_) if (prof_acc[i_]) atomicAdd(&g_knn_prof[i_], (unsigned long long)prof_acc[i_]); \
+  } while (0)
+#else
+#define PROF_T0(v)
+#define PROF_ADD(i, v)
+#define PROF_DECL
+#define PROF_FLUSH
+#endif
 __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
   uint32_t r;
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
@@ -296,7 +316,6 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   const int warp = warp_id(), lane = lane_id();
   const int n_pairs = (int)((n_q + 2 * C::BM - 1) / (2 * C::BM));
   const int n_kt = (int)((n_k + C::BN - 1) / C::BN);
-  const int n_seq = 2 * n_kt;  // outward sequence length (positions off the ends are skipped)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -306,7 +325,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       tc::mbar_init(a_empty, 2);  // one commit per MMA issuer
       for (int s = 0; s < C::STAGES; ++s) {
         tc::mbar_init(&b_full[s], 1);
-        tc::mbar_init(&b_empty[s], 1);
+        tc::mbar_init(&b_empty[s], 2);  // both issuers read every stage
       }
       for (int b = 0; b < 2 * C::NBUF; ++b) {
         tc::mbar_init(&t_full[b], 1);
@@ -321,6 +340,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  PROF_DECL;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -330,9 +350,8 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         tc::mbar_wait(a_empty, (pc & 1) ^ 1);
         tc::mbar_arrive_expect_tx(a_full, C::A_BYTES);
         for (int t = 0; t < 2; ++t) tc::tma_load_2d(a_base + t * C::TILE, &tq, a_full, 0, (pair * 2 + t) * C::BM);
-        for (int i = 0; i < n_seq; ++i) {
+        for (int i = 0; i < n_kt; ++i) {
           const int kt = outward_tile(st, i, n_kt);
-          if (kt < 0) continue;
           const int s = it % C::STAGES;
           tc::mbar_wait(&b_empty[s], ((it / C::STAGES) & 1) ^ 1);
           tc::mbar_arrive_expect_tx(&b_full[s], C::B_BYTES);
@@ -342,35 +361,39 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       }
     }
   } else if (warp <= 2) {
-    // Issuer p handles the key tiles of parity p.  Units of one parity always use the same
-    // TMEM buffer and stage parity (NBUF = 2, STAGES even): the issuers never share state.
-    const int p = warp - 1;
+    // Issuer t feeds query tile t: every key tile, into TMEM buffer (unit parity, t).  A
+    // tcgen05.commit stalls its issuing thread until the tensor pipe drains, so a single issuer
+    // leaves the pipe idle ~45% of the time; two issuers interleave.  Each qtile's MMA -> epilogue
+    // ring is then independent of the other qtile's epilogue progress.
+    const int t = warp - 1;
     if (lane == 0) {
+      PROF_T0(tot);
+      const uint32_t ab = tc::smem_u32(a_base + t * C::TILE);
       int it = 0, pc = 0;
       for (int pair = blockIdx.x; pair < n_pairs; pair += gridDim.x, ++pc) {
         tc::mbar_wait(a_full, pc & 1);
         for (int i = 0; i < n_kt; ++i, ++it) {
-          if ((it & 1) != p) continue;
           const int s = it % C::STAGES;
-          const int buf = it % C::NBUF;
+          const int buf = it & 1;
+          PROF_T0(w0);
           tc::mbar_wait(&b_full[s], (it / C::STAGES) & 1);
+          PROF_ADD(3, w0);
           const uint32_t bb = tc::smem_u32(b_base + s * C::B_BYTES);
+          PROF_T0(w1);
+          tc::mbar_wait(&t_empty[buf * 2 + t], ((it >> 1) & 1) ^ 1);
+          PROF_ADD(2, w1);
+          tc::tc_fence_after();
+          const uint32_t d = tmem + buf * (2 * C::BN) + t * C::BN;
 #pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            tc::mbar_wait(&t_empty[buf * 2 + t], ((it / C::NBUF) & 1) ^ 1);
-            tc::tc_fence_after();
-            const uint32_t ab = tc::smem_u32(a_base + t * C::TILE);
-            const uint32_t d = tmem + buf * (2 * C::BN) + t * C::BN;
-#pragma unroll
-            for (int kk = 0; kk < kD / 16; ++kk)  // K = 16 fp16 = 32 bytes per MMA
-              mma_f16(d, tc::smem_desc_sw128(ab + kk * 32, 16, 1024), tc::smem_desc_sw128(bb + kk * 32, 16, 1024),
-                      C::IDESC, kk > 0 ? 1u : 0u);
-            tc::mma_commit(&t_full[buf * 2 + t]);
-          }
+          for (int kk = 0; kk < kD / 16; ++kk)  // K = 16 fp16 = 32 bytes per MMA
+            mma_f16(d, tc::smem_desc_sw128(ab + kk * 32, 16, 1024), tc::smem_desc_sw128(bb + kk * 32, 16, 1024),
+                    C::IDESC, kk > 0 ? 1u : 0u);
+          tc::mma_commit(&t_full[buf * 2 + t]);
           tc::mma_commit(&b_empty[s]);
         }
         tc::mma_commit(a_empty);
       }
+      PROF_ADD(4, tot);
     }
   } else {
     const int e = warp - 3;            // 0 .. EPI_WARPS-1
@@ -378,7 +401,10 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
     const int t = (e >> 2) & 1;        // query tile of the pair
     const int hf = e >> 3;             // key-column slice of each tile (HALVES == 2)
     const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + t * C::BN + hf * C::COLS;
+    const uint32_t tf_bar = tc::smem_u32(&t_full[t]), te_bar = tc::smem_u32(&t_empty[t]);  // + buf * 16
+    const int n_k32 = (int)n_k;
     int it = 0;
+    PROF_T0(tot);
     for (int pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
       const int st = start_tile[pair];
       float L[KC];
@@ -397,20 +423,24 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         Qi[j] = -1;
       }
       const int64_t row = (int64_t)(pair * 2 + t) * C::BM + 32 * q + lane;
-      for (int i = 0; i < n_seq; ++i) {
+      for (int i = 0; i < n_kt; ++i, ++it) {
         const int kt = outward_tile(st, i, n_kt);
-        if (kt < 0) continue;
-        const int buf = it % C::NBUF;
-        tc::mbar_wait(&t_full[buf * 2 + t], (it / C::NBUF) & 1);
+        const int buf = it & 1;
+        PROF_T0(w0);
+        tc::mbar_wait_a(tf_bar + buf * 16, (it >> 1) & 1);
+        PROF_ADD(0, w0);
         tc::tc_fence_after();
         const int key0 = kt * C::BN + hf * C::COLS;
-        const int valid = (int)(n_k - key0 < C::COLS ? n_k - key0 : (int64_t)C::COLS);  // keys of the last tile may be padding
+        const int valid = n_k32 - key0;  // < COLS only in the last tile (padding keys)
+        const uint32_t tb = tl + buf * (2 * C::BN);
 #pragma unroll 1
         for (int c = 0; c < C::COLS / 32; ++c) {
-          const uint32_t ta = tl + buf * (2 * C::BN) + c * 32;
+          const uint32_t ta = tb + c * 32;
           uint32_t r[32];
+          PROF_T0(w2);
           tc::tmem_ld32(ta, r);
           tc::tmem_ld_wait();
+          PROF_ADD(5, w2);
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
@@ -425,6 +455,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
             // rare path: columns where any lane passes; each is re-read from TMEM (one
             // column per lane) and goes to the lane's small queue; a full queue on ANY lane
             // merges every lane's queue at once.
+            PROF_T0(w3);
             uint32_t mask = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) mask |= (v[j] < thr) ? (1u << j) : 0u;
@@ -446,12 +477,12 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
                 ++qn;
               }
             }
+            PROF_ADD(6, w3);
           }
         }
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&t_empty[buf * 2 + t]);
-        ++it;
+        if (lane == 0) tc::mbar_arrive_a(te_bar + buf * 16);
       }
       queue_merge<KC>(L, I, Qv, Qi, qn);
       if (row < n_q) {
@@ -460,7 +491,9 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         for (int j = 0; j < KC; ++j) o[j] = I[j];
       }
     }
+    PROF_ADD(1, tot);
   }
+  PROF_FLUSH;
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
@@ -621,6 +654,18 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   kern<<<(int)std::min<int64_t>(n_pairs, ctx->num_sms), Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, n_q, n_k, start, cand);
   SCB_LAUNCH_CHECK();
   if (ev1) SCB_CUDA(cudaEventRecord(ev1, s));
+#ifdef SCB_KNN_PROF
+  {
+    unsigned long long pr[8];
+    SCB_CUDA(cudaMemcpyFromSymbolAsync(pr, g_knn_prof, sizeof(pr), 0, cudaMemcpyDeviceToHost, s));
+    SCB_CUDA(cudaStreamSynchronize(s));
+    const double ne = (double)Cfg::EPI_WARPS * std::min<int64_t>(n_pairs, ctx->num_sms), nm = 2.0 * std::min<int64_t>(n_pairs, ctx->num_sms);
+    fprintf(stderr, "[knn prof] per epi warp: total %.3g cyc, t_full wait %.3g, tmem ld+wait %.3g, slow path %.3g | per issuer: total %.3g, t_empty wait %.3g, b_full wait %.3g\n",
+            pr[1] / ne, pr[0] / ne, pr[5] / ne, pr[6] / ne, pr[4] / nm, pr[2] / nm, pr[3] / nm);
+    const unsigned long long z[8] = {};
+    SCB_CUDA(cudaMemcpyToSymbolAsync(g_knn_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
+  }
+#endif
   knn_rerank_kernel<KCT><<<ceil_div(n_q, 8), 256, 0, s>>>(Qx, Kx, n_q, d, ld, perm_q, perm_k, cand, k, out_i, out_d);
   SCB_LAUNCH_CHECK();
   return SCB_OK;

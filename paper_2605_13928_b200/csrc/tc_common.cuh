@@ -38,20 +38,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Same wait, but the thread is suspended in hardware until the phase completes (or the hint,
-// in ns, expires) instead of re-issuing try_wait: waiting producer / MMA warps then leave the
-// issue slots of their sub-partition to the epilogue warps that share it.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
+// variants on a precomputed shared-window address (hot loops: no generic->shared conversion)
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(a),
-      "r"(parity), "r"(1000000u)
+      "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
 // generic-proxy smem writes -> visible to the async proxy (tensor core / TMA)
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -178,6 +178,110 @@ __global__ void k_pingpong(const __half* a, const __half* b, int units, long lon
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(tm);
 }
 
+// smem-operand pressure probe: 2 issuers, NST distinct B stages, distinct A per qtile (SS) or
+// A from TMEM (TS); epilogue arrives immediately.  unit = 2 qtiles x 4 MMAs (128xNx16).
+template <int N, bool TS, int NST>
+__global__ void k_ops(const __half* a, const __half* b, int units, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  __half* As = reinterpret_cast<__half*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));  // [2][128*64]
+  __half* Bs = As + 2 * 128 * 64;  // [NST][N*64]
+  __shared__ uint64_t t_full[4], t_empty[4], done[2];
+  __shared__ uint32_t slot;
+  for (int e = threadIdx.x; e < 128 * 64; e += blockDim.x) {
+    int r = e / 64, k = e % 64, chunk = k / 8, w = k % 8;
+    As[r * 64 + ((chunk ^ (r % 8)) * 8) + w] = a[r * 64 + k];
+    As[128 * 64 + r * 64 + ((chunk ^ (r % 8)) * 8) + w] = a[r * 64 + k];
+  }
+  for (int st = 0; st < NST; ++st)
+    for (int e = threadIdx.x; e < N * 64; e += blockDim.x) {
+      int r = e / 64, k = e % 64, chunk = k / 8, w = k % 8;
+      Bs[st * N * 64 + r * 64 + ((chunk ^ (r % 8)) * 8) + w] = b[(r % 128) * 64 + k];
+    }
+  tc::fence_proxy_async_smem();
+  if (threadIdx.x < 32) tc::tmem_alloc<512>(&slot);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) { tc::mbar_init(&t_full[i], 1); tc::mbar_init(&t_empty[i], 4); }
+    tc::mbar_init(&done[0], 1); tc::mbar_init(&done[1], 1);
+    tc::fence_barrier_init();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tm = slot;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr uint32_t ACOL = (4 * N + 31) / 32 * 32;  // A in TMEM after the accumulators (2 qtiles x 32 cols)
+  if (TS && warp < 4) {  // A rows -> TMEM (fp16 pairs packed in 32-bit columns)
+    const int row = 32 * warp + lane;
+    for (int t = 0; t < 2; ++t) {
+      uint32_t ar[32];
+      for (int j = 0; j < 32; ++j) {
+        __half2 h2 = __halves2half2(a[row * 64 + 2 * j], a[row * 64 + 2 * j + 1]);
+        ar[j] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+                   "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tm + ((32 * warp) << 16) + ACOL + t * 32),
+                   "r"(ar[0]), "r"(ar[1]), "r"(ar[2]), "r"(ar[3]), "r"(ar[4]), "r"(ar[5]), "r"(ar[6]), "r"(ar[7]), "r"(ar[8]),
+                   "r"(ar[9]), "r"(ar[10]), "r"(ar[11]), "r"(ar[12]), "r"(ar[13]), "r"(ar[14]), "r"(ar[15]), "r"(ar[16]),
+                   "r"(ar[17]), "r"(ar[18]), "r"(ar[19]), "r"(ar[20]), "r"(ar[21]), "r"(ar[22]), "r"(ar[23]), "r"(ar[24]),
+                   "r"(ar[25]), "r"(ar[26]), "r"(ar[27]), "r"(ar[28]), "r"(ar[29]), "r"(ar[30]), "r"(ar[31]));
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  long long t0 = clock64();
+  if (warp < 2) {
+    if (lane == 0) {
+      const int p = warp;
+      for (int u = 0; u < units; ++u) {
+        if ((u & 1) != p) continue;
+        const int buf = u & 1;
+        const uint32_t bb = tc::smem_u32(Bs) + (u % NST) * N * 128;
+        for (int t = 0; t < 2; ++t) {
+          tc::mbar_wait(&t_empty[buf * 2 + t], ((u >> 1) & 1) ^ 1);
+          tc::tc_fence_after();
+          const uint32_t d = tm + buf * (2 * N) + t * N;
+          for (int kk = 0; kk < 4; ++kk) {
+            uint64_t db = tc::smem_desc_sw128(bb + kk * 32, 16, 1024);
+            uint32_t ac = (kk > 0) ? 1u : 0u;
+            if (TS) {
+              asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                           "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+                           "r"(tm + ACOL + t * 32 + kk * 8), "l"(db), "r"(idesc), "r"(ac));
+            } else {
+              uint64_t da = tc::smem_desc_sw128(tc::smem_u32(As + t * 128 * 64) + kk * 32, 16, 1024);
+              asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                           "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(da), "l"(db),
+                           "r"(idesc), "r"(ac));
+            }
+          }
+          tc::mma_commit(&t_full[buf * 2 + t]);
+        }
+      }
+      tc::mma_commit(&done[p]);
+    }
+  } else if (warp < 10) {
+    const int e = warp - 2, t = e >> 2;
+    for (int u = 0; u < units; ++u) {
+      const int buf = u & 1;
+      tc::mbar_wait(&t_full[buf * 2 + t], (u >> 1) & 1);
+      tc::tc_fence_after();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&t_empty[buf * 2 + t]);
+    }
+  }
+  if (threadIdx.x == 0) { tc::mbar_wait(&done[0], 0); tc::mbar_wait(&done[1], 0); }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) *cyc = t1 - t0;
+  tc::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::tmem_dealloc<512>(tm);
+}
+
 int main() {
   std::vector<__half> ha(128 * 64), hb(128 * 64);
   std::vector<float> fa(128 * 64), fb(128 * 64);
@@ -234,6 +338,26 @@ int main() {
     run(k_pingpong<128, 2, false, true>, "N128 NBUF2 perUnit load", 128);
     run(k_pingpong<64, 4, true, true>, "N64 NBUF4 perQ load", 64);
     run(k_pingpong<64, 4, false, true>, "N64 NBUF4 perUnit load", 64);
+  }
+
+  {
+    const int units = 4000;
+    auto run2 = [&](auto kern, const char* name, int n, int nst, int grid = 1) {
+      int sm = 1024 + 2 * 128 * 64 * 2 + nst * n * 64 * 2;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      kern<<<grid, 320, sm>>>(da, db, units, dc);
+      cudaError_t e = cudaDeviceSynchronize();
+      long long c; cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+      printf("%-30s %.1f cycles/unit, %.1f cycles per 128x128x16-equiv MMA (%s)\n", name, (double)c / units,
+             (double)c / units / 8.0 * 128.0 / n, cudaGetErrorString(e));
+    };
+    run2(k_ops<128, false, 1>, "SS N128 1 stage", 128, 1);
+    run2(k_ops<128, false, 6>, "SS N128 6 stages", 128, 6);
+    run2(k_ops<128, false, 6>, "SS N128 6 stages grid 148", 128, 6, 148);
+    run2(k_ops<128, false, 6>, "SS N128 6 stages grid 148", 128, 6, 148);
+    run2(k_ops<128, false, 6>, "SS N128 6 stages grid 74", 128, 6, 74);
+    run2(k_ops<96, true, 6>, "TS N96 6 stages", 96, 6);
+    run2(k_ops<96, false, 6>, "SS N96 6 stages", 96, 6);
   }
   return 0;
 }
