@@ -257,6 +257,12 @@ def main():
         if kk in step_ms:
             stages[kk] = {"ms": round(step_ms[kk], 4)}
     stages["knn"]["candidates_kernel_ms"] = round(knn_ms, 4)
+    traffic = None  # dram bytes per launch of the kNN kernel from the committed ncu --set full capture
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "knn_traffic.json")
+    if os.path.exists(tpath) and world == 1:
+        tj = json.load(open(tpath))
+        if tj.get("cells") == N and tj.get("genes") == G:
+            traffic = int(tj["dram__bytes_read.sum"]) + int(tj["dram__bytes_write.sum"])
     gram_flops = float(N_sub_loc) * H * (H + 1)
     stages["pca"]["gram_flop_unique"] = gram_flops
 
@@ -269,35 +275,58 @@ def main():
         h_indptr.copy_(X.indptr)
         h_ind.copy_(X.indices)
         h_dat.copy_(X.data)
-        d_indptr, d_ind, d_dat = torch.empty_like(X.indptr), torch.empty_like(X.indices), torch.empty_like(X.data)
+        # two device input buffers: the H2D copy of step i+1 (copy stream) overlaps the compute
+        # of step i (compute stream); every step still copies its full input and reads back its graph
+        bufs = [(torch.empty_like(X.indptr), torch.empty_like(X.indices), torch.empty_like(X.data)) for _ in range(2)]
         k = p.n_neighbors
         o_i = torch.empty((N_sub_loc, k), dtype=torch.int32).pin_memory()
         o_d = torch.empty((N_sub_loc, k), dtype=torch.float32).pin_memory()
         del X
         torch.cuda.empty_cache()
+        comp = torch.cuda.current_stream()
+        cs = torch.cuda.Stream()
+        copied = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
+
+        def h2d(i):
+            b = bufs[i % 2]
+            with torch.cuda.stream(cs):
+                if i >= 2:
+                    cs.wait_event(consumed[i % 2])
+                b[0].copy_(h_indptr, non_blocking=True)
+                b[1].copy_(h_ind, non_blocking=True)
+                b[2].copy_(h_dat, non_blocking=True)
+                copied[i % 2].record(cs)
+
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
-            d_indptr.copy_(h_indptr, non_blocking=True)
-            d_ind.copy_(h_ind, non_blocking=True)
-            d_dat.copy_(h_dat, non_blocking=True)
-            Xe = DeviceCSR(d_indptr, d_ind, d_dat, G)
+        e0.record(cs)
+        h2d(0)
+        for i in range(args.steps):
+            if i + 1 < args.steps:
+                h2d(i + 1)
+            comp.wait_event(copied[i % 2])
+            b = bufs[i % 2]
+            Xe = DeviceCSR(b[0], b[1], b[2], G)
             r = pipeline.run(Xe, mt, p, comm=comm, timing=False)
+            consumed[i % 2].record(comp)
             if r.knn_index.shape[0] != o_i.shape[0]:
                 o_i = torch.empty(tuple(r.knn_index.shape), dtype=torch.int32).pin_memory()
                 o_d = torch.empty(tuple(r.knn_dist.shape), dtype=torch.float32).pin_memory()
             o_i.copy_(r.knn_index, non_blocking=True)
             o_d.copy_(r.knn_dist, non_blocking=True)
-        e1.record()
+        comp.wait_stream(cs)
+        e1.record(comp)
         barrier()
         e_ms = e0.elapsed_time(e1) / args.steps
         if comm is not None:
             e_ms = comm.allreduce_max(e_ms)
-        h2d = h_indptr.numel() * 8 + h_ind.numel() * 4 + h_dat.numel() * 4
-        d2h = o_i.numel() * 4 + o_d.numel() * 4
+        h2d_bytes = h_indptr.numel() * 8 + h_ind.numel() * 4 + h_dat.numel() * 4
+        d2h_bytes = o_i.numel() * 4 + o_d.numel() * 4
         e2e = {"value": N / (e_ms / 1e3), "unit": "cells/s", "ms_per_step": round(e_ms, 3),
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+               "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
+               "overlap": "pinned H2D of step i+1 on a copy stream overlaps the compute of step i "
+                          "(2 device input buffers); first copy and last compute are not overlapped"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -321,7 +350,8 @@ def main():
             "stages": stages,
             "roofline": {"kernel": "knn_candidates_kernel (tcgen05 kind::f16 distance GEMM + fused top-k)",
                          "bound": "tensor", "achieved": round(achieved, 2), "peak": round(f16_peak, 1),
-                         "unit": "TFLOP/s", "frac": round(achieved / f16_peak, 4), "traffic": None,
+                         "unit": "TFLOP/s", "frac": round(achieved / f16_peak, 4), "traffic": traffic,
+                         "traffic_unit": "bytes per launch (dram read+write, ncu --set full, profiles/r01/knn_traffic.json)",
                          "algo": f"2*Nq*N*d with d={p.n_comps}: {flops_knn:.3e} FLOP per launch",
                          "peak_basis": f"{basis} dense bf16 {bf16} TFLOP/s (FP16 operands run at the BF16 rate)"},
             "cpu_baseline": cpu,
