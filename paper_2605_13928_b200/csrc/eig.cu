@@ -398,7 +398,9 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     return SCB_OK;
   };
   SCB_TRY(orth(Q, 2));
-  const int kPower = 3, kMaxOuter = 60;
+  // filter degree: 6 converges the synthetic C3 spectrum in 3 outer steps (3 -> 5 steps, 8 -> 3 steps
+  // but slower ones; >= 12 overflows CholQR's conditioning), scratch/prof_eig_real.py
+  const int kPower = 6, kMaxOuter = 60;
   double host_res[kB];
   int outer = 0;
   const bool verbose = getenv("SCB_EIG_VERBOSE") != nullptr;
