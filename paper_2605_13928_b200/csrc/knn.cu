@@ -36,7 +36,7 @@ constexpr int kBuckets = 1 << 16; // PC1 counting-sort buckets
 // KC = per-warp list length, HALVES = epilogue warps per (query tile, TMEM lane quarter)
 template <int KC, int HALVES>
 struct KnnCfg {
-  static constexpr int BM = 128, BN = 128, STAGES = 8, NBUF = 2;  // TMEM: 2 bufs x 2 qtiles x 128 = 512 cols
+  static constexpr int BM = 128, BN = 128, STAGES = 12, NBUF = 2;  // TMEM: 2 bufs x 2 qtiles x 128 = 512 cols
   static constexpr int TILE = BM * kD * 2;              // 16 KB: 128 rows x 64 fp16
   static constexpr int A_BYTES = 2 * TILE;              // 2 query tiles
   static constexpr int B_BYTES = BN * kD * 2;           // 128 keys (16 KB)
