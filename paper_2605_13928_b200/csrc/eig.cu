@@ -8,6 +8,7 @@
 // continue until it falls below 1e-10 (or an iteration cap).  Sign rule: the
 // largest-|loading| entry of every component is positive (first index on ties).
 #include <cstdlib>
+#include <cublas_v2.h>
 #include "common.cuh"
 
 namespace scb {
@@ -20,63 +21,21 @@ constexpr int kLd = kB + 1;
 // opA: 0 -> A[M][K] (lda), 1 -> A^T where A is [K][M]; opB: 0 -> B[K][N], 1 -> B^T ([N][K]).
 // 64x64 tiles, 256 threads, 4x4 per thread, K chunk 16; split-K over blockIdx.z with
 // atomicAdd when gridDim.z > 1 (caller zeroes Cm and passes beta = 0).
-__global__ void __launch_bounds__(256) dgemm_kernel(int M, int N, int K, double alpha, const double* __restrict__ A,
-                                                    int lda, int opA, const double* __restrict__ B, int ldb, int opB,
-                                                    double beta, double* __restrict__ Cm, int ldc) {
-  __shared__ double As[16][64 + 1];
-  __shared__ double Bs[16][64 + 1];
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-  const int kchunk = (K + gridDim.z - 1) / gridDim.z;
-  const int kb = blockIdx.z * kchunk, ke = min(K, kb + kchunk);
-  double acc[4][4] = {};
-  for (int k0 = kb; k0 < ke; k0 += 16) {
-    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
-      const int kk = e / 64, mm = e % 64;
-      const int gk = k0 + kk;
-      double a = 0.0, b = 0.0;
-      if (gk < ke) {
-        const int gm = m0 + mm, gn = n0 + mm;
-        if (gm < M) a = opA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk];
-        if (gn < N) b = opB ? B[(size_t)gn * ldb + gk] : B[(size_t)gk * ldb + gn];
-      }
-      As[kk][mm] = a;
-      Bs[kk][mm] = b;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-    }
-    __syncthreads();
+// Plain fp64 GEMMs of the eigensolver (Cov x block, block^T x block, block x small) go to
+// cuBLAS: row-major C[M][N] = op(A) op(B) is column-major C^T = op(B)^T op(A)^T.
+static int dgemm(scb_ctx* ctx, int M, int N, int K, const double* A, int lda, int opA, const double* B, int ldb,
+                 int opB, double* Cm, int ldc, cudaStream_t s) {
+  if (!ctx->blas) {
+    cublasHandle_t h;
+    SCB_REQUIRE(cublasCreate(&h) == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasCreate failed");
+    ctx->blas = h;
   }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gm = m0 + ty * 4 + i, gn = n0 + tx * 4 + j;
-      if (gm < M && gn < N) {
-        double* c = Cm + (size_t)gm * ldc + gn;
-        if (gridDim.z > 1) atomicAdd(c, alpha * acc[i][j]);
-        else *c = alpha * acc[i][j] + (beta != 0.0 ? beta * *c : 0.0);
-      }
-    }
-}
-
-static int dgemm(int M, int N, int K, const double* A, int lda, int opA, const double* B, int ldb, int opB, double* Cm,
-                 int ldc, cudaStream_t s, int splitk = 1) {
-  dim3 g((N + 63) / 64, (M + 63) / 64, splitk);
-  if (splitk > 1) SCB_CUDA(cudaMemsetAsync(Cm, 0, sizeof(double) * (size_t)M * ldc, s));
-  dgemm_kernel<<<g, 256, 0, s>>>(M, N, K, 1.0, A, lda, opA, B, ldb, opB, 0.0, Cm, ldc);
-  SCB_LAUNCH_CHECK();
+  cublasHandle_t h = (cublasHandle_t)ctx->blas;
+  SCB_REQUIRE(cublasSetStream(h, s) == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasSetStream failed");
+  const double one = 1.0, zero = 0.0;
+  const cublasStatus_t st = cublasDgemm(h, opB ? CUBLAS_OP_T : CUBLAS_OP_N, opA ? CUBLAS_OP_T : CUBLAS_OP_N, N, M, K,
+                                        &one, B, ldb, A, lda, &zero, Cm, ldc);
+  SCB_REQUIRE(st == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasDgemm failed (%d)", (int)st);
   return SCB_OK;
 }
 
@@ -383,16 +342,15 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   init_block_kernel<<<h, kB, 0, s>>>(Q, h);
   SCB_LAUNCH_CHECK();
   SCB_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
-  const int splitk = std::max(1, std::min(16, h / 128));
   double* Rinv = S + kB * kB;  // scratch: W is only needed inside rayleigh_ritz
   auto orth = [&](double*& M, int reps) -> int {
     for (int rep = 0; rep < reps; ++rep) {  // CholQR(reps): M := M R^{-1}
-      SCB_TRY(dgemm(kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s, splitk));
+      SCB_TRY(dgemm(ctx, kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s));
       chol_kernel<<<1, 256, kSmemKB, s>>>(S, fail);
       SCB_LAUNCH_CHECK();
       triinv_kernel<<<1, kB, 2 * kSmemKB, s>>>(S, Rinv);
       SCB_LAUNCH_CHECK();
-      SCB_TRY(dgemm(h, kB, kB, M, kB, 0, Rinv, kB, 0, Y, kB, s));
+      SCB_TRY(dgemm(ctx, h, kB, kB, M, kB, 0, Rinv, kB, 0, Y, kB, s));
       std::swap(M, Y);
     }
     return SCB_OK;
@@ -416,7 +374,7 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     if (cheb_b <= 0.0) {
       // plain power steps until Ritz values are known
       for (int pw = 0; pw < kPower; ++pw) {
-        SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, 3));
+        SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s));
         std::swap(Q, Y);
       }
     } else {
@@ -425,12 +383,12 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
       const int eb = (int)((nel + 255) / 256);
       const double a2 = 2.0 / cheb_b;
       // Y1 = sigma Q  -> stored in Y
-      SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, V, kB, s, 3));
+      SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, V, kB, s));
       cheb_combine_kernel<<<eb, 256, 0, s>>>(V, Q, nullptr, nel, a2, -1.0, 0.0, Y);
       SCB_LAUNCH_CHECK();
       std::swap(Q, Yold);  // Yold = Y0
       for (int k = 1; k < kPower; ++k) {  // Y_{k+1} = 2 sigma Y_k - Y_{k-1}
-        SCB_TRY(dgemm(h, kB, h, cov, h, 0, Y, kB, 0, V, kB, s, 3));
+        SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Y, kB, 0, V, kB, s));
         cheb_combine_kernel<<<eb, 256, 0, s>>>(V, Y, Yold, nel, 2.0 * a2, -2.0, -1.0, Q);
         SCB_LAUNCH_CHECK();
         std::swap(Yold, Y);  // Yold = Y_k
@@ -440,16 +398,16 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     }
     SCB_TRY(orth(Q, 2));
     // Rayleigh-Ritz: T = Q^T Cov Q, T = W diag W^T; rotate Q := Q W (sorted descending)
-    SCB_TRY(dgemm(h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, 3));        // Y = Cov Q
-    SCB_TRY(dgemm(kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s, splitk));   // T = Q^T Y
+    SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s));        // Y = Cov Q
+    SCB_TRY(dgemm(ctx, kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s));   // T = Q^T Y
     jacobi_kernel<<<1, kJacThreads, 2 * kSmemKB, s>>>(S, W, 30);
     SCB_LAUNCH_CHECK();
     select_kernel<<<1, kB, 0, s>>>(S, kB, order, lam_all);
     SCB_LAUNCH_CHECK();
     gather_cols_kernel<<<kB, kB, 0, s>>>(W, order, kB, Wk);
     SCB_LAUNCH_CHECK();
-    SCB_TRY(dgemm(h, kB, kB, Q, kB, 0, Wk, kB, 0, Yold, kB, s));        // Ritz vectors (spare buffer)
-    SCB_TRY(dgemm(h, kB, kB, Y, kB, 0, Wk, kB, 0, V, kB, s));           // Cov * Ritz vectors
+    SCB_TRY(dgemm(ctx, h, kB, kB, Q, kB, 0, Wk, kB, 0, Yold, kB, s));        // Ritz vectors (spare buffer)
+    SCB_TRY(dgemm(ctx, h, kB, kB, Y, kB, 0, Wk, kB, 0, V, kB, s));           // Cov * Ritz vectors
     std::swap(Q, Yold);
     residual_kernel<<<n_comps, 256, 0, s>>>(V, Q, lam_all, h, kB, res);
     SCB_LAUNCH_CHECK();

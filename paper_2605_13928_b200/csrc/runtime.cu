@@ -1,4 +1,5 @@
 // Context, scratch arena and error reporting behind the C ABI.
+#include <cublas_v2.h>
 #include "common.cuh"
 #include <algorithm>
 #include <atomic>
@@ -77,6 +78,7 @@ extern "C" int scb_ctx_destroy(scb_ctx* ctx) {
   for (auto& w : ctx->ws)
     if (w.ptr) cudaFree(w.ptr);
   if (ctx->d_flag) cudaFree(ctx->d_flag);
+  if (ctx->blas) cublasDestroy((cublasHandle_t)ctx->blas);
   delete ctx;
   return SCB_OK;
 }
