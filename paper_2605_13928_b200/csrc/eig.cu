@@ -129,25 +129,37 @@ __global__ void __launch_bounds__(kB) triinv_kernel(const double* __restrict__ R
 // Round-robin tournament ordering in closed form: in round r, pair 0 = (kB-1, r) and pair
 // i >= 1 = ((r+i) mod (kB-1), (r-i) mod (kB-1)): kB/2 disjoint pairs, every pair once per
 // sweep.  Sweeps stop when the off-diagonal Frobenius norm is <= 1e-13 of the diagonal's.
-constexpr int kJacThreads = 256;
+constexpr int kJacThreads = 1024;
+constexpr int kPairs = kB / 2;
+constexpr int kBlocks = kPairs * (kPairs + 1) / 2;  // 2x2 blocks (k <= l) of the pair partition
 __device__ int g_jacobi_sweeps;  // debug: sweeps used by the last call
 
+// One round applies kB/2 disjoint rotations J_k at once: A := J^T A J, W := W J.  Every
+// element of A belongs to exactly one 2x2 block (rows of pair k, columns of pair l), updated
+// in a single pass as R_k^T B R_l by one thread (the k > l block is the mirror), so a round
+// is two barriers and one read + one write of A and W.
 __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict__ T, double* __restrict__ W, int sweeps) {
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
   double (*w)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn + kB * kLd);
-  __shared__ double cs[kB / 2], sn[kB / 2];
-  __shared__ int pp[kB / 2], qq[kB / 2];
+  __shared__ double cs[kPairs], sn[kPairs];
+  __shared__ int pp[kPairs], qq[kPairs];
+  __shared__ short2 blk[kBlocks];
   __shared__ double red[2][kJacThreads / 32];
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
     a[e / kB][e % kB] = T[e];
     w[e / kB][e % kB] = (e / kB == e % kB) ? 1.0 : 0.0;
   }
+  if (threadIdx.x == 0) {
+    int b = 0;
+    for (int k = 0; k < kPairs; ++k)
+      for (int l = k; l < kPairs; ++l) blk[b++] = make_short2((short)k, (short)l);
+  }
   __syncthreads();
   constexpr int M = kB - 1;
   for (int sw = 0; sw < sweeps; ++sw) {
     for (int rd = 0; rd < M; ++rd) {
-      if (threadIdx.x < kB / 2) {
+      if (threadIdx.x < kPairs) {
         const int i = threadIdx.x;
         int p, q;
         if (i == 0) { p = rd; q = M; }
@@ -167,22 +179,30 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
         sn[i] = s;
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < (kB / 2) * kB; e += blockDim.x) {  // rows: A := J^T A
-        const int k = e / kB, j = e % kB;
-        const int p = pp[k], q = qq[k];
-        const double c = cs[k], s = sn[k];
-        const double ap = a[p][j], aq = a[q][j];
-        a[p][j] = c * ap - s * aq;
-        a[q][j] = s * ap + c * aq;
+      for (int b = threadIdx.x; b < kBlocks; b += blockDim.x) {
+        const short2 kl = blk[b];
+        const int pk = pp[kl.x], qk = qq[kl.x], pl = pp[kl.y], ql = qq[kl.y];
+        const double ck = cs[kl.x], sk = sn[kl.x], cl = cs[kl.y], sl = sn[kl.y];
+        const double x00 = a[pk][pl], x01 = a[pk][ql], x10 = a[qk][pl], x11 = a[qk][ql];
+        const double y00 = ck * x00 - sk * x10, y01 = ck * x01 - sk * x11;  // rows: R_k^T
+        const double y10 = sk * x00 + ck * x10, y11 = sk * x01 + ck * x11;
+        const double z00 = cl * y00 - sl * y01, z01 = sl * y00 + cl * y01;  // columns: R_l
+        const double z10 = cl * y10 - sl * y11, z11 = sl * y10 + cl * y11;
+        a[pk][pl] = z00;
+        a[pk][ql] = z01;
+        a[qk][pl] = z10;
+        a[qk][ql] = z11;
+        if (kl.x != kl.y) {
+          a[pl][pk] = z00;
+          a[pl][qk] = z10;
+          a[ql][pk] = z01;
+          a[ql][qk] = z11;
+        }
       }
-      __syncthreads();
-      for (int e = threadIdx.x; e < (kB / 2) * kB; e += blockDim.x) {  // columns: A := A J, W := W J
-        const int k = e / kB, i = e % kB;
-        const int p = pp[k], q = qq[k];
-        const double c = cs[k], s = sn[k];
-        const double ap = a[i][p], aq = a[i][q];
-        a[i][p] = c * ap - s * aq;
-        a[i][q] = s * ap + c * aq;
+      for (int e = threadIdx.x; e < kB * kPairs; e += blockDim.x) {  // W := W J
+        const int i = e / kPairs, l = e % kPairs;
+        const int p = pp[l], q = qq[l];
+        const double c = cs[l], s = sn[l];
         const double wp = w[i][p], wq = w[i][q];
         w[i][p] = c * wp - s * wq;
         w[i][q] = s * wp + c * wq;
