@@ -324,7 +324,8 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int gl = q.g[k] - g0;
-        if (((q.valid >> k) & 1u) && gl >= 0 && gl < w && (!remap || remap[q.g[k]] >= 0)) {
+        // removed genes are accumulated too and dropped at the flush (no per-nonzero remap load)
+        if (((q.valid >> k) & 1u) && gl >= 0 && gl < w) {
           const float y = __fmul_rn(q.x[k], s);   // float32 normalized count
           const double yd = (double)y;
           // carry-free split: low 22 bits + high part; with <= 1024 rows per CTA neither u32
@@ -339,8 +340,10 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
             atomicAdd(&s2hi[gl], (uint32_t)h2);
           } else {  // rare huge y^2 (y > ~724): straight into the global limbs
             const int go = remap ? remap[q.g[k]] : q.g[k];
-            atomicAdd(&sums[2 * n_out + go], (unsigned long long)(h2 & 1023u) << 22);
-            atomicAdd(&sums[3 * n_out + go], (unsigned long long)(h2 >> 10));
+            if (go >= 0) {
+              atomicAdd(&sums[2 * n_out + go], (unsigned long long)(h2 & 1023u) << 22);
+              atomicAdd(&sums[3 * n_out + go], (unsigned long long)(h2 >> 10));
+            }
           }
         }
       }
