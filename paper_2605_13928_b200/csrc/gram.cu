@@ -2,45 +2,51 @@
 //
 // Z is the dense scaled HVG matrix [N cells][hp] (row-major fp32, hp % 128 == 0).  Both
 // UMMA operands are column blocks of Z read MN-major (genes contiguous): A = Z[k, i-block]^T
-// (M = 128 genes), B = Z[k, j-block]^T (N = BN genes), K = cells.  TMA brings [32 cells x
-// 32 genes] boxes (128-byte swizzle with 32-byte atoms: the MN-major TF32 layout) into smem; four converter warps split every
-// element into a TF32-exact high part (in place) and the fp32 remainder, and one thread
-// issues three tcgen05.mma.kind::tf32 per 8-cell step (hi*hi + hi*lo + lo*hi, "3xTF32",
-// ~fp32 accuracy) accumulating in TMEM.  Only tiles touching the upper triangle are
-// computed; split-K over cells fills the 148 SMs, and a deterministic reduce kernel sums
-// the K-slices and mirrors the result.
+// (M = 128 genes), B = Z[k, j-block]^T (N = BN genes), K = cells.  TMA brings fp32 [16 cells x
+// 32 genes] boxes into an fp32 staging ring; eight converter warps split every element into
+// BF16 hi = bf16(x) and lo = bf16(x - hi) (|x - hi - lo| <= 2^-17 |x|) written straight into the
+// MN-major 128-byte-swizzled BF16 operand layout of a second ring; one thread issues three
+// tcgen05.mma.kind::f16 per 16-cell step (hi*hi + hi*lo + lo*hi, "3xBF16"; the dropped lo*lo
+// term is <= 2^-16 relative) at the BF16 tensor rate (twice TF32's), accumulating in TMEM.
+// Only tiles touching the upper triangle are computed; split-K over cells fills the 148 SMs,
+// and a deterministic reduce kernel sums the K-slices in fp64 and mirrors the result.
 #include <vector>
+#include <cuda_bf16.h>
 #include "tc_common.cuh"
 
 namespace scb {
 
-constexpr int kGemmThreads = 192;  // warp0 TMA, warp1 MMA, warps 2..5 convert + epilogue
+constexpr int kConvWarps = 12;
+constexpr int kGemmThreads = 32 * (2 + kConvWarps);  // warp0 TMA, warp1 MMA, converters (2..5 also epilogue)
 
-template <int BN, int STAGES>
+template <int BN>
 struct GramCfg {
   static constexpr int BM = 128;
-  static constexpr int KB = 16;                       // cells per stage (4-stage ring fits smem)
-  static constexpr int A_BYTES = BM * KB * 4;         // 16 KB
-  static constexpr int B_BYTES = BN * KB * 4;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BOX = KB * 128;                // one [KB cells x 32 genes] TMA box = MN chunk stride (LBO)
-  static constexpr int SMEM = 2 * STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr uint32_t IDESC = tc::idesc_tf32(BM, BN, true, true);
+  static constexpr int KB = 16;                       // cells per stage = one MMA K step
+  static constexpr int G = BM + BN;                   // genes per stage (A then B)
+  static constexpr int F_BYTES = G * KB * 4;          // fp32 staging: G/32 TMA boxes of [KB x 32]
+  static constexpr int BOX = KB * 128;                // one fp32 box, and one 64-gene BF16 chunk
+  static constexpr int PLANE = G * KB * 2;            // one BF16 plane (A chunks then B chunks)
+  static constexpr int C_BYTES = 2 * PLANE;           // hi + lo
+  static constexpr int NF = 4, NC = 4;                // ring depths
+  static constexpr int SMEM = NF * F_BYTES + NC * C_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t IDESC = tc::idesc_bf16(BM, BN, true, true);
 };
 
-template <int BN, int STAGES>
+template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ tiles, int n_tiles, int64_t n_rows,
             int64_t rows_per_slice, int hp, float* __restrict__ partial) {
-  using C = GramCfg<BN, STAGES>;
+  using C = GramCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* hi_base = smem;                                   // [STAGES][A | B]
-  uint8_t* lo_base = smem + STAGES * C::STAGE_BYTES;         // [STAGES][A | B]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * STAGES * C::STAGE_BYTES);
-  uint64_t* conv = full + STAGES;
-  uint64_t* empty = conv + STAGES;
-  uint64_t* done = empty + STAGES;
+  uint8_t* f_base = smem;                                    // [NF][G/32 boxes]
+  uint8_t* c_base = smem + C::NF * C::F_BYTES;               // [NC][hi plane | lo plane]
+  uint64_t* f_full = reinterpret_cast<uint64_t*>(c_base + C::NC * C::C_BYTES);
+  uint64_t* f_empty = f_full + C::NF;
+  uint64_t* c_full = f_empty + C::NF;
+  uint64_t* c_empty = c_full + C::NC;
+  uint64_t* done = c_empty + C::NC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = warp_id(), lane = lane_id();
@@ -55,10 +61,13 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
   if (warp == 0) {
     if (lane == 0) {
       tc::tma_prefetch(&tmap);
-      for (int s = 0; s < STAGES; ++s) {
-        tc::mbar_init(&full[s], 1);
-        tc::mbar_init(&conv[s], 4);
-        tc::mbar_init(&empty[s], 1);
+      for (int s = 0; s < C::NF; ++s) {
+        tc::mbar_init(&f_full[s], 1);
+        tc::mbar_init(&f_empty[s], kConvWarps);
+      }
+      for (int s = 0; s < C::NC; ++s) {
+        tc::mbar_init(&c_full[s], kConvWarps);
+        tc::mbar_init(&c_empty[s], 1);
       }
       tc::mbar_init(done, 1);
       tc::fence_barrier_init();
@@ -74,90 +83,104 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
   if (warp == 0) {
     if (lane == 0) {
       for (int it = 0; it < num_kb; ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        tc::mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* a = hi_base + s * C::STAGE_BYTES;
-        uint8_t* b = a + C::A_BYTES;
+        const int s = it % C::NF;
+        tc::mbar_wait(&f_empty[s], ((it / C::NF) & 1) ^ 1);
+        uint8_t* f = f_base + s * C::F_BYTES;
         const int k0 = (int)(k_begin + (int64_t)it * C::KB);
-        tc::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+        tc::mbar_arrive_expect_tx(&f_full[s], C::F_BYTES);
 #pragma unroll
-        for (int c = 0; c < C::BM / 32; ++c) tc::tma_load_2d(a + c * C::BOX, &tmap, &full[s], i0 + 32 * c, k0);
+        for (int c = 0; c < C::BM / 32; ++c) tc::tma_load_2d(f + c * C::BOX, &tmap, &f_full[s], i0 + 32 * c, k0);
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) tc::tma_load_2d(b + c * C::BOX, &tmap, &full[s], j0 + 32 * c, k0);
+        for (int c = 0; c < BN / 32; ++c)
+          tc::tma_load_2d(f + (C::BM / 32 + c) * C::BOX, &tmap, &f_full[s], j0 + 32 * c, k0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       for (int it = 0; it < num_kb; ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        tc::mbar_wait(&conv[s], ph);
+        const int s = it % C::NC;
+        tc::mbar_wait(&c_full[s], (it / C::NC) & 1);
         tc::tc_fence_after();
-        const uint32_t ah = tc::smem_u32(hi_base + s * C::STAGE_BYTES);
-        const uint32_t bh = ah + C::A_BYTES;
-        const uint32_t al = tc::smem_u32(lo_base + s * C::STAGE_BYTES);
-        const uint32_t bl = al + C::A_BYTES;
-#pragma unroll
-        for (int k = 0; k < C::KB / 8; ++k) {
-          // MN-major TF32: 128B_BASE32B layout, 4-cell atoms (SBO 512), 32-gene chunks 4 KB apart
-          const uint32_t off = k * 1024;  // next 8 cells
-          const uint64_t dah = tc::smem_desc_sw128_b32(ah + off, C::BOX, 512);
-          const uint64_t dbh = tc::smem_desc_sw128_b32(bh + off, C::BOX, 512);
-          const uint64_t dal = tc::smem_desc_sw128_b32(al + off, C::BOX, 512);
-          const uint64_t dbl = tc::smem_desc_sw128_b32(bl + off, C::BOX, 512);
-          const uint32_t acc0 = (it > 0 || k > 0) ? 1u : 0u;
-          tc::mma_tf32(tmem, dah, dbh, C::IDESC, acc0);
-          tc::mma_tf32(tmem, dah, dbl, C::IDESC, 1u);
-          tc::mma_tf32(tmem, dal, dbh, C::IDESC, 1u);
-        }
-        tc::mma_commit(&empty[s]);
+        // MN-major BF16, 128-byte swizzle: 64-gene chunks (LBO = chunk stride), 8-cell row
+        // groups 1 KB apart (SBO)
+        const uint32_t ah = tc::smem_u32(c_base + s * C::C_BYTES);
+        const uint32_t bh = ah + (C::BM / 64) * C::BOX;
+        const uint32_t al = ah + C::PLANE;
+        const uint32_t bl = bh + C::PLANE;
+        const uint64_t dah = tc::smem_desc_sw128(ah, C::BOX, 1024);
+        const uint64_t dbh = tc::smem_desc_sw128(bh, C::BOX, 1024);
+        const uint64_t dal = tc::smem_desc_sw128(al, C::BOX, 1024);
+        const uint64_t dbl = tc::smem_desc_sw128(bl, C::BOX, 1024);
+        tc::mma_f16(tmem, dah, dbh, C::IDESC, it > 0 ? 1u : 0u);
+        tc::mma_f16(tmem, dah, dbl, C::IDESC, 1u);
+        tc::mma_f16(tmem, dal, dbh, C::IDESC, 1u);
+        tc::mma_commit(&c_empty[s]);
       }
       tc::mma_commit(done);
     }
   } else {
-    // ---- converters: split the freshly loaded stage into TF32 hi (in place) + lo
-    const int ct = threadIdx.x - 64;  // 0..127
+    // ---- converters: fp32 stage -> BF16 hi/lo planes in the MN-major swizzled layout.  Thread
+    // (gq, c0) owns gene quad gq (4 genes = one 16-byte fp32 unit) of cell rows c0, c0 + R, ...
+    constexpr int QUADS = C::G / 4;                  // gene quads per cell row
+    constexpr int R = 32 * kConvWarps / QUADS;       // cell rows covered per pass
+    static_assert((32 * kConvWarps) % QUADS == 0, "converter tiling");
+    const int ct = threadIdx.x - 64;
+    const int gq = ct % QUADS, c0 = ct / QUADS;
+    const int g = 4 * gq;
+    const int f_col = (g >> 5) * C::BOX, f_unit = (g & 31) >> 2;   // fp32 box, 16-byte unit in its row
+    const int c_col = (g >> 6) * C::BOX, c_unit = (g & 63) >> 3, c_half = (g & 7) * 2;
     for (int it = 0; it < num_kb; ++it) {
-      const int s = it % STAGES;
-      const uint32_t ph = (it / STAGES) & 1;
-      tc::mbar_wait(&full[s], ph);
-      float4* h = reinterpret_cast<float4*>(hi_base + s * C::STAGE_BYTES);
-      float4* l = reinterpret_cast<float4*>(lo_base + s * C::STAGE_BYTES);
-#pragma unroll 4
-      for (int v = ct; v < C::STAGE_BYTES / 16; v += 128) {
-        float4 x = h[v], xh, xl;
-        tc::split_tf32(x.x, xh.x, xl.x);
-        tc::split_tf32(x.y, xh.y, xl.y);
-        tc::split_tf32(x.z, xh.z, xl.z);
-        tc::split_tf32(x.w, xh.w, xl.w);
-        h[v] = xh;
-        l[v] = xl;
+      const int fs = it % C::NF, cs = it % C::NC;
+      tc::mbar_wait(&f_full[fs], (it / C::NF) & 1);
+      tc::mbar_wait(&c_empty[cs], ((it / C::NC) & 1) ^ 1);
+      const uint8_t* f = f_base + fs * C::F_BYTES + f_col;
+      uint8_t* hi = c_base + cs * C::C_BYTES + c_col + c_half;
+      uint8_t* lo = hi + C::PLANE;
+#pragma unroll
+      for (int c = c0; c < C::KB; c += R) {
+        const float4 x = *reinterpret_cast<const float4*>(f + c * 128 + ((f_unit ^ (c & 7)) << 4));
+        const __nv_bfloat162 h0 = __floats2bfloat162_rn(x.x, x.y), h1 = __floats2bfloat162_rn(x.z, x.w);
+        const float2 a = __bfloat1622float2(h0), b = __bfloat1622float2(h1);
+        const __nv_bfloat162 l0 = __floats2bfloat162_rn(x.x - a.x, x.y - a.y);
+        const __nv_bfloat162 l1 = __floats2bfloat162_rn(x.z - b.x, x.w - b.y);
+        const int off = c * 128 + ((c_unit ^ (c & 7)) << 4);
+        uint2 hv, lv;
+        hv.x = *reinterpret_cast<const uint32_t*>(&h0);
+        hv.y = *reinterpret_cast<const uint32_t*>(&h1);
+        lv.x = *reinterpret_cast<const uint32_t*>(&l0);
+        lv.y = *reinterpret_cast<const uint32_t*>(&l1);
+        *reinterpret_cast<uint2*>(hi + off) = hv;
+        *reinterpret_cast<uint2*>(lo + off) = lv;
       }
       tc::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&conv[s]);
-    }
-    // ---- epilogue: TMEM -> registers -> partial[slice] (rows i0.., cols j0..)
-    tc::mbar_wait(done, 0);
-    tc::tc_fence_after();
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = i0 + 32 * q + lane;
-    float* out = partial + (size_t)slice * hp * hp + (size_t)row * hp + j0;
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      uint32_t r[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + c * 32, r);
-      tc::tmem_ld_wait();
-      if (num_kb == 0) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = 0u;
+      if (lane == 0) {
+        tc::mbar_arrive(&f_empty[fs]);
+        tc::mbar_arrive(&c_full[cs]);
       }
-      float4* o4 = reinterpret_cast<float4*>(out + c * 32);
+    }
+    // ---- epilogue (warps 2..5): TMEM -> registers -> partial[slice] (rows i0.., cols j0..)
+    if (warp < 6) {
+      tc::mbar_wait(done, 0);
+      tc::tc_fence_after();
+      const int q = warp & 3;  // TMEM lane quarter this warp may access
+      const int row = i0 + 32 * q + lane;
+      float* out = partial + (size_t)slice * hp * hp + (size_t)row * hp + j0;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + c * 32, r);
+        tc::tmem_ld_wait();
+        if (num_kb == 0) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
-                            __uint_as_float(r[4 * j + 3]));
+          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        }
+        float4* o4 = reinterpret_cast<float4*>(out + c * 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                              __uint_as_float(r[4 * j + 3]));
+      }
     }
   }
   tc::tc_fence_before();
@@ -176,11 +199,11 @@ __global__ void gram_reduce_kernel(const float* __restrict__ partial, int slices
   C[(size_t)j * hp + i] = s;
 }
 
-template <int BN, int STAGES>
+template <int BN>
 static int launch_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int hp, double* C, cudaStream_t s) {
-  using Cfg = GramCfg<BN, STAGES>;
+  using Cfg = GramCfg<BN>;
   CUtensorMap tmap;
-  SCB_TRY(make_tmap_2d_f32(&tmap, Z, (uint64_t)std::max<int64_t>(n_rows, 1), hp, hp, 32, Cfg::KB, /*atom32=*/true));
+  SCB_TRY(make_tmap_2d_f32(&tmap, Z, (uint64_t)std::max<int64_t>(n_rows, 1), hp, hp, 32, Cfg::KB, /*atom32=*/false));
   // upper-triangle tile list
   std::vector<int2> tl;
   for (int bi = 0; bi < hp / Cfg::BM; ++bi)
@@ -199,7 +222,7 @@ static int launch_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int hp, dou
   float* partial = (float*)ws;
   int2* d_tiles = (int2*)((char*)ws + ((part_bytes + 255) / 256) * 256);
   SCB_CUDA(cudaMemcpyAsync(d_tiles, tl.data(), n_tiles * sizeof(int2), cudaMemcpyHostToDevice, s));
-  auto kern = gram_kernel<BN, STAGES>;
+  auto kern = gram_kernel<BN>;
   SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   kern<<<n_tiles * slices, kGemmThreads, Cfg::SMEM, s>>>(tmap, d_tiles, n_tiles, n_rows, rows_per_slice, hp, partial);
   SCB_LAUNCH_CHECK();
@@ -219,6 +242,6 @@ extern "C" int scb_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp
   SCB_REQUIRE(hp > 0 && hp % 128 == 0, SCB_ERR_ARG, "scb_gram: hp must be a multiple of 128");
   SCB_REQUIRE(n_rows >= 0 && n_rows < (1ll << 31), SCB_ERR_ARG, "scb_gram: n_rows out of range");
   cudaStream_t s = (cudaStream_t)stream;
-  if (hp % 256 == 0) return launch_gram<256, 4>(ctx, Z, n_rows, hp, C, s);
-  return launch_gram<128, 6>(ctx, Z, n_rows, hp, C, s);
+  if (hp % 256 == 0) return launch_gram<256>(ctx, Z, n_rows, hp, C, s);
+  return launch_gram<128>(ctx, Z, n_rows, hp, C, s);
 }
