@@ -5,8 +5,8 @@
 // (M = 128 genes), B = Z[k, j-block]^T (N = BN genes), K = cells.  TMA brings fp32 [16 cells x
 // 32 genes] boxes into an fp32 staging ring; eight converter warps split every element into
 // BF16 hi = bf16(x) and lo = bf16(x - hi) (|x - hi - lo| <= 2^-17 |x|) written straight into the
-// MN-major 128-byte-swizzled BF16 operand layout of a second ring; one thread issues three
-// tcgen05.mma.kind::f16 per 16-cell step (hi*hi + hi*lo + lo*hi, "3xBF16"; the dropped lo*lo
+// MN-major 128-byte-swizzled BF16 operand layout of a second ring; two threads (even / odd steps, one TMEM
+// accumulator each) issue three tcgen05.mma.kind::f16 per 16-cell step (hi*hi + hi*lo + lo*hi, "3xBF16"; the dropped lo*lo
 // term is <= 2^-16 relative) at the BF16 tensor rate (twice TF32's), accumulating in TMEM.
 // Only tiles touching the upper triangle are computed; split-K over cells fills the 148 SMs,
 // and a deterministic reduce kernel sums the K-slices in fp64 and mirrors the result.
@@ -17,18 +17,19 @@
 namespace scb {
 
 constexpr int kConvWarps = 12;
-constexpr int kGemmThreads = 32 * (2 + kConvWarps);  // warp0 TMA, warp1 MMA, converters (2..5 also epilogue)
+constexpr int kConv0 = 3;                                   // first converter warp
+constexpr int kGemmThreads = 32 * (kConv0 + kConvWarps);   // warp0 TMA, warps 1-2 MMA, converters (3..6 also epilogue)
 
 template <int BN>
 struct GramCfg {
   static constexpr int BM = 128;
-  static constexpr int KB = 16;                       // cells per stage = one MMA K step
+  static constexpr int KB = 32;                       // cells per stage = two MMA K steps
   static constexpr int G = BM + BN;                   // genes per stage (A then B)
   static constexpr int F_BYTES = G * KB * 4;          // fp32 staging: G/32 TMA boxes of [KB x 32]
   static constexpr int BOX = KB * 128;                // one fp32 box, and one 64-gene BF16 chunk
   static constexpr int PLANE = G * KB * 2;            // one BF16 plane (A chunks then B chunks)
   static constexpr int C_BYTES = 2 * PLANE;           // hi + lo
-  static constexpr int NF = 4, NC = 4;                // ring depths
+  static constexpr int NF = 2, NC = 2;                // ring depths
   static constexpr int SMEM = NF * F_BYTES + NC * C_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t IDESC = tc::idesc_bf16(BM, BN, true, true);
 };
@@ -69,11 +70,11 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
         tc::mbar_init(&c_full[s], kConvWarps);
         tc::mbar_init(&c_empty[s], 1);
       }
-      tc::mbar_init(done, 1);
+      tc::mbar_init(done, 2);
       tc::fence_barrier_init();
     }
     __syncwarp();
-    tc::tmem_alloc<BN>(tmem_slot);
+    tc::tmem_alloc<2 * BN>(tmem_slot);  // one accumulator per MMA issuer
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -95,9 +96,14 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
           tc::tma_load_2d(f + (C::BM / 32 + c) * C::BOX, &tmap, &f_full[s], j0 + 32 * c, k0);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp <= 2) {
+    // two issuers (stage parity p) into two accumulators: a tcgen05.commit stalls its thread until
+    // the tensor pipe drains, so a single issuer committing every 3 MMAs leaves the pipe idle;
+    // the epilogue adds the two accumulators (deterministic)
+    const int p = warp - 1;
     if (lane == 0) {
-      for (int it = 0; it < num_kb; ++it) {
+      const uint32_t acc = tmem + p * BN;
+      for (int it = p; it < num_kb; it += 2) {
         const int s = it % C::NC;
         tc::mbar_wait(&c_full[s], (it / C::NC) & 1);
         tc::tc_fence_after();
@@ -107,13 +113,17 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
         const uint32_t bh = ah + (C::BM / 64) * C::BOX;
         const uint32_t al = ah + C::PLANE;
         const uint32_t bl = bh + C::PLANE;
-        const uint64_t dah = tc::smem_desc_sw128(ah, C::BOX, 1024);
-        const uint64_t dbh = tc::smem_desc_sw128(bh, C::BOX, 1024);
-        const uint64_t dal = tc::smem_desc_sw128(al, C::BOX, 1024);
-        const uint64_t dbl = tc::smem_desc_sw128(bl, C::BOX, 1024);
-        tc::mma_f16(tmem, dah, dbh, C::IDESC, it > 0 ? 1u : 0u);
-        tc::mma_f16(tmem, dah, dbl, C::IDESC, 1u);
-        tc::mma_f16(tmem, dal, dbh, C::IDESC, 1u);
+#pragma unroll
+        for (int kk = 0; kk < C::KB / 16; ++kk) {  // 16 cells = 16 rows of 128 B per K step
+          const uint32_t ko = kk * 2048;
+          const uint64_t dah = tc::smem_desc_sw128(ah + ko, C::BOX, 1024);
+          const uint64_t dbh = tc::smem_desc_sw128(bh + ko, C::BOX, 1024);
+          const uint64_t dal = tc::smem_desc_sw128(al + ko, C::BOX, 1024);
+          const uint64_t dbl = tc::smem_desc_sw128(bl + ko, C::BOX, 1024);
+          tc::mma_f16(acc, dah, dbh, C::IDESC, (it > p || kk > 0) ? 1u : 0u);
+          tc::mma_f16(acc, dah, dbl, C::IDESC, 1u);
+          tc::mma_f16(acc, dal, dbh, C::IDESC, 1u);
+        }
         tc::mma_commit(&c_empty[s]);
       }
       tc::mma_commit(done);
@@ -124,7 +134,7 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
     constexpr int QUADS = C::G / 4;                  // gene quads per cell row
     constexpr int R = 32 * kConvWarps / QUADS;       // cell rows covered per pass
     static_assert((32 * kConvWarps) % QUADS == 0, "converter tiling");
-    const int ct = threadIdx.x - 64;
+    const int ct = threadIdx.x - 32 * kConv0;
     const int gq = ct % QUADS, c0 = ct / QUADS;
     const int g = 4 * gq;
     const int f_col = (g >> 5) * C::BOX, f_unit = (g & 31) >> 2;   // fp32 box, 16-byte unit in its row
@@ -133,8 +143,9 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
       const int fs = it % C::NF, cs = it % C::NC;
       tc::mbar_wait(&f_full[fs], (it / C::NF) & 1);
       tc::mbar_wait(&c_empty[cs], ((it / C::NC) & 1) ^ 1);
-      const uint8_t* f = f_base + fs * C::F_BYTES + f_col;
-      uint8_t* hi = c_base + cs * C::C_BYTES + c_col + c_half;
+      // addressed from the __shared__ symbol itself so the compiler emits LDS/STS, not generic LD/ST
+      const uint8_t* f = smem_raw + (f_base - smem_raw) + fs * C::F_BYTES + f_col;
+      uint8_t* hi = smem_raw + (c_base - smem_raw) + cs * C::C_BYTES + c_col + c_half;
       uint8_t* lo = hi + C::PLANE;
 #pragma unroll
       for (int c = c0; c < C::KB; c += R) {
@@ -159,8 +170,8 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
         tc::mbar_arrive(&c_full[cs]);
       }
     }
-    // ---- epilogue (warps 2..5): TMEM -> registers -> partial[slice] (rows i0.., cols j0..)
-    if (warp < 6) {
+    // ---- epilogue (warps 3..6): TMEM -> registers -> partial[slice] (rows i0.., cols j0..)
+    if (warp < kConv0 + 4) {
       tc::mbar_wait(done, 0);
       tc::tc_fence_after();
       const int q = warp & 3;  // TMEM lane quarter this warp may access
@@ -168,24 +179,23 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
       float* out = partial + (size_t)slice * hp * hp + (size_t)row * hp + j0;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + c * 32, r);
+        uint32_t r0[32], r1[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + c * 32, r0);
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + BN + c * 32, r1);
         tc::tmem_ld_wait();
-        if (num_kb == 0) {
+        float v[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = 0u;
-        }
+        for (int j = 0; j < 32; ++j)
+          v[j] = (num_kb > 0 ? __uint_as_float(r0[j]) : 0.0f) + (num_kb > 1 ? __uint_as_float(r1[j]) : 0.0f);
         float4* o4 = reinterpret_cast<float4*>(out + c * 32);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
-                              __uint_as_float(r[4 * j + 3]));
+        for (int j = 0; j < 8; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
       }
     }
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<BN>(tmem);
+  if (warp == 0) tc::tmem_dealloc<2 * BN>(tmem);
 }
 
 // sum K-slices for i <= j, write C[i][j] and C[j][i] (fixed slice order: deterministic)
