@@ -223,17 +223,21 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
 }
 
 // Compacting copy: each lane's 4-element quad contributes its kept count to a warp-wide
-// exclusive scan so the output stays in row order.
+// exclusive scan so the output stays in row order.  The (up to 128) kept elements of a warp
+// step are staged in shared memory and written back 32 consecutive elements per instruction
+// (full 128-byte lines instead of four lane-strided partial-sector stores per quad).
 __global__ void __launch_bounds__(kRowThreads)
 subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                    const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
                    const int32_t* __restrict__ remap, const int64_t* __restrict__ row_pos,
                    const int64_t* __restrict__ new_indptr, const float* __restrict__ row_scale,
                    int32_t* __restrict__ out_idx, float* __restrict__ out_val) {
+  __shared__ int s_idx[kRowThreads / 32][128];
+  __shared__ float s_val[kRowThreads / 32][128];
   const int64_t nnz = indptr[n_rows];
-  const int lane = lane_id();
+  const int lane = lane_id(), w = warp_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + w; r < n_rows; r += warps) {
     if (!cmask[r]) continue;
     const int64_t kr = row_pos[r];
     const float s = row_scale ? row_scale[kr] : 1.0f;
@@ -253,20 +257,28 @@ subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
         const int t = __shfl_up_sync(0xffffffffu, incl, d);
         if (lane >= d) incl += t;
       }
-      int64_t pos = o + incl - kc;
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      int pos = incl - kc;
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (ng[k] >= 0) {
-          out_idx[pos] = ng[k];
-          out_val[pos] = row_scale ? log1pf(__fmul_rn(q.x[k], s)) : q.x[k];
+          s_idx[w][pos] = ng[k];
+          s_val[w][pos] = row_scale ? log1pf(__fmul_rn(q.x[k], s)) : q.x[k];
           ++pos;
         }
-      o += __shfl_sync(0xffffffffu, incl, 31);
+      __syncwarp();
+      for (int j = lane; j < tot; j += 32) {
+        out_idx[o + j] = s_idx[w][j];
+        out_val[o + j] = s_val[w][j];
+      }
+      __syncwarp();
+      o += tot;
     });
   }
 }
 
 // ============================================================================ normalize + log1p
+
 __global__ void __launch_bounds__(kRowThreads)
 normalize_log1p_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ data, int64_t n_rows,
                        double target_sum, float* __restrict__ out, float* __restrict__ row_scale) {
@@ -631,7 +643,7 @@ scale_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
   uint32_t* s2hi = sm + 3 * n_slots;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
-    stream_row<2>(indices, ldata, indptr[r], indptr[r + 1], nnz, [&](const Quad& q) {
+    stream_row<4>(indices, ldata, indptr[r], indptr[r + 1], nnz, [&](const Quad& q) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (!((q.valid >> k) & 1u)) continue;
