@@ -504,7 +504,9 @@ template <int KC>
 __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __restrict__ Kx, int64_t n_q, int d,
                                   int ld, const int* __restrict__ perm_q, const int* __restrict__ perm_k,
                                   const int* __restrict__ cand, int k, int* __restrict__ out_i, float* __restrict__ out_d) {
-  constexpr int PER = KC / 32;
+  constexpr int PER = (KC + 31) / 32;  // KC not a multiple of 32: the upper lanes carry no candidate
+  constexpr int NS = PER * 32;         // sort width (power of two up to 64)
+  static_assert(NS == 32 || NS == 64, "rerank sort width");
   const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
   if (i >= n_q) return;
   const int l = lane_id();
@@ -516,7 +518,7 @@ __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __re
   int ii[PER];
 #pragma unroll
   for (int p = 0; p < PER; ++p) {
-    const int c = cand[i * KC + p * 32 + l];
+    const int c = (p * 32 + l < KC) ? cand[i * KC + p * 32 + l] : -1;
     ii[p] = (c >= 0) ? perm_k[c] : -1;
     dd[p] = INFINITY;
   }
@@ -539,7 +541,7 @@ __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __re
     return da < db || (da == db && (unsigned)ia < (unsigned)ib);
   };
 #pragma unroll
-  for (int size = 2; size <= KC; size <<= 1) {
+  for (int size = 2; size <= NS; size <<= 1) {
 #pragma unroll
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
 #pragma unroll
@@ -687,6 +689,7 @@ extern "C" int scb_knn_timed(scb_ctx* ctx, const float* queries, int64_t n_queri
   cudaStream_t s = (cudaStream_t)stream;
   cudaEvent_t e0 = (cudaEvent_t)ev_start, e1 = (cudaEvent_t)ev_end;
   if (k_cand == 32) return launch_knn<16, 2>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
+  if (k <= 32) return launch_knn<48, 1>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
   return launch_knn<64, 1>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
 }
 

@@ -29,7 +29,7 @@ def test_knn_matches_oracle_c1():
     np.testing.assert_allclose(dist, o["knn_dist"], rtol=1e-4, atol=1e-4)
 
 
-@pytest.mark.parametrize("n,d,k", [(1000, 50, 15), (3001, 50, 30), (517, 20, 8)])
+@pytest.mark.parametrize("n,d,k", [(1000, 50, 15), (3001, 50, 30), (517, 20, 8), (900, 40, 48)])
 def test_knn_random_exact(n, d, k):
     import torch
     from paper_2605_13928_b200 import pp
