@@ -388,6 +388,7 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     cudaEventCreate(&ev1);
     cudaEventRecord(ev0, s);
   }
+  double prev_worst = 1.0;  // relative residual of the previous outer step
   double cheb_b = 0.0;  // top of the damped interval [0, b] (smallest Ritz value of the block)
   double* Yold = CV;      // h x kB scratch for the three-term recurrence (CV reused below)
   for (; outer < kMaxOuter; ++outer) {
@@ -420,7 +421,10 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     // Rayleigh-Ritz: T = Q^T Cov Q, T = W diag W^T; rotate Q := Q W (sorted descending)
     SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s));        // Y = Cov Q
     SCB_TRY(dgemm(ctx, kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s));   // T = Q^T Y
-    jacobi_kernel<<<1, kJacThreads, 2 * kSmemKB, s>>>(S, W, 30);
+    // Far from convergence the Rayleigh-Ritz step only has to supply the filter bound and a
+    // reasonable rotation (every Jacobi rotation is exactly orthogonal, so a partial sweep
+    // count never damages the subspace): 2 sweeps.  Near convergence it runs to completion.
+    jacobi_kernel<<<1, kJacThreads, 2 * kSmemKB, s>>>(S, W, prev_worst > 1e-4 ? 2 : 30);
     SCB_LAUNCH_CHECK();
     select_kernel<<<1, kB, 0, s>>>(S, kB, order, lam_all);
     SCB_LAUNCH_CHECK();
@@ -437,7 +441,7 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     SCB_CUDA(cudaMemcpyAsync(&lamb, lam_all + kB - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
     SCB_CUDA(cudaStreamSynchronize(s));
     cheb_b = std::max(lamb, 1e-12 * lam0);
-    double worst = 0.0;
+    double worst = 0.0;  // max residual / lambda_1 of the wanted Ritz pairs
     for (int j = 0; j < n_comps; ++j) worst = std::max(worst, host_res[j]);
     if (verbose) {
       cudaEventRecord(ev1, s);
@@ -449,6 +453,7 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
       fprintf(stderr, "[scb_pca_eig] outer %d residual %.3e (lam0 %.4e) jacobi sweeps %d elapsed %.2f ms\n", outer + 1,
               worst, lam0, sweeps, ms);
     }
+    prev_worst = worst / std::max(lam0, 1e-300);
     if (worst <= 1e-9 * std::max(lam0, 1e-300)) break;
   }
   // V := the n_comps leading Ritz vectors (columns 0..n_comps-1 of Q, already sorted)
