@@ -39,6 +39,18 @@ static int dgemm(scb_ctx* ctx, int M, int N, int K, const double* A, int lda, in
   return SCB_OK;
 }
 
+// M[h][kB] (row-major) := M R^{-1} with R upper triangular [kB][kB] (row-major): column-major
+// this is M^T := R^{-T} M^T, a left solve with the lower-triangular column-major view of R.
+static int trsm_right_upper(scb_ctx* ctx, int h, const double* R, double* M, cudaStream_t s) {
+  cublasHandle_t hd = (cublasHandle_t)ctx->blas;
+  SCB_REQUIRE(cublasSetStream(hd, s) == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasSetStream failed");
+  const double one = 1.0;
+  const cublasStatus_t st = cublasDtrsm(hd, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                                        CUBLAS_DIAG_NON_UNIT, kB, h, &one, R, kB, M, kB);
+  SCB_REQUIRE(st == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasDtrsm failed (%d)", (int)st);
+  return SCB_OK;
+}
+
 // ------------------------------------------------------------------ covariance
 __global__ void cov_build_kernel(const double* __restrict__ Cg, int hp, int h, int ones_col, int64_t n,
                                  double* __restrict__ cov, double* __restrict__ mean) {
@@ -79,24 +91,28 @@ __global__ void init_block_kernel(double* __restrict__ Q, int h) {
 
 // ------------------------------------------------------------------ Cholesky QR
 // In place Cholesky of the kB x kB Gram S = Q^T Q (one CTA), S -> R (upper, row-major).
-__global__ void __launch_bounds__(256) chol_kernel(double* __restrict__ S, int* __restrict__ fail) {
+constexpr int kCholThreads = 1024;  // 32 x 32 thread grid over the trailing matrix
+__global__ void __launch_bounds__(kCholThreads) chol_kernel(double* __restrict__ S, int* __restrict__ fail) {
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) a[e / kB][e % kB] = S[e];
   __syncthreads();
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int k = 0; k < kB; ++k) {
+    // every thread derives the pivot itself (no extra barrier): row k of R = a[k][j] / sqrt(a_kk)
+    double d = a[k][k];
+    if (!(d > 0.0)) d = 1e-300;
+    const double r = sqrt(d), inv = 1.0 / r;
+    __syncthreads();  // all pivots read before row k is rescaled
     if (threadIdx.x == 0) {
-      double d = a[k][k];
-      if (!(d > 0.0)) { *fail = 1; d = 1e-300; }
-      a[k][k] = sqrt(d);
+      if (!(a[k][k] > 0.0)) *fail = 1;
+      a[k][k] = r;
     }
+    for (int j = k + 1 + threadIdx.x; j < kB; j += blockDim.x) a[k][j] *= inv;
     __syncthreads();
-    const double inv = 1.0 / a[k][k];
-    for (int j = k + 1 + threadIdx.x; j < kB; j += blockDim.x) a[k][j] *= inv;  // row k of R
-    __syncthreads();
-    for (int e = threadIdx.x; e < (kB - k - 1) * (kB - k - 1); e += blockDim.x) {
-      const int i = k + 1 + e / (kB - k - 1), j = k + 1 + e % (kB - k - 1);
-      if (j >= i) a[i][j] -= a[k][i] * a[k][j];
+    for (int i = k + 1 + ty; i < kB; i += 32) {
+      const double aki = a[k][i];
+      for (int j = i + tx; j < kB; j += 32) a[i][j] -= aki * a[k][j];
     }
     __syncthreads();
   }
@@ -106,23 +122,6 @@ __global__ void __launch_bounds__(256) chol_kernel(double* __restrict__ S, int* 
   }
 }
 
-// Rinv = R^{-1} for the upper-triangular kB x kB R (one CTA; column j solved by thread j:
-// R x = e_j by back substitution over the smem copy of R).
-__global__ void __launch_bounds__(kB) triinv_kernel(const double* __restrict__ R, double* __restrict__ Rinv) {
-  extern __shared__ double dyn[];
-  double (*r)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
-  double (*x)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn + kB * kLd);
-  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) r[e / kB][e % kB] = R[e];
-  __syncthreads();
-  const int j = threadIdx.x;
-  for (int i = kB - 1; i >= 0; --i) {
-    double v = (i == j) ? 1.0 : 0.0;
-    for (int l = i + 1; l <= j; ++l) v -= r[i][l] * x[l][j];
-    x[i][j] = (i <= j) ? v / r[i][i] : 0.0;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) Rinv[e] = x[e / kB][e % kB];
-}
 
 // ------------------------------------------------------------------ Jacobi (one CTA)
 // Cyclic two-sided Jacobi on the symmetric kB x kB matrix T; W accumulates rotations.
@@ -334,7 +333,6 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   const int kSmemKB = kB * kLd * 8;
   SCB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemKB));
   SCB_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSmemKB));
-  SCB_CUDA(cudaFuncSetAttribute(triinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSmemKB));
   // workspace: cov h*h, Q h*kB, Y h*kB, S kB*kB, W kB*kB, Wk kB*n, V h*n, CV h*n, mean h, misc
   const size_t nd = (size_t)h * h + 2 * (size_t)h * kB + 3 * kB * kB + (size_t)kB * kB + 2 * (size_t)h * kB +
                     h + 4 * kB + 64;
@@ -344,7 +342,7 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   double* Q = cov + (size_t)h * h;
   double* Y = Q + (size_t)h * kB;
   double* S = Y + (size_t)h * kB;
-  double* W = S + 2 * kB * kB;  // S, Rinv
+  double* W = S + 2 * kB * kB;
   double* Wk = W + kB * kB;
   double* V = Wk + (size_t)kB * kB;
   double* CV = V + (size_t)h * kB;
@@ -362,16 +360,12 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   init_block_kernel<<<h, kB, 0, s>>>(Q, h);
   SCB_LAUNCH_CHECK();
   SCB_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
-  double* Rinv = S + kB * kB;  // scratch: W is only needed inside rayleigh_ritz
   auto orth = [&](double*& M, int reps) -> int {
     for (int rep = 0; rep < reps; ++rep) {  // CholQR(reps): M := M R^{-1}
       SCB_TRY(dgemm(ctx, kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s));
-      chol_kernel<<<1, 256, kSmemKB, s>>>(S, fail);
+      chol_kernel<<<1, kCholThreads, kSmemKB, s>>>(S, fail);
       SCB_LAUNCH_CHECK();
-      triinv_kernel<<<1, kB, 2 * kSmemKB, s>>>(S, Rinv);
-      SCB_LAUNCH_CHECK();
-      SCB_TRY(dgemm(ctx, h, kB, kB, M, kB, 0, Rinv, kB, 0, Y, kB, s));
-      std::swap(M, Y);
+      SCB_TRY(trsm_right_upper(ctx, h, S, M, s));  // M := M R^{-1} in place
     }
     return SCB_OK;
   };
