@@ -1,9 +1,12 @@
 #!/bin/bash
-# bench (1M) + ncu launch list of the same command + one --set full capture of the kNN kernel
+# bench (1M) + ncu launch list of the same command (input generation excluded) + one --set full
+# capture of the kNN candidates kernel
 set -x
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:^(?!.*(synth|sgemm)).*' -c 400 --csv \
+    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:knn_candidates -c 1 -o gpurun_out/knn_full_1m \
     python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_knn.log 2>&1
-tail -c 600 gpurun_out/bench.json
+tail -2 gpurun_out/pytest_gpu.log
+tail -c 400 gpurun_out/bench.json
