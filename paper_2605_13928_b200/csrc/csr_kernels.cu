@@ -27,6 +27,7 @@ static int grid_for(scb_ctx* ctx, int ctas_per_sm) { return ctx->num_sms * ctas_
 // CTAs also write the per-cell metrics and, for the HVG pass, the per-row positions where
 // the original gene index crosses each HVG tile boundary (splits[r][t-1] = #entries with
 // gene < t*split_w, relative to the row start).
+template <int NSPLIT>
 __global__ void __launch_bounds__(kQcThreads)
 qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
           const float* __restrict__ data, int64_t n_rows, int32_t n_cols,
@@ -61,16 +62,16 @@ qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indice
     const int64_t b = indptr[r], e = indptr[r + 1];
     uint32_t cnt = 0;
     unsigned long long sum = 0, summt = 0;
-    int sc[kMaxSplit] = {0, 0, 0};
+    int sc[NSPLIT > 0 ? NSPLIT : 1] = {};
     stream_row<2>(indices, data, b, e, nnz, [&](const Quad& q) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (!((q.valid >> k) & 1u)) continue;
         const int g = q.g[k];
         const float x = q.x[k];
-        bad |= !(x >= 0.0f && x == rintf(x) && x < 16777216.0f) || g < 0 || g >= n_cols;
+        bad |= !(x >= 0.0f && x == rintf(x) && x < 16777216.0f) || (unsigned)g >= (unsigned)n_cols;
 #pragma unroll
-        for (int t = 0; t < kMaxSplit; ++t) sc[t] += (t < n_split && g < (t + 1) * split_w) ? 1 : 0;
+        for (int t = 0; t < NSPLIT; ++t) sc[t] += (g < (t + 1) * split_w) ? 1 : 0;
         if (x > 0.0f && !bad) {
           const uint32_t xv = (uint32_t)x;
           cnt += 1;
@@ -79,8 +80,10 @@ qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indice
           const int gl = g - g0;
           if (gl >= 0 && gl < w) {
             atomicAdd(&s_cells[gl], 1u);
-            const uint32_t old = atomicAdd(&s_tot[gl], xv);
-            if (old > 0xffffffffu - xv) atomicAdd(&g_total[g], 1ull << 32);  // rare carry
+            // low 12 bits in smem (fire-and-forget: <= 2^20 rows per CTA keep the word below
+            // 2^32), the rare higher part straight into the global u64 total
+            atomicAdd(&s_tot[gl], xv & 0xFFFu);
+            if (xv > 0xFFFu) atomicAdd(&g_total[g], (unsigned long long)(xv & ~0xFFFu));
           }
         }
       }
@@ -90,14 +93,15 @@ qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indice
       sum = warp_sum(sum);
       summt = warp_sum(summt);
 #pragma unroll
-      for (int t = 0; t < kMaxSplit; ++t) sc[t] = warp_sum(sc[t]);
+      for (int t = 0; t < NSPLIT; ++t) sc[t] = warp_sum(sc[t]);
       if (lane == 0) {
         n_genes[r] = (int32_t)cnt;
         const double sd = (double)sum, md = (double)summt;
         total[r] = sd;
         total_mt[r] = md;
         pct[r] = __ddiv_rn(__dmul_rn(100.0, md), sd);
-        for (int t = 0; t < n_split; ++t) splits[r * n_split + t] = sc[t];
+#pragma unroll
+        for (int t = 0; t < NSPLIT; ++t) splits[r * NSPLIT + t] = sc[t];
       }
     }
   }
@@ -762,13 +766,23 @@ extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t
   SCB_CUDA(cudaMemsetAsync(ws, 0, ws_bytes + 8, s));
   SCB_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), s));
   const size_t smem = (size_t)tile_w * 8 + (size_t)mt_words * 4;
-  SCB_CUDA(cudaFuncSetAttribute(qc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int n_split = hvg_row_splits ? n_tiles_hvg - 1 : 0;
   if (n_rows > 0) {
-    dim3 grid(grid_for(ctx, 1), n_tiles);
-    qc_kernel<<<grid, kQcThreads, smem, s>>>(indptr, indices, data, n_rows, n_cols, mt_mask, tile_w, n_split,
-                                             kHvgTileW, hvg_row_splits, n_genes, total, total_mt, pct, g_cells,
-                                             g_total, ctx->d_flag);
+    // each CTA sees at most 2^20 rows, so its 12-bit partial gene totals cannot overflow a u32
+    dim3 grid((unsigned)std::max<int64_t>(grid_for(ctx, 1), (n_rows + (1 << 20) - 1) >> 20), n_tiles);
+    auto launch = [&](auto kern) {
+      SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<grid, kQcThreads, smem, s>>>(indptr, indices, data, n_rows, n_cols, mt_mask, tile_w, n_split, kHvgTileW,
+                                          hvg_row_splits, n_genes, total, total_mt, pct, g_cells, g_total, ctx->d_flag);
+      return SCB_OK;
+    };
+    static_assert(kMaxSplit == 3, "qc_kernel is instantiated for 0..3 row splits");
+    switch (n_split) {
+      case 0: SCB_TRY(launch(qc_kernel<0>)); break;
+      case 1: SCB_TRY(launch(qc_kernel<1>)); break;
+      case 2: SCB_TRY(launch(qc_kernel<2>)); break;
+      default: SCB_TRY(launch(qc_kernel<3>)); break;
+    }
     SCB_LAUNCH_CHECK();
   }
   qc_finalize<<<ceil_div(n_cols, 256), 256, 0, s>>>(g_cells, g_total, n_cols, n_cells, gene_total);
