@@ -83,3 +83,26 @@ def test_scale(dev_state):
     full = sc.Z.cpu().numpy()
     assert np.all(full[:, sc.ones_col] == 1.0)
     assert np.all(full[:, sc.H + 1:] == 0.0)
+
+
+def test_qc_large_counts_exact():
+    """Counts >= 2^12 take the global high-part path of the gene totals; up to 2^24 - 1."""
+    import torch
+    import paper_2605_13928_b200 as scb
+    from oracle import pipeline as op
+    rng = np.random.default_rng(11)
+    n, g = 3000, 700
+    dense = (rng.random((n, g)) < 0.2) * rng.integers(1, 50, (n, g))
+    big = rng.random((n, g)) < 0.01
+    dense = np.where(big, rng.integers(4096, 1 << 24, (n, g)), dense).astype(np.float32)
+    dense[:, 5] = np.where(dense[:, 5] > 0, (1 << 24) - 1, 0)      # a gene of maximal counts
+    import scipy.sparse as sp
+    A = sp.csr_matrix(dense)
+    X = op.CSR(A.indptr.astype(np.int64), A.indices.astype(np.int32), A.data.astype(np.float32), g)
+    mt = np.zeros(g, np.uint8)
+    mt[:7] = 1
+    ref = op.qc_metrics(X, mt)
+    Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, g)
+    qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
+    for k in ["n_genes_by_counts", "total_counts", "total_counts_mt", "n_cells_by_counts", "gene_total_counts"]:
+        np.testing.assert_array_equal(qc[k].cpu().numpy(), ref[k], err_msg=k)
