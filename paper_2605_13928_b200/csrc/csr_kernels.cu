@@ -634,7 +634,10 @@ hvg_select_kernel(const unsigned long long* __restrict__ sums, int32_t G, int64_
 __global__ void __launch_bounds__(kRowThreads)
 scale_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                   const float* __restrict__ ldata, int64_t n_rows, int32_t n_cols,
-                  const int32_t* __restrict__ slot, int32_t n_slots, unsigned long long* __restrict__ sums) {
+                  const int32_t* __restrict__ slot, int32_t n_slots, int64_t rows_per_block,
+                  unsigned long long* __restrict__ sums) {
+  // CTA = block of <= 1024 rows: the carry-free (22-bit low, high) split of every fixed-point
+  // value keeps both u32 words below 2^32, so all smem atomics are fire-and-forget
   const int64_t nnz = indptr[n_rows];
   extern __shared__ uint32_t sm[];
   int16_t* s_slot = reinterpret_cast<int16_t*>(sm + 4 * n_slots);
@@ -645,8 +648,9 @@ scale_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
   uint32_t* s1hi = sm + n_slots;
   uint32_t* s2lo = sm + 2 * n_slots;
   uint32_t* s2hi = sm + 3 * n_slots;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r1 = min(n_rows, r0 + rows_per_block);
+  for (int64_t r = r0 + warp_id(); r < r1; r += (blockDim.x >> 5)) {
     stream_row<4>(indices, ldata, indptr[r], indptr[r + 1], nnz, [&](const Quad& q) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -654,18 +658,25 @@ scale_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         const int j = s_slot[q.g[k]];
         if (j >= 0) {
           const double l = (double)q.x[k];
-          fx_add(&s1lo[j], &s1hi[j], fx_round(l * 268435456.0));        // l * 2^28
-          fx_add(&s2lo[j], &s2hi[j], fx_round((l * l) * 16777216.0));    // l^2 * 2^24
+          const uint64_t v1 = fx_round(l * 268435456.0);        // l * 2^28
+          const uint64_t v2 = fx_round((l * l) * 16777216.0);   // l^2 * 2^24
+          atomicAdd(&s1lo[j], (uint32_t)(v1 & 0x3FFFFFu));
+          atomicAdd(&s1hi[j], (uint32_t)(v1 >> 22));
+          atomicAdd(&s2lo[j], (uint32_t)(v2 & 0x3FFFFFu));
+          atomicAdd(&s2hi[j], (uint32_t)(v2 >> 22));
         }
       }
     });
   }
   __syncthreads();
+  // limbs: value = limb0 + limb1 * 2^32; a word pair holds lo + hi * 2^22
   for (int i = threadIdx.x; i < n_slots; i += blockDim.x) {
-    if (s1lo[i]) atomicAdd(&sums[i], (unsigned long long)s1lo[i]);
-    if (s1hi[i]) atomicAdd(&sums[n_slots + i], (unsigned long long)s1hi[i]);
-    if (s2lo[i]) atomicAdd(&sums[2 * n_slots + i], (unsigned long long)s2lo[i]);
-    if (s2hi[i]) atomicAdd(&sums[3 * n_slots + i], (unsigned long long)s2hi[i]);
+    const unsigned long long a0 = (unsigned long long)s1lo[i] + ((unsigned long long)(s1hi[i] & 1023u) << 22);
+    const unsigned long long b0 = (unsigned long long)s2lo[i] + ((unsigned long long)(s2hi[i] & 1023u) << 22);
+    if (a0) atomicAdd(&sums[i], a0);
+    if (s1hi[i] >> 10) atomicAdd(&sums[n_slots + i], (unsigned long long)(s1hi[i] >> 10));
+    if (b0) atomicAdd(&sums[2 * n_slots + i], b0);
+    if (s2hi[i] >> 10) atomicAdd(&sums[3 * n_slots + i], (unsigned long long)(s2hi[i] >> 10));
   }
 }
 
@@ -925,9 +936,9 @@ extern "C" int scb_scale_gene_sums(scb_ctx* ctx, const int64_t* indptr, const in
   SCB_REQUIRE(smem <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_scale_gene_sums: too many genes for one CTA");
   if (n_rows == 0) return SCB_OK;
   SCB_CUDA(cudaFuncSetAttribute(scale_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int per_sm = std::max(1, std::min(4, (int)(kSmemLimit / (smem + 1024))));
-  scale_sums_kernel<<<grid_for(ctx, per_sm), kRowThreads, smem, (cudaStream_t)stream>>>(
-      indptr, indices, ldata, n_rows, n_cols, slot, n_slots, (unsigned long long*)sums);
+  const int64_t rpb = 1024;  // <= 1024 rows per CTA (carry-free fixed point)
+  scale_sums_kernel<<<(unsigned)((n_rows + rpb - 1) / rpb), kRowThreads, smem, (cudaStream_t)stream>>>(
+      indptr, indices, ldata, n_rows, n_cols, slot, n_slots, rpb, (unsigned long long*)sums);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
