@@ -180,10 +180,17 @@ def main():
     from paper_2605_13928_b200.dist import Comm, shard_rows
     from paper_2605_13928_b200.pp import DeviceCSR
 
+    local = local % max(1, torch.cuda.device_count())  # (functional multi-rank check on one GPU)
     torch.cuda.set_device(local)
     comm = None
     if world > 1:
-        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # SCB_DIST_BACKEND=gloo: functional check of the multi-rank path where only one GPU is
+        # available (collectives through host copies; not a timing configuration)
+        backend = os.environ.get("SCB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            td.init_process_group(backend)
         comm = Comm()
     p = _params(args)
     N, G = args.cells, args.genes
@@ -238,6 +245,7 @@ def main():
 
     # ---- sizes for the roofline bookkeeping
     Z_in = X.nnz
+    Z_total = Z_in if comm is None else comm.allreduce_int(Z_in)
     N_sub_loc = res.X_log.n_rows
     Z_sub = res.X_log.nnz
     H = int(res.hvg_index.numel())
@@ -341,9 +349,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic NB counts generated on device (oracle/synth.py model, seed %d)" % args.seed,
-            "config": {"workload": f"C3: {N} cells x {G} genes (~{Z_in * world / N / G:.1%} dense), full QC->normalize->"
+            "config": {"workload": f"C3: {N} cells x {G} genes (~{Z_total / N / G:.1%} dense), full QC->normalize->"
                                    f"log1p->HVG(seurat,{args.hvg})->scale->PCA(50)->kNN(k={args.k}, exact)",
-                       "cells": N, "genes": G, "nnz": int(Z_in * world), "kept_cells": int(n_keys), "hvg": H,
+                       "cells": N, "genes": G, "nnz": int(Z_total), "kept_cells": int(n_keys), "hvg": H,
                        "parallelism": f"cells sharded x{world}", "l2": "inputs (14 GB) >> L2 (126 MB); no flush needed",
                        "gen_seconds": round(gen_s, 1)},
             "step_ms": {kk: round(v, 3) for kk, v in step_ms.items()},
