@@ -346,10 +346,18 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
           const double yd = (double)y;
           // carry-free split: low 22 bits + high part; with <= 1024 rows per CTA neither u32
           // word can overflow, so both adds are fire-and-forget (no returned value needed)
-          const uint64_t v1 = fx_round(yd * 268435456.0);        // y * 2^28   (< 2^42)
+          const uint64_t v1 = fx_round(yd * 268435456.0);        // y * 2^28
           const uint64_t v2 = fx_round((yd * yd) * 16777216.0);   // y^2 * 2^24
-          atomicAdd(&s1lo[gl], (uint32_t)(v1 & 0x3FFFFFu));
-          atomicAdd(&s1hi[gl], (uint32_t)(v1 >> 22));
+          if (v1 < (1ull << 43)) {  // y < 2^15 (target_sum 1e4 bounds y by 1e4)
+            atomicAdd(&s1lo[gl], (uint32_t)(v1 & 0x3FFFFFu));
+            atomicAdd(&s1hi[gl], (uint32_t)(v1 >> 22));
+          } else {  // rare huge y (e.g. CPM normalization): straight into the global limbs
+            const int go = remap ? remap[q.g[k]] : q.g[k];
+            if (go >= 0) {
+              atomicAdd(&sums[go], v1 & 0xFFFFFFFFull);
+              atomicAdd(&sums[n_out + go], v1 >> 32);
+            }
+          }
           atomicAdd(&s2lo[gl], (uint32_t)(v2 & 0x3FFFFFu));
           const uint64_t h2 = v2 >> 22;
           if (h2 < (1ull << 21)) {
@@ -660,10 +668,22 @@ scale_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
           const double l = (double)q.x[k];
           const uint64_t v1 = fx_round(l * 268435456.0);        // l * 2^28
           const uint64_t v2 = fx_round((l * l) * 16777216.0);   // l^2 * 2^24
-          atomicAdd(&s1lo[j], (uint32_t)(v1 & 0x3FFFFFu));
-          atomicAdd(&s1hi[j], (uint32_t)(v1 >> 22));
-          atomicAdd(&s2lo[j], (uint32_t)(v2 & 0x3FFFFFu));
-          atomicAdd(&s2hi[j], (uint32_t)(v2 >> 22));
+          // high words stay below 2^32 for values < 2^43 (|l| < 2^15, l^2 < 2^19); larger ones
+          // (not log-normalized data) go straight to the global limbs
+          if (v1 < (1ull << 43)) {
+            atomicAdd(&s1lo[j], (uint32_t)(v1 & 0x3FFFFFu));
+            atomicAdd(&s1hi[j], (uint32_t)(v1 >> 22));
+          } else {
+            atomicAdd(&sums[j], v1 & 0xFFFFFFFFull);
+            atomicAdd(&sums[n_slots + j], v1 >> 32);
+          }
+          if (v2 < (1ull << 43)) {
+            atomicAdd(&s2lo[j], (uint32_t)(v2 & 0x3FFFFFu));
+            atomicAdd(&s2hi[j], (uint32_t)(v2 >> 22));
+          } else {
+            atomicAdd(&sums[2 * n_slots + j], v2 & 0xFFFFFFFFull);
+            atomicAdd(&sums[3 * n_slots + j], v2 >> 32);
+          }
         }
       }
     });

@@ -106,3 +106,26 @@ def test_qc_large_counts_exact():
     qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
     for k in ["n_genes_by_counts", "total_counts", "total_counts_mt", "n_cells_by_counts", "gene_total_counts"]:
         np.testing.assert_array_equal(qc[k].cpu().numpy(), ref[k], err_msg=k)
+
+
+def test_cpm_normalization_hvg_and_scale_exact():
+    """target_sum = 1e6 (CPM): normalized values beyond 2^15 take the global-limb path of the
+    HVG sums; the statistics stay bit-exact and the scaled values within tolerance."""
+    import dataclasses
+    import torch
+    import paper_2605_13928_b200 as scb
+    from oracle import pipeline as op
+    X, mt = c1_inputs()
+    p = dataclasses.replace(C1["params"], target_sum=1e6)
+    o = op.run(X, mt, p, with_knn=False)
+    Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, X.n_cols)
+    qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
+    cm, gm, kept = scb.filter_masks(qc, p.min_genes, p.max_genes, p.max_pct_mt, p.min_cells)
+    Xl = scb.normalize_log1p(scb.subset(Xd, cm, gm, kept), p.target_sum)
+    hvg_mask, hvg_index, st = scb.highly_variable_genes(Xl, p.n_top_genes, p.n_bins)
+    np.testing.assert_array_equal(hvg_mask.cpu().numpy(), o["hvg_mask"])
+    np.testing.assert_array_equal(st["means"].cpu().numpy(), o["hvg_stats"]["means"])
+    np.testing.assert_array_equal(st["variances"].cpu().numpy(), o["hvg_stats"]["variances"])
+    sc = scb.scale(Xl, hvg_index, p.max_value)
+    np.testing.assert_allclose(sc.mean.cpu().numpy(), o["scale_mean"], rtol=1e-7)
+    np.testing.assert_allclose(sc.inv_std.cpu().numpy(), o["scale_inv_std"], rtol=1e-7)
