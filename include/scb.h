@@ -145,9 +145,10 @@ SCB_API int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* 
                     float* Z, int64_t ldz, int32_t ones_col, void* stream);
 
 /* ---- a7: partial Gram matrix C = Z^T Z (float64 [hp][hp], full symmetric) on the
- * 5th-gen tensor cores (tcgen05, 3xTF32 split products, FP32 accumulate in TMEM per
- * <=64k-cell K-slice, slices summed in float64; operands staged by TMA).  hp = ldz must
- * be a multiple of 128; n_rows any. */
+ * 5th-gen tensor cores (tcgen05 kind::f16, "3xBF16": x = hi + lo with hi = bf16(x),
+ * lo = bf16(x - hi), products hi*hi + hi*lo + lo*hi, <= 2^-16 relative each; FP32 accumulate
+ * in TMEM per <=64k-cell K-slice, slices summed in float64; operands staged by TMA).
+ * hp = ldz must be a multiple of 128; n_rows any. */
 SCB_API int scb_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp, double* C, void* stream);
 
 /* ---- a8: top-n_comps eigenpairs of the centred covariance
@@ -166,9 +167,12 @@ SCB_API int scb_project(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp
 
 /* ---- a9: sc.pp.neighbors(n_neighbors=k, method exact, metric euclidean): for each query
  * row, the k nearest key rows (self included) ordered by (distance, index).  Candidate
- * distances on tcgen05 (TF32) with a fused per-row top-k_cand, then exact FP32 re-rank.
- * queries/keys float32 [n][ld] (ld = 64, columns >= d zero); key_offset = global index of
- * keys[0] is added to the reported indices' base for sharded queries (0 single GPU). */
+ * scores on tcgen05 (kind::f16 operands, FP32 accumulate) with a fused per-row candidate
+ * top-list, then exact FP32 re-rank.  k_cand (32 or 64, >= k) is the minimum candidate
+ * count: k <= 16 keeps two 16-entry lists per row (one per key-column half; the top-k of
+ * the union lies in the union of the per-half top-16), 16 < k <= 32 one 48-entry list,
+ * k <= 64 one 64-entry list.  queries/keys float32 [n][ld] (d + 2 <= 64, columns >= d
+ * ignored); for sharded queries pass the full key matrix (returned indices index keys). */
 SCB_API int scb_knn(scb_ctx* ctx, const float* queries, int64_t n_queries, const float* keys,
             int64_t n_keys, int32_t d, int32_t ld, int32_t k, int32_t k_cand,
             int32_t* knn_index, float* knn_dist, void* stream);
