@@ -209,6 +209,13 @@ __global__ void gram_reduce_kernel(const float* __restrict__ partial, int slices
   C[(size_t)j * hp + i] = s;
 }
 
+// Cells per K-slice.  tcgen05's FP32 accumulation truncates toward zero; with kind::f16 MMAs
+// the Gram loses ~2.4 ulp per MMA (measured: 64k-cell slices -> 4.6e-4 relative error on the
+// diagonal and a PCA subspace angle of 7.8e-4 at C2; 16k -> 1.9e-4 / 3.6e-4; 8k -> 1.1e-4 /
+// 2.2e-4, scratch/gram_precision.py).  The slices are summed in fp64; 8k cells costs ~2 GB of
+// partials at 1M cells and no measurable time.
+constexpr int64_t kSliceCells = 8192;
+
 template <int BN>
 static int launch_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int hp, double* C, cudaStream_t s) {
   using Cfg = GramCfg<BN>;
@@ -220,10 +227,9 @@ static int launch_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int hp, dou
     for (int bj = 0; bj < hp / BN; ++bj)
       if (bj * BN + BN - 1 >= bi * Cfg::BM) tl.push_back(make_int2(bi, bj));
   const int n_tiles = (int)tl.size();
-  // K-slices: fill the SMs and keep each fp32 TMEM accumulation <= 64k cells (the slices
-  // are summed in fp64), which bounds the fp32 accumulation error at ~1e-6 relative.
+  // K-slices: fill the SMs and keep each fp32 TMEM accumulation <= kSliceCells cells
   const int64_t kbs = (n_rows + Cfg::KB - 1) / Cfg::KB;
-  int64_t sl = std::max<int64_t>((ctx->num_sms + n_tiles - 1) / n_tiles, (n_rows + 65535) / 65536);
+  int64_t sl = std::max<int64_t>((ctx->num_sms + n_tiles - 1) / n_tiles, (n_rows + kSliceCells - 1) / kSliceCells);
   const int slices = (int)std::max<int64_t>(1, std::min<int64_t>(sl, kbs));
   const int64_t rows_per_slice = ((kbs + slices - 1) / slices) * Cfg::KB;
   const size_t part_bytes = (size_t)slices * hp * hp * 4;
