@@ -9,6 +9,7 @@
 // largest-|loading| entry of every component is positive (first index on ties).
 #include <cstdlib>
 #include <cublas_v2.h>
+#include <cusolverDn.h>
 #include "common.cuh"
 
 namespace scb {
@@ -48,6 +49,56 @@ static int trsm_right_upper(scb_ctx* ctx, int h, const double* R, double* M, cud
   const cublasStatus_t st = cublasDtrsm(hd, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
                                         CUBLAS_DIAG_NON_UNIT, kB, h, &one, R, kB, M, kB);
   SCB_REQUIRE(st == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasDtrsm failed (%d)", (int)st);
+  return SCB_OK;
+}
+
+// M[h][kB] (row-major) := an orthonormal basis of its column space by Householder QR
+// (cuSOLVER geqrf + orgqr on the column-major transpose, via cublasDgeam); robust to rank
+// deficiency.  tmp: h * kB doubles.  Used only when CholQR breaks down.
+static int householder_orth(scb_ctx* ctx, int h, double* M, double* tmp, cudaStream_t s) {
+  if (!ctx->solver) {
+    cusolverDnHandle_t sh;
+    SCB_REQUIRE(cusolverDnCreate(&sh) == CUSOLVER_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cusolverDnCreate failed");
+    ctx->solver = sh;
+  }
+  cusolverDnHandle_t sh = (cusolverDnHandle_t)ctx->solver;
+  cublasHandle_t bh = (cublasHandle_t)ctx->blas;
+  SCB_REQUIRE(cusolverDnSetStream(sh, s) == CUSOLVER_STATUS_SUCCESS && cublasSetStream(bh, s) == CUBLAS_STATUS_SUCCESS,
+              SCB_ERR_CUDA, "scb_pca_eig: set stream failed");
+  const double one = 1.0, zero = 0.0;
+  // row-major M[h][kB] is column-major kB x h; tmp := its transpose (column-major h x kB)
+  SCB_REQUIRE(cublasDgeam(bh, CUBLAS_OP_T, CUBLAS_OP_N, h, kB, &one, M, kB, &zero, tmp, h, tmp, h) ==
+                  CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: geam failed");
+  int lw1 = 0, lw2 = 0;
+  SCB_REQUIRE(cusolverDnDgeqrf_bufferSize(sh, h, kB, tmp, h, &lw1) == CUSOLVER_STATUS_SUCCESS, SCB_ERR_CUDA,
+              "scb_pca_eig: geqrf_bufferSize failed");
+  void* ws;
+  const size_t need = (size_t)(kB + std::max(lw1, 1)) * 8 + 64;
+  SCB_TRY(ws_get(ctx, 3, need, &ws, s));
+  double* tau = (double*)ws;
+  double* work = tau + kB;
+  int* info = (int*)((char*)ws + need - 16);
+  SCB_REQUIRE(cusolverDnDgeqrf(sh, h, kB, tmp, h, tau, work, lw1, info) == CUSOLVER_STATUS_SUCCESS, SCB_ERR_CUDA,
+              "scb_pca_eig: geqrf failed");
+  SCB_REQUIRE(cusolverDnDorgqr_bufferSize(sh, h, kB, kB, tmp, h, tau, &lw2) == CUSOLVER_STATUS_SUCCESS, SCB_ERR_CUDA,
+              "scb_pca_eig: orgqr_bufferSize failed");
+  if (lw2 > lw1) {
+    const size_t need2 = (size_t)(kB + lw2) * 8 + 64;
+    SCB_TRY(ws_get(ctx, 3, need2, &ws, s));
+    tau = (double*)ws;  // tau must survive: recompute geqrf into the larger buffer
+    work = tau + kB;
+    info = (int*)((char*)ws + need2 - 16);
+    SCB_REQUIRE(cublasDgeam(bh, CUBLAS_OP_T, CUBLAS_OP_N, h, kB, &one, M, kB, &zero, tmp, h, tmp, h) ==
+                    CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: geam failed");
+    SCB_REQUIRE(cusolverDnDgeqrf(sh, h, kB, tmp, h, tau, work, lw2, info) == CUSOLVER_STATUS_SUCCESS, SCB_ERR_CUDA,
+                "scb_pca_eig: geqrf failed");
+    lw1 = lw2;
+  }
+  SCB_REQUIRE(cusolverDnDorgqr(sh, h, kB, kB, tmp, h, tau, work, std::max(lw1, lw2), info) == CUSOLVER_STATUS_SUCCESS,
+              SCB_ERR_CUDA, "scb_pca_eig: orgqr failed");
+  // back to row-major M[h][kB]: column-major kB x h = transpose of tmp
+  SCB_REQUIRE(cublasDgeam(bh, CUBLAS_OP_T, CUBLAS_OP_N, kB, h, &one, tmp, h, &zero, M, kB, M, kB) ==
+                  CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: geam failed");
   return SCB_OK;
 }
 
@@ -321,9 +372,10 @@ __global__ void mean_out_kernel(const double* __restrict__ m, int h, int hp, flo
 
 using namespace scb;
 
-extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, int32_t ones_col, int64_t n_cells,
-                           int32_t n_comps, int32_t n_comps_pad, double* eigenvalues, float* components_t,
-                           float* col_mean, double* trace, void* stream) {
+static int pca_eig_impl(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, int32_t ones_col, int64_t n_cells,
+                        int32_t n_comps, int32_t n_comps_pad, double* eigenvalues, float* components_t,
+                        float* col_mean, double* trace, void* stream, bool use_qr, bool* broke) {
+  *broke = false;
   SCB_REQUIRE(ctx && C && eigenvalues && components_t && col_mean && trace, SCB_ERR_ARG, "scb_pca_eig: null argument");
   SCB_REQUIRE(n_comps >= 1 && n_comps <= kB - 16 && n_comps <= h && n_comps_pad >= n_comps, SCB_ERR_ARG,
               "scb_pca_eig: need 1 <= n_comps <= %d and <= h", kB - 16);
@@ -361,6 +413,7 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   SCB_LAUNCH_CHECK();
   SCB_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
   auto orth = [&](double*& M, int reps) -> int {
+    if (use_qr) return householder_orth(ctx, h, M, Y, s);  // rank-deficient fallback
     for (int rep = 0; rep < reps; ++rep) {  // CholQR(reps): M := M R^{-1}
       SCB_TRY(dgemm(ctx, kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s));
       chol_kernel<<<1, kCholThreads, kSmemKB, s>>>(S, fail);
@@ -433,7 +486,13 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
     SCB_CUDA(cudaMemcpyAsync(host_res, res, sizeof(double) * n_comps, cudaMemcpyDeviceToHost, s));
     SCB_CUDA(cudaMemcpyAsync(&lam0, lam_all, sizeof(double), cudaMemcpyDeviceToHost, s));
     SCB_CUDA(cudaMemcpyAsync(&lamb, lam_all + kB - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+    int hfail_now = 0;
+    SCB_CUDA(cudaMemcpyAsync(&hfail_now, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
     SCB_CUDA(cudaStreamSynchronize(s));
+    if (hfail_now) {  // Cholesky-QR broke down (block rank-deficient): caller retries with QR
+      *broke = true;
+      return SCB_OK;
+    }
     cheb_b = std::max(lamb, 1e-12 * lam0);
     double worst = 0.0;  // max residual / lambda_1 of the wanted Ritz pairs
     for (int j = 0; j < n_comps; ++j) worst = std::max(worst, host_res[j]);
@@ -456,7 +515,10 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   int hfail = 0;
   SCB_CUDA(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
   SCB_CUDA(cudaStreamSynchronize(s));
-  SCB_REQUIRE(hfail == 0, SCB_ERR_DATA, "scb_pca_eig: Cholesky-QR breakdown (rank-deficient subspace)");
+  if (hfail) {
+    *broke = true;
+    return SCB_OK;
+  }
   SCB_CUDA(cudaMemcpyAsync(eigenvalues, lam_all, sizeof(double) * n_comps, cudaMemcpyDeviceToDevice, s));
   finalize_components_kernel<<<n_comps, 256, 0, s>>>(V, h, n_comps, hp, n_comps_pad, components_t);
   SCB_LAUNCH_CHECK();
@@ -466,5 +528,21 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
   }
   mean_out_kernel<<<(hp + 255) / 256, 256, 0, s>>>(mean, h, hp, col_mean);
   SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
+extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, int32_t ones_col, int64_t n_cells,
+                           int32_t n_comps, int32_t n_comps_pad, double* eigenvalues, float* components_t,
+                           float* col_mean, double* trace, void* stream) {
+  // CholQR2 orthonormalisation; if the block turns rank-deficient (fewer than kB + 1 cells, or
+  // duplicated cells: the covariance has rank < kB) the solve is redone with Householder QR,
+  // which completes the basis with arbitrary orthonormal directions
+  bool broke = false;
+  SCB_TRY(pca_eig_impl(ctx, C, h, hp, ones_col, n_cells, n_comps, n_comps_pad, eigenvalues, components_t, col_mean,
+                       trace, stream, false, &broke));
+  if (!broke) return SCB_OK;
+  SCB_TRY(pca_eig_impl(ctx, C, h, hp, ones_col, n_cells, n_comps, n_comps_pad, eigenvalues, components_t, col_mean,
+                       trace, stream, true, &broke));
+  SCB_REQUIRE(!broke, SCB_ERR_DATA, "scb_pca_eig: orthonormalisation breakdown");
   return SCB_OK;
 }

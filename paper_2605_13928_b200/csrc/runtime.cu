@@ -1,5 +1,6 @@
 // Context, scratch arena and error reporting behind the C ABI.
 #include <cublas_v2.h>
+#include <cusolverDn.h>
 #include "common.cuh"
 #include <algorithm>
 #include <atomic>
@@ -79,6 +80,7 @@ extern "C" int scb_ctx_destroy(scb_ctx* ctx) {
     if (w.ptr) cudaFree(w.ptr);
   if (ctx->d_flag) cudaFree(ctx->d_flag);
   if (ctx->blas) cublasDestroy((cublasHandle_t)ctx->blas);
+  if (ctx->solver) cusolverDnDestroy((cusolverDnHandle_t)ctx->solver);
   delete ctx;
   return SCB_OK;
 }
