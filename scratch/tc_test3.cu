@@ -180,7 +180,7 @@ __global__ void k_pingpong(const __half* a, const __half* b, int units, long lon
 
 // smem-operand pressure probe: 2 issuers, NST distinct B stages, distinct A per qtile (SS) or
 // A from TMEM (TS); epilogue arrives immediately.  unit = 2 qtiles x 4 MMAs (128xNx16).
-template <int N, bool TS, int NST>
+template <int N, bool TS, int NST, bool WRITER = false>
 __global__ void k_ops(const __half* a, const __half* b, int units, long long* cyc) {
   extern __shared__ __align__(1024) uint8_t dsm[];
   __half* As = reinterpret_cast<__half*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));  // [2][128*64]
@@ -262,6 +262,14 @@ __global__ void k_ops(const __half* a, const __half* b, int units, long long* cy
       }
       tc::mma_commit(&done[p]);
     }
+  } else if (WRITER && warp >= 10) {
+    // simulated TMA traffic: N * 128 bytes written per unit (one key tile), 2 warps
+    float4* wbuf = reinterpret_cast<float4*>(Bs + NST * N * 64);  // scratch after the B stages
+    const int wl = (warp - 10) * 32 + lane;
+    for (int u = 0; u < units; ++u) {
+      for (int i = wl; i < N * 8; i += 64) wbuf[i & 1023] = make_float4((float)u, 0.f, 0.f, 0.f);
+      __syncwarp();
+    }
   } else if (warp < 10) {
     const int e = warp - 2, t = e >> 2;
     for (int u = 0; u < units; ++u) {
@@ -342,22 +350,20 @@ int main() {
 
   {
     const int units = 4000;
-    auto run2 = [&](auto kern, const char* name, int n, int nst, int grid = 1) {
-      int sm = 1024 + 2 * 128 * 64 * 2 + nst * n * 64 * 2;
+    auto run2 = [&](auto kern, const char* name, int n, int nst, int grid = 1, int threads = 320) {
+      int sm = 1024 + 2 * 128 * 64 * 2 + nst * n * 64 * 2 + 16384;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      kern<<<grid, 320, sm>>>(da, db, units, dc);
+      kern<<<grid, threads, sm>>>(da, db, units, dc);
       cudaError_t e = cudaDeviceSynchronize();
       long long c; cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
       printf("%-30s %.1f cycles/unit, %.1f cycles per 128x128x16-equiv MMA (%s)\n", name, (double)c / units,
              (double)c / units / 8.0 * 128.0 / n, cudaGetErrorString(e));
     };
-    run2(k_ops<128, false, 1>, "SS N128 1 stage", 128, 1);
-    run2(k_ops<128, false, 6>, "SS N128 6 stages", 128, 6);
-    run2(k_ops<128, false, 6>, "SS N128 6 stages grid 148", 128, 6, 148);
-    run2(k_ops<128, false, 6>, "SS N128 6 stages grid 148", 128, 6, 148);
-    run2(k_ops<128, false, 6>, "SS N128 6 stages grid 74", 128, 6, 74);
-    run2(k_ops<96, true, 6>, "TS N96 6 stages", 96, 6);
-    run2(k_ops<96, false, 6>, "SS N96 6 stages", 96, 6);
+    run2(k_ops<128, false, 6>, "SS N128 6st g148", 128, 6, 148);
+    run2(k_ops<128, false, 6, true>, "SS N128 6st g148 +writer", 128, 6, 148, 384);
+    run2(k_ops<96, true, 6>, "TS N96 6st g148", 96, 6, 148);
+    run2(k_ops<96, true, 6, true>, "TS N96 6st g148 +writer", 96, 6, 148, 384);
+    run2(k_ops<96, false, 6, true>, "SS N96 6st g148 +writer", 96, 6, 148, 384);
   }
   return 0;
 }
