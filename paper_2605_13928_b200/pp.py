@@ -142,10 +142,9 @@ def subset(X: DeviceCSR, cell_mask, gene_mask, n_kept=None, target_sum=None):
     return out
 
 
-def subset_normalize(X: DeviceCSR, cell_mask, gene_mask, n_kept, target_sum: float = 1e4):
-    """Fused subset + normalize_total + log1p (two streaming passes over X).  Returns the
-    log-normalized kept matrix, the gene remap (new column or -1) and the per-ORIGINAL-row
-    normalization factor (0 for dropped rows) used by hvg_gene_sums on X itself."""
+def subset_count_scale(X: DeviceCSR, cell_mask, gene_mask, n_kept, target_sum: float = 1e4):
+    """First pass of the fused subset + normalize: gene remap, kept-row offsets, per-kept-row and
+    per-ORIGINAL-row normalization factors (0 for dropped rows).  One host sync (kept nnz)."""
     dev = X.device
     nk, gk = n_kept
     remap = torch.empty(X.n_cols, dtype=torch.int32, device=dev)
@@ -156,11 +155,26 @@ def subset_normalize(X: DeviceCSR, cell_mask, gene_mask, n_kept, target_sum: flo
     _lib.call("scb_subset_count", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols, _p(cell_mask),
               _p(gene_mask), _p(remap), _p(new_indptr), float(target_sum), _p(row_scale), _p(row_scale_orig), s)
     nnz = int(new_indptr[nk].item())
+    return remap, new_indptr, row_scale, row_scale_orig, nnz
+
+
+def subset_fill_log(X: DeviceCSR, cell_mask, remap, new_indptr, row_scale, nnz: int, n_genes_kept: int) -> DeviceCSR:
+    """Second pass: compacted kept matrix with log1p(x * row_scale) values."""
+    dev = X.device
     ind = torch.empty(nnz, dtype=torch.int32, device=dev)
     logv = torch.empty(nnz, dtype=torch.float32, device=dev)
-    _lib.call("scb_subset_fill", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, _p(cell_mask), _p(remap),
-              _p(new_indptr), _p(row_scale), _p(ind), _p(logv), s)
-    return DeviceCSR(new_indptr, ind, logv, gk, row_scale=row_scale), remap, row_scale_orig
+    _lib.call("scb_subset_fill", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, _p(cell_mask),
+              _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(logv), _stream(dev))
+    return DeviceCSR(new_indptr, ind, logv, n_genes_kept, row_scale=row_scale)
+
+
+def subset_normalize(X: DeviceCSR, cell_mask, gene_mask, n_kept, target_sum: float = 1e4):
+    """Fused subset + normalize_total + log1p (two streaming passes over X).  Returns the
+    log-normalized kept matrix, the gene remap (new column or -1) and the per-ORIGINAL-row
+    normalization factor (0 for dropped rows) used by hvg_gene_sums on X itself."""
+    remap, new_indptr, row_scale, row_scale_orig, nnz = subset_count_scale(X, cell_mask, gene_mask, n_kept, target_sum)
+    X_log = subset_fill_log(X, cell_mask, remap, new_indptr, row_scale, nnz, n_kept[1])
+    return X_log, remap, row_scale_orig
 
 
 # ----------------------------------------------------------------------------- norm_hvg
