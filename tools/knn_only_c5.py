@@ -1,5 +1,14 @@
-# C5-style kNN-only: 1M x 50 embedding, k = 30 (k_cand 64 path) and k = 15, timing + recall on a query subset
-import sys, torch, numpy as np
+"""C5 kNN-only stress on one B200: a 1M x 50 Gaussian-mixture embedding (30 clusters, decaying
+per-component spread), k = 15 and k = 30, device time of the whole pp.neighbors call and of the
+candidate kernel, and recall against an exact fp64 brute force on 2000 random queries.  Prints
+one JSON line per k.
+
+usage: python tools/knn_only_c5.py [n]
+"""
+import json
+import sys
+
+import torch
 sys.path.insert(0, ".")
 from paper_2605_13928_b200 import pp
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1000000
@@ -18,4 +27,7 @@ for k in (15, 30):
     D = torch.cdist(X[q].double(), X.double())
     ref = D.topk(k, largest=False).indices
     hit = sum(len(set(ref[i].tolist()) & set(idx[q[i]].tolist())) for i in range(len(q)))
-    print(f"k={k}: total {a.elapsed_time(b):.1f} ms, candidates {t[0].elapsed_time(t[1]):.1f} ms, recall {hit / (len(q) * k):.5f}")
+    print(json.dumps({"config": f"C5 (1 GPU): {n} x 50 embedding, k={k}", "total_ms": round(a.elapsed_time(b), 2),
+                      "candidates_kernel_ms": round(t[0].elapsed_time(t[1]), 2),
+                      "recall_2000_random_queries": hit / (len(q) * k),
+                      "tflops_algorithmic": 2 * n * n * 50 / (t[0].elapsed_time(t[1]) / 1e3) / 1e12}), flush=True)
