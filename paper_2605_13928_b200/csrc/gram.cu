@@ -198,6 +198,138 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
   if (warp == 0) tc::tmem_dealloc<2 * BN>(tmem);
 }
 
+// ---- variant fed by pre-split BF16 planes (written by scb_scale_dense_split): no converter
+// warps and no fp32 staging -- TMA brings the hi and lo boxes straight into the MN-major
+// 128-byte-swizzled operand layout, so shared memory carries only the TMA writes and the MMA
+// operand reads (the fp32 variant is bound by the converter's extra smem traffic).
+template <int BN>
+struct GramSplitCfg {
+  static constexpr int BM = 128;
+  static constexpr int KB = 32;                       // cells per stage = two MMA K steps
+  static constexpr int BOX = KB * 128;                // one [KB cells x 64 genes] BF16 box
+  static constexpr int PLANE = (BM + BN) * KB * 2;    // hi or lo plane of one stage
+  static constexpr int STAGE = 2 * PLANE;
+  static constexpr int STAGES = 4;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static constexpr uint32_t IDESC = tc::idesc_bf16(BM, BN, true, true);
+};
+constexpr int kGramSplitThreads = 32 * 7;  // warp0 TMA, warps 1-2 MMA, warps 3..6 epilogue
+
+template <int BN>
+__global__ void __launch_bounds__(kGramSplitThreads, 1)
+gram_split_kernel(const __grid_constant__ CUtensorMap thi, const __grid_constant__ CUtensorMap tlo,
+                  const int2* __restrict__ tiles, int n_tiles, int64_t n_rows, int64_t rows_per_slice, int hp,
+                  float* __restrict__ partial) {
+  using C = GramSplitCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* done = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int tile = blockIdx.x % n_tiles;
+  const int slice = blockIdx.x / n_tiles;
+  const int2 t = tiles[tile];
+  const int i0 = t.x * C::BM, j0 = t.y * BN;
+  const int64_t k_begin = (int64_t)slice * rows_per_slice;
+  const int64_t k_end = min(n_rows, k_begin + rows_per_slice);
+  const int num_kb = (k_end > k_begin) ? (int)((k_end - k_begin + C::KB - 1) / C::KB) : 0;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch(&thi);
+      tc::tma_prefetch(&tlo);
+      for (int s = 0; s < C::STAGES; ++s) {
+        tc::mbar_init(&full[s], 1);
+        tc::mbar_init(&empty[s], 1);
+      }
+      tc::mbar_init(done, 2);
+      tc::fence_barrier_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<2 * BN>(tmem_slot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int it = 0; it < num_kb; ++it) {
+        const int s = it % C::STAGES;
+        tc::mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+        uint8_t* hi = smem + s * C::STAGE;
+        uint8_t* lo = hi + C::PLANE;
+        const int k0 = (int)(k_begin + (int64_t)it * C::KB);
+        tc::mbar_arrive_expect_tx(&full[s], C::STAGE);
+#pragma unroll
+        for (int c = 0; c < C::BM / 64; ++c) {
+          tc::tma_load_2d(hi + c * C::BOX, &thi, &full[s], i0 + 64 * c, k0);
+          tc::tma_load_2d(lo + c * C::BOX, &tlo, &full[s], i0 + 64 * c, k0);
+        }
+#pragma unroll
+        for (int c = 0; c < BN / 64; ++c) {
+          tc::tma_load_2d(hi + (C::BM / 64 + c) * C::BOX, &thi, &full[s], j0 + 64 * c, k0);
+          tc::tma_load_2d(lo + (C::BM / 64 + c) * C::BOX, &tlo, &full[s], j0 + 64 * c, k0);
+        }
+      }
+    }
+  } else if (warp <= 2) {
+    const int p = warp - 1;  // stage parity: two issuers into two accumulators (see gram_kernel)
+    if (lane == 0) {
+      const uint32_t acc = tmem + p * BN;
+      for (int it = p; it < num_kb; it += 2) {
+        const int s = it % C::STAGES;
+        tc::mbar_wait(&full[s], (it / C::STAGES) & 1);
+        tc::tc_fence_after();
+        const uint32_t ah = tc::smem_u32(smem + s * C::STAGE);
+        const uint32_t bh = ah + (C::BM / 64) * C::BOX;
+        const uint32_t al = ah + C::PLANE;
+        const uint32_t bl = bh + C::PLANE;
+#pragma unroll
+        for (int kk = 0; kk < C::KB / 16; ++kk) {
+          const uint32_t ko = kk * 2048;
+          const uint64_t dah = tc::smem_desc_sw128(ah + ko, C::BOX, 1024);
+          const uint64_t dbh = tc::smem_desc_sw128(bh + ko, C::BOX, 1024);
+          const uint64_t dal = tc::smem_desc_sw128(al + ko, C::BOX, 1024);
+          const uint64_t dbl = tc::smem_desc_sw128(bl + ko, C::BOX, 1024);
+          tc::mma_f16(acc, dah, dbh, C::IDESC, (it > p || kk > 0) ? 1u : 0u);
+          tc::mma_f16(acc, dah, dbl, C::IDESC, 1u);
+          tc::mma_f16(acc, dal, dbh, C::IDESC, 1u);
+        }
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(done);
+    }
+  } else {
+    tc::mbar_wait(done, 0);
+    tc::tc_fence_after();
+    const int q = warp & 3;
+    const int row = i0 + 32 * q + lane;
+    float* out = partial + (size_t)slice * hp * hp + (size_t)row * hp + j0;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t r0[32], r1[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + c * 32, r0);
+      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + BN + c * 32, r1);
+      tc::tmem_ld_wait();
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        v[j] = (num_kb > 0 ? __uint_as_float(r0[j]) : 0.0f) + (num_kb > 1 ? __uint_as_float(r1[j]) : 0.0f);
+      float4* o4 = reinterpret_cast<float4*>(out + c * 32);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<2 * BN>(tmem);
+}
+
 // sum K-slices for i <= j, write C[i][j] and C[j][i] (fixed slice order: deterministic)
 __global__ void gram_reduce_kernel(const float* __restrict__ partial, int slices, int hp, double* __restrict__ C) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -217,30 +349,49 @@ __global__ void gram_reduce_kernel(const float* __restrict__ partial, int slices
 constexpr int64_t kSliceCells = 8192;
 
 template <int BN>
-static int launch_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int hp, double* C, cudaStream_t s) {
-  using Cfg = GramCfg<BN>;
-  CUtensorMap tmap;
-  SCB_TRY(make_tmap_2d_f32(&tmap, Z, (uint64_t)std::max<int64_t>(n_rows, 1), hp, hp, 32, Cfg::KB, /*atom32=*/false));
+static int launch_gram(scb_ctx* ctx, const float* Z, const uint16_t* Zhi, const uint16_t* Zlo, int64_t n_rows, int hp,
+                       double* C, cudaStream_t s) {
+  const bool split = Zhi != nullptr;
+  constexpr int BM = 128;
+  const int KB = split ? GramSplitCfg<BN>::KB : GramCfg<BN>::KB;
+  CUtensorMap tmap, thi, tlo;
+  const uint64_t rows = (uint64_t)std::max<int64_t>(n_rows, 1);
+  if (split) {
+    SCB_TRY(make_tmap_2d(&thi, Zhi, rows, hp, hp, 2, 64, KB, /*atom32=*/false));
+    SCB_TRY(make_tmap_2d(&tlo, Zlo, rows, hp, hp, 2, 64, KB, /*atom32=*/false));
+  } else {
+    SCB_TRY(make_tmap_2d_f32(&tmap, Z, rows, hp, hp, 32, KB, /*atom32=*/false));
+  }
   // upper-triangle tile list
   std::vector<int2> tl;
-  for (int bi = 0; bi < hp / Cfg::BM; ++bi)
+  for (int bi = 0; bi < hp / BM; ++bi)
     for (int bj = 0; bj < hp / BN; ++bj)
-      if (bj * BN + BN - 1 >= bi * Cfg::BM) tl.push_back(make_int2(bi, bj));
+      if (bj * BN + BN - 1 >= bi * BM) tl.push_back(make_int2(bi, bj));
   const int n_tiles = (int)tl.size();
   // K-slices: fill the SMs and keep each fp32 TMEM accumulation <= kSliceCells cells
-  const int64_t kbs = (n_rows + Cfg::KB - 1) / Cfg::KB;
+  const int64_t kbs = (n_rows + KB - 1) / KB;
   int64_t sl = std::max<int64_t>((ctx->num_sms + n_tiles - 1) / n_tiles, (n_rows + kSliceCells - 1) / kSliceCells);
   const int slices = (int)std::max<int64_t>(1, std::min<int64_t>(sl, kbs));
-  const int64_t rows_per_slice = ((kbs + slices - 1) / slices) * Cfg::KB;
+  const int64_t rows_per_slice = ((kbs + slices - 1) / slices) * KB;
   const size_t part_bytes = (size_t)slices * hp * hp * 4;
   void* ws;
   SCB_TRY(ws_get(ctx, 0, part_bytes + n_tiles * sizeof(int2) + 256, &ws, s));
   float* partial = (float*)ws;
   int2* d_tiles = (int2*)((char*)ws + ((part_bytes + 255) / 256) * 256);
   SCB_CUDA(cudaMemcpyAsync(d_tiles, tl.data(), n_tiles * sizeof(int2), cudaMemcpyHostToDevice, s));
-  auto kern = gram_kernel<BN>;
-  SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  kern<<<n_tiles * slices, kGemmThreads, Cfg::SMEM, s>>>(tmap, d_tiles, n_tiles, n_rows, rows_per_slice, hp, partial);
+  if (split) {
+    using Cfg = GramSplitCfg<BN>;
+    auto kern = gram_split_kernel<BN>;
+    SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    kern<<<n_tiles * slices, kGramSplitThreads, Cfg::SMEM, s>>>(thi, tlo, d_tiles, n_tiles, n_rows, rows_per_slice, hp,
+                                                                partial);
+  } else {
+    using Cfg = GramCfg<BN>;
+    auto kern = gram_kernel<BN>;
+    SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    kern<<<n_tiles * slices, kGemmThreads, Cfg::SMEM, s>>>(tmap, d_tiles, n_tiles, n_rows, rows_per_slice, hp,
+                                                           partial);
+  }
   SCB_LAUNCH_CHECK();
   dim3 g((hp + 255) / 256, hp);
   gram_reduce_kernel<<<g, 256, 0, s>>>(partial, slices, hp, C);
@@ -258,6 +409,16 @@ extern "C" int scb_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp
   SCB_REQUIRE(hp > 0 && hp % 128 == 0, SCB_ERR_ARG, "scb_gram: hp must be a multiple of 128");
   SCB_REQUIRE(n_rows >= 0 && n_rows < (1ll << 31), SCB_ERR_ARG, "scb_gram: n_rows out of range");
   cudaStream_t s = (cudaStream_t)stream;
-  if (hp % 256 == 0) return launch_gram<256>(ctx, Z, n_rows, hp, C, s);
-  return launch_gram<128>(ctx, Z, n_rows, hp, C, s);
+  if (hp % 256 == 0) return launch_gram<256>(ctx, Z, nullptr, nullptr, n_rows, hp, C, s);
+  return launch_gram<128>(ctx, Z, nullptr, nullptr, n_rows, hp, C, s);
+}
+
+extern "C" int scb_gram_split(scb_ctx* ctx, const uint16_t* Zhi, const uint16_t* Zlo, int64_t n_rows, int32_t hp,
+                              double* C, void* stream) {
+  SCB_REQUIRE(ctx && Zhi && Zlo && C, SCB_ERR_ARG, "scb_gram_split: null argument");
+  SCB_REQUIRE(hp > 0 && hp % 128 == 0, SCB_ERR_ARG, "scb_gram_split: hp must be a multiple of 128");
+  SCB_REQUIRE(n_rows >= 0 && n_rows < (1ll << 31), SCB_ERR_ARG, "scb_gram_split: n_rows out of range");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (hp % 256 == 0) return launch_gram<256>(ctx, nullptr, Zhi, Zlo, n_rows, hp, C, s);
+  return launch_gram<128>(ctx, nullptr, Zhi, Zlo, n_rows, hp, C, s);
 }

@@ -240,6 +240,8 @@ class Scaled:
     ones_col: int
     mean: torch.Tensor
     inv_std: torch.Tensor
+    Z_hi: Optional[torch.Tensor] = None  # BF16 planes hi = bf16(Z), lo = bf16(Z - hi) for the Gram
+    Z_lo: Optional[torch.Tensor] = None
 
     @property
     def ld(self):
@@ -276,13 +278,22 @@ def scale_finalize(sums, n_cells: int):
     return mean, inv
 
 
-def scale_dense(X_log: DeviceCSR, slot, H, mean, inv, max_value=10.0, out=None) -> Scaled:
+def scale_dense(X_log: DeviceCSR, slot, H, mean, inv, max_value=10.0, out=None, split: bool = False) -> Scaled:
+    """Dense clipped z-scores; with ``split`` also the BF16 hi/lo planes the Gram reads directly."""
     ld = padded_width(H)
-    Z = out if out is not None else torch.empty((X_log.n_rows, ld), dtype=torch.float32, device=X_log.device)
-    _lib.call("scb_scale_dense", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
-              X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value), _p(Z), ld, H,
-              _stream(X_log.device))
-    return Scaled(Z, H, H, mean, inv)
+    dev = X_log.device
+    Z = out if out is not None else torch.empty((X_log.n_rows, ld), dtype=torch.float32, device=dev)
+    if not split:
+        _lib.call("scb_scale_dense", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
+                  X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value), _p(Z), ld, H,
+                  _stream(dev))
+        return Scaled(Z, H, H, mean, inv)
+    hi = torch.empty((X_log.n_rows, ld), dtype=torch.bfloat16, device=dev)
+    lo = torch.empty((X_log.n_rows, ld), dtype=torch.bfloat16, device=dev)
+    _lib.call("scb_scale_dense_split", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
+              X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value), _p(Z), _p(hi), _p(lo),
+              ld, H, _stream(dev))
+    return Scaled(Z, H, H, mean, inv, hi, lo)
 
 
 def scale(X_log: DeviceCSR, hvg_index: torch.Tensor, max_value: float = 10.0) -> Scaled:
@@ -306,10 +317,15 @@ class PCAResult:
 
 
 def gram(sc: Scaled, out=None):
-    """Partial (local) Gram matrix Z^T Z, float64 [ld][ld] (tcgen05, 3xTF32)."""
+    """Partial (local) Gram matrix Z^T Z, float64 [ld][ld] (tcgen05, 3xBF16; from the pre-split
+    BF16 planes when scale_dense produced them)."""
     ld = sc.ld
     C = out if out is not None else torch.empty((ld, ld), dtype=torch.float64, device=sc.Z.device)
-    _lib.call("scb_gram", _ctx(sc.Z), _p(sc.Z), sc.Z.shape[0], ld, _p(C), _stream(sc.Z.device))
+    if sc.Z_hi is not None:
+        _lib.call("scb_gram_split", _ctx(sc.Z), _p(sc.Z_hi), _p(sc.Z_lo), sc.Z.shape[0], ld, _p(C),
+                  _stream(sc.Z.device))
+    else:
+        _lib.call("scb_gram", _ctx(sc.Z), _p(sc.Z), sc.Z.shape[0], ld, _p(C), _stream(sc.Z.device))
     return C
 
 
