@@ -1,4 +1,5 @@
-"""GPU parity of PCA: tcgen05 Gram (3xTF32), float64 eigensolve, tcgen05 projection."""
+"""GPU parity of PCA: tcgen05 Gram (3xBF16, fp32-fed and pre-split-plane-fed), float64 eigensolve,
+tcgen05 projection."""
 import numpy as np
 import pytest
 
@@ -30,8 +31,8 @@ def test_gram_matches_fp64(n, h):
     ref = Zp.T @ Zp
     scale = np.sqrt(np.outer(np.diag(ref), np.diag(ref)))
     err = np.abs(C - ref) / np.maximum(scale, 1e-30)
-    # tcgen05 FP32 accumulation rounds toward zero: a systematic ~1e-8-per-cell relative bias
-    # on monotone sums (the diagonal) within one K-slice; slices are <= 64k cells.
+    # tcgen05 FP32 accumulation rounds toward zero: a systematic relative bias on monotone sums
+    # (the diagonal) within one K-slice; slices are <= 8k cells.
     assert err.max() < 1e-3, err.max()
     off = err.copy()
     np.fill_diagonal(off, 0)
@@ -68,3 +69,21 @@ def test_pca_matches_oracle():
     resid = X - Xo @ (Vo.T @ V)
     assert np.abs(resid).max() < 1e-3 * np.abs(Xo).max(), np.abs(resid).max()
     assert np.all(r.X_pca.cpu().numpy()[:, k:] == 0)
+
+
+@pytest.mark.parametrize("n,h", [(3001, 200), (20011, 1000)])
+def test_gram_split_planes_match_converter_path(n, h):
+    """scale_dense_split's BF16 planes feed gram_split_kernel: the operands and the MMA sequence
+    equal the in-kernel-converter path, so the Gram agrees to rounding of the slice sums."""
+    import torch
+    from paper_2605_13928_b200 import _lib, pp
+    rng = np.random.default_rng(n + h)
+    Z = rng.standard_normal((n, h)).astype(np.float32)
+    sc = _scaled_from_host(Z, h)
+    hi = sc.Z.to(torch.bfloat16)
+    lo = (sc.Z - hi.float()).to(torch.bfloat16)
+    split = pp.Scaled(sc.Z, h, h, None, None, hi, lo)
+    C1 = pp.gram(sc).cpu().numpy()
+    C2 = pp.gram(split).cpu().numpy()
+    scale = np.sqrt(np.outer(np.diag(C1), np.diag(C1)))
+    assert (np.abs(C1 - C2) / np.maximum(scale, 1e-30)).max() < 1e-6
