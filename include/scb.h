@@ -144,13 +144,6 @@ SCB_API int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* 
                     int32_t n_slots, const double* mean, const double* inv_std, double max_value,
                     float* Z, int64_t ldz, int32_t ones_col, void* stream);
 
-/* ---- a6 (split): as scb_scale_dense, and also the BF16 planes Zhi = bf16(Z), Zlo = bf16(Z - Zhi)
- * (uint16 storage, [n_rows][ldz], 16-byte aligned, ldz % 8 == 0) that scb_gram_split consumes. */
-SCB_API int scb_scale_dense_split(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                    const float* logdata, int64_t n_rows, int32_t n_cols, const int32_t* gene_slot,
-                    int32_t n_slots, const double* mean, const double* inv_std, double max_value,
-                    float* Z, uint16_t* Zhi, uint16_t* Zlo, int64_t ldz, int32_t ones_col, void* stream);
-
 /* ---- a7: partial Gram matrix C = Z^T Z (float64 [hp][hp], full symmetric) on the
  * 5th-gen tensor cores (tcgen05 kind::f16, "3xBF16": x = hi + lo with hi = bf16(x),
  * lo = bf16(x - hi), products hi*hi + hi*lo + lo*hi, <= 2^-16 relative each; FP32 accumulate
@@ -158,8 +151,13 @@ SCB_API int scb_scale_dense_split(scb_ctx* ctx, const int64_t* indptr, const int
  * hp = ldz must be a multiple of 128; n_rows any. */
 SCB_API int scb_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp, double* C, void* stream);
 
-/* ---- a7 from the pre-split BF16 planes of scb_scale_dense_split (same products, same result
- * up to summation order): TMA feeds the operands directly, no in-kernel conversion. */
+/* ---- a7 operand prep: BF16 planes Zhi = bf16(Z), Zlo = bf16(Z - Zhi) (uint16 storage,
+ * [n_rows][ld], ld % 4 == 0) in one streaming pass. */
+SCB_API int scb_split_bf16(scb_ctx* ctx, const float* Z, int64_t n_rows, int64_t ld, uint16_t* Zhi, uint16_t* Zlo,
+                           void* stream);
+
+/* ---- a7 from the BF16 planes of scb_split_bf16 (the same operands and MMA sequence as
+ * scb_gram): TMA feeds the tensor cores directly, no in-kernel conversion. */
 SCB_API int scb_gram_split(scb_ctx* ctx, const uint16_t* Zhi, const uint16_t* Zlo, int64_t n_rows, int32_t hp,
                            double* C, void* stream);
 

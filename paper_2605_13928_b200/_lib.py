@@ -36,8 +36,7 @@ SIGNATURES = {
     "scb_scale_dense": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_dbl, c_ptr, c_i64, c_i32, c_ptr],
     "scb_gram": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
     "scb_gram_split": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
-    "scb_scale_dense_split": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_dbl, c_ptr, c_ptr,
-                              c_ptr, c_i64, c_i32, c_ptr],
+    "scb_split_bf16": [c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr],
     "scb_pca_eig": [c_ptr, c_ptr, c_i32, c_i32, c_i32, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_project": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_i32, c_ptr],
     "scb_knn": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_i32, c_i32, c_i32, c_ptr, c_ptr, c_ptr],

@@ -766,21 +766,6 @@ scale_dense_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
 }
 
 
-// Z -> BF16 planes hi = bf16(z), lo = bf16(z - hi): one streaming pass (16-byte loads, 8-byte
-// stores), run after scale_dense while Z's rows are still partly in L2
-__global__ void __launch_bounds__(256)
-split_bf16_kernel(const float4* __restrict__ Z, int64_t n4, uint2* __restrict__ hi, uint2* __restrict__ lo) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = Z[i];
-    const __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
-    const float2 a0 = __bfloat1622float2(h0), a1 = __bfloat1622float2(h1);
-    const __nv_bfloat162 l0 = __floats2bfloat162_rn(v.x - a0.x, v.y - a0.y);
-    const __nv_bfloat162 l1 = __floats2bfloat162_rn(v.z - a1.x, v.w - a1.y);
-    hi[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
-    lo[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
-  }
-}
-
 }  // namespace scb
 
 // ============================================================================ C ABI
@@ -990,51 +975,24 @@ extern "C" int scb_scale_finalize(scb_ctx* ctx, const uint64_t* sums, int32_t n_
   return SCB_OK;
 }
 
-static int scale_dense_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* ldata,
-                            int64_t n_rows, int32_t n_cols, const int32_t* slot, int32_t n_slots, const double* mean,
-                            const double* inv_std, double max_value, float* Z, __nv_bfloat16* Zhi,
-                            __nv_bfloat16* Zlo, int64_t ldz, int32_t ones_col, void* stream) {
-  SCB_REQUIRE(ctx && indptr && indices && ldata && slot && mean && inv_std && Z, SCB_ERR_ARG,
-              "scb_scale_dense: null argument");
-  SCB_REQUIRE(ldz % 8 == 0 && ldz >= n_slots && ones_col < ldz, SCB_ERR_ARG,
-              "scb_scale_dense: ldz must be a multiple of 8 and >= n_slots");
-  SCB_REQUIRE(((uintptr_t)Z & 15) == 0 && ((uintptr_t)Zhi & 15) == 0 && ((uintptr_t)Zlo & 15) == 0, SCB_ERR_ARG,
-              "scb_scale_dense: Z (and the planes) must be 16-byte aligned");
-  SCB_REQUIRE(aligned16(indices) && aligned16(ldata), SCB_ERR_ARG, "scb_scale_dense: 16-byte alignment");
-  SCB_REQUIRE((Zhi != nullptr) == (Zlo != nullptr), SCB_ERR_ARG, "scb_scale_dense: give both planes or neither");
-  const size_t smem = (size_t)ldz * 4 + (size_t)((n_cols + 3) & ~3) * 2 + (size_t)n_slots * 16;
-  SCB_REQUIRE(smem <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_scale_dense: too many genes");
-  if (n_rows == 0) return SCB_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  SCB_CUDA(cudaFuncSetAttribute(scale_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int per_sm = std::max(1, std::min(4, (int)(kSmemLimit / (smem + 1024))));
-  scale_dense_kernel<<<grid_for(ctx, per_sm), kRowThreads, smem, s>>>(
-      indptr, indices, ldata, n_rows, n_cols, slot, n_slots, mean, inv_std, max_value, Z, ldz, ones_col);
-  SCB_LAUNCH_CHECK();
-  if (Zhi) {
-    const int64_t n4 = n_rows * ldz / 4;
-    split_bf16_kernel<<<grid_for(ctx, 8), 256, 0, s>>>(reinterpret_cast<const float4*>(Z), n4,
-                                                       reinterpret_cast<uint2*>(Zhi), reinterpret_cast<uint2*>(Zlo));
-    SCB_LAUNCH_CHECK();
-  }
-  return SCB_OK;
-}
-
 extern "C" int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
                                const float* ldata, int64_t n_rows, int32_t n_cols, const int32_t* slot,
                                int32_t n_slots, const double* mean, const double* inv_std, double max_value,
                                float* Z, int64_t ldz, int32_t ones_col, void* stream) {
-  return scale_dense_impl(ctx, indptr, indices, ldata, n_rows, n_cols, slot, n_slots, mean, inv_std, max_value, Z,
-                          nullptr, nullptr, ldz, ones_col, stream);
+  SCB_REQUIRE(ctx && indptr && indices && ldata && slot && mean && inv_std && Z, SCB_ERR_ARG,
+              "scb_scale_dense: null argument");
+  SCB_REQUIRE(ldz % 4 == 0 && ldz >= n_slots && ones_col < ldz, SCB_ERR_ARG,
+              "scb_scale_dense: ldz must be a multiple of 4 and >= n_slots");
+  SCB_REQUIRE(((uintptr_t)Z & 15) == 0, SCB_ERR_ARG, "scb_scale_dense: Z must be 16-byte aligned");
+  SCB_REQUIRE(aligned16(indices) && aligned16(ldata), SCB_ERR_ARG, "scb_scale_dense: 16-byte alignment");
+  const size_t smem = (size_t)ldz * 4 + (size_t)((n_cols + 3) & ~3) * 2 + (size_t)n_slots * 16;
+  SCB_REQUIRE(smem <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_scale_dense: too many genes");
+  if (n_rows == 0) return SCB_OK;
+  SCB_CUDA(cudaFuncSetAttribute(scale_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int per_sm = std::max(1, std::min(4, (int)(kSmemLimit / (smem + 1024))));
+  scale_dense_kernel<<<grid_for(ctx, per_sm), kRowThreads, smem, (cudaStream_t)stream>>>(
+      indptr, indices, ldata, n_rows, n_cols, slot, n_slots, mean, inv_std, max_value, Z, ldz, ones_col);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
 }
 
-extern "C" int scb_scale_dense_split(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                                     const float* ldata, int64_t n_rows, int32_t n_cols, const int32_t* slot,
-                                     int32_t n_slots, const double* mean, const double* inv_std, double max_value,
-                                     float* Z, uint16_t* Zhi, uint16_t* Zlo, int64_t ldz, int32_t ones_col,
-                                     void* stream) {
-  SCB_REQUIRE(Zhi && Zlo, SCB_ERR_ARG, "scb_scale_dense_split: null plane");
-  return scale_dense_impl(ctx, indptr, indices, ldata, n_rows, n_cols, slot, n_slots, mean, inv_std, max_value, Z,
-                          reinterpret_cast<__nv_bfloat16*>(Zhi), reinterpret_cast<__nv_bfloat16*>(Zlo), ldz, ones_col,
-                          stream);
-}

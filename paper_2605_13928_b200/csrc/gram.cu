@@ -198,6 +198,21 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
   if (warp == 0) tc::tmem_dealloc<2 * BN>(tmem);
 }
 
+// Z -> BF16 planes hi = bf16(z), lo = bf16(z - hi): one streaming pass (16-byte loads, 8-byte
+// stores); the Gram then reads the planes through TMA with no in-kernel conversion
+__global__ void __launch_bounds__(256)
+split_bf16_kernel(const float4* __restrict__ Z, int64_t n4, uint2* __restrict__ hi, uint2* __restrict__ lo) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = Z[i];
+    const __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
+    const float2 a0 = __bfloat1622float2(h0), a1 = __bfloat1622float2(h1);
+    const __nv_bfloat162 l0 = __floats2bfloat162_rn(v.x - a0.x, v.y - a0.y);
+    const __nv_bfloat162 l1 = __floats2bfloat162_rn(v.z - a1.x, v.w - a1.y);
+    hi[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+    lo[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
+  }
+}
+
 // ---- variant fed by pre-split BF16 planes (written by scb_scale_dense_split): no converter
 // warps and no fp32 staging -- TMA brings the hi and lo boxes straight into the MN-major
 // 128-byte-swizzled operand layout, so shared memory carries only the TMA writes and the MMA
@@ -421,4 +436,17 @@ extern "C" int scb_gram_split(scb_ctx* ctx, const uint16_t* Zhi, const uint16_t*
   cudaStream_t s = (cudaStream_t)stream;
   if (hp % 256 == 0) return launch_gram<256>(ctx, nullptr, Zhi, Zlo, n_rows, hp, C, s);
   return launch_gram<128>(ctx, nullptr, Zhi, Zlo, n_rows, hp, C, s);
+}
+
+extern "C" int scb_split_bf16(scb_ctx* ctx, const float* Z, int64_t n_rows, int64_t ld, uint16_t* Zhi, uint16_t* Zlo,
+                              void* stream) {
+  SCB_REQUIRE(ctx && Z && Zhi && Zlo, SCB_ERR_ARG, "scb_split_bf16: null argument");
+  SCB_REQUIRE(ld % 4 == 0 && ((uintptr_t)Z & 15) == 0 && ((uintptr_t)Zhi & 7) == 0 && ((uintptr_t)Zlo & 7) == 0,
+              SCB_ERR_ARG, "scb_split_bf16: ld % 4 == 0 and aligned buffers required");
+  if (n_rows == 0) return SCB_OK;
+  const int64_t n4 = n_rows * ld / 4;
+  split_bf16_kernel<<<ctx->num_sms * 8, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(Z), n4, reinterpret_cast<uint2*>(Zhi), reinterpret_cast<uint2*>(Zlo));
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
 }

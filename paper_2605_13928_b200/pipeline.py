@@ -121,7 +121,7 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
     if comm is not None:
         comm.allreduce_(ssum)
     mean, inv = pp.scale_finalize(ssum, n_total)
-    sc = pp.scale_dense(X_log, slot, H, mean, inv, p.max_value, split=True)
+    sc = pp.scale_dense(X_log, slot, H, mean, inv, p.max_value)
 
     # ------------------------------------------------------------------ pca
     tm.step("pca")

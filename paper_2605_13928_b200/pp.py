@@ -278,22 +278,15 @@ def scale_finalize(sums, n_cells: int):
     return mean, inv
 
 
-def scale_dense(X_log: DeviceCSR, slot, H, mean, inv, max_value=10.0, out=None, split: bool = False) -> Scaled:
-    """Dense clipped z-scores; with ``split`` also the BF16 hi/lo planes the Gram reads directly."""
+def scale_dense(X_log: DeviceCSR, slot, H, mean, inv, max_value=10.0, out=None) -> Scaled:
+    """Dense clipped z-scores Z[N][ld] (float32) of the HVG columns, plus the ones column."""
     ld = padded_width(H)
     dev = X_log.device
     Z = out if out is not None else torch.empty((X_log.n_rows, ld), dtype=torch.float32, device=dev)
-    if not split:
-        _lib.call("scb_scale_dense", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
-                  X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value), _p(Z), ld, H,
-                  _stream(dev))
-        return Scaled(Z, H, H, mean, inv)
-    hi = torch.empty((X_log.n_rows, ld), dtype=torch.bfloat16, device=dev)
-    lo = torch.empty((X_log.n_rows, ld), dtype=torch.bfloat16, device=dev)
-    _lib.call("scb_scale_dense_split", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
-              X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value), _p(Z), _p(hi), _p(lo),
-              ld, H, _stream(dev))
-    return Scaled(Z, H, H, mean, inv, hi, lo)
+    _lib.call("scb_scale_dense", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
+              X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value), _p(Z), ld, H,
+              _stream(dev))
+    return Scaled(Z, H, H, mean, inv)
 
 
 def scale(X_log: DeviceCSR, hvg_index: torch.Tensor, max_value: float = 10.0) -> Scaled:
@@ -316,12 +309,24 @@ class PCAResult:
     n_comps: int
 
 
-def gram(sc: Scaled, out=None):
-    """Partial (local) Gram matrix Z^T Z, float64 [ld][ld] (tcgen05, 3xBF16; from the pre-split
-    BF16 planes when scale_dense produced them)."""
+def split_planes(sc: Scaled) -> Scaled:
+    """BF16 operand planes of Z for the Gram: hi = bf16(Z), lo = bf16(Z - hi) (one streaming pass)."""
+    n, ld = sc.Z.shape
+    if sc.Z_hi is None:
+        sc.Z_hi = torch.empty((n, ld), dtype=torch.bfloat16, device=sc.Z.device)
+        sc.Z_lo = torch.empty((n, ld), dtype=torch.bfloat16, device=sc.Z.device)
+    _lib.call("scb_split_bf16", _ctx(sc.Z), _p(sc.Z), n, ld, _p(sc.Z_hi), _p(sc.Z_lo), _stream(sc.Z.device))
+    return sc
+
+
+def gram(sc: Scaled, out=None, planes: bool = True):
+    """Partial (local) Gram matrix Z^T Z, float64 [ld][ld] (tcgen05, 3xBF16).  ``planes`` (default)
+    splits Z into BF16 hi/lo planes first and feeds them to the tensor cores by TMA; ``planes=False``
+    converts fp32 tiles inside the Gram kernel instead (no extra 4 B/element of HBM, slower)."""
     ld = sc.ld
     C = out if out is not None else torch.empty((ld, ld), dtype=torch.float64, device=sc.Z.device)
-    if sc.Z_hi is not None:
+    if planes:
+        split_planes(sc)
         _lib.call("scb_gram_split", _ctx(sc.Z), _p(sc.Z_hi), _p(sc.Z_lo), sc.Z.shape[0], ld, _p(C),
                   _stream(sc.Z.device))
     else:

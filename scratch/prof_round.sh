@@ -12,3 +12,7 @@ ncu --set full --import-source on --clock-control none -k regex:knn_candidates -
 fi
 tail -2 gpurun_out/pytest_gpu.log
 tail -c 300 gpurun_out/bench.json
+if [ "$1" == "gram" ]; then
+ncu --set full --import-source on --clock-control none -k 'regex:gram_split|split_bf16' -c 2 -o gpurun_out/gram_full_1m \
+    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_gram.log 2>&1
+fi

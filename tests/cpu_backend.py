@@ -107,7 +107,7 @@ def scale_finalize(sums, n_cells):
     return torch.as_tensor(mean), torch.as_tensor(1.0 / std)
 
 
-def scale_dense(X_log, slot, H, mean, inv, max_value=10.0, out=None, split=False):  # noqa: ARG001 (no planes here)
+def scale_dense(X_log, slot, H, mean, inv, max_value=10.0, out=None):
     A = _csr(X_log)
     ld = padded_width(H)
     m, iv = _np(mean), _np(inv)
@@ -121,7 +121,7 @@ def scale_dense(X_log, slot, H, mean, inv, max_value=10.0, out=None, split=False
     return Scaled(torch.as_tensor(Z), H, H, mean, inv)
 
 
-def gram(sc, out=None):
+def gram(sc, out=None, planes=True):  # noqa: ARG001 (no BF16 planes on the CPU)
     Z = _np(sc.Z).astype(np.float64)
     return torch.as_tensor(Z.T @ Z)
 

@@ -73,17 +73,19 @@ def test_pca_matches_oracle():
 
 @pytest.mark.parametrize("n,h", [(3001, 200), (20011, 1000)])
 def test_gram_split_planes_match_converter_path(n, h):
-    """scale_dense_split's BF16 planes feed gram_split_kernel: the operands and the MMA sequence
-    equal the in-kernel-converter path, so the Gram agrees to rounding of the slice sums."""
+    """scb_split_bf16's planes are bit-exact round-to-nearest BF16 (hi) and BF16(Z - hi) (lo); fed
+    to gram_split_kernel they give the operands and MMA sequence of the in-kernel-converter path,
+    so the two Grams agree to rounding of the fp64 slice sums."""
     import torch
-    from paper_2605_13928_b200 import _lib, pp
+    from paper_2605_13928_b200 import pp
     rng = np.random.default_rng(n + h)
     Z = rng.standard_normal((n, h)).astype(np.float32)
     sc = _scaled_from_host(Z, h)
+    C1 = pp.gram(sc, planes=False).cpu().numpy()
+    C2 = pp.gram(sc).cpu().numpy()
     hi = sc.Z.to(torch.bfloat16)
     lo = (sc.Z - hi.float()).to(torch.bfloat16)
-    split = pp.Scaled(sc.Z, h, h, None, None, hi, lo)
-    C1 = pp.gram(sc).cpu().numpy()
-    C2 = pp.gram(split).cpu().numpy()
+    assert torch.equal(sc.Z_hi.view(torch.int16), hi.view(torch.int16))
+    assert torch.equal(sc.Z_lo.view(torch.int16), lo.view(torch.int16))
     scale = np.sqrt(np.outer(np.diag(C1), np.diag(C1)))
     assert (np.abs(C1 - C2) / np.maximum(scale, 1e-30)).max() < 1e-6
