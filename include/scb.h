@@ -100,7 +100,7 @@ SCB_API int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32_t*
 /* ---- a2 pass 2: writes the compacted CSR.  If row_scale != NULL the values written are
  * log1p(x * row_scale[kept_row]) (fused normalize_total + log1p), else raw x. */
 SCB_API int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* data,
-                    int64_t n_rows, const uint8_t* cell_mask, const int32_t* gene_remap,
+                    int64_t n_rows, int32_t n_cols, const uint8_t* cell_mask, const int32_t* gene_remap,
                     const int64_t* new_indptr, const float* row_scale, int32_t* new_indices,
                     float* new_data, void* stream);
 

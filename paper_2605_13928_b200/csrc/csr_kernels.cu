@@ -9,6 +9,7 @@
 // Integer sums are exact and order independent, so results are deterministic and
 // identical across 1/2/4/8-way cell sharding.
 #include <cuda_bf16.h>
+#include <type_traits>
 #include "common.cuh"
 #include "scan.cuh"
 #include "stream.cuh"
@@ -17,14 +18,53 @@ namespace scb {
 
 constexpr int kRowThreads = 512;          // threads per CTA of the row-streaming kernels
 constexpr int kQcThreads = 1024;          // QC: one CTA per SM (gene histogram fills smem)
+constexpr int kHvgThreads = 1024;         // HVG sums: one CTA per SM (gene tile fills smem)
 constexpr int kMaxSplit = 3;              // gene tiles of the HVG pass: up to 4 (G <= ~58k)
 constexpr int kHvgTileW = (int)(227 * 1024 / 16);  // genes per HVG tile (4 u32 words each)
 constexpr size_t kSmemLimit = 227 * 1024;  // opt-in dynamic shared memory per CTA
 
 static int grid_for(scb_ctx* ctx, int ctas_per_sm) { return ctx->num_sms * ctas_per_sm; }
 
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// Kept-gene map in shared memory: word i = (kept bits of genes [32i, 32i+32), number of kept
+// genes before gene 32i), so remap[g] = prefix + popc(bits below g) -- a conflict-light LDS.64
+// instead of a scattered global gather per nonzero.
+__device__ __forceinline__ void build_gene_map(const int32_t* __restrict__ remap, int32_t n_cols, uint2* s_map) {
+  const int n_words = (n_cols + 31) >> 5;
+  for (int wi = warp_id(); wi < n_words; wi += (blockDim.x >> 5)) {
+    const int g = wi * 32 + lane_id();
+    const int rv = g < n_cols ? remap[g] : -1;
+    const unsigned bits = __ballot_sync(0xffffffffu, rv >= 0);
+    const int first = __shfl_sync(0xffffffffu, rv, bits ? __ffs(bits) - 1 : 0);
+    if (lane_id() == 0) s_map[wi] = make_uint2(bits, bits ? (unsigned)first : 0u);
+  }
+}
+__device__ __forceinline__ int map_gene(const uint2* s_map, int32_t n_cols, int g) {
+  if ((unsigned)g >= (unsigned)n_cols) return -1;
+  const uint2 w = s_map[g >> 5];
+  const unsigned sh = (unsigned)g & 31u;
+  return ((w.x >> sh) & 1u) ? (int)(w.y + __popc(w.x & ((1u << sh) - 1u))) : -1;
+}
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int32_t lds_s16(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.s16 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+// fire-and-forget shared add on a shared-window address (native ATOMS.ADD, no return value)
+__device__ __forceinline__ void red_shared_add(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 // ============================================================================ QC
-// smem: n_cells u32[W], total_lo u32[W] for a gene tile [g0, g0+W), mt bitmask.  The tile-0
+// smem: n_cells u32[W], total_lo u32[W] for a gene tile [g0, g0+W), mt flag byte per gene.  The tile-0
 // CTAs also write the per-cell metrics and, for the HVG pass, the per-row positions where
 // the original gene index crosses each HVG tile boundary (splits[r][t-1] = #entries with
 // gene < t*split_w, relative to the row start).
@@ -43,51 +83,96 @@ qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indice
   const int w = min(tile_w, n_cols - g0);
   uint32_t* s_cells = sm;
   uint32_t* s_tot = sm + tile_w;
-  uint32_t* s_mt = sm + 2 * tile_w;  // bitmask over ALL genes
-  const int mt_words = (n_cols + 31) >> 5;
+  uint8_t* s_mt = reinterpret_cast<uint8_t*>(sm + 2 * tile_w);  // 0/1 per gene, ALL genes
   for (int i = threadIdx.x; i < 2 * tile_w; i += blockDim.x) sm[i] = 0;
-  for (int i = threadIdx.x; i < mt_words; i += blockDim.x) {
-    uint32_t m = 0;
-    for (int bb = 0; bb < 32; ++bb) {
-      const int g = i * 32 + bb;
-      if (g < n_cols && mt_mask[g]) m |= 1u << bb;
-    }
-    s_mt[i] = m;
-  }
+  for (int i = threadIdx.x; i < n_cols; i += blockDim.x) s_mt[i] = mt_mask[i] ? 1 : 0;
   __syncthreads();
   const bool row_owner = (tile == 0);
   const int lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  // shared-window addresses biased by the tile origin: gene g lives at a + 4g
+  const uint32_t a_cells = smem_addr(s_cells) - 4u * (uint32_t)g0;
+  const uint32_t a_tot = smem_addr(s_tot) - 4u * (uint32_t)g0;
+  const uint32_t a_mt = smem_addr(s_mt);
+  // per-lane dummy gene of the tile for masked elements' zero adds (distinct lanes -> distinct
+  // banks; a shared dummy would serialise the warp's atomics on one address)
+  const int gd = g0 + lane % max(w, 1);
   bool bad = false;
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
     const int64_t b = indptr[r], e = indptr[r + 1];
     uint32_t cnt = 0;
     unsigned long long sum = 0, summt = 0;
     int sc[NSPLIT > 0 ? NSPLIT : 1] = {};
-    stream_row<2>(indices, data, b, e, nnz, [&](const Quad& q) {
+    // Per quad.  x + 2^23 is exact iff x is an integer in [0, 2^23) (then its low mantissa bits
+    // are the count), so FADD/FADD/FSETP validate and convert; anything else (x >= 2^23,
+    // negative, fractional, NaN, bad gene index) sends the whole quad through the exact rare
+    // check once.  Masked-out (or invalid) elements become (per-lane dummy gene, count 0),
+    // which the branch-free accumulation below adds harmlessly.
+    auto quad = [&](const Quad& q, auto full_tag) {
+      constexpr bool kFull = decltype(full_tag)::value;
+      int g[4];
+      uint32_t xv[4];
+      bool ok_all = true;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (!((q.valid >> k) & 1u)) continue;
-        const int g = q.g[k];
         const float x = q.x[k];
-        bad |= !(x >= 0.0f && x == rintf(x) && x < 16777216.0f) || (unsigned)g >= (unsigned)n_cols;
-#pragma unroll
-        for (int t = 0; t < NSPLIT; ++t) sc[t] += (g < (t + 1) * split_w) ? 1 : 0;
-        if (x > 0.0f && !bad) {
-          const uint32_t xv = (uint32_t)x;
-          cnt += 1;
-          sum += xv;
-          if ((s_mt[g >> 5] >> (g & 31)) & 1u) summt += xv;
-          const int gl = g - g0;
-          if (gl >= 0 && gl < w) {
-            atomicAdd(&s_cells[gl], 1u);
-            // low 12 bits in smem (fire-and-forget: <= 2^20 rows per CTA keep the word below
-            // 2^32), the rare higher part straight into the global u64 total
-            atomicAdd(&s_tot[gl], xv & 0xFFFu);
-            if (xv > 0xFFFu) atomicAdd(&g_total[g], (unsigned long long)(xv & ~0xFFFu));
-          }
+        const float t = x + 8388608.0f;
+        xv[k] = __float_as_uint(t) - 0x4B000000u;
+        g[k] = q.g[k];
+        const bool ok = (t - 8388608.0f == x) & (xv[k] < (1u << 23)) & ((unsigned)g[k] < (unsigned)n_cols);
+        if (kFull) {
+          ok_all &= ok;
+        } else {
+          const bool v = (q.valid >> k) & 1u;
+          ok_all &= ok | !v;
+          if (!v) { xv[k] = 0u; g[k] = gd; }
         }
       }
+      if (!ok_all) {  // rare: exact check per element
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (!kFull && !((q.valid >> k) & 1u)) continue;
+          const float x = q.x[k];
+          const bool ok = (x >= 0.0f && x == rintf(x) && x < 16777216.0f) && (unsigned)q.g[k] < (unsigned)n_cols;
+          bad |= !ok;
+          xv[k] = ok ? (uint32_t)x : 0u;
+          g[k] = ok ? q.g[k] : gd;
+        }
+      }
+      uint32_t qsum = 0, qmt = 0, hi_any = 0;  // 4 counts < 2^24 fit a u32
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int t2 = 0; t2 < NSPLIT; ++t2) {
+          const bool v = kFull || ((q.valid >> k) & 1u);
+          sc[t2] += (v & (q.g[k] < (t2 + 1) * split_w)) ? 1 : 0;
+        }
+        cnt += (xv[k] != 0u) ? 1u : 0u;
+        qsum += xv[k];
+        qmt += lds_u8(a_mt + (uint32_t)g[k]) * xv[k];
+        // low 12 bits in smem (fire-and-forget: <= 2^20 rows per CTA keep the word below
+        // 2^32); zero increments land on the tile's first gene
+        const bool in_tile = (unsigned)(g[k] - g0) < (unsigned)w;
+        const uint32_t ga = 4u * (uint32_t)(in_tile ? g[k] : gd);
+        red_shared_add(a_cells + ga, (in_tile & (xv[k] != 0u)) ? 1u : 0u);
+        red_shared_add(a_tot + ga, in_tile ? (xv[k] & 0xFFFu) : 0u);
+        hi_any |= in_tile ? xv[k] : 0u;
+      }
+      if (hi_any > 0xFFFu) {  // rare: higher parts straight into the global u64 totals
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (((unsigned)(g[k] - g0) < (unsigned)w) & (xv[k] > 0xFFFu))
+            atomicAdd(&g_total[g[k]], (unsigned long long)(xv[k] & ~0xFFFu));
+      }
+      sum += qsum;
+      summt += qmt;
+    };
+    stream_row<2>(indices, data, b, e, nnz, [&](const Quad& q) {
+      if (q.valid == 0u) return;
+      if (q.valid == 0xFu)
+        quad(q, std::true_type{});
+      else
+        quad(q, std::false_type{});
     });
     if (row_owner) {
       cnt = warp_sum(cnt);
@@ -191,9 +276,12 @@ __global__ void gene_remap_kernel(const uint8_t* gmask, int32_t n, int32_t* rema
 __global__ void __launch_bounds__(kRowThreads)
 subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                     const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
-                    const int32_t* __restrict__ remap, const int64_t* __restrict__ row_pos,
+                    const int32_t* __restrict__ remap, int32_t n_cols, const int64_t* __restrict__ row_pos,
                     int64_t* __restrict__ cnt, double target_sum, float* __restrict__ row_scale,
                     float* __restrict__ row_scale_orig) {
+  extern __shared__ uint2 s_map[];
+  build_gene_map(remap, n_cols, s_map);
+  __syncthreads();
   const int64_t nnz = indptr[n_rows];
   const int lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -205,10 +293,10 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
     const int64_t b = indptr[r], e = indptr[r + 1];
     int c = 0;
     double sum = 0.0;
-    stream_row<2>(indices, row_scale ? data : nullptr, b, e, nnz, [&](const Quad& q) {
+    stream_row_pipe<1>(indices, row_scale ? data : nullptr, b, e, nnz, [&](const Quad& q) {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (((q.valid >> k) & 1u) && remap[q.g[k]] >= 0) {
+        if (((q.valid >> k) & 1u) && map_gene(s_map, n_cols, q.g[k]) >= 0) {
           ++c;
           sum += (double)q.x[k];
         }
@@ -234,11 +322,14 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
 __global__ void __launch_bounds__(kRowThreads)
 subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                    const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
-                   const int32_t* __restrict__ remap, const int64_t* __restrict__ row_pos,
+                   const int32_t* __restrict__ remap, int32_t n_cols, const int64_t* __restrict__ row_pos,
                    const int64_t* __restrict__ new_indptr, const float* __restrict__ row_scale,
                    int32_t* __restrict__ out_idx, float* __restrict__ out_val) {
   __shared__ int s_idx[kRowThreads / 32][128];
   __shared__ float s_val[kRowThreads / 32][128];
+  extern __shared__ uint2 s_map[];
+  build_gene_map(remap, n_cols, s_map);
+  __syncthreads();
   const int64_t nnz = indptr[n_rows];
   const int lane = lane_id(), w = warp_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -248,12 +339,12 @@ subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
     const float s = row_scale ? row_scale[kr] : 1.0f;
     const int64_t b = indptr[r], e = indptr[r + 1];
     int64_t o = new_indptr[kr];
-    stream_row<2>(indices, data, b, e, nnz, [&](const Quad& q) {
+    stream_row_pipe<1>(indices, data, b, e, nnz, [&](const Quad& q) {
       int ng[4];
       int kc = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        ng[k] = ((q.valid >> k) & 1u) ? remap[q.g[k]] : -1;
+        ng[k] = ((q.valid >> k) & 1u) ? map_gene(s_map, n_cols, q.g[k]) : -1;
         kc += ng[k] >= 0 ? 1 : 0;
       }
       int incl = kc;
@@ -307,7 +398,7 @@ normalize_log1p_kernel(const int64_t* __restrict__ indptr, const float* __restri
 // so each nonzero is read exactly once; without them every tile CTA filters whole rows.
 __device__ __forceinline__ uint64_t fx_round(double v) { return (uint64_t)__double2ull_rn(v); }
 
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __launch_bounds__(kHvgThreads)
 hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                 const float* __restrict__ data, const float* __restrict__ row_scale, int64_t n_rows,
                 int32_t n_cols, const int32_t* __restrict__ remap, int32_t n_out, int32_t tile_w,
@@ -323,6 +414,8 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
   uint32_t* s1hi = sm + tile_w;
   uint32_t* s2lo = sm + 2 * tile_w;
   uint32_t* s2hi = sm + 3 * tile_w;
+  const uint32_t a1lo = smem_addr(s1lo), a1hi = smem_addr(s1hi), a2lo = smem_addr(s2lo), a2hi = smem_addr(s2hi);
+  const int dl = lane_id() % max(w, 1);  // per-lane dummy slot for zero adds (no same-address serialisation)
   for (int i = threadIdx.x; i < 4 * tile_w; i += blockDim.x) sm[i] = 0;
   __syncthreads();
   const int64_t r0 = rblk * rows_per_block;
@@ -337,34 +430,58 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
       if (tile > 0) b = rb + splits[r * ns + tile - 1];
       if (tile < ns) e = rb + splits[r * ns + tile];
     }
+    // Per quad: y = fl(x * s); v1 = round(y * 2^28) (exact scaling in f32, one RN conversion),
+    // v2 = round((y * 2^12)^2) (exact square in f64, one RN conversion) -- the same integers as
+    // the oracle's round(y * 2^28), round(y^2 * 2^24).  Carry-free split: low 22 bits + high
+    // part; with <= 1024 rows per CTA neither u32 word can overflow, so all four adds are
+    // fire-and-forget and unconditional (out-of-tile / masked elements add 0 to a per-lane dummy
+    // gene of the tile).
+    // Values outside the fast range (y >= 2^15 for the sum, y >= ~724 for the sum of squares)
+    // go to the global limbs.
     stream_row<2>(indices, data, b, e, nnz, [&](const Quad& q) {
+      if (q.valid == 0u) return;
+      uint64_t v1[4], v2[4];
+      uint32_t ga[4];
+      bool rare = false;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int gl = q.g[k] - g0;
-        // removed genes are accumulated too and dropped at the flush (no per-nonzero remap load)
-        if (((q.valid >> k) & 1u) && gl >= 0 && gl < w) {
-          const float y = __fmul_rn(q.x[k], s);   // float32 normalized count
-          const double yd = (double)y;
-          // carry-free split: low 22 bits + high part; with <= 1024 rows per CTA neither u32
-          // word can overflow, so both adds are fire-and-forget (no returned value needed)
-          const uint64_t v1 = fx_round(yd * 268435456.0);        // y * 2^28
-          const uint64_t v2 = fx_round((yd * yd) * 16777216.0);   // y^2 * 2^24
-          if (v1 < (1ull << 43)) {  // y < 2^15 (target_sum 1e4 bounds y by 1e4)
-            atomicAdd(&s1lo[gl], (uint32_t)(v1 & 0x3FFFFFu));
-            atomicAdd(&s1hi[gl], (uint32_t)(v1 >> 22));
-          } else {  // rare huge y (e.g. CPM normalization): straight into the global limbs
-            const int go = remap ? remap[q.g[k]] : q.g[k];
+        const bool in = ((q.valid >> k) & 1u) && gl >= 0 && gl < w;
+        const float y = __fmul_rn(q.x[k], s);  // float32 normalized count
+        v1[k] = in ? (uint64_t)__float2ull_rn(__fmul_rn(y, 268435456.0f)) : 0ull;
+        const double y12 = (double)__fmul_rn(y, 4096.0f);
+        v2[k] = in ? (uint64_t)__double2ull_rn(__dmul_rn(y12, y12)) : 0ull;
+        ga[k] = 4u * (uint32_t)(in ? gl : dl);
+        rare |= (v1[k] >= (1ull << 43)) | ((v2[k] >> 22) >= (1ull << 21));
+      }
+      if (!rare) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          red_shared_add(a1lo + ga[k], (uint32_t)(v1[k] & 0x3FFFFFu));
+          red_shared_add(a1hi + ga[k], (uint32_t)(v1[k] >> 22));
+          red_shared_add(a2lo + ga[k], (uint32_t)(v2[k] & 0x3FFFFFu));
+          red_shared_add(a2hi + ga[k], (uint32_t)(v2[k] >> 22));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int gi = q.g[k];
+          if (v1[k] < (1ull << 43)) {
+            red_shared_add(a1lo + ga[k], (uint32_t)(v1[k] & 0x3FFFFFu));
+            red_shared_add(a1hi + ga[k], (uint32_t)(v1[k] >> 22));
+          } else {  // huge y (e.g. CPM normalization): straight into the global limbs
+            const int go = remap ? remap[gi] : gi;
             if (go >= 0) {
-              atomicAdd(&sums[go], v1 & 0xFFFFFFFFull);
-              atomicAdd(&sums[n_out + go], v1 >> 32);
+              atomicAdd(&sums[go], v1[k] & 0xFFFFFFFFull);
+              atomicAdd(&sums[n_out + go], v1[k] >> 32);
             }
           }
-          atomicAdd(&s2lo[gl], (uint32_t)(v2 & 0x3FFFFFu));
-          const uint64_t h2 = v2 >> 22;
+          red_shared_add(a2lo + ga[k], (uint32_t)(v2[k] & 0x3FFFFFu));
+          const uint64_t h2 = v2[k] >> 22;
           if (h2 < (1ull << 21)) {
-            atomicAdd(&s2hi[gl], (uint32_t)h2);
-          } else {  // rare huge y^2 (y > ~724): straight into the global limbs
-            const int go = remap ? remap[q.g[k]] : q.g[k];
+            red_shared_add(a2hi + ga[k], (uint32_t)h2);
+          } else {  // huge y^2 (y > ~724)
+            const int go = remap ? remap[gi] : gi;
             if (go >= 0) {
               atomicAdd(&sums[2 * n_out + go], (unsigned long long)(h2 & 1023u) << 22);
               atomicAdd(&sums[3 * n_out + go], (unsigned long long)(h2 >> 10));
@@ -640,7 +757,7 @@ hvg_select_kernel(const unsigned long long* __restrict__ sums, int32_t G, int64_
 }
 
 // ============================================================================ scale
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __launch_bounds__(kRowThreads, 2)
 scale_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                   const float* __restrict__ ldata, int64_t n_rows, int32_t n_cols,
                   const int32_t* __restrict__ slot, int32_t n_slots, int64_t rows_per_block,
@@ -657,33 +774,52 @@ scale_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
   uint32_t* s1hi = sm + n_slots;
   uint32_t* s2lo = sm + 2 * n_slots;
   uint32_t* s2hi = sm + 3 * n_slots;
+  const uint32_t a1lo = smem_addr(s1lo), a1hi = smem_addr(s1hi), a2lo = smem_addr(s2lo), a2hi = smem_addr(s2hi);
+  const uint32_t a_slot = smem_addr(s_slot);
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t r1 = min(n_rows, r0 + rows_per_block);
   for (int64_t r = r0 + warp_id(); r < r1; r += (blockDim.x >> 5)) {
-    stream_row<4>(indices, ldata, indptr[r], indptr[r + 1], nnz, [&](const Quad& q) {
+    // per quad: slot lookups first; quads without an HVG entry cost four LDS; HVG entries get
+    // v1 = round(l * 2^28) (exact f32 scaling, one RN conversion) and v2 = round((l * 2^12)^2)
+    // (exact f64 square) -- the oracle's round(l * 2^28), round(l^2 * 2^24).  High words
+    // stay below 2^32 for values < 2^43 (|l| < 2^15, l^2 < 2^19); larger ones (not
+    // log-normalized data) go straight to the global limbs.
+    stream_row_pipe<1>(indices, ldata, indptr[r], indptr[r + 1], nnz, [&](const Quad& q) {
+      int j[4];
+      bool any = false;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (!((q.valid >> k) & 1u)) continue;
-        const int j = s_slot[q.g[k]];
-        if (j >= 0) {
-          const double l = (double)q.x[k];
-          const uint64_t v1 = fx_round(l * 268435456.0);        // l * 2^28
-          const uint64_t v2 = fx_round((l * l) * 16777216.0);   // l^2 * 2^24
-          // high words stay below 2^32 for values < 2^43 (|l| < 2^15, l^2 < 2^19); larger ones
-          // (not log-normalized data) go straight to the global limbs
+        j[k] = ((q.valid >> k) & 1u) ? (int)lds_s16(a_slot + 2u * (uint32_t)q.g[k]) : -1;
+        any |= j[k] >= 0;
+      }
+      if (!any) return;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (j[k] < 0) continue;  // most entries are not HVGs: skip their atomics entirely
+        const float l = q.x[k];
+        const uint64_t v1 = (uint64_t)__float2ull_rn(__fmul_rn(l, 268435456.0f));
+        const double l12 = (double)__fmul_rn(l, 4096.0f);
+        const uint64_t v2 = (uint64_t)__double2ull_rn(__dmul_rn(l12, l12));
+        const uint32_t ja = 4u * (uint32_t)j[k];
+        if ((v1 | v2) < (1ull << 43)) {
+          red_shared_add(a1lo + ja, (uint32_t)(v1 & 0x3FFFFFu));
+          red_shared_add(a1hi + ja, (uint32_t)(v1 >> 22));
+          red_shared_add(a2lo + ja, (uint32_t)(v2 & 0x3FFFFFu));
+          red_shared_add(a2hi + ja, (uint32_t)(v2 >> 22));
+        } else {  // rare
           if (v1 < (1ull << 43)) {
-            atomicAdd(&s1lo[j], (uint32_t)(v1 & 0x3FFFFFu));
-            atomicAdd(&s1hi[j], (uint32_t)(v1 >> 22));
+            red_shared_add(a1lo + ja, (uint32_t)(v1 & 0x3FFFFFu));
+            red_shared_add(a1hi + ja, (uint32_t)(v1 >> 22));
           } else {
-            atomicAdd(&sums[j], v1 & 0xFFFFFFFFull);
-            atomicAdd(&sums[n_slots + j], v1 >> 32);
+            atomicAdd(&sums[j[k]], v1 & 0xFFFFFFFFull);
+            atomicAdd(&sums[n_slots + j[k]], v1 >> 32);
           }
           if (v2 < (1ull << 43)) {
-            atomicAdd(&s2lo[j], (uint32_t)(v2 & 0x3FFFFFu));
-            atomicAdd(&s2hi[j], (uint32_t)(v2 >> 22));
+            red_shared_add(a2lo + ja, (uint32_t)(v2 & 0x3FFFFFu));
+            red_shared_add(a2hi + ja, (uint32_t)(v2 >> 22));
           } else {
-            atomicAdd(&sums[2 * n_slots + j], v2 & 0xFFFFFFFFull);
-            atomicAdd(&sums[3 * n_slots + j], v2 >> 32);
+            atomicAdd(&sums[2 * n_slots + j[k]], v2 & 0xFFFFFFFFull);
+            atomicAdd(&sums[3 * n_slots + j[k]], v2 >> 32);
           }
         }
       }
@@ -787,8 +923,9 @@ extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t
   SCB_REQUIRE(n_tiles_hvg - 1 <= kMaxSplit, SCB_ERR_UNSUPPORTED, "scb_qc_metrics: too many genes (max %d)",
               (kMaxSplit + 1) * kHvgTileW);
   cudaStream_t s = (cudaStream_t)stream;
-  const int mt_words = (n_cols + 31) / 32;
-  const int max_w = (int)((kSmemLimit - mt_words * 4) / 8);
+  const size_t mt_bytes = ((size_t)n_cols + 15) & ~(size_t)15;
+  SCB_REQUIRE(mt_bytes + 8 * 1024 <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_qc_metrics: too many genes");
+  const int max_w = (int)((kSmemLimit - mt_bytes) / 8);
   const int n_tiles = ceil_div(n_cols, max_w);
   const int tile_w = ceil_div(n_cols, n_tiles);
   void* ws;
@@ -798,7 +935,7 @@ extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t
   unsigned long long* g_total = (unsigned long long*)((char*)ws + ((size_t)n_cols * 4 + 7) / 8 * 8);
   SCB_CUDA(cudaMemsetAsync(ws, 0, ws_bytes + 8, s));
   SCB_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), s));
-  const size_t smem = (size_t)tile_w * 8 + (size_t)mt_words * 4;
+  const size_t smem = (size_t)tile_w * 8 + mt_bytes;
   const int n_split = hvg_row_splits ? n_tiles_hvg - 1 : 0;
   if (n_rows > 0) {
     // each CTA sees at most 2^20 rows, so its 12-bit partial gene totals cannot overflow a u32
@@ -864,9 +1001,12 @@ extern "C" int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32
   int64_t* cnt = row_pos + (n_rows + 1);
   SCB_TRY(scan_u8_to_i64(ctx, cmask, n_rows, row_pos, s));
   if (n_rows > 0) {
-    subset_count_kernel<<<grid_for(ctx, 4), kRowThreads, 0, s>>>(indptr, indices, data, n_rows, cmask, remap,
-                                                                 row_pos, cnt, target_sum, row_scale,
-                                                                 row_scale_orig);
+    const size_t map_bytes = (size_t)((n_cols + 31) / 32) * 8;
+    SCB_REQUIRE(map_bytes <= 64 * 1024, SCB_ERR_UNSUPPORTED, "scb_subset_count: too many genes");
+    SCB_CUDA(cudaFuncSetAttribute(subset_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_bytes));
+    subset_count_kernel<<<grid_for(ctx, 4), kRowThreads, map_bytes, s>>>(indptr, indices, data, n_rows, cmask,
+                                                                         remap, n_cols, row_pos, cnt, target_sum,
+                                                                         row_scale, row_scale_orig);
     SCB_LAUNCH_CHECK();
   }
   // number of kept rows is row_pos[n_rows]; scan cnt[0..kept) -> new_indptr (device-side length)
@@ -875,7 +1015,7 @@ extern "C" int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32
 }
 
 extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                               const float* data, int64_t n_rows, const uint8_t* cmask,
+                               const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
                                int32_t* new_indices, float* new_data, void* stream) {
   SCB_REQUIRE(ctx && indptr && indices && data && cmask && remap && new_indptr && new_indices && new_data,
@@ -887,9 +1027,12 @@ extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_
   int64_t* row_pos = (int64_t*)ws;
   SCB_TRY(scan_u8_to_i64(ctx, cmask, n_rows, row_pos, s));
   if (n_rows > 0) {
-    subset_fill_kernel<<<grid_for(ctx, 4), kRowThreads, 0, s>>>(indptr, indices, data, n_rows, cmask, remap,
-                                                                row_pos, new_indptr, row_scale, new_indices,
-                                                                new_data);
+    const size_t map_bytes = (size_t)((n_cols + 31) / 32) * 8;
+    SCB_REQUIRE(map_bytes <= 64 * 1024, SCB_ERR_UNSUPPORTED, "scb_subset_fill: too many genes");
+    SCB_CUDA(cudaFuncSetAttribute(subset_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_bytes));
+    subset_fill_kernel<<<grid_for(ctx, 4), kRowThreads, map_bytes, s>>>(indptr, indices, data, n_rows, cmask,
+                                                                        remap, n_cols, row_pos, new_indptr,
+                                                                        row_scale, new_indices, new_data);
     SCB_LAUNCH_CHECK();
   }
   return SCB_OK;
@@ -922,7 +1065,7 @@ extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int3
   int64_t rows_per_block = std::max<int64_t>(64, std::min<int64_t>(1024, n_rows / (2 * ctx->num_sms) + 1));
   const int64_t n_blocks = (n_rows + rows_per_block - 1) / rows_per_block;
   SCB_CUDA(cudaFuncSetAttribute(hvg_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kRowThreads, smem, (cudaStream_t)stream>>>(
+  hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, (cudaStream_t)stream>>>(
       indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles,
       row_splits, rows_per_block, (unsigned long long*)sums);
   SCB_LAUNCH_CHECK();

@@ -33,42 +33,75 @@ struct Quad {
   unsigned valid;  // bit k: element p+k inside [b, e)
 };
 
+// one window of U quads starting at `base` (lane l: elements base + 128u + 4l .. +3)
+template <int U>
+__device__ __forceinline__ void load_window(const int* __restrict__ idx, const float* __restrict__ val, int64_t base,
+                                            int64_t b, int64_t e, int64_t nnz, Quad (&q)[U]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t p = base + 128 * u + 4 * lane;
+    q[u].p = p;
+    q[u].valid = 0;
+    if (p < e) {
+      if (p + 4 <= nnz) {
+        const int4 iv = ld_nc_v4(idx + p);
+        q[u].g[0] = iv.x; q[u].g[1] = iv.y; q[u].g[2] = iv.z; q[u].g[3] = iv.w;
+        if (val) {
+          const float4 dv = ld_nc_v4(val + p);
+          q[u].x[0] = dv.x; q[u].x[1] = dv.y; q[u].x[2] = dv.z; q[u].x[3] = dv.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          q[u].g[k] = (p + k < nnz) ? idx[p + k] : 0;
+          if (val) q[u].x[k] = (p + k < nnz) ? val[p + k] : 0.0f;
+        }
+      }
+      if (!val) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[u].x[k] = 0.0f;
+      }
+      // valid bits of p+k in [b, e): only a row's first and last quads are partial
+      const int64_t rem = e - p;  // >= 1
+      uint32_t m = rem >= 4 ? 0xFu : ((1u << (uint32_t)rem) - 1u);
+      if (p < b) m &= 0xFu << (uint32_t)(b - p);
+      q[u].valid = m;
+    }
+  }
+}
+
 template <int U, typename F>
 __device__ __forceinline__ void stream_row(const int* __restrict__ idx, const float* __restrict__ val, int64_t b,
                                            int64_t e, int64_t nnz, F&& f) {
-  const int lane = lane_id();
   for (int64_t base = b & ~int64_t(3); base < e; base += 128 * U) {
     Quad q[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t p = base + 128 * u + 4 * lane;
-      q[u].p = p;
-      q[u].valid = 0;
-      if (p < e) {
-        if (p + 4 <= nnz) {
-          const int4 iv = ld_nc_v4(idx + p);
-          q[u].g[0] = iv.x; q[u].g[1] = iv.y; q[u].g[2] = iv.z; q[u].g[3] = iv.w;
-          if (val) {
-            const float4 dv = ld_nc_v4(val + p);
-            q[u].x[0] = dv.x; q[u].x[1] = dv.y; q[u].x[2] = dv.z; q[u].x[3] = dv.w;
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            q[u].g[k] = (p + k < nnz) ? idx[p + k] : 0;
-            if (val) q[u].x[k] = (p + k < nnz) ? val[p + k] : 0.0f;
-          }
-        }
-        if (!val) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) q[u].x[k] = 0.0f;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) q[u].valid |= (p + k >= b && p + k < e) ? (1u << k) : 0u;
-      }
-    }
+    load_window<U>(idx, val, base, b, e, nnz, q);
 #pragma unroll
     for (int u = 0; u < U; ++u) f(q[u]);
+  }
+}
+
+// Software-pipelined variant: the next window's loads are issued before the current window
+// is processed, so a warp always has U x 1 KB in flight while it computes (for kernels whose
+// per-element work is long enough to expose the load latency).
+template <int U, typename F>
+__device__ __forceinline__ void stream_row_pipe(const int* __restrict__ idx, const float* __restrict__ val, int64_t b,
+                                                int64_t e, int64_t nnz, F&& f) {
+  int64_t base = b & ~int64_t(3);
+  if (base >= e) return;
+  Quad cur[U];
+  load_window<U>(idx, val, base, b, e, nnz, cur);
+  for (;;) {
+    const int64_t nb = base + 128 * U;
+    Quad nxt[U];
+    if (nb < e) load_window<U>(idx, val, nb, b, e, nnz, nxt);
+#pragma unroll
+    for (int u = 0; u < U; ++u) f(cur[u]);
+    if (nb >= e) break;
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+    base = nb;
   }
 }
 

@@ -135,7 +135,7 @@ def subset(X: DeviceCSR, cell_mask, gene_mask, n_kept=None, target_sum=None):
     nnz = int(new_indptr[nk].item())
     ind = torch.empty(nnz, dtype=torch.int32, device=dev)
     dat = torch.empty(nnz, dtype=torch.float32, device=dev)
-    _lib.call("scb_subset_fill", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, _p(cell_mask),
+    _lib.call("scb_subset_fill", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols, _p(cell_mask),
               _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(dat), s)
     out = DeviceCSR(new_indptr, ind, dat, gk)
     out.row_scale = row_scale
@@ -163,8 +163,8 @@ def subset_fill_log(X: DeviceCSR, cell_mask, remap, new_indptr, row_scale, nnz: 
     dev = X.device
     ind = torch.empty(nnz, dtype=torch.int32, device=dev)
     logv = torch.empty(nnz, dtype=torch.float32, device=dev)
-    _lib.call("scb_subset_fill", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, _p(cell_mask),
-              _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(logv), _stream(dev))
+    _lib.call("scb_subset_fill", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols,
+              _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(logv), _stream(dev))
     return DeviceCSR(new_indptr, ind, logv, n_genes_kept, row_scale=row_scale)
 
 

@@ -17,9 +17,12 @@ def main(path, title="", exclude=""):
     start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[start]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[start + 1:]:
         if len(r) <= vi or not r[vi]:
+            continue
+        if mi is not None and r[mi] != "gpu__time_duration.sum":  # other metrics of a multi-metric list
             continue
         name = r[ki].split("(")[0].replace("void ", "").strip()
         if exclude and re.search(exclude, name):
