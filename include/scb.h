@@ -75,8 +75,9 @@ SCB_API int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
 /* Number of gene tiles T the HVG column pass uses for n_cols genes.  If T > 1, passing
  * hvg_row_splits (int32 [n_rows][T-1]) to scb_qc_metrics records, per row, how many entries
  * have a gene index below each tile boundary; scb_hvg_gene_sums then streams every nonzero
- * exactly once (otherwise each tile re-reads whole rows).  indices/data arrays of every CSR
- * entry point must be 16-byte aligned. */
+ * exactly once (otherwise each tile re-reads whole rows); rows whose column indices are not
+ * sorted are detected there and the pass is redone without splits.  indices/data arrays of
+ * every CSR entry point must be 16-byte aligned. */
 SCB_API int32_t scb_hvg_tiles(int32_t n_cols);
 
 /* ---- a2: sc.pp.filter_cells(min_genes, max_genes) + pct_counts_mt < max_pct_mt, and

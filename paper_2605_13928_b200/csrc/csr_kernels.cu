@@ -199,6 +199,12 @@ qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indice
   }
 }
 
+__global__ void add_u64_kernel(const unsigned long long* __restrict__ a, unsigned long long* __restrict__ b,
+                               int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] += a[i];
+}
+
 __global__ void qc_finalize(const uint32_t* g_cells, const unsigned long long* g_total, int32_t n,
                             int32_t* n_cells, double* gene_total) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -403,7 +409,7 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
                 const float* __restrict__ data, const float* __restrict__ row_scale, int64_t n_rows,
                 int32_t n_cols, const int32_t* __restrict__ remap, int32_t n_out, int32_t tile_w,
                 int32_t n_tiles, const int32_t* __restrict__ splits, int64_t rows_per_block,
-                unsigned long long* __restrict__ sums) {
+                unsigned long long* __restrict__ sums, int* __restrict__ order_flag) {
   const int64_t nnz = indptr[n_rows];
   extern __shared__ uint32_t sm[];
   const int tile = blockIdx.x % n_tiles;
@@ -421,11 +427,13 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
   const int64_t r0 = rblk * rows_per_block;
   const int64_t r1 = min(n_rows, r0 + rows_per_block);
   const int ns = n_tiles - 1;
+  const bool split_mode = splits && ns > 0;
+  bool out_of_order = false;
   for (int64_t r = r0 + warp_id(); r < r1; r += (blockDim.x >> 5)) {
     const float s = row_scale[r];
     if (s == 0.0f) continue;
     int64_t b = indptr[r], e = indptr[r + 1];
-    if (splits && ns > 0) {
+    if (split_mode) {
       const int64_t rb = b;
       if (tile > 0) b = rb + splits[r * ns + tile - 1];
       if (tile < ns) e = rb + splits[r * ns + tile];
@@ -447,6 +455,9 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
       for (int k = 0; k < 4; ++k) {
         const int gl = q.g[k] - g0;
         const bool in = ((q.valid >> k) & 1u) && gl >= 0 && gl < w;
+        // with row splits every entry of the streamed sub-range must belong to this tile (true
+        // for sorted rows); anything else means unsorted indices -> the host reruns unsplit
+        out_of_order |= split_mode & ((q.valid >> k) & 1u) & !in;
         const float y = __fmul_rn(q.x[k], s);  // float32 normalized count
         v1[k] = in ? (uint64_t)__float2ull_rn(__fmul_rn(y, 268435456.0f)) : 0ull;
         const double y12 = (double)__fmul_rn(y, 4096.0f);
@@ -491,6 +502,7 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
       }
     });
   }
+  if (out_of_order) atomicOr(order_flag, 1);
   __syncthreads();
   unsigned long long* l0 = sums;               // stat 0 limb 0
   unsigned long long* l1 = sums + n_out;       // stat 0 limb 1
@@ -1065,9 +1077,40 @@ extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int3
   int64_t rows_per_block = std::max<int64_t>(64, std::min<int64_t>(1024, n_rows / (2 * ctx->num_sms) + 1));
   const int64_t n_blocks = (n_rows + rows_per_block - 1) / rows_per_block;
   SCB_CUDA(cudaFuncSetAttribute(hvg_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, (cudaStream_t)stream>>>(
-      indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles,
-      row_splits, rows_per_block, (unsigned long long*)sums);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool split = row_splits && n_tiles > 1;
+  if (!split) {
+    hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
+        indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, nullptr,
+        rows_per_block, (unsigned long long*)sums, ctx->d_flag + 1);
+    SCB_LAUNCH_CHECK();
+    return SCB_OK;
+  }
+  // The row splits assume sorted column indices within each row (canonical CSR).  The split
+  // pass accumulates into scratch; if it saw an entry outside its tile (unsorted row) the
+  // scratch is recomputed with every tile filtering whole rows, then added into sums (+=).
+  const size_t sbytes = (size_t)4 * n_out * sizeof(uint64_t);
+  void* ws;
+  SCB_TRY(ws_get(ctx, 2, sbytes, &ws, s));
+  unsigned long long* tmp = (unsigned long long*)ws;
+  int* order_flag = ctx->d_flag + 1;
+  SCB_CUDA(cudaMemsetAsync(tmp, 0, sbytes, s));
+  SCB_CUDA(cudaMemsetAsync(order_flag, 0, sizeof(int), s));
+  hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
+      indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, row_splits,
+      rows_per_block, tmp, order_flag);
+  SCB_LAUNCH_CHECK();
+  int flag = 0;
+  SCB_CUDA(cudaMemcpyAsync(&flag, order_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SCB_CUDA(cudaStreamSynchronize(s));
+  if (flag) {
+    SCB_CUDA(cudaMemsetAsync(tmp, 0, sbytes, s));
+    hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
+        indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, nullptr,
+        rows_per_block, tmp, order_flag);
+    SCB_LAUNCH_CHECK();
+  }
+  add_u64_kernel<<<ceil_div(4 * n_out, 256), 256, 0, s>>>(tmp, (unsigned long long*)sums, (int64_t)4 * n_out);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }

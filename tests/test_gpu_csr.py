@@ -1,7 +1,10 @@
 """GPU parity of the CSR stages (QC, masks, subset, normalize+log1p, HVG, scale) vs the oracle."""
+import functools
+
 import numpy as np
 import pytest
 
+from oracle.synth import SynthSpec, generate_csr, mt_mask
 from tests.gpu_fixtures import C1, c1_inputs, c1_oracle
 
 pytestmark = pytest.mark.gpu
@@ -129,3 +132,41 @@ def test_cpm_normalization_hvg_and_scale_exact():
     sc = scb.scale(Xl, hvg_index, p.max_value)
     np.testing.assert_allclose(sc.mean.cpu().numpy(), o["scale_mean"], rtol=1e-7)
     np.testing.assert_allclose(sc.inv_std.cpu().numpy(), o["scale_inv_std"], rtol=1e-7)
+
+
+@functools.lru_cache(maxsize=1)
+def _wide_case():
+    from oracle import pipeline as op
+    spec = SynthSpec(3000, 20000, seed=7)
+    ip, ix, d = generate_csr(spec)
+    X = op.CSR(ip, ix, d, spec.n_genes)
+    mt = mt_mask(spec)
+    p = op.Params(min_genes=50, max_pct_mt=20.0, n_top_genes=1000, n_neighbors=15)
+    return spec, ip, ix, d, mt, p, op.run(X, mt, p, with_knn=False)
+
+
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_hvg_row_splits_sorted_and_unsorted_rows(shuffle):
+    """> 1 HVG gene tile (20k genes): QC's per-row tile splits let each tile stream only its
+    sub-range of a row.  With the column indices of every row shuffled (non-canonical CSR) the
+    split pass detects entries outside its tile and is redone unsplit; the HVG statistics stay
+    bit-exact against the oracle either way."""
+    import torch
+    from paper_2605_13928_b200 import _lib, pipeline, pp
+    spec, ip, ix, d, mt, p, o = _wide_case()
+    if shuffle:
+        rng = np.random.default_rng(3)
+        ix = ix.copy()
+        d = d.copy()
+        for r in range(len(ip) - 1):
+            perm = ip[r] + rng.permutation(ip[r + 1] - ip[r])
+            ix[ip[r]:ip[r + 1]] = ix[perm]
+            d[ip[r]:ip[r + 1]] = d[perm]
+    assert int(_lib.call("scb_hvg_tiles", spec.n_genes)) > 1
+    Xd = pp.DeviceCSR.from_host(ip, ix, d, spec.n_genes)
+    pp_ = pipeline.Params(min_genes=p.min_genes, max_pct_mt=p.max_pct_mt, min_cells=p.min_cells,
+                          n_top_genes=p.n_top_genes)
+    r = pipeline.run(Xd, torch.as_tensor(mt, device="cuda"), pp_, with_knn=False, timing=False)
+    np.testing.assert_array_equal(r.hvg_mask.cpu().numpy(), o["hvg_mask"])
+    np.testing.assert_array_equal(r.hvg_stats["means"].cpu().numpy(), o["hvg_stats"]["means"])
+    np.testing.assert_array_equal(r.hvg_stats["variances"].cpu().numpy(), o["hvg_stats"]["variances"])
