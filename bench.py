@@ -29,7 +29,8 @@ METRIC = "cells/sec end-to-end QC→kNN at 1M cells ×25k genes, 1/2/4/8 B200; p
 def _params(args):
     from paper_2605_13928_b200.pipeline import Params
     return Params(min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3, target_sum=1e4,
-                  n_top_genes=args.hvg, n_bins=20, max_value=10.0, n_comps=50, n_neighbors=args.k)
+                  n_top_genes=args.hvg, n_bins=20, max_value=10.0, n_comps=50, n_neighbors=args.k,
+                  regress_out=args.regress_out)
 
 
 def _peaks():
@@ -96,12 +97,14 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def _step_bytes(Z_in, N, G, Z_sub, N_sub, H, ld):
+def _step_bytes(Z_in, N, G, Z_sub, N_sub, H, ld, regress_out=False):
     """Algorithmic HBM bytes per step."""
     return {
         "qc": 8 * Z_in + 8 * (N + 1),
         "norm_hvg": 8 * Z_in + (8 * Z_in + 8 * Z_sub) + 8 * Z_in + 4 * N,  # count, fill, hvg sums
-        "regress": 8 * Z_sub + (8 * Z_sub + 4 * N_sub * ld),                  # scale sums, dense scale
+        # scale: scale sums + dense scale; regress_out: dense log (8Z' + 4N ld), Aᵀl read (4N ld),
+        # in-place residual scaling (8N ld)
+        "regress": (8 * Z_sub + 16 * N_sub * ld) if regress_out else (8 * Z_sub + (8 * Z_sub + 4 * N_sub * ld)),
         "project": 4 * N_sub * ld + 4 * N_sub * 64,
     }
 
@@ -165,6 +168,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=10000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--regress-out", action="store_true",
+                    help="add sc.pp.regress_out(total_counts, pct_counts_mt) before scale (paper Table 1 step 4)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -255,7 +260,7 @@ def main():
     f16_peak = bf16  # dense FP16 == dense BF16 tensor rate
     flops_knn = 2.0 * N_sub_loc * n_keys * p.n_comps
     achieved = flops_knn / (knn_ms / 1e3) / 1e12
-    sb = _step_bytes(Z_in, X.n_rows, G, Z_sub, N_sub_loc, H, ld)
+    sb = _step_bytes(Z_in, X.n_rows, G, Z_sub, N_sub_loc, H, ld, args.regress_out)
     stages = {}
     for kk in ("qc", "norm_hvg", "regress"):
         if kk in step_ms and step_ms[kk] > 0:
@@ -350,7 +355,8 @@ def main():
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic NB counts generated on device (oracle/synth.py model, seed %d)" % args.seed,
             "config": {"workload": f"C3: {N} cells x {G} genes (~{Z_total / N / G:.1%} dense), full QC->normalize->"
-                                   f"log1p->HVG(seurat,{args.hvg})->scale->PCA(50)->kNN(k={args.k}, exact)",
+                                   f"log1p->HVG(seurat,{args.hvg})->{'regress_out+' if args.regress_out else ''}scale->PCA(50)->"
+                                   f"kNN(k={args.k}, exact)",
                        "cells": N, "genes": G, "nnz": int(Z_total), "kept_cells": int(n_keys), "hvg": H,
                        "parallelism": f"cells sharded x{world}", "l2": "inputs (14 GB) >> L2 (126 MB); no flush needed",
                        "gen_seconds": round(gen_s, 1)},

@@ -145,6 +145,28 @@ SCB_API int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* 
                     int32_t n_slots, const double* mean, const double* inv_std, double max_value,
                     float* Z, int64_t ldz, int32_t ones_col, void* stream);
 
+/* ---- f2 (optional, paper Table 1 step 4): sc.pp.regress_out(["total_counts",
+ * "pct_counts_mt"]) fused with scale.  Replaces scale_gene_sums/finalize:
+ *   1. scb_regress_cov_sums: sums6 = {n, Σtc, Σtc², Σpct, Σpct², Σtc·pct} over the kept
+ *      cells (float64; all-reduced across ranks);
+ *   2. scb_regress_design: standardised covariates design[2][n_kept] (kept-row order);
+ *   3. scb_scale_dense with mean = 0, inv_std = 1, max_value = +inf -> Z holds l (dense);
+ *   4. scb_regress_xty: xty[4][H] += {Σl, Σa1·l, Σa2·l, Σl²} per gene (all-reduced);
+ *   5. scb_regress_finalize: beta[3][H] (OLS) and inv_std[H] of the residuals;
+ *   6. scb_regress_apply: Z[:, :H] = min((l - beta0 - a1 beta1 - a2 beta2) * inv_std, max). */
+SCB_API int scb_regress_cov_sums(scb_ctx* ctx, const double* total_counts, const double* pct_counts_mt,
+                         const uint8_t* cell_mask, int64_t n_rows, double* sums6, void* stream);
+SCB_API int scb_regress_design(scb_ctx* ctx, const double* total_counts, const double* pct_counts_mt,
+                       const uint8_t* cell_mask, int64_t n_rows, const double* sums6, int64_t n_kept,
+                       double* design, void* stream);
+SCB_API int scb_regress_xty(scb_ctx* ctx, const float* Z, int64_t n_rows, int64_t ld, int32_t n_slots,
+                    const double* design, double* xty, void* stream);
+SCB_API int scb_regress_finalize(scb_ctx* ctx, const double* xty, const double* sums6, int32_t n_slots,
+                         double* beta, double* inv_std, void* stream);
+SCB_API int scb_regress_apply(scb_ctx* ctx, float* Z, int64_t n_rows, int64_t ld, int32_t n_slots,
+                      const double* design, const double* beta, const double* inv_std, double max_value,
+                      void* stream);
+
 /* ---- a7: partial Gram matrix C = Z^T Z (float64 [hp][hp], full symmetric) on the
  * 5th-gen tensor cores (tcgen05 kind::f16, "3xBF16": x = hi + lo with hi = bf16(x),
  * lo = bf16(x - hi), products hi*hi + hi*lo + lo*hi, <= 2^-16 relative each; FP32 accumulate

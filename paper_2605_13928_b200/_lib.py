@@ -37,6 +37,11 @@ SIGNATURES = {
     "scb_gram": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
     "scb_gram_split": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
     "scb_split_bf16": [c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr],
+    "scb_regress_cov_sums": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
+    "scb_regress_design": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr],
+    "scb_regress_xty": [c_ptr, c_ptr, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_ptr],
+    "scb_regress_finalize": [c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr],
+    "scb_regress_apply": [c_ptr, c_ptr, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_dbl, c_ptr],
     "scb_pca_eig": [c_ptr, c_ptr, c_i32, c_i32, c_i32, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_project": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_i32, c_ptr],
     "scb_knn": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_i32, c_i32, c_i32, c_ptr, c_ptr, c_ptr],

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_tile_sums(F f, int64_t n, i
   if (threadIdx.x == 0) sums[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(int64_t* sums, int64_t nb) {
+static __global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(int64_t* sums, int64_t nb) {
   __shared__ int64_t sbuf[33];
   __shared__ int64_t carry;
   if (threadIdx.x == 0) carry = 0;

@@ -38,6 +38,7 @@ class Params:
     max_value: float = 10.0
     n_comps: int = 50
     n_neighbors: int = 15
+    regress_out: bool = False  # sc.pp.regress_out(["total_counts", "pct_counts_mt"]) before scale
 
 
 @dataclasses.dataclass
@@ -117,11 +118,23 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
     tm.step("regress")
     H = int(hvg_index.numel())
     slot = pp.gene_slots(hvg_index, gk)
-    ssum = pp.scale_gene_sums(X_log, slot, H)
-    if comm is not None:
-        comm.allreduce_(ssum)
-    mean, inv = pp.scale_finalize(ssum, n_total)
-    sc = pp.scale_dense(X_log, slot, H, mean, inv, p.max_value)
+    if p.regress_out:
+        s6 = pp.regress_cov_sums(qc, cm)
+        if comm is not None:
+            comm.allreduce_(s6)
+        design = pp.regress_design(qc, cm, s6, nk_local)
+        sc = pp.regress_dense_log(X_log, slot, H)
+        xty = pp.regress_xty(sc, design)
+        if comm is not None:
+            comm.allreduce_(xty)
+        beta, inv = pp.regress_finalize(xty, s6)
+        sc = pp.regress_apply(sc, design, beta, inv, p.max_value)
+    else:
+        ssum = pp.scale_gene_sums(X_log, slot, H)
+        if comm is not None:
+            comm.allreduce_(ssum)
+        mean, inv = pp.scale_finalize(ssum, n_total)
+        sc = pp.scale_dense(X_log, slot, H, mean, inv, p.max_value)
 
     # ------------------------------------------------------------------ pca
     tm.step("pca")

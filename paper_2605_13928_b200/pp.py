@@ -298,6 +298,72 @@ def scale(X_log: DeviceCSR, hvg_index: torch.Tensor, max_value: float = 10.0) ->
     return scale_dense(X_log, slot, H, mean, inv, max_value)
 
 
+# ----------------------------------------------------------------------------- regress_out
+def regress_cov_sums(qc: dict, cell_mask: torch.Tensor) -> torch.Tensor:
+    """float64[6] = (n, Σtc, Σtc², Σpct, Σpct², Σtc·pct) over the kept cells (all-reduce across ranks)."""
+    tc, pc = qc["total_counts"], qc["pct_counts_mt"]
+    out = torch.empty(6, dtype=torch.float64, device=tc.device)
+    _lib.call("scb_regress_cov_sums", _ctx(tc), _p(tc), _p(pc), _p(cell_mask), tc.numel(), _p(out), _stream(tc.device))
+    return out
+
+
+def regress_design(qc: dict, cell_mask: torch.Tensor, sums6: torch.Tensor, n_kept: int) -> torch.Tensor:
+    """Standardised covariates float64 [2][n_kept] (kept-row order)."""
+    tc, pc = qc["total_counts"], qc["pct_counts_mt"]
+    a = torch.empty((2, n_kept), dtype=torch.float64, device=tc.device)
+    _lib.call("scb_regress_design", _ctx(tc), _p(tc), _p(pc), _p(cell_mask), tc.numel(), _p(sums6), int(n_kept),
+              _p(a), _stream(tc.device))
+    return a
+
+
+def regress_dense_log(X_log: DeviceCSR, slot, H: int) -> Scaled:
+    """Dense log values of the HVG columns (scale_dense with mean 0, inv_std 1, no clip)."""
+    dev = X_log.device
+    zeros = torch.zeros(H, dtype=torch.float64, device=dev)
+    ones = torch.ones(H, dtype=torch.float64, device=dev)
+    return scale_dense(X_log, slot, H, zeros, ones, float("inf"))
+
+
+def regress_xty(L: Scaled, design: torch.Tensor, xty=None) -> torch.Tensor:
+    """xty float64 [4][H] += (Σl, Σa1·l, Σa2·l, Σl²) per gene (all-reduce across ranks)."""
+    if xty is None:
+        xty = torch.zeros((4, L.H), dtype=torch.float64, device=L.Z.device)
+    _lib.call("scb_regress_xty", _ctx(L.Z), _p(L.Z), L.Z.shape[0], L.ld, L.H, _p(design), _p(xty), _stream(L.Z.device))
+    return xty
+
+
+def regress_finalize(xty: torch.Tensor, sums6: torch.Tensor):
+    H = xty.shape[1]
+    beta = torch.empty((3, H), dtype=torch.float64, device=xty.device)
+    inv = torch.empty(H, dtype=torch.float64, device=xty.device)
+    _lib.call("scb_regress_finalize", _ctx(xty), _p(xty), _p(sums6), H, _p(beta), _p(inv), _stream(xty.device))
+    return beta, inv
+
+
+def regress_apply(L: Scaled, design, beta, inv, max_value: float = 10.0) -> Scaled:
+    """In place: Z[:, :H] = min((l - fit) * inv_std, max_value); returns the Scaled view
+    (mean 0 -- the residual mean is zero by construction)."""
+    _lib.call("scb_regress_apply", _ctx(L.Z), _p(L.Z), L.Z.shape[0], L.ld, L.H, _p(design), _p(beta), _p(inv),
+              float(max_value), _stream(L.Z.device))
+    L.mean = torch.zeros(L.H, dtype=torch.float64, device=L.Z.device)
+    L.inv_std = inv
+    return L
+
+
+def regress_out_scale(X_log: DeviceCSR, hvg_index: torch.Tensor, qc: dict, cell_mask: torch.Tensor,
+                      max_value: float = 10.0) -> Scaled:
+    """sc.pp.regress_out(adata[:, hvg], ["total_counts", "pct_counts_mt"]) + sc.pp.scale(max_value)
+    (paper Table 1 step 4).  ``qc``/``cell_mask`` are the QC metrics and cell mask of the ORIGINAL
+    rows; X_log holds the kept rows in order."""
+    H = int(hvg_index.numel())
+    slot = gene_slots(hvg_index, X_log.n_cols)
+    s6 = regress_cov_sums(qc, cell_mask)
+    design = regress_design(qc, cell_mask, s6, X_log.n_rows)
+    L = regress_dense_log(X_log, slot, H)
+    beta, inv = regress_finalize(regress_xty(L, design), s6)
+    return regress_apply(L, design, beta, inv, max_value)
+
+
 # ----------------------------------------------------------------------------- pca
 @dataclasses.dataclass
 class PCAResult:

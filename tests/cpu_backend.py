@@ -121,6 +121,55 @@ def scale_dense(X_log, slot, H, mean, inv, max_value=10.0, out=None):
     return Scaled(torch.as_tensor(Z), H, H, mean, inv)
 
 
+def regress_cov_sums(qc, cell_mask):
+    k = _np(cell_mask).astype(bool)
+    return torch.as_tensor(op.regress_cov_sums(_np(qc["total_counts"])[k], _np(qc["pct_counts_mt"])[k]))
+
+
+def regress_design(qc, cell_mask, sums6, n_kept):
+    k = _np(cell_mask).astype(bool)
+    a1, a2, _ = op.regress_design(_np(qc["total_counts"])[k], _np(qc["pct_counts_mt"])[k], _np(sums6))
+    assert len(a1) == n_kept
+    return torch.as_tensor(np.stack([a1, a2]))
+
+
+def regress_dense_log(X_log, slot, H):
+    return scale_dense(X_log, slot, H, torch.zeros(H, dtype=torch.float64), torch.ones(H, dtype=torch.float64),
+                       float("inf"))
+
+
+def regress_xty(L, design, xty=None):
+    Lh = _np(L.Z)[:, :L.H].astype(np.float64)
+    a = _np(design)
+    v = np.stack([Lh.sum(0), a[0] @ Lh, a[1] @ Lh, (Lh * Lh).sum(0)])
+    return torch.as_tensor(v) if xty is None else xty + torch.as_tensor(v)
+
+
+def regress_finalize(xty, sums6):
+    S0, S1, S2, Q = _np(xty)
+    s6 = _np(sums6)
+    n = s6[0]
+    m1, m2 = s6[1] / n, s6[3] / n
+    v1, v2 = max(s6[2] / n - m1 * m1, 0.0), max(s6[4] / n - m2 * m2, 0.0)
+    s1, s2 = (np.sqrt(v1) if v1 > 0 else 1.0), (np.sqrt(v2) if v2 > 0 else 1.0)
+    c = (s6[5] - n * m1 * m2) / (s1 * s2)
+    b0 = S0 / n
+    det = n * n - c * c
+    b1, b2 = ((n * S1 - c * S2) / det, (n * S2 - c * S1) / det) if det > 1e-12 * n * n else (S1 / n, 0 * S1)
+    var = (Q - (b0 * S0 + b1 * S1 + b2 * S2)) / (n - 1.0)
+    std = np.sqrt(np.where(var > 0, var, 0.0))
+    std = np.where(std == 0, 1.0, std)
+    return torch.as_tensor(np.stack([b0, b1, b2])), torch.as_tensor(1.0 / std)
+
+
+def regress_apply(L, design, beta, inv, max_value=10.0):
+    Z = _np(L.Z).copy()
+    a, b, iv = _np(design), _np(beta), _np(inv)
+    fit = b[0][None, :] + a[0][:, None] * b[1][None, :] + a[1][:, None] * b[2][None, :]
+    Z[:, :L.H] = np.minimum((Z[:, :L.H].astype(np.float64) - fit) * iv[None, :], max_value).astype(np.float32)
+    return Scaled(torch.as_tensor(Z), L.H, L.ones_col, torch.zeros(L.H, dtype=torch.float64), inv)
+
+
 def gram(sc, out=None, planes=True):  # noqa: ARG001 (no BF16 planes on the CPU)
     Z = _np(sc.Z).astype(np.float64)
     return torch.as_tensor(Z.T @ Z)

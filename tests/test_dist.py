@@ -22,15 +22,15 @@ def _port():
     return p
 
 
-def _params():
+def _params(regress_out=False):
     from paper_2605_13928_b200.pipeline import Params
     P = mg.PARAMS
     return Params(min_genes=P.min_genes, max_genes=P.max_genes, max_pct_mt=P.max_pct_mt, min_cells=P.min_cells,
                   target_sum=P.target_sum, n_top_genes=P.n_top_genes, n_bins=P.n_bins, max_value=P.max_value,
-                  n_comps=P.n_comps, n_neighbors=P.n_neighbors)
+                  n_comps=P.n_comps, n_neighbors=P.n_neighbors, regress_out=regress_out)
 
 
-def _run(rank, world, port, out_dir):
+def _run(rank, world, port, out_dir, regress_out=False):
     import tests.cpu_backend as cb
     from paper_2605_13928_b200 import pipeline
     from paper_2605_13928_b200.dist import Comm, shard_rows
@@ -46,8 +46,8 @@ def _run(rank, world, port, out_dir):
     ip = g["indptr"][r0:r1 + 1] - g["indptr"][r0]
     sl = slice(int(g["indptr"][r0]), int(g["indptr"][r1]))
     X = DeviceCSR(torch.as_tensor(ip), torch.as_tensor(g["indices"][sl]), torch.as_tensor(g["data"][sl]), 300)
-    res = pipeline.run(X, torch.as_tensor(g["mt_mask"]), _params(), comm=comm, timing=False)
-    np.savez(os.path.join(out_dir, f"r{rank}_w{world}.npz"), cell_mask=res.cell_mask.numpy(),
+    res = pipeline.run(X, torch.as_tensor(g["mt_mask"]), _params(regress_out), comm=comm, timing=False)
+    np.savez(os.path.join(out_dir, f"r{rank}_w{world}.npz"), cell_mask=res.cell_mask.numpy(), Z=res.scaled.values().numpy(),
              gene_mask=res.gene_mask.numpy(), hvg=res.hvg_mask.numpy(), mean=res.scaled.mean.numpy(),
              inv=res.scaled.inv_std.numpy(), comps=res.pca.components.numpy(), var=res.pca.variance.numpy(),
              xpca=res.pca.X_pca.numpy()[:, :res.pca.n_comps], knn=res.knn_index.numpy(), n=res.n_cells_total)
@@ -76,3 +76,25 @@ def test_two_rank_gloo_matches_single_process(tmp_path):
     g = np.load("tests/golden/g600x300.npz")
     np.testing.assert_array_equal(one["hvg"], g["hvg_mask"])
     np.testing.assert_array_equal(one["knn"], g["knn_idx"])
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_regress_out_matches_single_process_and_oracle(tmp_path):
+    """regress_out path: all-reduced covariate sums and Aᵀl partials give the single-process
+    residual scaling (float64 sums in a different order: tolerance, not bit-exact), and the
+    single-process result equals the oracle's regress_out_scale."""
+    from oracle import pipeline as op
+    _run(0, 1, 0, str(tmp_path), True)
+    mp.spawn(_run, args=(2, _port(), str(tmp_path), True), nprocs=2, join=True)
+    one = np.load(tmp_path / "r0_w1.npz")
+    parts = [np.load(tmp_path / f"r{r}_w2.npz") for r in range(2)]
+    for p in parts:
+        np.testing.assert_allclose(p["inv"], one["inv"], rtol=1e-10)
+    np.testing.assert_allclose(np.concatenate([p["Z"] for p in parts]), one["Z"], rtol=1e-5, atol=1e-5)
+    g = np.load("tests/golden/g600x300.npz")
+    X = op.CSR(g["indptr"], g["indices"], g["data"], 300)
+    P = mg.PARAMS
+    import dataclasses
+    o = op.run(X, g["mt_mask"], dataclasses.replace(P, regress_out=True), with_knn=False)
+    np.testing.assert_allclose(one["Z"], o["Z"], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(one["inv"], o["scale_inv_std"], rtol=1e-10)

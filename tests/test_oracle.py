@@ -102,6 +102,46 @@ def test_scale_clip_upper_only():
     del rows, rng
 
 
+def _regress_case(seed=5, n=600, g=60, h=12):
+    rng = np.random.default_rng(seed)
+    M = sp.random(n, g, density=0.3, random_state=seed, format="csr", dtype=np.float64)
+    M.data = np.floor(M.data * 20) + 1
+    M.sort_indices()
+    X = op.CSR(M.indptr.astype(np.int64), M.indices.astype(np.int32), M.data.astype(np.float32), g)
+    Xl, _, _ = op.normalize_log1p(X, 1e4)
+    hvg = np.zeros(g, np.uint8)
+    hvg[rng.choice(g, h, replace=False)] = 1
+    tk = rng.integers(500, 5000, n).astype(np.float64)
+    pk = rng.uniform(0, 15, n)
+    return Xl, hvg, tk, pk
+
+
+def test_regress_out_matches_lstsq_residuals():
+    """The standardised-design normal-equation fit equals OLS on [1, total_counts, pct_mt]
+    (numpy lstsq) and the residual scaling equals np.std(ddof=1) of the explicit residuals."""
+    Xl, hvg, tk, pk = _regress_case()
+    Z, beta, inv = op.regress_out_scale(Xl, hvg, tk, pk, max_value=1e30)
+    cols = np.nonzero(hvg)[0]
+    L = np.asarray(sp.csr_matrix((Xl.data, Xl.indices, Xl.indptr), shape=(Xl.n_rows, Xl.n_cols)).todense(),
+                   np.float64)[:, cols]
+    A = np.stack([np.ones_like(tk), tk, pk], 1)
+    B, *_ = np.linalg.lstsq(A, L, rcond=None)
+    R = L - A @ B
+    assert np.abs(R.mean(0)).max() < 1e-10
+    Zref = (R - R.mean(0)) / R.std(0, ddof=1)
+    np.testing.assert_allclose(Z, Zref, rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(1.0 / inv, R.std(0, ddof=1), rtol=1e-9)
+
+
+def test_regress_out_clip_and_constant_gene():
+    Xl, hvg, tk, pk = _regress_case(seed=9)
+    Z, _, inv = op.regress_out_scale(Xl, hvg, tk, pk, max_value=1.5)
+    assert Z.max() <= 1.5
+    # a covariate that is constant -> std 0 -> 1 and the fit still works (collinear with 1)
+    Z2, _, _ = op.regress_out_scale(Xl, hvg, tk, np.full_like(pk, 3.0), max_value=1e30)
+    assert np.isfinite(Z2).all()
+
+
 # ----------------------------------------------------------------------------- golden fixtures
 @pytest.fixture(scope="module")
 def golden():
