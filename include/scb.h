@@ -62,6 +62,24 @@ SCB_API unsigned long long scb_launch_count(void);
 SCB_API int scb_ctx_create(int device, scb_ctx** out);
 SCB_API int scb_ctx_destroy(scb_ctx* ctx);
 
+/* ---- f1 ingest (sc.read_10x_mtx / sc.read_mtx): MatrixMarket coordinate data lines -> COO
+ * on the device.  text holds the whole file (16-byte aligned, readable up to
+ * roundup(n_bytes, 16)); data_offset = first data line (the host parses the banner, comments
+ * and size line); field 0 = integer, 1 = real, 2 = pattern.  row/col receive 0-based file
+ * coordinates in file order, val the values as float32.  SCB_ERR_DATA if the number of data
+ * lines differs from nnz or a line is malformed / out of range. */
+SCB_API int scb_mtx_parse(scb_ctx* ctx, const char* text, int64_t data_offset, int64_t n_bytes, int32_t field,
+                  int64_t nnz, int64_t n_file_rows, int64_t n_file_cols, int32_t* row, int32_t* col,
+                  float* val, void* stream);
+
+/* ---- COO -> CSR over `major` (cells = file columns of a 10x matrix.mtx): indptr
+ * int64[n_major+1], indices (minor, ascending within each row), data.  Input already in CSR
+ * order (major non-decreasing, minor strictly increasing within a row) is converted without
+ * moving entries (indices/data may alias minor/val); otherwise a counting scatter plus a
+ * per-row sort (rows <= 8192 entries).  Duplicate (major, minor) entries: SCB_ERR_DATA. */
+SCB_API int scb_coo_to_csr(scb_ctx* ctx, const int32_t* major, const int32_t* minor, const float* val, int64_t nnz,
+                   int32_t n_major, int64_t* indptr, int32_t* indices, float* data, void* stream);
+
 /* ---- a1: sc.pp.calculate_qc_metrics(qc_vars=["mt"], percent_top=None, log1p=False)
  * Per cell: n_genes_by_counts, total_counts, total_counts_mt, pct_counts_mt.
  * Per gene: n_cells_by_counts, total_counts (exact; counts must be non-negative

@@ -37,6 +37,8 @@ SIGNATURES = {
     "scb_gram": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
     "scb_gram_split": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
     "scb_split_bf16": [c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr],
+    "scb_mtx_parse": [c_ptr, c_ptr, c_i64, c_i64, c_i32, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr],
+    "scb_coo_to_csr": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_regress_cov_sums": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     "scb_regress_design": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr],
     "scb_regress_xty": [c_ptr, c_ptr, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_ptr],
