@@ -185,6 +185,25 @@ SCB_API int scb_regress_apply(scb_ctx* ctx, float* Z, int64_t n_rows, int64_t ld
                       const double* design, const double* beta, const double* inv_std, double max_value,
                       void* stream);
 
+/* ---- f3 sc.pp.neighbors graph outputs (umap-learn fuzzy_simplicial_set on the exact kNN,
+ * set_op_mix_ratio 1, local_connectivity 1).  knn_idx/knn_dist are [rows][k] as returned by
+ * scb_knn (self included).  scb_knn_dist_sum: sum of all distances (the caller divides by
+ * N*k for the global mean, all-reduced across ranks).  scb_umap_weights: per local row
+ * sigma, rho and membership strengths w[rows][k] (row0 = global index of the first row).
+ * scb_fuzzy_union_rows / _fill: rows [r0, r1) of C = W + Wᵀ - W∘Wᵀ (f32, scipy's evaluation
+ * order) from the global (all-gathered) idx/w: indptr int64[r1-r0+1] first, then cols/vals
+ * (sorted by column).  scb_knn_distances_csr: `distances` (non-zero kNN distances, sorted by
+ * column; cols/vals need rows*k capacity). */
+SCB_API int scb_knn_dist_sum(scb_ctx* ctx, const float* knn_dist, int64_t n, double* sum, void* stream);
+SCB_API int scb_umap_weights(scb_ctx* ctx, const int32_t* knn_idx, const float* knn_dist, int64_t n_rows, int32_t k,
+                     int64_t row0, const double* mean_dist, float* sigma, float* rho, float* w, void* stream);
+SCB_API int scb_fuzzy_union_rows(scb_ctx* ctx, const int32_t* idx_all, const float* w_all, int64_t n_all, int32_t k,
+                         int64_t r0, int64_t r1, int64_t* indptr, void* stream);
+SCB_API int scb_fuzzy_union_fill(scb_ctx* ctx, const int32_t* idx_all, const float* w_all, int64_t n_all, int32_t k,
+                         int64_t r0, int64_t r1, const int64_t* indptr, int32_t* cols, float* vals, void* stream);
+SCB_API int scb_knn_distances_csr(scb_ctx* ctx, const int32_t* knn_idx, const float* knn_dist, int64_t n_rows,
+                          int32_t k, int64_t* indptr, int32_t* cols, float* vals, void* stream);
+
 /* ---- a7: partial Gram matrix C = Z^T Z (float64 [hp][hp], full symmetric) on the
  * 5th-gen tensor cores (tcgen05 kind::f16, "3xBF16": x = hi + lo with hi = bf16(x),
  * lo = bf16(x - hi), products hi*hi + hi*lo + lo*hi, <= 2^-16 relative each; FP32 accumulate

@@ -37,6 +37,11 @@ SIGNATURES = {
     "scb_gram": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
     "scb_gram_split": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
     "scb_split_bf16": [c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr],
+    "scb_knn_dist_sum": [c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
+    "scb_umap_weights": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+    "scb_fuzzy_union_rows": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_i64, c_i64, c_ptr, c_ptr],
+    "scb_fuzzy_union_fill": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr],
+    "scb_knn_distances_csr": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_mtx_parse": [c_ptr, c_ptr, c_i64, c_i64, c_i32, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_coo_to_csr": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_regress_cov_sums": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],

@@ -39,6 +39,7 @@ class Params:
     n_comps: int = 50
     n_neighbors: int = 15
     regress_out: bool = False  # sc.pp.regress_out(["total_counts", "pct_counts_mt"]) before scale
+    connectivities: bool = False  # also sc.pp.neighbors' distances/connectivities (umap fuzzy graph)
 
 
 @dataclasses.dataclass
@@ -56,6 +57,7 @@ class Result:
     knn_dist: torch.Tensor
     n_cells_total: int
     step_ms: dict
+    graph: Optional[pp.NeighborsGraph] = None
 
 
 class _Timer:
@@ -162,5 +164,9 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
         ki, kd = pp.neighbors(Xp, p.n_neighbors, n_comps=p.n_comps, keys=keys, timer=knn_timer)
     else:
         ki = kd = None
+    graph = None
+    if with_knn and p.connectivities:
+        tm.step("graph")
+        graph = pp.neighbors_graph(ki, kd, comm=comm)
     ms = tm.finish()
-    return Result(qc, cm, gm, X_log, hvg_mask, hvg_index, st, sc, res_pca, ki, kd, n_total, ms)
+    return Result(qc, cm, gm, X_log, hvg_mask, hvg_index, st, sc, res_pca, ki, kd, n_total, ms, graph)

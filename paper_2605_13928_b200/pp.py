@@ -456,3 +456,54 @@ def neighbors(X_pca: torch.Tensor, n_neighbors: int = 15, n_comps: Optional[int]
     _lib.call("scb_knn_timed", _ctx(X_pca), _p(X_pca), nq, _p(keys), nk, d, X_pca.stride(0), k, kc, _p(idx), _p(dist),
               _stream(dev), e0, e1)
     return idx, dist
+
+
+# ----------------------------------------------------------------------------- neighbors graph
+@dataclasses.dataclass
+class NeighborsGraph:
+    """sc.pp.neighbors' sparse outputs for this rank's rows: `distances` (kNN distances without
+    the self edge) and `connectivities` (umap fuzzy_simplicial_set), both CSR over all cells,
+    plus the per-cell sigma/rho of the membership strengths."""
+    distances: DeviceCSR
+    connectivities: DeviceCSR
+    sigma: torch.Tensor
+    rho: torch.Tensor
+
+
+def neighbors_graph(knn_idx: torch.Tensor, knn_dist: torch.Tensor, comm=None) -> NeighborsGraph:
+    """Graph outputs of sc.pp.neighbors(method="umap") from the exact kNN (self included).
+    With ``comm`` the rows are this rank's shard (in rank order); the membership strengths of
+    all cells are all-gathered (N x k x 8 B) and each rank builds its own rows."""
+    dev = knn_idx.device
+    n, k = knn_idx.shape
+    ctx, s = _ctx(knn_idx), _stream(dev)
+    tot = torch.zeros(1, dtype=torch.float64, device=dev)
+    _lib.call("scb_knn_dist_sum", ctx, _p(knn_dist), n * k, _p(tot), s)
+    n_all, r0 = n, 0
+    if comm is not None:
+        comm.allreduce_(tot)
+        counts = comm.allgather_rows(torch.tensor([[n]], dtype=torch.int64, device=dev)).view(-1).tolist()
+        r0 = int(sum(counts[:comm.rank]))
+        n_all = int(sum(counts))
+    mean = tot / float(n_all * k)
+    sigma = torch.empty(n, dtype=torch.float32, device=dev)
+    rho = torch.empty(n, dtype=torch.float32, device=dev)
+    w = torch.empty((n, k), dtype=torch.float32, device=dev)
+    _lib.call("scb_umap_weights", ctx, _p(knn_idx), _p(knn_dist), n, k, r0, _p(mean), _p(sigma), _p(rho), _p(w), s)
+    idx_all, w_all = knn_idx, w
+    if comm is not None:
+        idx_all, w_all = comm.allgather_rows(knn_idx), comm.allgather_rows(w)
+    indptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    _lib.call("scb_fuzzy_union_rows", ctx, _p(idx_all), _p(w_all), n_all, k, r0, r0 + n, _p(indptr), s)
+    nnz = int(indptr[n].item())
+    cols = torch.empty(nnz, dtype=torch.int32, device=dev)
+    vals = torch.empty(nnz, dtype=torch.float32, device=dev)
+    _lib.call("scb_fuzzy_union_fill", ctx, _p(idx_all), _p(w_all), n_all, k, r0, r0 + n, _p(indptr), _p(cols),
+              _p(vals), s)
+    dptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    dcols = torch.empty(n * k, dtype=torch.int32, device=dev)
+    dvals = torch.empty(n * k, dtype=torch.float32, device=dev)
+    _lib.call("scb_knn_distances_csr", ctx, _p(knn_idx), _p(knn_dist), n, k, _p(dptr), _p(dcols), _p(dvals), s)
+    dn = int(dptr[n].item())
+    return NeighborsGraph(DeviceCSR(dptr, dcols[:dn], dvals[:dn], n_all), DeviceCSR(indptr, cols, vals, n_all),
+                          sigma, rho)
