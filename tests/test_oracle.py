@@ -256,3 +256,57 @@ def test_knn_tie_order_by_index():
     np.testing.assert_array_equal(i[0], [0, 1, 2, 3, 4, 5])
     np.testing.assert_array_equal(i[1], [1, 5, 0, 3, 4, 2])
     np.testing.assert_allclose(d[1][:2], [0.0, 0.0])
+
+
+def _smooth_knn_dist_loop(distances, k, n_iter=64):
+    """Literal transcription of umap-learn 0.5 smooth_knn_dist (local_connectivity 1,
+    bandwidth 1) -- the loop the vectorised oracle restates."""
+    target = np.log2(k)
+    n = distances.shape[0]
+    rho = np.zeros(n, np.float32)
+    result = np.zeros(n, np.float32)
+    mean_distances = np.mean(distances)
+    for i in range(n):
+        lo, hi, mid = 0.0, np.inf, 1.0
+        ith = distances[i]
+        nz = ith[ith > 0.0]
+        if nz.shape[0] >= 1:
+            rho[i] = nz[0]
+        for _ in range(n_iter):
+            psum = 0.0
+            for j in range(1, distances.shape[1]):
+                d = distances[i, j] - rho[i]
+                psum += np.exp(-(float(d) / mid)) if d > 0 else 1.0  # numba: f32 / f64 -> f64
+            if np.fabs(psum - target) < 1e-5:
+                break
+            if psum > target:
+                hi = mid
+                mid = (lo + hi) / 2.0
+            else:
+                lo = mid
+                mid = mid * 2 if hi == np.inf else (lo + hi) / 2.0
+        result[i] = mid
+        if rho[i] > 0.0:
+            if result[i] < 1e-3 * np.mean(ith):
+                result[i] = 1e-3 * np.mean(ith)
+        elif result[i] < 1e-3 * mean_distances:
+            result[i] = 1e-3 * mean_distances
+    return result, rho
+
+
+def test_umap_graph_oracle_vs_literal_loop_and_properties():
+    rng = np.random.default_rng(2)
+    E = rng.standard_normal((400, 6)).astype(np.float32)
+    E[7] = E[3]  # an exact duplicate -> a zero non-self distance
+    ki, kd = op.knn(E, 12)
+    sig, rho = op.smooth_knn_dist(kd, 12)
+    sig_l, rho_l = _smooth_knn_dist_loop(kd, 12)
+    np.testing.assert_array_equal(rho, rho_l)
+    np.testing.assert_allclose(sig, sig_l, rtol=1e-6)
+    C, Dm, _, _ = op.umap_connectivities(ki, kd, 400)
+    assert abs(C - C.T).max() == 0 and C.data.min() > 0 and C.data.max() <= 1.0
+    assert C.has_sorted_indices and Dm.nnz == (kd > 0).sum()
+    # each row's membership strengths (self 0, nearest non-self neighbour 1) sum to log2(k)
+    W = op.membership_strengths(ki, kd, sig, rho)
+    excess = W.sum(1) - np.log2(12)
+    assert np.abs(excess[rho > 0]).max() < 1e-3
