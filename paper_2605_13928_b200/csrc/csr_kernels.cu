@@ -41,6 +41,23 @@ __device__ __forceinline__ void build_gene_map(const int32_t* __restrict__ remap
     if (lane_id() == 0) s_map[wi] = make_uint2(bits, bits ? (unsigned)first : 0u);
   }
 }
+// kept-gene map: int16 remap table when n_cols <= 32767 (one LDS.S16 per lookup), else the
+// bit/prefix words above
+template <bool SMALL>
+__device__ __forceinline__ void build_map(const int32_t* __restrict__ remap, int32_t n_cols, void* smem) {
+  if (SMALL) {
+    int16_t* t = reinterpret_cast<int16_t*>(smem);
+    for (int i = threadIdx.x; i < n_cols; i += blockDim.x) t[i] = (int16_t)remap[i];
+  } else {
+    build_gene_map(remap, n_cols, reinterpret_cast<uint2*>(smem));
+  }
+}
+__device__ __forceinline__ int map_gene(const uint2* s_map, int32_t n_cols, int g);
+template <bool SMALL>
+__device__ __forceinline__ int lookup_map(const void* smem, int32_t n_cols, int g) {
+  if (SMALL) return (unsigned)g < (unsigned)n_cols ? (int)reinterpret_cast<const int16_t*>(smem)[g] : -1;
+  return map_gene(reinterpret_cast<const uint2*>(smem), n_cols, g);
+}
 __device__ __forceinline__ int map_gene(const uint2* s_map, int32_t n_cols, int g) {
   if ((unsigned)g >= (unsigned)n_cols) return -1;
   const uint2 w = s_map[g >> 5];
@@ -68,7 +85,7 @@ __device__ __forceinline__ void red_shared_add(uint32_t a, uint32_t v) {
 // CTAs also write the per-cell metrics and, for the HVG pass, the per-row positions where
 // the original gene index crosses each HVG tile boundary (splits[r][t-1] = #entries with
 // gene < t*split_w, relative to the row start).
-template <int NSPLIT>
+template <int NSPLIT, bool SINGLE_TILE>
 __global__ void __launch_bounds__(kQcThreads)
 qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
           const float* __restrict__ data, int64_t n_rows, int32_t n_cols,
@@ -152,7 +169,8 @@ qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indice
         qmt += lds_u8(a_mt + (uint32_t)g[k]) * xv[k];
         // low 12 bits in smem (fire-and-forget: <= 2^20 rows per CTA keep the word below
         // 2^32); zero increments land on the tile's first gene
-        const bool in_tile = (unsigned)(g[k] - g0) < (unsigned)w;
+        // one tile covering every gene (G <= ~28k): every validated gene index is in it
+        const bool in_tile = SINGLE_TILE || (unsigned)(g[k] - g0) < (unsigned)w;
         const uint32_t ga = 4u * (uint32_t)(in_tile ? g[k] : gd);
         red_shared_add(a_cells + ga, (in_tile & (xv[k] != 0u)) ? 1u : 0u);
         red_shared_add(a_tot + ga, in_tile ? (xv[k] & 0xFFFu) : 0u);
@@ -161,7 +179,7 @@ qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indice
       if (hi_any > 0xFFFu) {  // rare: higher parts straight into the global u64 totals
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (((unsigned)(g[k] - g0) < (unsigned)w) & (xv[k] > 0xFFFu))
+          if ((SINGLE_TILE || (unsigned)(g[k] - g0) < (unsigned)w) & (xv[k] > 0xFFFu))
             atomicAdd(&g_total[g[k]], (unsigned long long)(xv[k] & ~0xFFFu));
       }
       sum += qsum;
@@ -279,6 +297,7 @@ __global__ void gene_remap_kernel(const uint8_t* gmask, int32_t n, int32_t* rema
 
 // Count kept entries (and kept total) per original row; writes counts into
 // cnt[kept_row] where kept_row = row_pos[r] (exclusive scan of cell_mask).
+template <bool SMALL>
 __global__ void __launch_bounds__(kRowThreads)
 subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                     const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
@@ -286,7 +305,7 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
                     int64_t* __restrict__ cnt, double target_sum, float* __restrict__ row_scale,
                     float* __restrict__ row_scale_orig) {
   extern __shared__ uint2 s_map[];
-  build_gene_map(remap, n_cols, s_map);
+  build_map<SMALL>(remap, n_cols, s_map);
   __syncthreads();
   const int64_t nnz = indptr[n_rows];
   const int lane = lane_id();
@@ -302,7 +321,7 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
     stream_row_pipe<1>(indices, row_scale ? data : nullptr, b, e, nnz, [&](const Quad& q) {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (((q.valid >> k) & 1u) && map_gene(s_map, n_cols, q.g[k]) >= 0) {
+        if (((q.valid >> k) & 1u) && lookup_map<SMALL>(s_map, n_cols, q.g[k]) >= 0) {
           ++c;
           sum += (double)q.x[k];
         }
@@ -325,6 +344,7 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
 // exclusive scan so the output stays in row order.  The (up to 128) kept elements of a warp
 // step are staged in shared memory and written back 32 consecutive elements per instruction
 // (full 128-byte lines instead of four lane-strided partial-sector stores per quad).
+template <bool SMALL>
 __global__ void __launch_bounds__(kRowThreads)
 subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                    const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
@@ -334,7 +354,7 @@ subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
   __shared__ int s_idx[kRowThreads / 32][128];
   __shared__ float s_val[kRowThreads / 32][128];
   extern __shared__ uint2 s_map[];
-  build_gene_map(remap, n_cols, s_map);
+  build_map<SMALL>(remap, n_cols, s_map);
   __syncthreads();
   const int64_t nnz = indptr[n_rows];
   const int lane = lane_id(), w = warp_id();
@@ -350,7 +370,7 @@ subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
       int kc = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        ng[k] = ((q.valid >> k) & 1u) ? map_gene(s_map, n_cols, q.g[k]) : -1;
+        ng[k] = ((q.valid >> k) & 1u) ? lookup_map<SMALL>(s_map, n_cols, q.g[k]) : -1;
         kc += ng[k] >= 0 ? 1 : 0;
       }
       int incl = kc;
@@ -959,11 +979,20 @@ extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t
       return SCB_OK;
     };
     static_assert(kMaxSplit == 3, "qc_kernel is instantiated for 0..3 row splits");
-    switch (n_split) {
-      case 0: SCB_TRY(launch(qc_kernel<0>)); break;
-      case 1: SCB_TRY(launch(qc_kernel<1>)); break;
-      case 2: SCB_TRY(launch(qc_kernel<2>)); break;
-      default: SCB_TRY(launch(qc_kernel<3>)); break;
+    if (n_tiles == 1) {
+      switch (n_split) {
+        case 0: SCB_TRY(launch(qc_kernel<0, true>)); break;
+        case 1: SCB_TRY(launch(qc_kernel<1, true>)); break;
+        case 2: SCB_TRY(launch(qc_kernel<2, true>)); break;
+        default: SCB_TRY(launch(qc_kernel<3, true>)); break;
+      }
+    } else {
+      switch (n_split) {
+        case 0: SCB_TRY(launch(qc_kernel<0, false>)); break;
+        case 1: SCB_TRY(launch(qc_kernel<1, false>)); break;
+        case 2: SCB_TRY(launch(qc_kernel<2, false>)); break;
+        default: SCB_TRY(launch(qc_kernel<3, false>)); break;
+      }
     }
     SCB_LAUNCH_CHECK();
   }
@@ -1013,12 +1042,13 @@ extern "C" int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32
   int64_t* cnt = row_pos + (n_rows + 1);
   SCB_TRY(scan_u8_to_i64(ctx, cmask, n_rows, row_pos, s));
   if (n_rows > 0) {
-    const size_t map_bytes = (size_t)((n_cols + 31) / 32) * 8;
+    const bool small = n_cols <= 32767;
+    const size_t map_bytes = small ? (size_t)((n_cols + 7) & ~7) * 2 : (size_t)((n_cols + 31) / 32) * 8;
     SCB_REQUIRE(map_bytes <= 64 * 1024, SCB_ERR_UNSUPPORTED, "scb_subset_count: too many genes");
-    SCB_CUDA(cudaFuncSetAttribute(subset_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_bytes));
-    subset_count_kernel<<<grid_for(ctx, 4), kRowThreads, map_bytes, s>>>(indptr, indices, data, n_rows, cmask,
-                                                                         remap, n_cols, row_pos, cnt, target_sum,
-                                                                         row_scale, row_scale_orig);
+    auto kern = small ? subset_count_kernel<true> : subset_count_kernel<false>;
+    SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_bytes));
+    kern<<<grid_for(ctx, 4), kRowThreads, map_bytes, s>>>(indptr, indices, data, n_rows, cmask, remap, n_cols,
+                                                          row_pos, cnt, target_sum, row_scale, row_scale_orig);
     SCB_LAUNCH_CHECK();
   }
   // number of kept rows is row_pos[n_rows]; scan cnt[0..kept) -> new_indptr (device-side length)
@@ -1039,12 +1069,13 @@ extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_
   int64_t* row_pos = (int64_t*)ws;
   SCB_TRY(scan_u8_to_i64(ctx, cmask, n_rows, row_pos, s));
   if (n_rows > 0) {
-    const size_t map_bytes = (size_t)((n_cols + 31) / 32) * 8;
+    const bool small = n_cols <= 32767;
+    const size_t map_bytes = small ? (size_t)((n_cols + 7) & ~7) * 2 : (size_t)((n_cols + 31) / 32) * 8;
     SCB_REQUIRE(map_bytes <= 64 * 1024, SCB_ERR_UNSUPPORTED, "scb_subset_fill: too many genes");
-    SCB_CUDA(cudaFuncSetAttribute(subset_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_bytes));
-    subset_fill_kernel<<<grid_for(ctx, 4), kRowThreads, map_bytes, s>>>(indptr, indices, data, n_rows, cmask,
-                                                                        remap, n_cols, row_pos, new_indptr,
-                                                                        row_scale, new_indices, new_data);
+    auto kern = small ? subset_fill_kernel<true> : subset_fill_kernel<false>;
+    SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_bytes));
+    kern<<<grid_for(ctx, 4), kRowThreads, map_bytes, s>>>(indptr, indices, data, n_rows, cmask, remap, n_cols,
+                                                          row_pos, new_indptr, row_scale, new_indices, new_data);
     SCB_LAUNCH_CHECK();
   }
   return SCB_OK;

@@ -170,3 +170,27 @@ def test_hvg_row_splits_sorted_and_unsorted_rows(shuffle):
     np.testing.assert_array_equal(r.hvg_mask.cpu().numpy(), o["hvg_mask"])
     np.testing.assert_array_equal(r.hvg_stats["means"].cpu().numpy(), o["hvg_stats"]["means"])
     np.testing.assert_array_equal(r.hvg_stats["variances"].cpu().numpy(), o["hvg_stats"]["variances"])
+
+
+def test_pipeline_40k_genes_bitmap_map_and_three_hvg_tiles():
+    """G > 32767 takes the bit/prefix kept-gene map in subset and three HVG gene tiles; masks,
+    kept matrix and HVG statistics stay bit-exact."""
+    import torch
+    from paper_2605_13928_b200 import pipeline, pp
+    from oracle import pipeline as op
+    spec = SynthSpec(1500, 40000, seed=9)
+    ip, ix, d = generate_csr(spec)
+    mt = mt_mask(spec)
+    p = op.Params(min_genes=50, max_pct_mt=20.0, n_top_genes=1000, n_neighbors=15)
+    o = op.run(op.CSR(ip, ix, d, spec.n_genes), mt, p, with_knn=False)
+    Xd = pp.DeviceCSR.from_host(ip, ix, d, spec.n_genes)
+    pp_ = pipeline.Params(min_genes=p.min_genes, max_pct_mt=p.max_pct_mt, min_cells=p.min_cells,
+                          n_top_genes=p.n_top_genes)
+    r = pipeline.run(Xd, torch.as_tensor(mt, device="cuda"), pp_, with_knn=False, timing=False)
+    np.testing.assert_array_equal(r.cell_mask.cpu().numpy(), o["cell_mask"])
+    np.testing.assert_array_equal(r.gene_mask.cpu().numpy(), o["gene_mask"])
+    lip, lix, _, _ = r.X_log.to_host()
+    np.testing.assert_array_equal(lip, o["X_log"].indptr)
+    np.testing.assert_array_equal(lix, o["X_log"].indices)
+    np.testing.assert_array_equal(r.hvg_mask.cpu().numpy(), o["hvg_mask"])
+    np.testing.assert_array_equal(r.hvg_stats["variances"].cpu().numpy(), o["hvg_stats"]["variances"])
