@@ -102,9 +102,9 @@ def _step_bytes(Z_in, N, G, Z_sub, N_sub, H, ld, regress_out=False):
     return {
         "qc": 8 * Z_in + 8 * (N + 1),
         "norm_hvg": 8 * Z_in + (8 * Z_in + 8 * Z_sub) + 8 * Z_in + 4 * N,  # count, fill, hvg sums
-        # scale: scale sums + dense scale; regress_out: dense log (8Z' + 4N ld), Aᵀl read (4N ld),
-        # in-place residual scaling (8N ld)
-        "regress": (8 * Z_sub + 16 * N_sub * ld) if regress_out else (8 * Z_sub + (8 * Z_sub + 4 * N_sub * ld)),
+        # scale: dense scale (its gene sums are fused into the subset fill pass of norm_hvg);
+        # regress_out: dense log (8Z' + 4N ld), Aᵀl read (4N ld), in-place residual scaling (8N ld)
+        "regress": (8 * Z_sub + 16 * N_sub * ld) if regress_out else (8 * Z_sub + 4 * N_sub * ld),
         "project": 4 * N_sub * ld + 4 * N_sub * 64,
     }
 

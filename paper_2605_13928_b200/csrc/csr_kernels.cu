@@ -399,6 +399,111 @@ subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
   }
 }
 
+// Fused variant: the same compaction + log1p, and the scale step's fixed-point gene sums of the
+// HVG columns taken while the log values are produced (saves the scale pass's full re-read of
+// the kept matrix).  CTA = block of <= 1024 rows (carry-free 22-bit split, as scale_sums);
+// smem: int32 per original gene = new index | (slot + 1) << 16 (-1: dropped; slot -1: not an HVG),
+// 4 u32 words per HVG.  Requires n_cols <= 32767.
+constexpr int kFillSumsThreads = 1024;
+__global__ void __launch_bounds__(kFillSumsThreads)
+subset_fill_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                        const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
+                        const int32_t* __restrict__ remap, int32_t n_cols, const int32_t* __restrict__ slot_new,
+                        int32_t n_slots, const int64_t* __restrict__ row_pos, const int64_t* __restrict__ new_indptr,
+                        const float* __restrict__ row_scale, int64_t rows_per_block, int32_t* __restrict__ out_idx,
+                        float* __restrict__ out_val, unsigned long long* __restrict__ sums) {
+  __shared__ int s_idx[kFillSumsThreads / 32][128];
+  __shared__ float s_val[kFillSumsThreads / 32][128];
+  extern __shared__ int32_t dyn_tab[];
+  int32_t* tab = dyn_tab;
+  uint32_t* ss = reinterpret_cast<uint32_t*>(dyn_tab + ((n_cols + 3) & ~3));
+  for (int g = threadIdx.x; g < n_cols; g += blockDim.x) {
+    const int r = remap[g];
+    // kept: (slot + 1) << 16 | new index (both < 2^15, so the word stays non-negative); dropped: -1
+    tab[g] = r < 0 ? -1 : (int32_t)((uint32_t)r | ((uint32_t)(slot_new[r] + 1) << 16));
+  }
+  for (int i = threadIdx.x; i < 4 * n_slots; i += blockDim.x) ss[i] = 0;
+  __syncthreads();
+  const uint32_t a1lo = smem_addr(ss), a1hi = a1lo + 4u * n_slots, a2lo = a1lo + 8u * n_slots,
+                 a2hi = a1lo + 12u * n_slots;
+  const int64_t nnz = indptr[n_rows];
+  const int lane = lane_id(), w = warp_id();
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r1 = min(n_rows, r0 + rows_per_block);
+  for (int64_t r = r0 + w; r < r1; r += (blockDim.x >> 5)) {
+    if (!cmask[r]) continue;
+    const int64_t kr = row_pos[r];
+    const float s = row_scale[kr];
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    int64_t o = new_indptr[kr];
+    stream_row_pipe<1>(indices, data, b, e, nnz, [&](const Quad& q) {
+      int ng[4], sl[4];
+      int kc = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int g = q.g[k];
+        const int32_t t = (((q.valid >> k) & 1u) && (unsigned)g < (unsigned)n_cols) ? tab[g] : -1;
+        ng[k] = t < 0 ? -1 : (t & 0xFFFF);
+        sl[k] = t < 0 ? -1 : (int)((uint32_t)t >> 16) - 1;
+        kc += ng[k] >= 0 ? 1 : 0;
+      }
+      int incl = kc;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      int pos = incl - kc;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (ng[k] >= 0) {
+          const float l = log1pf(__fmul_rn(q.x[k], s));
+          s_idx[w][pos] = ng[k];
+          s_val[w][pos] = l;
+          ++pos;
+          if (sl[k] >= 0) {  // HVG column: scale sums (same integers as scale_sums_kernel)
+            const uint64_t v1 = (uint64_t)__float2ull_rn(__fmul_rn(l, 268435456.0f));
+            const double l12 = (double)__fmul_rn(l, 4096.0f);
+            const uint64_t v2 = (uint64_t)__double2ull_rn(__dmul_rn(l12, l12));
+            const uint32_t ja = 4u * (uint32_t)sl[k];
+            if ((v1 | v2) < (1ull << 43)) {
+              red_shared_add(a1lo + ja, (uint32_t)(v1 & 0x3FFFFFu));
+              red_shared_add(a1hi + ja, (uint32_t)(v1 >> 22));
+              red_shared_add(a2lo + ja, (uint32_t)(v2 & 0x3FFFFFu));
+              red_shared_add(a2hi + ja, (uint32_t)(v2 >> 22));
+            } else {  // rare (not log-normalized scale): straight into the global limbs
+              atomicAdd(&sums[sl[k]], v1 & 0xFFFFFFFFull);
+              atomicAdd(&sums[n_slots + sl[k]], v1 >> 32);
+              atomicAdd(&sums[2 * n_slots + sl[k]], v2 & 0xFFFFFFFFull);
+              atomicAdd(&sums[3 * n_slots + sl[k]], v2 >> 32);
+            }
+          }
+        }
+      __syncwarp();
+      for (int j = lane; j < tot; j += 32) {
+        out_idx[o + j] = s_idx[w][j];
+        out_val[o + j] = s_val[w][j];
+      }
+      __syncwarp();
+      o += tot;
+    });
+  }
+  __syncthreads();
+  const uint32_t* s1lo = ss;
+  const uint32_t* s1hi = ss + n_slots;
+  const uint32_t* s2lo = ss + 2 * n_slots;
+  const uint32_t* s2hi = ss + 3 * n_slots;
+  for (int i = threadIdx.x; i < n_slots; i += blockDim.x) {
+    const unsigned long long a0 = (unsigned long long)s1lo[i] + ((unsigned long long)(s1hi[i] & 1023u) << 22);
+    const unsigned long long b0 = (unsigned long long)s2lo[i] + ((unsigned long long)(s2hi[i] & 1023u) << 22);
+    if (a0) atomicAdd(&sums[i], a0);
+    if (s1hi[i] >> 10) atomicAdd(&sums[n_slots + i], (unsigned long long)(s1hi[i] >> 10));
+    if (b0) atomicAdd(&sums[2 * n_slots + i], b0);
+    if (s2hi[i] >> 10) atomicAdd(&sums[3 * n_slots + i], (unsigned long long)(s2hi[i] >> 10));
+  }
+}
+
 // ============================================================================ normalize + log1p
 
 __global__ void __launch_bounds__(kRowThreads)
@@ -1078,6 +1183,34 @@ extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_
                                                           row_pos, new_indptr, row_scale, new_indices, new_data);
     SCB_LAUNCH_CHECK();
   }
+  return SCB_OK;
+}
+
+extern "C" int scb_subset_fill_scale_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                                          const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+                                          const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
+                                          const int32_t* slot, int32_t n_slots, int32_t* new_indices,
+                                          float* new_data, uint64_t* sums, void* stream) {
+  SCB_REQUIRE(ctx && indptr && indices && data && cmask && remap && new_indptr && row_scale && slot && new_indices &&
+                  new_data && sums,
+              SCB_ERR_ARG, "scb_subset_fill_scale_sums: null argument");
+  SCB_REQUIRE(aligned16(indices) && aligned16(data), SCB_ERR_ARG, "scb_subset_fill_scale_sums: 16-byte alignment");
+  SCB_REQUIRE(n_cols <= 32767 && n_slots > 0 && n_slots < 32767, SCB_ERR_UNSUPPORTED,
+              "scb_subset_fill_scale_sums: needs n_cols <= 32767 (use subset_fill + scale_gene_sums)");
+  const size_t smem = (size_t)((n_cols + 3) & ~3) * 4 + (size_t)n_slots * 16;
+  SCB_REQUIRE(smem + 32 * 1024 <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_subset_fill_scale_sums: too many genes");
+  cudaStream_t s = (cudaStream_t)stream;
+  void* ws;
+  SCB_TRY(ws_get(ctx, 1, (size_t)(n_rows + 1) * 8 * 2, &ws, s));
+  int64_t* row_pos = (int64_t*)ws;
+  SCB_TRY(scan_u8_to_i64(ctx, cmask, n_rows, row_pos, s));
+  if (n_rows == 0) return SCB_OK;
+  const int64_t rpb = 1024;  // carry-free fixed point
+  SCB_CUDA(cudaFuncSetAttribute(subset_fill_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  subset_fill_sums_kernel<<<(unsigned)((n_rows + rpb - 1) / rpb), kFillSumsThreads, smem, s>>>(
+      indptr, indices, data, n_rows, cmask, remap, n_cols, slot, n_slots, row_pos, new_indptr, row_scale, rpb,
+      new_indices, new_data, (unsigned long long*)sums);
+  SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
 

@@ -108,18 +108,27 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
 
     # ------------------------------------------------------------------ norm_hvg
     tm.step("norm_hvg")
-    X_log, remap, row_scale_orig = pp.subset_normalize(X, cm, gm, (nk_local, gk), p.target_sum)
-    # HVG statistics of the normalized counts straight from the raw matrix (remapped genes)
+    # subset + normalize: pass 1 (kept counts, row factors); the HVG statistics come straight
+    # from the raw matrix (remapped genes, per-original-row factors); pass 2 writes the kept
+    # log1p matrix and, for the plain scale path, accumulates the scale step's gene sums of
+    # the selected HVG columns on the way (no second read of the kept matrix)
+    remap, new_indptr, row_scale, row_scale_orig, nnz = pp.subset_count_scale(X, cm, gm, (nk_local, gk),
+                                                                             p.target_sum)
     sums = pp.hvg_gene_sums(X, counts=X.data, row_scale=row_scale_orig, gene_remap=remap, n_out=gk,
                             row_splits=qc["hvg_row_splits"])
     if comm is not None:
         comm.allreduce_(sums)
     hvg_mask, hvg_index, st = pp.hvg_select(sums, n_total, p.n_top_genes, p.n_bins)
+    H = int(hvg_index.numel())
+    slot = pp.gene_slots(hvg_index, gk)
+    ssum = None
+    if p.regress_out:
+        X_log = pp.subset_fill_log(X, cm, remap, new_indptr, row_scale, nnz, gk)
+    else:
+        X_log, ssum = pp.subset_fill_log_scale_sums(X, cm, remap, new_indptr, row_scale, nnz, gk, slot, H)
 
     # ------------------------------------------------------------------ regress (scale)
     tm.step("regress")
-    H = int(hvg_index.numel())
-    slot = pp.gene_slots(hvg_index, gk)
     if p.regress_out:
         s6 = pp.regress_cov_sums(qc, cm)
         if comm is not None:
@@ -132,7 +141,8 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
         beta, inv = pp.regress_finalize(xty, s6)
         sc = pp.regress_apply(sc, design, beta, inv, p.max_value)
     else:
-        ssum = pp.scale_gene_sums(X_log, slot, H)
+        if ssum is None:
+            ssum = pp.scale_gene_sums(X_log, slot, H)
         if comm is not None:
             comm.allreduce_(ssum)
         mean, inv = pp.scale_finalize(ssum, n_total)

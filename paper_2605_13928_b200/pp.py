@@ -177,6 +177,24 @@ def subset_normalize(X: DeviceCSR, cell_mask, gene_mask, n_kept, target_sum: flo
     return X_log, remap, row_scale_orig
 
 
+def subset_fill_log_scale_sums(X: DeviceCSR, cell_mask, remap, new_indptr, row_scale, nnz: int, n_genes_kept: int,
+                               slot: torch.Tensor, H: int, sums=None):
+    """subset_fill_log fused with the scale step's gene sums of the HVG columns (``slot``: int32
+    per kept gene, -1 = not an HVG).  Returns (X_log, sums u64[2][2][H]) or (X_log, None) when
+    the fused kernel does not apply (more than 32767 input genes) -- then use scale_gene_sums."""
+    if X.n_cols > 32767:
+        return subset_fill_log(X, cell_mask, remap, new_indptr, row_scale, nnz, n_genes_kept), None
+    dev = X.device
+    ind = torch.empty(nnz, dtype=torch.int32, device=dev)
+    logv = torch.empty(nnz, dtype=torch.float32, device=dev)
+    if sums is None:
+        sums = torch.zeros((2, 2, H), dtype=torch.int64, device=dev)
+    _lib.call("scb_subset_fill_scale_sums", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols,
+              _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(slot), H, _p(ind), _p(logv), _p(sums),
+              _stream(dev))
+    return DeviceCSR(new_indptr, ind, logv, n_genes_kept, row_scale=row_scale), sums
+
+
 # ----------------------------------------------------------------------------- norm_hvg
 def normalize_log1p(X: DeviceCSR, target_sum: float = 1e4) -> DeviceCSR:
     """sc.pp.normalize_total(target_sum) followed by sc.pp.log1p (out of place).  The result

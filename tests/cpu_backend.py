@@ -50,6 +50,26 @@ def subset_normalize(X, cm, gm, n_kept, target_sum=1e4):
     return out, torch.as_tensor(remap), torch.as_tensor(rso)
 
 
+def subset_count_scale(X, cm, gm, n_kept, target_sum=1e4):
+    """First pass (CPU stand-in): returns (remap, new_indptr, row_scale, row_scale_orig, nnz); the
+    second pass below recomputes the kept matrix from the same inputs."""
+    Xl, remap, rso = subset_normalize(X, cm, gm, n_kept, target_sum)
+    _PASS[id(X)] = Xl
+    return remap, Xl.indptr, Xl.row_scale, rso, int(Xl.nnz)
+
+
+_PASS = {}
+
+
+def subset_fill_log(X, cm, remap, new_indptr, row_scale, nnz, n_genes_kept):
+    return _PASS.pop(id(X))
+
+
+def subset_fill_log_scale_sums(X, cm, remap, new_indptr, row_scale, nnz, n_genes_kept, slot, H, sums=None):
+    Xl = subset_fill_log(X, cm, remap, new_indptr, row_scale, nnz, n_genes_kept)
+    return Xl, scale_gene_sums(Xl, slot, H)
+
+
 def _limbs(idx, v32, n, f1, f2):
     v64 = v32.astype(np.float64)
     out = np.zeros((2, 2, n), dtype=np.int64)

@@ -194,3 +194,36 @@ def test_pipeline_40k_genes_bitmap_map_and_three_hvg_tiles():
     np.testing.assert_array_equal(lix, o["X_log"].indices)
     np.testing.assert_array_equal(r.hvg_mask.cpu().numpy(), o["hvg_mask"])
     np.testing.assert_array_equal(r.hvg_stats["variances"].cpu().numpy(), o["hvg_stats"]["variances"])
+
+
+def test_fused_fill_scale_sums_equal_separate_pass():
+    """The fill pass's fused HVG scale sums are the same integers scale_gene_sums computes
+    from the written log matrix, and the written matrix is unchanged."""
+    import torch
+    import paper_2605_13928_b200 as scb
+    from paper_2605_13928_b200 import pp
+    X, mt = c1_inputs()
+    p = C1["params"]
+    Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, X.n_cols)
+    qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
+    cm, gm, kept = scb.filter_masks(qc, p.min_genes, p.max_genes, p.max_pct_mt, p.min_cells)
+    _, hvg_index, _ = scb.highly_variable_genes(scb.normalize_log1p(scb.subset(Xd, cm, gm, kept), p.target_sum),
+                                                p.n_top_genes, p.n_bins)
+    remap, nip, rs, rso, nnz = pp.subset_count_scale(Xd, cm, gm, kept, p.target_sum)
+    ref = pp.subset_fill_log(Xd, cm, remap, nip, rs, nnz, kept[1])
+    H = int(hvg_index.numel())
+    slot = pp.gene_slots(hvg_index, kept[1])
+    fused, sums = pp.subset_fill_log_scale_sums(Xd, cm, remap, nip, rs, nnz, kept[1], slot, H)
+    assert sums is not None
+    assert torch.equal(fused.indices, ref.indices) and torch.equal(fused.data, ref.data)
+    sep = pp.scale_gene_sums(ref, slot, H)
+
+    def canonical(t):  # exact integer limb0 + limb1 * 2^32 (the limb split depends on the row blocks)
+        a = t.cpu().numpy().astype(object)
+        return a[:, 0] + a[:, 1] * (1 << 32)
+
+    assert (canonical(sums) == canonical(sep)).all()
+    n = int(kept[0])
+    m1, i1 = pp.scale_finalize(sums, n)
+    m2, i2 = pp.scale_finalize(sep, n)
+    assert torch.equal(m1, m2) and torch.equal(i1, i2)
