@@ -403,16 +403,19 @@ def split_planes(sc: Scaled) -> Scaled:
     return sc
 
 
-def gram(sc: Scaled, out=None, planes: bool = True):
+def gram(sc: Scaled, out=None, planes: bool = True, keep_planes: bool = False):
     """Partial (local) Gram matrix Z^T Z, float64 [ld][ld] (tcgen05, 3xBF16).  ``planes`` (default)
     splits Z into BF16 hi/lo planes first and feeds them to the tensor cores by TMA; ``planes=False``
-    converts fp32 tiles inside the Gram kernel instead (no extra 4 B/element of HBM, slower)."""
+    converts fp32 tiles inside the Gram kernel instead (no extra 4 B/element of HBM, slower).  The
+    planes (4 B per element) are released after the call unless ``keep_planes``."""
     ld = sc.ld
     C = out if out is not None else torch.empty((ld, ld), dtype=torch.float64, device=sc.Z.device)
     if planes:
         split_planes(sc)
         _lib.call("scb_gram_split", _ctx(sc.Z), _p(sc.Z_hi), _p(sc.Z_lo), sc.Z.shape[0], ld, _p(C),
                   _stream(sc.Z.device))
+        if not keep_planes:  # stream-ordered release: the caching allocator reuses them after the Gram
+            sc.Z_hi = sc.Z_lo = None
     else:
         _lib.call("scb_gram", _ctx(sc.Z), _p(sc.Z), sc.Z.shape[0], ld, _p(C), _stream(sc.Z.device))
     return C

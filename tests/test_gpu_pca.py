@@ -82,7 +82,7 @@ def test_gram_split_planes_match_converter_path(n, h):
     Z = rng.standard_normal((n, h)).astype(np.float32)
     sc = _scaled_from_host(Z, h)
     C1 = pp.gram(sc, planes=False).cpu().numpy()
-    C2 = pp.gram(sc).cpu().numpy()
+    C2 = pp.gram(sc, keep_planes=True).cpu().numpy()
     hi = sc.Z.to(torch.bfloat16)
     lo = (sc.Z - hi.float()).to(torch.bfloat16)
     assert torch.equal(sc.Z_hi.view(torch.int16), hi.view(torch.int16))
