@@ -214,6 +214,14 @@ SCB_API int scb_fuzzy_union_fill(scb_ctx* ctx, const int32_t* idx_all, const flo
 SCB_API int scb_knn_distances_csr(scb_ctx* ctx, const int32_t* knn_idx, const float* knn_dist, int64_t n_rows,
                           int32_t k, int64_t* indptr, int32_t* cols, float* vals, void* stream);
 
+/* ---- f3 sc.tl.umap layout: umap-learn optimize_layout_euclidean (2-D) on the connectivities
+ * CSR (indptr/indices/weights, nnz entries, w_max = max weight), edge-parallel SGD for n_epochs
+ * epochs from `init` (rows of >= 2 floats, stride init_ld; rescaled to [0, 10] as umap does);
+ * a, b = the curve parameters of (min_dist, spread); emb receives float32 [n_vertices][2]. */
+SCB_API int scb_umap_layout(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* weights,
+                    int64_t n_vertices, int64_t nnz, float w_max, const float* init, int64_t init_ld,
+                    int32_t n_epochs, float a, float b, int32_t neg_rate, uint64_t seed, float* emb, void* stream);
+
 /* ---- a7: partial Gram matrix C = Z^T Z (float64 [hp][hp], full symmetric) on the
  * 5th-gen tensor cores (tcgen05 kind::f16, "3xBF16": x = hi + lo with hi = bf16(x),
  * lo = bf16(x - hi), products hi*hi + hi*lo + lo*hi, <= 2^-16 relative each; FP32 accumulate

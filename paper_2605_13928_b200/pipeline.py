@@ -40,6 +40,8 @@ class Params:
     n_neighbors: int = 15
     regress_out: bool = False  # sc.pp.regress_out(["total_counts", "pct_counts_mt"]) before scale
     connectivities: bool = False  # also sc.pp.neighbors' distances/connectivities (umap fuzzy graph)
+    umap: bool = False  # also sc.tl.umap (layout from X_pca[:, :2]; implies connectivities)
+    umap_epochs: Optional[int] = None
 
 
 @dataclasses.dataclass
@@ -58,6 +60,7 @@ class Result:
     n_cells_total: int
     step_ms: dict
     graph: Optional[pp.NeighborsGraph] = None
+    umap: Optional[torch.Tensor] = None
 
 
 class _Timer:
@@ -174,9 +177,14 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
         ki, kd = pp.neighbors(Xp, p.n_neighbors, n_comps=p.n_comps, keys=keys, timer=knn_timer)
     else:
         ki = kd = None
-    graph = None
-    if with_knn and p.connectivities:
+    graph = emb = None
+    if with_knn and (p.connectivities or p.umap):
         tm.step("graph")
         graph = pp.neighbors_graph(ki, kd, comm=comm)
+    if with_knn and p.umap:
+        if comm is not None:
+            raise NotImplementedError("umap layout is single-GPU (the layout SGD needs the whole graph)")
+        tm.step("umap")
+        emb = pp.umap_layout(graph.connectivities, Xp[:, :2], n_epochs=p.umap_epochs)
     ms = tm.finish()
-    return Result(qc, cm, gm, X_log, hvg_mask, hvg_index, st, sc, res_pca, ki, kd, n_total, ms, graph)
+    return Result(qc, cm, gm, X_log, hvg_mask, hvg_index, st, sc, res_pca, ki, kd, n_total, ms, graph, emb)

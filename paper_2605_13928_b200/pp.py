@@ -14,6 +14,7 @@ from __future__ import annotations
 import dataclasses
 from typing import Optional
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -528,3 +529,37 @@ def neighbors_graph(knn_idx: torch.Tensor, knn_dist: torch.Tensor, comm=None) ->
     dn = int(dptr[n].item())
     return NeighborsGraph(DeviceCSR(dptr, dcols[:dn], dvals[:dn], n_all), DeviceCSR(indptr, cols, vals, n_all),
                           sigma, rho)
+
+
+# ----------------------------------------------------------------------------- umap layout
+def umap_ab(min_dist: float = 0.5, spread: float = 1.0):
+    """umap's find_ab_params: fit 1 / (1 + a x^(2b)) to the (min_dist, spread) target curve
+    (scipy curve_fit on the host; two scalars)."""
+    from scipy.optimize import curve_fit
+
+    def curve(x, a, b):
+        return 1.0 / (1.0 + a * x ** (2 * b))
+    xv = np.linspace(0, spread * 3, 300)
+    yv = np.where(xv < min_dist, 1.0, np.exp(-(xv - min_dist) / spread))
+    (a, b), _ = curve_fit(curve, xv, yv)
+    return float(a), float(b)
+
+
+def umap_layout(connectivities: DeviceCSR, init: torch.Tensor, n_epochs: Optional[int] = None,
+                min_dist: float = 0.5, spread: float = 1.0, negative_sample_rate: int = 5, seed: int = 0):
+    """sc.tl.umap(min_dist, spread, init_pos=<obsm key>) on the device: umap-learn's
+    optimize_layout_euclidean as edge-parallel SGD (see csrc/umap.cu).  ``init`` = [N][>=2]
+    float32 starting coordinates (e.g. X_pca's first two columns); n_epochs defaults as umap
+    (500 for <= 10k cells, else 200).  Returns float32 [N][2]."""
+    n = connectivities.n_rows
+    if n_epochs is None:
+        n_epochs = 500 if n <= 10000 else 200
+    a, b = umap_ab(min_dist, spread)
+    w = connectivities.data
+    w_max = float(w.max().item()) if w.numel() else 1.0
+    emb = torch.empty((n, 2), dtype=torch.float32, device=w.device)
+    init = init.contiguous()
+    _lib.call("scb_umap_layout", _ctx(w), _p(connectivities.indptr), _p(connectivities.indices), _p(w), n,
+              int(w.numel()), w_max, _p(init), init.stride(0), int(n_epochs), a, b, int(negative_sample_rate),
+              int(seed), _p(emb), _stream(w.device))
+    return emb
