@@ -30,7 +30,7 @@ def _params(args):
     from paper_2605_13928_b200.pipeline import Params
     return Params(min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3, target_sum=1e4,
                   n_top_genes=args.hvg, n_bins=20, max_value=10.0, n_comps=50, n_neighbors=args.k,
-                  regress_out=args.regress_out, connectivities=args.graph, umap=args.umap)
+                  regress_out=args.regress_out, connectivities=args.graph, umap=args.umap, cluster=args.cluster)
 
 
 def _peaks():
@@ -171,6 +171,7 @@ def main():
     ap.add_argument("--graph", action="store_true",
                     help="also build sc.pp.neighbors' distances/connectivities (umap fuzzy graph) in the step")
     ap.add_argument("--umap", action="store_true", help="also run sc.tl.umap (layout) in the step (1 GPU)")
+    ap.add_argument("--cluster", action="store_true", help="also run the Louvain/Leiden-core clustering (1 GPU)")
     ap.add_argument("--regress-out", action="store_true",
                     help="add sc.pp.regress_out(total_counts, pct_counts_mt) before scale (paper Table 1 step 4)")
     args = ap.parse_args()
@@ -218,7 +219,9 @@ def main():
         torch.cuda.synchronize()
 
     # ---- warm-up
+    res = None
     for _ in range(args.warmup):
+        res = None
         res = pipeline.run(X, mt, p, comm=comm, timing=False)
     barrier()
 
@@ -233,6 +236,7 @@ def main():
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record()
         for i in range(args.steps):
+            res = None  # release the previous step's outputs before this step allocates its own
             res = pipeline.run(X, mt, p, comm=comm, timing=True, knn_timer=(k_start[i], k_end[i]))
             for kk, v in res.step_ms.items():
                 step_ms_acc[kk] = step_ms_acc.get(kk, 0.0) + v
@@ -269,7 +273,7 @@ def main():
         if kk in step_ms and step_ms[kk] > 0:
             stages[kk] = {"ms": round(step_ms[kk], 4), "algo_GBps": round(sb[kk] / (step_ms[kk] / 1e3) / 1e9, 1),
                           "frac_hbm": round(sb[kk] / (step_ms[kk] / 1e3) / 1e9 / hbm, 4)}
-    for kk in ("pca", "knn", "graph", "umap"):
+    for kk in ("pca", "knn", "graph", "umap", "cluster"):
         if kk in step_ms:
             stages[kk] = {"ms": round(step_ms[kk], 4)}
     stages["knn"]["candidates_kernel_ms"] = round(knn_ms, 4)
@@ -324,6 +328,7 @@ def main():
             comp.wait_event(copied[i % 2])
             b = bufs[i % 2]
             Xe = DeviceCSR(b[0], b[1], b[2], G)
+            r = None
             r = pipeline.run(Xe, mt, p, comm=comm, timing=False)
             consumed[i % 2].record(comp)
             if r.knn_index.shape[0] != o_i.shape[0]:
@@ -359,7 +364,7 @@ def main():
             "data": "synthetic NB counts generated on device (oracle/synth.py model, seed %d)" % args.seed,
             "config": {"workload": f"C3: {N} cells x {G} genes (~{Z_total / N / G:.1%} dense), full QC->normalize->"
                                    f"log1p->HVG(seurat,{args.hvg})->{'regress_out+' if args.regress_out else ''}scale->PCA(50)->"
-                                   f"kNN(k={args.k}, exact){'+umap graph' if args.graph or args.umap else ''}{'+umap layout' if args.umap else ''}",
+                                   f"kNN(k={args.k}, exact){'+umap graph' if args.graph or args.umap or args.cluster else ''}{'+umap layout' if args.umap else ''}{'+clustering' if args.cluster else ''}",
                        "cells": N, "genes": G, "nnz": int(Z_total), "kept_cells": int(n_keys), "hvg": H,
                        "parallelism": f"cells sharded x{world}", "l2": "inputs (14 GB) >> L2 (126 MB); no flush needed",
                        "gen_seconds": round(gen_s, 1)},

@@ -222,6 +222,15 @@ SCB_API int scb_umap_layout(scb_ctx* ctx, const int64_t* indptr, const int32_t* 
                     int64_t n_vertices, int64_t nnz, float w_max, const float* init, int64_t init_ld,
                     int32_t n_epochs, float a, float b, int32_t neg_rate, uint64_t seed, float* emb, void* stream);
 
+/* ---- f3 clustering on the neighbors graph (sc.tl.louvain / the local-moving + aggregation
+ * core of sc.tl.leiden): multi-level modularity optimisation with resolution gamma on the
+ * symmetric CSR (indptr/indices/weights), deterministic (2^-32 fixed-point weights, hash-bucketed
+ * synchronous moves, ties to the smaller community).  labels (device int32[n]) are numbered
+ * by decreasing community size; n_communities / modularity are host outputs. */
+SCB_API int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* weights, int64_t n,
+                int64_t nnz, double resolution, int32_t max_levels, int32_t max_iters, uint32_t seed,
+                int32_t* labels, int32_t* n_communities, double* modularity, void* stream);
+
 /* ---- a7: partial Gram matrix C = Z^T Z (float64 [hp][hp], full symmetric) on the
  * 5th-gen tensor cores (tcgen05 kind::f16, "3xBF16": x = hi + lo with hi = bf16(x),
  * lo = bf16(x - hi), products hi*hi + hi*lo + lo*hi, <= 2^-16 relative each; FP32 accumulate

@@ -41,6 +41,8 @@ class Params:
     regress_out: bool = False  # sc.pp.regress_out(["total_counts", "pct_counts_mt"]) before scale
     connectivities: bool = False  # also sc.pp.neighbors' distances/connectivities (umap fuzzy graph)
     umap: bool = False  # also sc.tl.umap (layout from X_pca[:, :2]; implies connectivities)
+    cluster: bool = False  # also community detection (sc.tl.louvain / leiden core) on connectivities
+    resolution: float = 1.0
     umap_epochs: Optional[int] = None
 
 
@@ -61,6 +63,8 @@ class Result:
     step_ms: dict
     graph: Optional[pp.NeighborsGraph] = None
     umap: Optional[torch.Tensor] = None
+    clusters: Optional[torch.Tensor] = None
+    modularity: Optional[float] = None
 
 
 class _Timer:
@@ -177,8 +181,9 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
         ki, kd = pp.neighbors(Xp, p.n_neighbors, n_comps=p.n_comps, keys=keys, timer=knn_timer)
     else:
         ki = kd = None
-    graph = emb = None
-    if with_knn and (p.connectivities or p.umap):
+    graph = emb = labels = None
+    q = None
+    if with_knn and (p.connectivities or p.umap or p.cluster):
         tm.step("graph")
         graph = pp.neighbors_graph(ki, kd, comm=comm)
     if with_knn and p.umap:
@@ -186,5 +191,10 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
             raise NotImplementedError("umap layout is single-GPU (the layout SGD needs the whole graph)")
         tm.step("umap")
         emb = pp.umap_layout(graph.connectivities, Xp[:, :2], n_epochs=p.umap_epochs)
+    if with_knn and p.cluster:
+        if comm is not None:
+            raise NotImplementedError("clustering is single-GPU (it contracts the whole graph)")
+        tm.step("cluster")
+        labels, _, q = pp.louvain(graph.connectivities, resolution=p.resolution)
     ms = tm.finish()
-    return Result(qc, cm, gm, X_log, hvg_mask, hvg_index, st, sc, res_pca, ki, kd, n_total, ms, graph, emb)
+    return Result(qc, cm, gm, X_log, hvg_mask, hvg_index, st, sc, res_pca, ki, kd, n_total, ms, graph, emb, labels, q)

@@ -563,3 +563,20 @@ def umap_layout(connectivities: DeviceCSR, init: torch.Tensor, n_epochs: Optiona
               int(w.numel()), w_max, _p(init), init.stride(0), int(n_epochs), a, b, int(negative_sample_rate),
               int(seed), _p(emb), _stream(w.device))
     return emb
+
+
+# ----------------------------------------------------------------------------- clustering
+def louvain(connectivities: DeviceCSR, resolution: float = 1.0, max_levels: int = 10, max_iters: int = 10,
+            seed: int = 0):
+    """Community detection on the neighbors graph (sc.tl.louvain; the local-moving + aggregation
+    core of sc.tl.leiden), deterministic (csrc/cluster.cu).  Returns (labels int32 [N] ordered
+    by decreasing community size, n_communities, modularity)."""
+    import ctypes
+    G = connectivities
+    lab = torch.empty(G.n_rows, dtype=torch.int32, device=G.data.device)
+    nc = ctypes.c_int32(0)
+    q = ctypes.c_double(0.0)
+    _lib.call("scb_louvain", _ctx(G.data), _p(G.indptr), _p(G.indices), _p(G.data), G.n_rows, int(G.data.numel()),
+              float(resolution), int(max_levels), int(max_iters), int(seed) & 0xFFFFFFFF, _p(lab),
+              ctypes.addressof(nc), ctypes.addressof(q), _stream(G.data.device))
+    return lab, int(nc.value), float(q.value)
