@@ -224,7 +224,7 @@ SCB_API int scb_umap_layout(scb_ctx* ctx, const int64_t* indptr, const int32_t* 
 
 /* ---- f3 clustering on the neighbors graph (sc.tl.louvain / the local-moving + aggregation
  * core of sc.tl.leiden): multi-level modularity optimisation with resolution gamma on the
- * symmetric CSR (indptr/indices/weights), deterministic (2^-32 fixed-point weights, hash-bucketed
+ * symmetric CSR (indptr/indices/weights), deterministic (2^-32 fixed-point weights, 8 hash-bucketed
  * synchronous moves, ties to the smaller community).  labels (device int32[n]) are numbered
  * by decreasing community size; n_communities / modularity are host outputs. */
 SCB_API int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* weights, int64_t n,

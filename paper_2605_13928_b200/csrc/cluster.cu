@@ -6,7 +6,7 @@
 //             and the per-node community links are then exact integer sums, independent of
 //             summation order, so the device and the oracle (oracle/pipeline.py louvain) take
 //             the same decisions;
-//   moving    nodes are split into 4 hash buckets; per bucket, a warp per node accumulates its
+//   moving    nodes are split into 8 hash buckets; per bucket, a warp per node accumulates its
 //             links to neighbouring communities in a shared-memory hash table and picks
 //             argmax_c  w_ic - gamma k_i tot_c / 2m  (tot_a excludes the node itself; ties ->
 //             smaller c; moves only on a strict gain), then the bucket's moves are applied
@@ -30,7 +30,7 @@ namespace scb {
 
 constexpr int kTab = 1024;      // hash slots per warp
 constexpr int kClWarps = 8;     // warps per CTA in the moving kernel
-constexpr int kBuckets = 4;
+constexpr int kBuckets = 8;
 
 __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   x ^= x >> 16;

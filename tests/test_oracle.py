@@ -310,3 +310,25 @@ def test_umap_graph_oracle_vs_literal_loop_and_properties():
     W = op.membership_strengths(ki, kd, sig, rho)
     excess = W.sum(1) - np.log2(12)
     assert np.abs(excess[rho > 0]).max() < 1e-3
+
+
+def test_louvain_oracle_quality_vs_networkx():
+    """The deterministic bucketed-synchronous modularity optimisation (the algorithm csrc/cluster.cu
+    implements) reaches the modularity of networkx's sequential Louvain on a weakly clustered
+    single-cell-like graph (independent implementation as the quality reference)."""
+    nx = pytest.importorskip("networkx")
+    rng = np.random.default_rng(4)
+    centers = rng.standard_normal((6, 8)) * 1.2
+    lab = rng.integers(0, 6, 1500)
+    E = (centers[lab] + rng.standard_normal((1500, 8))).astype(np.float32)
+    ki, kd = op.knn(E, 15)
+    C, _, _, _ = op.umap_connectivities(ki, kd, 1500)
+    _, nc, q = op.louvain(C, seed=3)
+    G = nx.from_scipy_sparse_array(C)
+    qs = [nx.community.modularity(G, nx.community.louvain_communities(G, weight="weight", seed=s), weight="weight")
+          for s in (0, 1, 2)]
+    assert q >= min(qs) - 0.01, (q, qs)
+    # modularity reported by the oracle equals networkx's formula on its own partition
+    labels, _, q2 = op.louvain(C, seed=3)
+    comms = [set(np.nonzero(labels == c)[0].tolist()) for c in range(labels.max() + 1)]
+    assert abs(nx.community.modularity(G, comms, weight="weight") - q2) < 1e-6
