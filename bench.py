@@ -171,7 +171,7 @@ def main():
     ap.add_argument("--graph", action="store_true",
                     help="also build sc.pp.neighbors' distances/connectivities (umap fuzzy graph) in the step")
     ap.add_argument("--umap", action="store_true", help="also run sc.tl.umap (layout) in the step (1 GPU)")
-    ap.add_argument("--cluster", action="store_true", help="also run the Louvain/Leiden-core clustering (1 GPU)")
+    ap.add_argument("--cluster", action="store_true", help="also run Leiden clustering on the graph (1 GPU)")
     ap.add_argument("--regress-out", action="store_true",
                     help="add sc.pp.regress_out(total_counts, pct_counts_mt) before scale (paper Table 1 step 4)")
     args = ap.parse_args()
@@ -364,7 +364,7 @@ def main():
             "data": "synthetic NB counts generated on device (oracle/synth.py model, seed %d)" % args.seed,
             "config": {"workload": f"C3: {N} cells x {G} genes (~{Z_total / N / G:.1%} dense), full QC->normalize->"
                                    f"log1p->HVG(seurat,{args.hvg})->{'regress_out+' if args.regress_out else ''}scale->PCA(50)->"
-                                   f"kNN(k={args.k}, exact){'+umap graph' if args.graph or args.umap or args.cluster else ''}{'+umap layout' if args.umap else ''}{'+clustering' if args.cluster else ''}",
+                                   f"kNN(k={args.k}, exact){'+umap graph' if args.graph or args.umap or args.cluster else ''}{'+umap layout' if args.umap else ''}{'+leiden' if args.cluster else ''}",
                        "cells": N, "genes": G, "nnz": int(Z_total), "kept_cells": int(n_keys), "hvg": H,
                        "parallelism": f"cells sharded x{world}", "l2": "inputs (14 GB) >> L2 (126 MB); no flush needed",
                        "gen_seconds": round(gen_s, 1)},

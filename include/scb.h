@@ -230,6 +230,13 @@ SCB_API int scb_umap_layout(scb_ctx* ctx, const int64_t* indptr, const int32_t* 
 SCB_API int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* weights, int64_t n,
                 int64_t nnz, double resolution, int32_t max_levels, int32_t max_iters, uint32_t seed,
                 int32_t* labels, int32_t* n_communities, double* modularity, void* stream);
+/* sc.tl.leiden: the same local moving, then Leiden's refinement of each level's partition
+ * (singletons join well-connected sub-communities with the largest non-negative gain) and
+ * aggregation by the refined partition, each aggregate node starting the next level in its
+ * unrefined community (labels = that partition). */
+SCB_API int scb_leiden(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* weights, int64_t n,
+               int64_t nnz, double resolution, int32_t max_levels, int32_t max_iters, uint32_t seed,
+               int32_t* labels, int32_t* n_communities, double* modularity, void* stream);
 
 /* ---- a7: partial Gram matrix C = Z^T Z (float64 [hp][hp], full symmetric) on the
  * 5th-gen tensor cores (tcgen05 kind::f16, "3xBF16": x = hi + lo with hi = bf16(x),

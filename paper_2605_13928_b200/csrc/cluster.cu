@@ -193,6 +193,132 @@ __global__ void modularity_kernel(const int64_t* __restrict__ indptr, const int3
   }
 }
 
+// ---------------------------------------------------------------- Leiden refinement
+__global__ void init_tot_kernel(const int32_t* __restrict__ comm, const long long* __restrict__ k, int64_t n,
+                                unsigned long long* __restrict__ tot) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&tot[comm[i]], (unsigned long long)k[i]);
+}
+
+// R_s, |s| and the external weight ext_s = w(s, C - s) of every sub-community of the refined
+// partition (exact integers)
+__global__ void refine_stats_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ nbr,
+                                    const long long* __restrict__ W, int64_t n, const long long* __restrict__ k,
+                                    const int32_t* __restrict__ comm, const int32_t* __restrict__ ref,
+                                    unsigned long long* __restrict__ R, unsigned int* __restrict__ cnt,
+                                    unsigned long long* __restrict__ ext) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    const int ru = ref[u], cu = comm[u];
+    atomicAdd(&R[ru], (unsigned long long)k[u]);
+    atomicAdd(&cnt[ru], 1u);
+    long long e_sum = 0;
+    for (int64_t e = indptr[u]; e < indptr[u + 1]; ++e) {
+      const int x = nbr[e];
+      if (x != u && comm[x] == cu && ref[x] != ru) e_sum += W[e];
+    }
+    if (e_sum) atomicAdd(&ext[ru], (unsigned long long)e_sum);
+  }
+}
+
+__global__ void __launch_bounds__(kClWarps * 32)
+refine_decide_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ nbr,
+                     const long long* __restrict__ W, int64_t n, const long long* __restrict__ k,
+                     const int32_t* __restrict__ comm, const int32_t* __restrict__ ref,
+                     const unsigned long long* __restrict__ K, const unsigned long long* __restrict__ R,
+                     const unsigned int* __restrict__ cnt, const unsigned long long* __restrict__ ext,
+                     const unsigned long long* __restrict__ m2p, double gamma, int bucket, uint32_t seed,
+                     int32_t* __restrict__ newref) {
+  extern __shared__ unsigned char cl_smem[];
+  const int wid = warp_id(), lane = lane_id();
+  int* keys = reinterpret_cast<int*>(cl_smem) + wid * kTab;
+  unsigned long long* vals =
+      reinterpret_cast<unsigned long long*>(cl_smem + (size_t)kClWarps * kTab * 4) + (size_t)wid * kTab;
+  const double m2 = (double)(long long)*m2p;
+  for (int64_t v = (int64_t)blockIdx.x * kClWarps + wid; v < n; v += (int64_t)gridDim.x * kClWarps) {
+    if ((int)(mix32((uint32_t)v ^ seed ^ 0x9E3779B9u) % kBuckets) != bucket) continue;
+    if (ref[v] != v || cnt[v] != 1u) {  // only singletons move
+      if (lane == 0) newref[v] = ref[v];
+      continue;
+    }
+    const int C = comm[v];
+    const long long kv = k[v];
+    for (int t = lane; t < kTab; t += 32) { keys[t] = -1; vals[t] = 0ull; }
+    __syncwarp();
+    bool overflow = false;
+    long long wvc = 0;
+    const int64_t e0 = indptr[v], e1 = indptr[v + 1];
+    for (int64_t base = e0; base < e1; base += 32) {
+      const int64_t e = base + lane;
+      if (e < e1) {
+        const int x = nbr[e];
+        if (x != v && comm[x] == C) {
+          wvc += W[e];
+          const int sx = ref[x];
+          uint32_t h = mix32((uint32_t)sx) & (kTab - 1);
+          for (int probes = 0;; ++probes) {
+            const int prev = atomicCAS(&keys[h], -1, sx);
+            if (prev == -1 || prev == sx) {
+              atomicAdd(&vals[h], (unsigned long long)W[e]);
+              break;
+            }
+            if (probes + 1 >= kTab) { overflow = true; break; }
+            h = (h + 1) & (kTab - 1);
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, overflow)) { overflow = true; break; }
+    }
+    __syncwarp();
+    wvc = warp_sum(wvc);
+    const double kd = (double)kv;
+    const long long KC = (long long)K[C];
+    double bq = -1e300;
+    int bs = INT32_MAX;
+    if (!overflow && (double)wvc >= gamma * kd * (double)(KC - kv) / m2) {
+      for (int t = lane; t < kTab; t += 32) {
+        const int sx = keys[t];
+        if (sx < 0) continue;
+        const long long Rs = (long long)R[sx];
+        if (!((double)(long long)ext[sx] >= gamma * (double)Rs * (double)(KC - Rs) / m2)) continue;
+        const double dq = (double)(long long)vals[t] - gamma * kd * (double)Rs / m2;
+        if (better(dq, sx, bq, bs)) { bq = dq; bs = sx; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oq = __shfl_xor_sync(0xffffffffu, bq, o);
+      const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+      if (better(oq, os, bq, bs)) { bq = oq; bs = os; }
+    }
+    if (lane == 0) newref[v] = (bs != INT32_MAX && bq >= 0.0) ? bs : (int)v;
+    __syncwarp();
+  }
+}
+
+__global__ void refine_apply_kernel(int64_t n, int32_t* __restrict__ ref, const int32_t* __restrict__ newref, int bucket,
+                                    uint32_t seed) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    if ((int)(mix32((uint32_t)v ^ seed ^ 0x9E3779B9u) % kBuckets) == bucket) ref[v] = newref[v];
+}
+
+__global__ void iota_kernel(int32_t* __restrict__ x, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = (int32_t)i;
+}
+
+__global__ void map_kernel(int32_t* __restrict__ x, int64_t n, const int32_t* __restrict__ m) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = m[x[i]];
+}
+
+// next level: aggregate node rank_ref[ref[i]] starts in community rank_comm[comm[i]]
+__global__ void carry_comm_kernel(int64_t n, const int32_t* __restrict__ ref, const int32_t* __restrict__ comm,
+                                  const int64_t* __restrict__ rank_ref, const int64_t* __restrict__ rank_comm,
+                                  int32_t* __restrict__ next_comm) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    next_comm[rank_ref[ref[i]]] = (int32_t)rank_comm[comm[i]];
+}
+
 }  // namespace scb
 
 using namespace scb;
@@ -211,14 +337,16 @@ struct DevBuf {
     SCB_CUDA(cudaMallocAsync(&buf.p, std::max<size_t>((size_t)(bytes), 16), s));         \
   } while (0)
 
-extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* weights,
-                           int64_t n, int64_t nnz, double resolution, int32_t max_levels, int32_t max_iters,
-                           uint32_t seed, int32_t* labels, int32_t* n_communities, double* modularity, void* stream) {
+static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* weights, int64_t n,
+                        int64_t nnz, double resolution, int32_t max_levels, int32_t max_iters, uint32_t seed,
+                        int32_t* labels, int32_t* n_communities, double* modularity, void* stream, bool leiden) {
   SCB_REQUIRE(ctx && indptr && indices && weights && labels && n_communities && modularity, SCB_ERR_ARG,
-              "scb_louvain: null argument");
-  SCB_REQUIRE(n > 0 && n < INT32_MAX && max_levels >= 1 && max_iters >= 1, SCB_ERR_ARG, "scb_louvain: bad arguments");
+              "scb_louvain/scb_leiden: null argument");
+  SCB_REQUIRE(n > 0 && n < INT32_MAX && max_levels >= 1 && max_iters >= 1, SCB_ERR_ARG,
+              "scb_louvain/scb_leiden: bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   const int grid = ctx->num_sms * 8;
+  const bool dbg = getenv("SCB_CLUSTER_DEBUG") != nullptr;
   {
     // the level buffers come from the stream-ordered pool; keep its memory mapped between
     // levels/calls (the default release threshold 0 unmaps it at every synchronisation, which
@@ -233,6 +361,7 @@ extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
   CL_ALLOC(W0, nnz * 8);
   to_fixed_kernel<<<grid, 256, 0, s>>>(weights, nnz, (long long*)W0.p);
   SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #1 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
   CL_ALLOC(cell_b, n * 4);
   int32_t* node_of_cell = (int32_t*)cell_b.p;  // cell -> node of the current level
   CL_ALLOC(scal_b, 64);
@@ -246,7 +375,10 @@ extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
   DevBuf next_ip, next_nb, next_W;  // owned storage of the current coarse level
   const size_t cl_smem = (size_t)kClWarps * kTab * (4 + 8);
   SCB_CUDA(cudaFuncSetAttribute(move_decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem));
+  SCB_CUDA(cudaFuncSetAttribute(refine_decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem));
   bool first = true;
+  DevBuf carry;  // Leiden: partition P carried into the current level (aggregate node -> community)
+  bool leiden_done = false;
   const bool verbose = getenv("SCB_CLUSTER_VERBOSE") != nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (verbose) {
@@ -267,9 +399,16 @@ extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
     SCB_CUDA(cudaMemsetAsync(m2, 0, 8, s));
     strength_kernel<<<grid, 256, 0, s>>>(cur_ip, cur_W, cur_n, k, comm, tot, m2);
     SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #2 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
     if (first) {  // node_of_cell := identity (comm starts as the identity)
       SCB_CUDA(cudaMemcpyAsync(node_of_cell, comm, n * 4, cudaMemcpyDeviceToDevice, s));
       first = false;
+    } else if (leiden) {  // start from the carried partition P
+      SCB_CUDA(cudaMemcpyAsync(comm, carry.p, cur_n * 4, cudaMemcpyDeviceToDevice, s));
+      SCB_CUDA(cudaMemsetAsync(tot, 0, cur_n * 8, s));
+      init_tot_kernel<<<grid, 256, 0, s>>>(comm, k, cur_n, tot);
+      SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #3 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
     }
     unsigned long long total_moves = 0;
     for (int it = 0; it < max_iters; ++it) {
@@ -278,8 +417,10 @@ extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
         move_decide_kernel<<<ctx->num_sms * 4, kClWarps * 32, cl_smem, s>>>(cur_ip, cur_nb, cur_W, cur_n, k, comm, tot,
                                                                              m2, resolution, b, seed, newc);
         SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #4 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
         move_apply_kernel<<<grid, 256, 0, s>>>(cur_n, k, comm, newc, tot, b, seed, moved);
         SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #5 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
       }
       unsigned long long mv = 0;
       SCB_CUDA(cudaMemcpyAsync(&mv, moved, 8, cudaMemcpyDeviceToHost, s));
@@ -295,28 +436,93 @@ extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
       }
       if (mv == 0) break;
     }
-    if (total_moves == 0) break;
-    // renumber communities (order of their smallest node id) and contract the graph
+    // renumber communities (order of their smallest node id)
     DevBuf lused, lrank;
     CL_ALLOC(lused, cur_n);
     CL_ALLOC(lrank, (cur_n + 1) * 8);
-    SCB_CUDA(cudaMemsetAsync(lused.p, 0, cur_n, s));
-    used_kernel<<<grid, 256, 0, s>>>(comm, cur_n, (uint8_t*)lused.p);
-    SCB_LAUNCH_CHECK();
     int64_t* rank = (int64_t*)lrank.p;
-    SCB_TRY(scan_u8_to_i64(ctx, (const uint8_t*)lused.p, cur_n, rank, s));
     int64_t n_new = 0;
-    SCB_CUDA(cudaMemcpyAsync(&n_new, rank + cur_n, 8, cudaMemcpyDeviceToHost, s));
-    SCB_CUDA(cudaStreamSynchronize(s));
-    compose_kernel<<<grid, 256, 0, s>>>(node_of_cell, n, comm, rank);
-    SCB_LAUNCH_CHECK();
-    if (n_new == cur_n) break;
+    auto renumber = [&](const int32_t* part, int64_t* rk, int64_t* count) -> int {
+      SCB_CUDA(cudaMemsetAsync(lused.p, 0, cur_n, s));
+      used_kernel<<<grid, 256, 0, s>>>(part, cur_n, (uint8_t*)lused.p);
+      SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #6 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      SCB_TRY(scan_u8_to_i64(ctx, (const uint8_t*)lused.p, cur_n, rk, s));
+      SCB_CUDA(cudaMemcpyAsync(count, rk + cur_n, 8, cudaMemcpyDeviceToHost, s));
+      SCB_CUDA(cudaStreamSynchronize(s));
+      return SCB_OK;
+    };
+    const int32_t* agg = comm;  // partition the graph is aggregated by
+    DevBuf lref, lnewref, lR, lcnt, lext, lrank2;
+    if (!leiden) {
+      if (total_moves == 0) break;
+      SCB_TRY(renumber(comm, rank, &n_new));
+      compose_kernel<<<grid, 256, 0, s>>>(node_of_cell, n, comm, rank);
+      SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #7 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      if (n_new == cur_n) break;
+    } else {
+      // refinement of P inside each community (singletons merge into well-connected
+      // sub-communities), one synchronous pass per bucket
+      CL_ALLOC(lref, cur_n * 4);
+      CL_ALLOC(lnewref, cur_n * 4);
+      CL_ALLOC(lR, cur_n * 8);
+      CL_ALLOC(lcnt, cur_n * 4);
+      CL_ALLOC(lext, cur_n * 8);
+      int32_t* ref = (int32_t*)lref.p;
+      iota_kernel<<<grid, 256, 0, s>>>(ref, cur_n);
+      SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #8 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      for (int b = 0; b < kBuckets; ++b) {
+        SCB_CUDA(cudaMemsetAsync(lR.p, 0, cur_n * 8, s));
+        SCB_CUDA(cudaMemsetAsync(lcnt.p, 0, cur_n * 4, s));
+        SCB_CUDA(cudaMemsetAsync(lext.p, 0, cur_n * 8, s));
+        refine_stats_kernel<<<grid, 256, 0, s>>>(cur_ip, cur_nb, cur_W, cur_n, k, comm, ref,
+                                                 (unsigned long long*)lR.p, (unsigned int*)lcnt.p,
+                                                 (unsigned long long*)lext.p);
+        SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #9 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+        refine_decide_kernel<<<ctx->num_sms * 4, kClWarps * 32, cl_smem, s>>>(
+            cur_ip, cur_nb, cur_W, cur_n, k, comm, ref, tot, (const unsigned long long*)lR.p,
+            (const unsigned int*)lcnt.p, (const unsigned long long*)lext.p, m2, resolution, b, seed,
+            (int32_t*)lnewref.p);
+        SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #10 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+        refine_apply_kernel<<<grid, 256, 0, s>>>(cur_n, ref, (const int32_t*)lnewref.p, b, seed);
+        SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #11 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      }
+      int64_t n_comm = 0;
+      CL_ALLOC(lrank2, (cur_n + 1) * 8);
+      int64_t* rank_comm = (int64_t*)lrank2.p;
+      SCB_TRY(renumber(comm, rank_comm, &n_comm));
+      SCB_TRY(renumber(ref, rank, &n_new));
+      if ((total_moves == 0 && n_new == n_comm) || n_new == cur_n) {  // final: labels = P
+        compose_kernel<<<grid, 256, 0, s>>>(node_of_cell, n, comm, rank_comm);
+        SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #12 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+        leiden_done = true;
+        break;
+      }
+      compose_kernel<<<grid, 256, 0, s>>>(node_of_cell, n, ref, rank);
+      SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #13 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      DevBuf nxt;
+      CL_ALLOC(nxt, n_new * 4);
+      carry_comm_kernel<<<grid, 256, 0, s>>>(cur_n, ref, comm, rank, rank_comm, (int32_t*)nxt.p);
+      SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #14 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      std::swap(carry.p, nxt.p);
+      carry.s = s;
+      agg = ref;
+    }
     DevBuf kin, kout, vout, ukeys, usum, nuniq, tmp;
     CL_ALLOC(kin, cur_nnz * 8);
     CL_ALLOC(kout, cur_nnz * 8);
     CL_ALLOC(vout, cur_nnz * 8);
-    edge_keys_kernel<<<grid, 256, 0, s>>>(cur_ip, cur_nb, cur_n, comm, rank, n_new, (unsigned long long*)kin.p);
+    edge_keys_kernel<<<grid, 256, 0, s>>>(cur_ip, cur_nb, cur_n, agg, rank, n_new, (unsigned long long*)kin.p);
     SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #15 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
     int end_bit = 1;
     while (end_bit < 64 && ((unsigned long long)n_new * (unsigned long long)n_new) > (1ull << end_bit)) ++end_bit;
     size_t tb1 = 0, tb2 = 0;
@@ -343,6 +549,7 @@ extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
     coarse_csr_kernel<<<grid, 256, 0, s>>>((const unsigned long long*)ukeys.p, nu, n_new, (int64_t*)cip.p,
                                            (int32_t*)cnb.p);
     SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #16 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
     // the coarse level becomes current (ownership moves into next_*)
     std::swap(next_ip.p, cip.p);
     std::swap(next_nb.p, cnb.p);
@@ -354,6 +561,11 @@ extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
     cur_n = n_new;
     cur_nnz = nu;
   }
+  if (leiden && !leiden_done && carry.p) {  // max_levels reached: labels = the carried P
+    map_kernel<<<grid, 256, 0, s>>>(node_of_cell, n, (const int32_t*)carry.p);
+    SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #17 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+  }
   // labels by decreasing community size (ties: smallest member), modularity on the input graph
   DevBuf ltot2;
   CL_ALLOC(ltot2, (size_t)n * 8);
@@ -362,6 +574,7 @@ extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
   modularity_kernel<<<grid, 256, 0, s>>>(indptr, indices, (const long long*)W0.p, n, node_of_cell, in_sum,
                                          (unsigned long long*)ltot2.p);
   SCB_LAUNCH_CHECK();
+    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #18 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
   std::vector<int32_t> h_lab(n);
   std::vector<unsigned long long> h_tot(n);
   unsigned long long h_in = 0, h_m2 = 0;
@@ -398,4 +611,18 @@ extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* i
   *n_communities = n_c;
   *modularity = q;
   return SCB_OK;
+}
+
+extern "C" int scb_louvain(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* weights,
+                           int64_t n, int64_t nnz, double resolution, int32_t max_levels, int32_t max_iters,
+                           uint32_t seed, int32_t* labels, int32_t* n_communities, double* modularity, void* stream) {
+  return cluster_impl(ctx, indptr, indices, weights, n, nnz, resolution, max_levels, max_iters, seed, labels,
+                      n_communities, modularity, stream, false);
+}
+
+extern "C" int scb_leiden(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* weights,
+                          int64_t n, int64_t nnz, double resolution, int32_t max_levels, int32_t max_iters,
+                          uint32_t seed, int32_t* labels, int32_t* n_communities, double* modularity, void* stream) {
+  return cluster_impl(ctx, indptr, indices, weights, n, nnz, resolution, max_levels, max_iters, seed, labels,
+                      n_communities, modularity, stream, true);
 }

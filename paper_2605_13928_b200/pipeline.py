@@ -41,7 +41,8 @@ class Params:
     regress_out: bool = False  # sc.pp.regress_out(["total_counts", "pct_counts_mt"]) before scale
     connectivities: bool = False  # also sc.pp.neighbors' distances/connectivities (umap fuzzy graph)
     umap: bool = False  # also sc.tl.umap (layout from X_pca[:, :2]; implies connectivities)
-    cluster: bool = False  # also community detection (sc.tl.louvain / leiden core) on connectivities
+    cluster: bool = False  # also community detection on connectivities (sc.tl.leiden / sc.tl.louvain)
+    cluster_method: str = "leiden"
     resolution: float = 1.0
     umap_epochs: Optional[int] = None
 
@@ -195,6 +196,7 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
         if comm is not None:
             raise NotImplementedError("clustering is single-GPU (it contracts the whole graph)")
         tm.step("cluster")
-        labels, _, q = pp.louvain(graph.connectivities, resolution=p.resolution)
+        fn = pp.leiden if p.cluster_method == "leiden" else pp.louvain
+        labels, _, q = fn(graph.connectivities, resolution=p.resolution)
     ms = tm.finish()
     return Result(qc, cm, gm, X_log, hvg_mask, hvg_index, st, sc, res_pca, ki, kd, n_total, ms, graph, emb, labels, q)

@@ -567,16 +567,24 @@ def umap_layout(connectivities: DeviceCSR, init: torch.Tensor, n_epochs: Optiona
 
 # ----------------------------------------------------------------------------- clustering
 def louvain(connectivities: DeviceCSR, resolution: float = 1.0, max_levels: int = 10, max_iters: int = 10,
-            seed: int = 0):
-    """Community detection on the neighbors graph (sc.tl.louvain; the local-moving + aggregation
-    core of sc.tl.leiden), deterministic (csrc/cluster.cu).  Returns (labels int32 [N] ordered
-    by decreasing community size, n_communities, modularity)."""
+            seed: int = 0, _fn: str = "scb_louvain"):
+    """Community detection on the neighbors graph (sc.tl.louvain), deterministic
+    (csrc/cluster.cu).  Returns (labels int32 [N] ordered by decreasing community size,
+    n_communities, modularity)."""
     import ctypes
     G = connectivities
     lab = torch.empty(G.n_rows, dtype=torch.int32, device=G.data.device)
     nc = ctypes.c_int32(0)
     q = ctypes.c_double(0.0)
-    _lib.call("scb_louvain", _ctx(G.data), _p(G.indptr), _p(G.indices), _p(G.data), G.n_rows, int(G.data.numel()),
+    _lib.call(_fn, _ctx(G.data), _p(G.indptr), _p(G.indices), _p(G.data), G.n_rows, int(G.data.numel()),
               float(resolution), int(max_levels), int(max_iters), int(seed) & 0xFFFFFFFF, _p(lab),
               ctypes.addressof(nc), ctypes.addressof(q), _stream(G.data.device))
     return lab, int(nc.value), float(q.value)
+
+
+def leiden(connectivities: DeviceCSR, resolution: float = 1.0, max_levels: int = 10, max_iters: int = 10,
+           seed: int = 0):
+    """sc.tl.leiden(resolution): local moving, refinement (well-connected sub-communities) and
+    aggregation by the refined partition, deterministic (csrc/cluster.cu).  Returns (labels,
+    n_communities, modularity)."""
+    return louvain(connectivities, resolution, max_levels, max_iters, seed, _fn="scb_leiden")

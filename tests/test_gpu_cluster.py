@@ -35,3 +35,24 @@ def test_louvain_matches_oracle_and_recovers_clusters(resolution):
     assert q > 0.5
     if resolution == 1.0:
         assert adjusted_rand_score(truth, olab) > 0.9
+
+
+@pytest.mark.parametrize("resolution", [1.0, 0.5])
+def test_leiden_matches_oracle(resolution):
+    import scipy.sparse as sp
+    import scipy.sparse.csgraph as cg
+    from sklearn.metrics import adjusted_rand_score
+    from oracle import pipeline as op
+    from paper_2605_13928_b200 import pp
+    G, truth = _graph(n=1500, k=6, seed=11)
+    lab, nc, q = pp.leiden(G, resolution=resolution, seed=3)
+    ip, ix, w, n = G.to_host()
+    C = sp.csr_matrix((w, ix, ip), shape=(n, n))
+    olab, onc, oq = op.leiden(C, resolution=resolution, seed=3)
+    np.testing.assert_array_equal(lab.cpu().numpy(), olab)
+    assert nc == onc and abs(q - oq) <= 1e-12 * max(1.0, abs(oq))
+    for c in range(nc):  # Leiden's guarantee: every community is connected
+        idx = np.nonzero(olab == c)[0]
+        assert cg.connected_components(C[idx][:, idx], directed=False)[0] == 1
+    if resolution == 1.0:
+        assert adjusted_rand_score(truth, olab) > 0.9

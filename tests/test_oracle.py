@@ -332,3 +332,26 @@ def test_louvain_oracle_quality_vs_networkx():
     labels, _, q2 = op.louvain(C, seed=3)
     comms = [set(np.nonzero(labels == c)[0].tolist()) for c in range(labels.max() + 1)]
     assert abs(nx.community.modularity(G, comms, weight="weight") - q2) < 1e-6
+
+
+def test_leiden_oracle_quality_and_connectivity():
+    """The deterministic Leiden restatement: modularity at least networkx's sequential Louvain
+    (minus 0.01) on a weakly clustered graph, and every community connected."""
+    nx = pytest.importorskip("networkx")
+    import scipy.sparse.csgraph as cg
+    rng = np.random.default_rng(4)
+    centers = rng.standard_normal((6, 8)) * 1.2
+    lab = rng.integers(0, 6, 1500)
+    E = (centers[lab] + rng.standard_normal((1500, 8))).astype(np.float32)
+    ki, kd = op.knn(E, 15)
+    C, _, _, _ = op.umap_connectivities(ki, kd, 1500)
+    labels, nc, q = op.leiden(C, seed=3)
+    G = nx.from_scipy_sparse_array(C)
+    qs = [nx.community.modularity(G, nx.community.louvain_communities(G, weight="weight", seed=s), weight="weight")
+          for s in (0, 1, 2)]
+    assert q >= min(qs) - 0.01, (q, qs)
+    comms = [set(np.nonzero(labels == c)[0].tolist()) for c in range(nc)]
+    assert abs(nx.community.modularity(G, comms, weight="weight") - q) < 1e-6
+    for c in range(nc):
+        idx = np.nonzero(labels == c)[0]
+        assert cg.connected_components(C[idx][:, idx], directed=False)[0] == 1
