@@ -331,6 +331,16 @@ struct DevBuf {
 };
 }  // namespace
 
+// launch check; with SCB_CLUSTER_DEBUG set, also synchronise so a fault names its launch site
+#define CL_CHECK()                                                                              \
+  do {                                                                                          \
+    SCB_LAUNCH_CHECK();                                                                         \
+    if (dbg) {                                                                                  \
+      const cudaError_t _e = cudaStreamSynchronize(s);                                          \
+      SCB_REQUIRE(_e == cudaSuccess, SCB_ERR_CUDA, "cluster.cu:%d: %s", __LINE__, cudaGetErrorString(_e)); \
+    }                                                                                           \
+  } while (0)
+
 #define CL_ALLOC(buf, bytes)                                                              \
   do {                                                                                    \
     buf.s = s;                                                                            \
@@ -360,8 +370,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
   DevBuf W0, scal_b, cell_b;
   CL_ALLOC(W0, nnz * 8);
   to_fixed_kernel<<<grid, 256, 0, s>>>(weights, nnz, (long long*)W0.p);
-  SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #1 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+  CL_CHECK();
   CL_ALLOC(cell_b, n * 4);
   int32_t* node_of_cell = (int32_t*)cell_b.p;  // cell -> node of the current level
   CL_ALLOC(scal_b, 64);
@@ -398,8 +407,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
     unsigned long long* tot = (unsigned long long*)ltot.p;
     SCB_CUDA(cudaMemsetAsync(m2, 0, 8, s));
     strength_kernel<<<grid, 256, 0, s>>>(cur_ip, cur_W, cur_n, k, comm, tot, m2);
-    SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #2 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+    CL_CHECK();
     if (first) {  // node_of_cell := identity (comm starts as the identity)
       SCB_CUDA(cudaMemcpyAsync(node_of_cell, comm, n * 4, cudaMemcpyDeviceToDevice, s));
       first = false;
@@ -407,8 +415,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
       SCB_CUDA(cudaMemcpyAsync(comm, carry.p, cur_n * 4, cudaMemcpyDeviceToDevice, s));
       SCB_CUDA(cudaMemsetAsync(tot, 0, cur_n * 8, s));
       init_tot_kernel<<<grid, 256, 0, s>>>(comm, k, cur_n, tot);
-      SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #3 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      CL_CHECK();
     }
     unsigned long long total_moves = 0;
     for (int it = 0; it < max_iters; ++it) {
@@ -416,11 +423,9 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
       for (int b = 0; b < kBuckets; ++b) {
         move_decide_kernel<<<ctx->num_sms * 4, kClWarps * 32, cl_smem, s>>>(cur_ip, cur_nb, cur_W, cur_n, k, comm, tot,
                                                                              m2, resolution, b, seed, newc);
-        SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #4 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+        CL_CHECK();
         move_apply_kernel<<<grid, 256, 0, s>>>(cur_n, k, comm, newc, tot, b, seed, moved);
-        SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #5 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+        CL_CHECK();
       }
       unsigned long long mv = 0;
       SCB_CUDA(cudaMemcpyAsync(&mv, moved, 8, cudaMemcpyDeviceToHost, s));
@@ -445,8 +450,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
     auto renumber = [&](const int32_t* part, int64_t* rk, int64_t* count) -> int {
       SCB_CUDA(cudaMemsetAsync(lused.p, 0, cur_n, s));
       used_kernel<<<grid, 256, 0, s>>>(part, cur_n, (uint8_t*)lused.p);
-      SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #6 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      CL_CHECK();
       SCB_TRY(scan_u8_to_i64(ctx, (const uint8_t*)lused.p, cur_n, rk, s));
       SCB_CUDA(cudaMemcpyAsync(count, rk + cur_n, 8, cudaMemcpyDeviceToHost, s));
       SCB_CUDA(cudaStreamSynchronize(s));
@@ -458,8 +462,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
       if (total_moves == 0) break;
       SCB_TRY(renumber(comm, rank, &n_new));
       compose_kernel<<<grid, 256, 0, s>>>(node_of_cell, n, comm, rank);
-      SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #7 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      CL_CHECK();
       if (n_new == cur_n) break;
     } else {
       // refinement of P inside each community (singletons merge into well-connected
@@ -471,8 +474,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
       CL_ALLOC(lext, cur_n * 8);
       int32_t* ref = (int32_t*)lref.p;
       iota_kernel<<<grid, 256, 0, s>>>(ref, cur_n);
-      SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #8 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      CL_CHECK();
       for (int b = 0; b < kBuckets; ++b) {
         SCB_CUDA(cudaMemsetAsync(lR.p, 0, cur_n * 8, s));
         SCB_CUDA(cudaMemsetAsync(lcnt.p, 0, cur_n * 4, s));
@@ -480,17 +482,14 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
         refine_stats_kernel<<<grid, 256, 0, s>>>(cur_ip, cur_nb, cur_W, cur_n, k, comm, ref,
                                                  (unsigned long long*)lR.p, (unsigned int*)lcnt.p,
                                                  (unsigned long long*)lext.p);
-        SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #9 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+        CL_CHECK();
         refine_decide_kernel<<<ctx->num_sms * 4, kClWarps * 32, cl_smem, s>>>(
             cur_ip, cur_nb, cur_W, cur_n, k, comm, ref, tot, (const unsigned long long*)lR.p,
             (const unsigned int*)lcnt.p, (const unsigned long long*)lext.p, m2, resolution, b, seed,
             (int32_t*)lnewref.p);
-        SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #10 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+        CL_CHECK();
         refine_apply_kernel<<<grid, 256, 0, s>>>(cur_n, ref, (const int32_t*)lnewref.p, b, seed);
-        SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #11 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+        CL_CHECK();
       }
       int64_t n_comm = 0;
       CL_ALLOC(lrank2, (cur_n + 1) * 8);
@@ -499,19 +498,16 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
       SCB_TRY(renumber(ref, rank, &n_new));
       if ((total_moves == 0 && n_new == n_comm) || n_new == cur_n) {  // final: labels = P
         compose_kernel<<<grid, 256, 0, s>>>(node_of_cell, n, comm, rank_comm);
-        SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #12 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+        CL_CHECK();
         leiden_done = true;
         break;
       }
       compose_kernel<<<grid, 256, 0, s>>>(node_of_cell, n, ref, rank);
-      SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #13 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      CL_CHECK();
       DevBuf nxt;
       CL_ALLOC(nxt, n_new * 4);
       carry_comm_kernel<<<grid, 256, 0, s>>>(cur_n, ref, comm, rank, rank_comm, (int32_t*)nxt.p);
-      SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #14 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+      CL_CHECK();
       std::swap(carry.p, nxt.p);
       carry.s = s;
       agg = ref;
@@ -521,8 +517,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
     CL_ALLOC(kout, cur_nnz * 8);
     CL_ALLOC(vout, cur_nnz * 8);
     edge_keys_kernel<<<grid, 256, 0, s>>>(cur_ip, cur_nb, cur_n, agg, rank, n_new, (unsigned long long*)kin.p);
-    SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #15 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+    CL_CHECK();
     int end_bit = 1;
     while (end_bit < 64 && ((unsigned long long)n_new * (unsigned long long)n_new) > (1ull << end_bit)) ++end_bit;
     size_t tb1 = 0, tb2 = 0;
@@ -548,8 +543,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
     CL_ALLOC(cnb, nu * 4);
     coarse_csr_kernel<<<grid, 256, 0, s>>>((const unsigned long long*)ukeys.p, nu, n_new, (int64_t*)cip.p,
                                            (int32_t*)cnb.p);
-    SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #16 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+    CL_CHECK();
     // the coarse level becomes current (ownership moves into next_*)
     std::swap(next_ip.p, cip.p);
     std::swap(next_nb.p, cnb.p);
@@ -563,8 +557,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
   }
   if (leiden && !leiden_done && carry.p) {  // max_levels reached: labels = the carried P
     map_kernel<<<grid, 256, 0, s>>>(node_of_cell, n, (const int32_t*)carry.p);
-    SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #17 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+    CL_CHECK();
   }
   // labels by decreasing community size (ties: smallest member), modularity on the input graph
   DevBuf ltot2;
@@ -573,8 +566,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
   SCB_CUDA(cudaMemsetAsync(in_sum, 0, 8, s));
   modularity_kernel<<<grid, 256, 0, s>>>(indptr, indices, (const long long*)W0.p, n, node_of_cell, in_sum,
                                          (unsigned long long*)ltot2.p);
-  SCB_LAUNCH_CHECK();
-    if (dbg) { cudaError_t _e = cudaStreamSynchronize(s); if (_e != cudaSuccess) { fprintf(stderr, "[cluster dbg] after launch #18 (line %d): %s\n", __LINE__, cudaGetErrorString(_e)); return SCB_ERR_CUDA; } }
+  CL_CHECK();
   std::vector<int32_t> h_lab(n);
   std::vector<unsigned long long> h_tot(n);
   unsigned long long h_in = 0, h_m2 = 0;
