@@ -30,7 +30,8 @@ def _params(args):
     from paper_2605_13928_b200.pipeline import Params
     return Params(min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3, target_sum=1e4,
                   n_top_genes=args.hvg, n_bins=20, max_value=10.0, n_comps=50, n_neighbors=args.k,
-                  regress_out=args.regress_out, connectivities=args.graph, umap=args.umap, cluster=args.cluster)
+                  regress_out=args.regress_out, connectivities=args.graph, umap=args.umap, cluster=args.cluster or args.de,
+                  rank_genes=args.de)
 
 
 def _peaks():
@@ -172,6 +173,7 @@ def main():
                     help="also build sc.pp.neighbors' distances/connectivities (umap fuzzy graph) in the step")
     ap.add_argument("--umap", action="store_true", help="also run sc.tl.umap (layout) in the step (1 GPU)")
     ap.add_argument("--cluster", action="store_true", help="also run Leiden clustering on the graph (1 GPU)")
+    ap.add_argument("--de", action="store_true", help="also run Leiden + rank_genes_groups (t-test) (1 GPU)")
     ap.add_argument("--regress-out", action="store_true",
                     help="add sc.pp.regress_out(total_counts, pct_counts_mt) before scale (paper Table 1 step 4)")
     args = ap.parse_args()
@@ -273,7 +275,7 @@ def main():
         if kk in step_ms and step_ms[kk] > 0:
             stages[kk] = {"ms": round(step_ms[kk], 4), "algo_GBps": round(sb[kk] / (step_ms[kk] / 1e3) / 1e9, 1),
                           "frac_hbm": round(sb[kk] / (step_ms[kk] / 1e3) / 1e9 / hbm, 4)}
-    for kk in ("pca", "knn", "graph", "umap", "cluster"):
+    for kk in ("pca", "knn", "graph", "umap", "cluster", "rank_genes"):
         if kk in step_ms:
             stages[kk] = {"ms": round(step_ms[kk], 4)}
     stages["knn"]["candidates_kernel_ms"] = round(knn_ms, 4)
@@ -364,7 +366,7 @@ def main():
             "data": "synthetic NB counts generated on device (oracle/synth.py model, seed %d)" % args.seed,
             "config": {"workload": f"C3: {N} cells x {G} genes (~{Z_total / N / G:.1%} dense), full QC->normalize->"
                                    f"log1p->HVG(seurat,{args.hvg})->{'regress_out+' if args.regress_out else ''}scale->PCA(50)->"
-                                   f"kNN(k={args.k}, exact){'+umap graph' if args.graph or args.umap or args.cluster else ''}{'+umap layout' if args.umap else ''}{'+leiden' if args.cluster else ''}",
+                                   f"kNN(k={args.k}, exact){'+umap graph' if args.graph or args.umap or args.cluster or args.de else ''}{'+umap layout' if args.umap else ''}{'+leiden' if args.cluster or args.de else ''}{'+rank_genes_groups' if args.de else ''}",
                        "cells": N, "genes": G, "nnz": int(Z_total), "kept_cells": int(n_keys), "hvg": H,
                        "parallelism": f"cells sharded x{world}", "l2": "inputs (14 GB) >> L2 (126 MB); no flush needed",
                        "gen_seconds": round(gen_s, 1)},

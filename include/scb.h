@@ -238,6 +238,15 @@ SCB_API int scb_leiden(scb_ctx* ctx, const int64_t* indptr, const int32_t* indic
                int64_t nnz, double resolution, int32_t max_levels, int32_t max_iters, uint32_t seed,
                int32_t* labels, int32_t* n_communities, double* modularity, void* stream);
 
+/* ---- f5 sc.tl.rank_genes_groups(method="t-test", reference="rest") on the log-normalized
+ * kept matrix (CSR, ldata = log1p values) for cell labels 0..n_groups-1 (paper Table 1 step 9).
+ * Outputs [n_groups][n_cols] float64: scores (Welch t), logfoldchanges, pvals, pvals_adj
+ * (Benjamini-Hochberg per group); order int32 [n_groups][n_cols] = gene indices by decreasing
+ * score (ties: smaller index). */
+SCB_API int scb_rank_genes_groups(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* ldata,
+                          int64_t n_rows, int32_t n_cols, const int32_t* labels, int32_t n_groups, double* scores,
+                          double* logfoldchanges, double* pvals, double* pvals_adj, int32_t* order, void* stream);
+
 /* ---- a7: partial Gram matrix C = Z^T Z (float64 [hp][hp], full symmetric) on the
  * 5th-gen tensor cores (tcgen05 kind::f16, "3xBF16": x = hi + lo with hi = bf16(x),
  * lo = bf16(x - hi), products hi*hi + hi*lo + lo*hi, <= 2^-16 relative each; FP32 accumulate

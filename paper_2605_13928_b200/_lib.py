@@ -45,6 +45,8 @@ SIGNATURES = {
                     c_ptr],
     "scb_leiden": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_dbl, c_i32, c_i32, ctypes.c_uint32, c_ptr, c_ptr, c_ptr,
                    c_ptr],
+    "scb_rank_genes_groups": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+                              c_ptr],
     "scb_knn_dist_sum": [c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     "scb_umap_weights": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_fuzzy_union_rows": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_i64, c_i64, c_ptr, c_ptr],

@@ -44,6 +44,7 @@ class Params:
     cluster: bool = False  # also community detection on connectivities (sc.tl.leiden / sc.tl.louvain)
     cluster_method: str = "leiden"
     resolution: float = 1.0
+    rank_genes: bool = False  # also sc.tl.rank_genes_groups(t-test vs rest) over the clusters
     umap_epochs: Optional[int] = None
 
 
@@ -66,6 +67,7 @@ class Result:
     umap: Optional[torch.Tensor] = None
     clusters: Optional[torch.Tensor] = None
     modularity: Optional[float] = None
+    rank_genes: Optional[dict] = None
 
 
 class _Timer:
@@ -184,6 +186,7 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
         ki = kd = None
     graph = emb = labels = None
     q = None
+    n_c = 0
     if with_knn and (p.connectivities or p.umap or p.cluster):
         tm.step("graph")
         graph = pp.neighbors_graph(ki, kd, comm=comm)
@@ -197,6 +200,11 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
             raise NotImplementedError("clustering is single-GPU (it contracts the whole graph)")
         tm.step("cluster")
         fn = pp.leiden if p.cluster_method == "leiden" else pp.louvain
-        labels, _, q = fn(graph.connectivities, resolution=p.resolution)
+        labels, n_c, q = fn(graph.connectivities, resolution=p.resolution)
+    de = None
+    if with_knn and p.cluster and p.rank_genes and n_c >= 2:
+        tm.step("rank_genes")
+        de = pp.rank_genes_groups(X_log, labels, n_c)
     ms = tm.finish()
-    return Result(qc, cm, gm, X_log, hvg_mask, hvg_index, st, sc, res_pca, ki, kd, n_total, ms, graph, emb, labels, q)
+    return Result(qc, cm, gm, X_log, hvg_mask, hvg_index, st, sc, res_pca, ki, kd, n_total, ms, graph, emb, labels, q,
+                  de)

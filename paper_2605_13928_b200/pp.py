@@ -588,3 +588,21 @@ def leiden(connectivities: DeviceCSR, resolution: float = 1.0, max_levels: int =
     aggregation by the refined partition, deterministic (csrc/cluster.cu).  Returns (labels,
     n_communities, modularity)."""
     return louvain(connectivities, resolution, max_levels, max_iters, seed, _fn="scb_leiden")
+
+
+# ----------------------------------------------------------------------------- differential expression
+def rank_genes_groups(X_log: DeviceCSR, labels: torch.Tensor, n_groups: Optional[int] = None) -> dict:
+    """sc.tl.rank_genes_groups(groupby=labels, method="t-test", reference="rest") on the
+    log-normalized kept matrix (csrc/de.cu).  Returns float64 [n_groups][G] scores,
+    logfoldchanges, pvals, pvals_adj and int32 order (gene indices by decreasing score)."""
+    dev = X_log.device
+    K = int(labels.max().item()) + 1 if n_groups is None else int(n_groups)
+    G = X_log.n_cols
+    out = {k: torch.empty((K, G), dtype=torch.float64, device=dev)
+           for k in ("scores", "logfoldchanges", "pvals", "pvals_adj")}
+    out["order"] = torch.empty((K, G), dtype=torch.int32, device=dev)
+    lab = labels.to(device=dev, dtype=torch.int32).contiguous()
+    _lib.call("scb_rank_genes_groups", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
+              X_log.n_rows, G, _p(lab), K, _p(out["scores"]), _p(out["logfoldchanges"]), _p(out["pvals"]),
+              _p(out["pvals_adj"]), _p(out["order"]), _stream(dev))
+    return out
