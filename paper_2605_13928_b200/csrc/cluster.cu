@@ -354,6 +354,7 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
               "scb_louvain/scb_leiden: null argument");
   SCB_REQUIRE(n > 0 && n < INT32_MAX && max_levels >= 1 && max_iters >= 1, SCB_ERR_ARG,
               "scb_louvain/scb_leiden: bad arguments");
+  SCB_REQUIRE(nnz > 0, SCB_ERR_ARG, "scb_louvain/scb_leiden: the graph has no edges");
   cudaStream_t s = (cudaStream_t)stream;
   const int grid = ctx->num_sms * 8;
   const bool dbg = getenv("SCB_CLUSTER_DEBUG") != nullptr;
