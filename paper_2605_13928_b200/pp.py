@@ -566,20 +566,22 @@ def umap_layout(connectivities: DeviceCSR, init: torch.Tensor, n_epochs: Optiona
 
 
 # ----------------------------------------------------------------------------- clustering
-def louvain(connectivities: DeviceCSR, resolution: float = 1.0, max_levels: int = 10, max_iters: int = 10,
-            seed: int = 0, _fn: str = "scb_louvain"):
-    """Community detection on the neighbors graph (sc.tl.louvain), deterministic
-    (csrc/cluster.cu).  Returns (labels int32 [N] ordered by decreasing community size,
-    n_communities, modularity)."""
+def _cluster(fn: str, G: DeviceCSR, resolution: float, max_levels: int, max_iters: int, seed: int):
     import ctypes
-    G = connectivities
     lab = torch.empty(G.n_rows, dtype=torch.int32, device=G.data.device)
     nc = ctypes.c_int32(0)
     q = ctypes.c_double(0.0)
-    _lib.call(_fn, _ctx(G.data), _p(G.indptr), _p(G.indices), _p(G.data), G.n_rows, int(G.data.numel()),
+    _lib.call(fn, _ctx(G.data), _p(G.indptr), _p(G.indices), _p(G.data), G.n_rows, int(G.data.numel()),
               float(resolution), int(max_levels), int(max_iters), int(seed) & 0xFFFFFFFF, _p(lab),
               ctypes.addressof(nc), ctypes.addressof(q), _stream(G.data.device))
     return lab, int(nc.value), float(q.value)
+
+
+def louvain(connectivities: DeviceCSR, resolution: float = 1.0, max_levels: int = 10, max_iters: int = 10,
+            seed: int = 0):
+    """sc.tl.louvain(resolution) on the neighbors graph, deterministic (csrc/cluster.cu).  Returns
+    (labels int32 [N] ordered by decreasing community size, n_communities, modularity)."""
+    return _cluster("scb_louvain", connectivities, resolution, max_levels, max_iters, seed)
 
 
 def leiden(connectivities: DeviceCSR, resolution: float = 1.0, max_levels: int = 10, max_iters: int = 10,
@@ -587,7 +589,7 @@ def leiden(connectivities: DeviceCSR, resolution: float = 1.0, max_levels: int =
     """sc.tl.leiden(resolution): local moving, refinement (well-connected sub-communities) and
     aggregation by the refined partition, deterministic (csrc/cluster.cu).  Returns (labels,
     n_communities, modularity)."""
-    return louvain(connectivities, resolution, max_levels, max_iters, seed, _fn="scb_leiden")
+    return _cluster("scb_leiden", connectivities, resolution, max_levels, max_iters, seed)
 
 
 # ----------------------------------------------------------------------------- differential expression
