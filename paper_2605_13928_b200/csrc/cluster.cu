@@ -9,8 +9,10 @@
 //   moving    nodes are split into 8 hash buckets; per bucket, a warp per node accumulates its
 //             links to neighbouring communities in a shared-memory hash table and picks
 //             argmax_c  w_ic - gamma k_i tot_c / 2m  (tot_a excludes the node itself; ties ->
-//             smaller c; moves only on a strict gain), then the bucket's moves are applied
-//             (int64 atomics on tot); repeated until no node moves (or max_iters);
+//             smaller c; moves only on a strict gain; a node that moved in the previous
+//             iteration sits one out, which removes the 2-cycles synchronous moves produce), then
+//             the bucket's moves are applied (int64 atomics on tot); repeated until no node moves
+//             (or max_iters);
 //   aggregate communities are renumbered and the graph is contracted: (c_i, c_j) keys radix-
 //             sorted (CUB) and reduced by key into the next level's CSR (self loops keep the
 //             internal weight).
@@ -65,7 +67,8 @@ __global__ void __launch_bounds__(kClWarps * 32)
 move_decide_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ nbr, const long long* __restrict__ W,
                    int64_t n, const long long* __restrict__ k, const int32_t* __restrict__ comm,
                    const unsigned long long* __restrict__ tot, const unsigned long long* __restrict__ m2p,
-                   double gamma, int bucket, uint32_t seed, int32_t* __restrict__ newc) {
+                   double gamma, int bucket, uint32_t seed, const int32_t* __restrict__ last, int iter,
+                   int32_t* __restrict__ newc) {
   extern __shared__ unsigned char cl_smem[];
   const int wid = warp_id(), lane = lane_id();
   int* keys = reinterpret_cast<int*>(cl_smem) + wid * kTab;
@@ -75,6 +78,10 @@ move_decide_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
   for (int64_t i = (int64_t)blockIdx.x * kClWarps + wid; i < n; i += (int64_t)gridDim.x * kClWarps) {
     if ((int)(mix32((uint32_t)i ^ seed) % kBuckets) != bucket) continue;
     const int a = comm[i];
+    if (last[i] == iter - 1) {  // moved in the previous iteration: sits this one out (no 2-cycles)
+      if (lane == 0) newc[i] = a;
+      continue;
+    }
     const long long ki = k[i];
     for (int t = lane; t < kTab; t += 32) { keys[t] = -1; vals[t] = 0ull; }
     __syncwarp();
@@ -133,7 +140,8 @@ move_decide_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
 
 __global__ void move_apply_kernel(int64_t n, const long long* __restrict__ k, int32_t* __restrict__ comm,
                                   const int32_t* __restrict__ newc, unsigned long long* __restrict__ tot, int bucket,
-                                  uint32_t seed, unsigned long long* __restrict__ moved) {
+                                  uint32_t seed, int32_t* __restrict__ last, int iter,
+                                  unsigned long long* __restrict__ moved) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if ((int)(mix32((uint32_t)i ^ seed) % kBuckets) != bucket) continue;
     const int a = comm[i], c = newc[i];
@@ -141,6 +149,7 @@ __global__ void move_apply_kernel(int64_t n, const long long* __restrict__ k, in
     atomicAdd(&tot[c], (unsigned long long)k[i]);
     atomicAdd(&tot[a], (unsigned long long)(-k[i]));
     comm[i] = c;
+    last[i] = iter;
     atomicAdd(moved, 1ull);
   }
 }
@@ -418,14 +427,18 @@ static int cluster_impl(scb_ctx* ctx, const int64_t* indptr, const int32_t* indi
       init_tot_kernel<<<grid, 256, 0, s>>>(comm, k, cur_n, tot);
       CL_CHECK();
     }
+    DevBuf llast;
+    CL_ALLOC(llast, cur_n * 4);
+    int32_t* last = (int32_t*)llast.p;
+    SCB_CUDA(cudaMemsetAsync(last, 0xFE, cur_n * 4, s));  // 0xFEFEFEFE: "never moved"
     unsigned long long total_moves = 0;
     for (int it = 0; it < max_iters; ++it) {
       SCB_CUDA(cudaMemsetAsync(moved, 0, 8, s));
       for (int b = 0; b < kBuckets; ++b) {
         move_decide_kernel<<<ctx->num_sms * 4, kClWarps * 32, cl_smem, s>>>(cur_ip, cur_nb, cur_W, cur_n, k, comm, tot,
-                                                                             m2, resolution, b, seed, newc);
+                                                                             m2, resolution, b, seed, last, it, newc);
         CL_CHECK();
-        move_apply_kernel<<<grid, 256, 0, s>>>(cur_n, k, comm, newc, tot, b, seed, moved);
+        move_apply_kernel<<<grid, 256, 0, s>>>(cur_n, k, comm, newc, tot, b, seed, last, it, moved);
         CL_CHECK();
       }
       unsigned long long mv = 0;
