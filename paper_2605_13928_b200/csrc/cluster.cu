@@ -30,7 +30,7 @@
 
 namespace scb {
 
-constexpr int kTab = 1024;      // hash slots per warp
+constexpr int kTab = 512;       // hash slots per warp (48 KB per 8-warp CTA: 4 CTAs per SM)
 constexpr int kClWarps = 8;     // warps per CTA in the moving kernel
 constexpr int kBuckets = 8;
 
