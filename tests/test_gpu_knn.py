@@ -67,3 +67,20 @@ def test_knn_sharded_queries():
     full_i, _ = pp.neighbors(Xd, 15, n_comps=50)
     part_i, _ = pp.neighbors(Xd[1000:1700], 15, n_comps=50, keys=Xd)
     np.testing.assert_array_equal(part_i.cpu().numpy(), full_i.cpu().numpy()[1000:1700])
+
+
+@pytest.mark.parametrize("n,d,k", [(15, 1, 15), (128, 62, 15), (129, 3, 15), (255, 50, 15), (256, 50, 15),
+                                   (257, 50, 15), (384, 62, 64)])
+def test_knn_tile_boundaries_and_widths(n, d, k):
+    """Row counts around the 128-row query/key tiles and the 256-row query pairs (padding keys in
+    the last tile, a pair whose second tile is empty), the narrowest and widest embeddings
+    (d = 1, d = 62 = 64 - 2 augmented columns), k = n and the largest k."""
+    import torch
+    from paper_2605_13928_b200 import pp
+    rng = np.random.default_rng(1000 * n + d)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    ref_i, ref_d = op.knn(X, k)
+    idx, dist = pp.neighbors(torch.as_tensor(_pad(X)).cuda(), k, n_comps=d)
+    idx, dist = idx.cpu().numpy(), dist.cpu().numpy()
+    assert op.knn_recall(idx, ref_i) >= 0.999
+    np.testing.assert_allclose(dist, ref_d, rtol=1e-4, atol=1e-4)
