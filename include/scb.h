@@ -148,10 +148,12 @@ SCB_API int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t
 
 /* ---- a5: sc.pp.highly_variable_genes(flavor="seurat", n_top_genes, n_bins) from the
  * (all-reduced) gene sums.  Outputs per gene: means, variances, dispersions (log),
- * dispersions_norm, mean_bin; hvg_mask; hvg_index = sorted selected genes (int32[n_top]).
- * n_selected (device int32) = min(n_top, #genes with finite dispersions_norm). */
+ * dispersions_norm, mean_bin; hvg_mask; hvg_index = sorted selected genes (int32[n_cols]
+ * capacity).  ties = 1 (Scanpy): every gene with dispersions_norm >= the n_top-th largest
+ * finite value (more than n_top only on exact ties); ties = 0: exactly min(n_top, #finite),
+ * ties at the cutoff taken in gene-index order.  n_selected (device int32) = count. */
 SCB_API int scb_hvg_select(scb_ctx* ctx, const uint64_t* sums, int32_t n_cols, int64_t n_cells,
-                   int32_t n_top, int32_t n_bins, double* means, double* variances,
+                   int32_t n_top, int32_t n_bins, int32_t ties, double* means, double* variances,
                    double* dispersions, double* dispersions_norm, int32_t* mean_bin,
                    uint8_t* hvg_mask, int32_t* hvg_index, int32_t* n_selected, void* stream);
 
@@ -166,12 +168,14 @@ SCB_API int scb_scale_finalize(scb_ctx* ctx, const uint64_t* sums, int32_t n_slo
                        double* mean, double* inv_std, void* stream);
 
 /* ---- a6: sc.pp.scale(max_value) of the HVG columns into a dense row-major float32
- * matrix Z[n_rows][ldz]: column j < n_slots = min((l - mean)*inv_std, max_value);
+ * matrix Z[n_rows][ldz]: column j < n_slots = float(max(min((l - mean)*inv_std, max_value),
+ * min_value)) in fp64 (min_value = -max_value: Scanpy >= 1.10 / rapids-singlecell zero_center
+ * clip; -inf: upper clip only, Scanpy <= 1.9);
  * column ones_col (if >= 0) = 1.0; other columns up to ldz = 0. */
 SCB_API int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
                     const float* logdata, int64_t n_rows, int32_t n_cols, const int32_t* gene_slot,
                     int32_t n_slots, const double* mean, const double* inv_std, double max_value,
-                    float* Z, int64_t ldz, int32_t ones_col, void* stream);
+                    double min_value, float* Z, int64_t ldz, int32_t ones_col, void* stream);
 
 /* ---- f2 (optional, paper Table 1 step 4): sc.pp.regress_out(["total_counts",
  * "pct_counts_mt"]) fused with scale.  Replaces scale_gene_sums/finalize:
@@ -181,7 +185,7 @@ SCB_API int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* 
  *   3. scb_scale_dense with mean = 0, inv_std = 1, max_value = +inf -> Z holds l (dense);
  *   4. scb_regress_xty: xty[4][H] += {Σl, Σa1·l, Σa2·l, Σl²} per gene (all-reduced);
  *   5. scb_regress_finalize: beta[3][H] (OLS) and inv_std[H] of the residuals;
- *   6. scb_regress_apply: Z[:, :H] = min((l - beta0 - a1 beta1 - a2 beta2) * inv_std, max). */
+ *   6. scb_regress_apply: Z[:, :H] = clip((l - beta0 - a1 beta1 - a2 beta2) * inv_std, min, max). */
 SCB_API int scb_regress_cov_sums(scb_ctx* ctx, const double* total_counts, const double* pct_counts_mt,
                          const uint8_t* cell_mask, int64_t n_rows, double* sums6, void* stream);
 SCB_API int scb_regress_design(scb_ctx* ctx, const double* total_counts, const double* pct_counts_mt,
@@ -193,7 +197,7 @@ SCB_API int scb_regress_finalize(scb_ctx* ctx, const double* xty, const double* 
                          double* beta, double* inv_std, void* stream);
 SCB_API int scb_regress_apply(scb_ctx* ctx, float* Z, int64_t n_rows, int64_t ld, int32_t n_slots,
                       const double* design, const double* beta, const double* inv_std, double max_value,
-                      void* stream);
+                      double min_value, void* stream);
 
 /* ---- f3 sc.pp.neighbors graph outputs (umap-learn fuzzy_simplicial_set on the exact kNN,
  * set_op_mix_ratio 1, local_connectivity 1).  knn_idx/knn_dist are [rows][k] as returned by
@@ -296,16 +300,20 @@ SCB_API int scb_knn_timed(scb_ctx* ctx, const float* queries, int64_t n_queries,
                           int32_t d, int32_t ld, int32_t k, int32_t k_cand, int32_t* knn_index, float* knn_dist,
                           void* stream, void* ev_start, void* ev_end);
 
-/* ---- synthetic negative-binomial counts (oracle/synth.py specification), on device.
- * Rows [row0, row0+n_rows) of the matrix.  log mean of entry (c, g) =
- * log_s[c] + log_mu[g] + A[cell_type[c]][g] + Lf[c][g] where Lf = U B is the low-rank
- * factor term (float32 [n_rows][n_genes], computed by the caller).  Pass 1 (indptr ==
+/* ---- synthetic negative-binomial counts (oracle/synth.py specification, generator v2), on
+ * device; bit-identical to the CPU generator (fixed-order correctly rounded fp64 only).
+ * scb_synth_logmean: logmean[c][g] = (log_s[c] + log_mu[g]) + L, L = A[cell_type[c]][g], then
+ * L += U[c][r] * B[r][g] for r = 0..n_factors-1 (U f64 [n_rows][n_factors], B f64
+ * [n_factors][n_genes], n_factors <= 64).
+ * scb_synth_rows: rows [row0, row0+n_rows) given their logmean rows.  Pass 1 (indptr ==
  * NULL) writes nnz per row into row_nnz; pass 2 fills indices/data of a CSR whose indptr
  * (absolute offsets for these rows) the caller built from row_nnz. */
+SCB_API int scb_synth_logmean(scb_ctx* ctx, int64_t n_rows, int32_t n_genes, int32_t n_factors, const double* log_mu,
+                              const double* A, const int32_t* cell_type, const double* log_s, const double* U,
+                              const double* B, double* logmean, void* stream);
 SCB_API int scb_synth_rows(scb_ctx* ctx, uint64_t seed, int64_t row0, int64_t n_rows, int32_t n_genes,
-                           const double* log_mu, const double* A, const int32_t* cell_type, const double* log_s,
-                           const float* Lf, const int64_t* indptr, int64_t* row_nnz, int32_t* indices, float* data,
-                           void* stream);
+                           const double* logmean, const int64_t* indptr, int64_t* row_nnz, int32_t* indices,
+                           float* data, void* stream);
 
 #ifdef __cplusplus
 }

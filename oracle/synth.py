@@ -3,8 +3,11 @@
 This module is test/bench infrastructure: only ``tests/``, ``__graft_entry__.smoke()``
 and ``bench.py``'s CPU-baseline leg may import it.  The product path generates the
 same matrix on the GPU (``paper_2605_13928_b200/csrc/synth.cu``); both follow the
-one specification below, so a C1-sized matrix generated here and on the device is
-identical entry for entry (fp64 arithmetic, no FMA contraction in the sampler).
+one specification below and use only correctly rounded IEEE-754 fp64 operations
+(+, -, *, /, sqrt, rint, ldexp) in a fixed order for every per-entry quantity, so a
+matrix generated here and on the device is identical entry for entry.  This is
+checked on the GPU at C1 and on a 16k-row window of the C3 matrix
+(``tests/test_gpu_synth.py``).
 
 The reference (``/root/reference``) ships no data generator: the paper's workload is
 the 1M-cell 10x mouse-brain dataset, which is out of scope
@@ -21,6 +24,15 @@ the 1M-cell 10x mouse-brain dataset, which is out of scope
                       subspace well separated from the Marchenko-Pastur bulk;
 * counts              x_cg ~ NB(mean = s_c mu_g exp(L_cg), theta = 0.5), sampled by
                       inverse CDF from one counter-based uniform per (c, g).
+
+Per-entry arithmetic (generator version 2, identical on both sides):
+  L  = A[t, g]; L = L + U[c, r] * B[r, g] for r = 0..R-1 (each product and sum rounded);
+  x  = (log_s[c] + log_mu[g]) + L;  mu = det_exp(x) (below: Cody-Waite reduction,
+  degree-13 Taylor polynomial by Horner, exact ldexp);
+  p0 = sqrt(theta / (theta + mu))  (= (theta/(theta+mu))^theta for theta = 1/2);
+  nonzero iff u >= p0; value = inverse-CDF recurrence (``nb_inverse_cdf``).
+The per-gene and per-cell tables (log_mu, A, B, type, log_s, U) are computed on the
+host with numpy by both paths from the same formulas.
 
 Every random number is a pure function of (seed, stream, i, j) through the
 splitmix64 finaliser, so the matrix is independent of chunking and thread count.
@@ -123,6 +135,38 @@ def cell_tables(spec: SynthSpec, c0: int, c1: int, cum):
     return ctype, log_s, U
 
 
+# det_exp: exp(x) from correctly rounded fp64 operations only (same sequence in csrc/synth.cu)
+_INV_LN2 = float.fromhex("0x1.71547652b82fep+0")
+_LN2_HI = float.fromhex("0x1.62e42fee00000p-1")
+_LN2_LO = float.fromhex("0x1.a39ef35793c76p-33")
+_EXP_C = [float.fromhex(h) for h in (
+    "0x1.0000000000000p+0", "0x1.0000000000000p+0", "0x1.0000000000000p-1", "0x1.5555555555555p-3",
+    "0x1.5555555555555p-5", "0x1.1111111111111p-7", "0x1.6c16c16c16c17p-10", "0x1.a01a01a01a01ap-13",
+    "0x1.a01a01a01a01ap-16", "0x1.71de3a556c734p-19", "0x1.27e4fb7789f5cp-22", "0x1.ae64567f544e4p-26",
+    "0x1.1eed8eff8d898p-29", "0x1.6124613a86d09p-33")]
+
+
+def det_exp(x):
+    """exp(x) for |x| < 700: k = rint(x/ln2), r = (x - k ln2_hi) - k ln2_lo, Taylor-13 Horner, ldexp(p, k).
+    Relative error ~1 ulp; bit-identical to the device's ``det_exp`` (no FMA contraction there)."""
+    x = np.asarray(x, dtype=np.float64)
+    k = np.rint(x * _INV_LN2)
+    r = (x - k * _LN2_HI) - k * _LN2_LO
+    p = np.full_like(r, _EXP_C[13])
+    for c in _EXP_C[12::-1]:
+        p = p * r
+        p = p + c
+    return np.ldexp(p, k.astype(np.int32))
+
+
+def log_means(A_rows, U, B, log_s, log_mu):
+    """x[c, g] = (log_s[c] + log_mu[g]) + (A[t,g] + sum_r U[c,r] B[r,g]) in the fixed order."""
+    L = np.array(A_rows, dtype=np.float64, copy=True)
+    for r in range(U.shape[1]):
+        L += U[:, r:r + 1] * B[r][None, :]
+    return (log_s[:, None] + log_mu[None, :]) + L
+
+
 def nb_inverse_cdf(mu, u):
     """Smallest k with F_NB(k; mu, theta) > u, evaluated with the same fp64 recurrence the
     CUDA sampler uses (pk *= (k + theta) / (k + 1) * q; F += pk)."""
@@ -144,34 +188,42 @@ def nb_inverse_cdf(mu, u):
     return k
 
 
-def generate_csr(spec: SynthSpec, chunk_cells: int = 2048):
-    """Generate the full CSR (indptr i64[N+1], indices i32[Z], data f32[Z]) on the CPU.
+def _chunk_entries(spec: SynthSpec, c0: int, c1: int, tables):
+    log_mu, A, B, cum = tables
+    G = spec.n_genes
+    g = np.arange(G, dtype=np.uint64)
+    ctype, log_s, U = cell_tables(spec, c0, c1, cum)
+    mu = det_exp(log_means(A[ctype], U, B, log_s, log_mu))
+    c = np.arange(c0, c1, dtype=np.uint64)
+    u = uniform(spec.seed, S_COUNT, c[:, None], g[None, :])
+    p0 = np.sqrt(THETA / (THETA + mu))
+    rows, cols = np.nonzero(u >= p0)
+    vals = nb_inverse_cdf(mu[rows, cols], u[rows, cols])
+    return np.bincount(rows, minlength=c1 - c0), cols.astype(np.int32), vals.astype(np.float32)
+
+
+def generate_csr(spec: SynthSpec, chunk_cells: int = 2048, rows=None, threads: int = 1):
+    """Generate the CSR (indptr i64[n+1], indices i32[Z], data f32[Z]) of rows [r0, r1) (default:
+    all cells) on the CPU; ``threads`` > 1 runs row chunks concurrently (numpy releases the GIL).
 
     Practical up to a few times 1e8 dense entries; larger matrices are generated on the
     device by the product's ``synth`` kernels."""
-    N, G = spec.n_cells, spec.n_genes
-    log_mu, A, B, cum = gene_tables(spec)
-    g = np.arange(G, dtype=np.uint64)
-    ind_parts, dat_parts, nnz = [], [], np.zeros(N, dtype=np.int64)
-    for c0 in range(0, N, chunk_cells):
-        c1 = min(N, c0 + chunk_cells)
-        ctype, log_s, U = cell_tables(spec, c0, c1, cum)
-        L = A[ctype] + U @ B                          # (n, G)
-        mu = np.exp(log_s[:, None] + log_mu[None, :] + L)
-        c = np.arange(c0, c1, dtype=np.uint64)
-        u = uniform(spec.seed, S_COUNT, c[:, None], g[None, :])
-        theta = THETA
-        p0 = np.exp(theta * np.log(theta / (theta + mu)))
-        nzmask = u >= p0
-        rows, cols = np.nonzero(nzmask)
-        vals = nb_inverse_cdf(mu[rows, cols], u[rows, cols])
-        nnz[c0:c1] = np.bincount(rows, minlength=c1 - c0)
-        ind_parts.append(cols.astype(np.int32))
-        dat_parts.append(vals.astype(np.float32))
-    indptr = np.zeros(N + 1, dtype=np.int64)
+    r0, r1 = (0, spec.n_cells) if rows is None else rows
+    tables = gene_tables(spec)
+    starts = list(range(r0, r1, chunk_cells))
+    work = [(c0, min(r1, c0 + chunk_cells)) for c0 in starts]
+    if threads > 1 and len(work) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(threads) as ex:
+            parts = list(ex.map(lambda w: _chunk_entries(spec, w[0], w[1], tables), work))
+    else:
+        parts = [_chunk_entries(spec, a, b, tables) for a, b in work]
+    n = r1 - r0
+    nnz = np.concatenate([p[0] for p in parts]) if parts else np.zeros(0, np.int64)
+    indptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(nnz, out=indptr[1:])
-    indices = np.concatenate(ind_parts) if ind_parts else np.zeros(0, np.int32)
-    data = np.concatenate(dat_parts) if dat_parts else np.zeros(0, np.float32)
+    indices = np.concatenate([p[1] for p in parts]) if parts else np.zeros(0, np.int32)
+    data = np.concatenate([p[2] for p in parts]) if parts else np.zeros(0, np.float32)
     return indptr, indices, data
 
 

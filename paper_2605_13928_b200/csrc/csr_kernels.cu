@@ -694,7 +694,7 @@ hvg_select_kernel(const unsigned long long* __restrict__ sums, int32_t G, int64_
                   int32_t n_bins, double* __restrict__ means, double* __restrict__ vars,
                   double* __restrict__ disp, double* __restrict__ dnorm, int32_t* __restrict__ mbin,
                   uint8_t* __restrict__ mask, int32_t* __restrict__ hvg_index,
-                  int32_t* __restrict__ n_selected, double* __restrict__ mean_log) {
+                  int32_t* __restrict__ n_selected, double* __restrict__ mean_log, int32_t ties) {
   __shared__ double sred[32];
   __shared__ int ired[32];
   __shared__ double edges[kMaxBins + 1];
@@ -858,7 +858,9 @@ hvg_select_kernel(const unsigned long long* __restrict__ sums, int32_t G, int64_
     int before = tie_carry;
     for (int w2 = 0; w2 < warp_id(); ++w2) before += wtie[w2];
     before += __popc(bal & ((1u << lane_id()) - 1u));
-    bool sel = (need_total > 0) && g < G && k != 0ull && (k > thr || (tie && before < take_ties));
+    // ties == 1 (Scanpy): every gene whose disp_norm >= the n-th largest; ties == 0: exactly n,
+    // ties at the cutoff taken in gene-index order
+    bool sel = (need_total > 0) && g < G && k != 0ull && (k > thr || (tie && (ties == 1 || before < take_ties)));
     if (g < G) mask[g] = sel ? 1 : 0;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -890,7 +892,7 @@ hvg_select_kernel(const unsigned long long* __restrict__ sums, int32_t G, int64_
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *n_selected = need_total;
+  if (threadIdx.x == 0) *n_selected = sel_carry;
 }
 
 // ============================================================================ scale
@@ -997,8 +999,8 @@ __global__ void __launch_bounds__(kRowThreads)
 scale_dense_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                    const float* __restrict__ ldata, int64_t n_rows, int32_t n_cols,
                    const int32_t* __restrict__ slot, int32_t H, const double* __restrict__ mean,
-                   const double* __restrict__ inv, double max_value, float* __restrict__ Z, int64_t ldz,
-                   int32_t ones_col) {
+                   const double* __restrict__ inv, double max_value, double min_value, float* __restrict__ Z,
+                   int64_t ldz, int32_t ones_col) {
   const int64_t nnz = indptr[n_rows];
   extern __shared__ float zsm[];                        // background row [ldz]
   int16_t* s_slot = reinterpret_cast<int16_t*>(zsm + ldz);
@@ -1006,7 +1008,7 @@ scale_dense_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
   double* s_inv = s_mean + H;
   for (int j = threadIdx.x; j < ldz; j += blockDim.x) {
     float v = 0.0f;
-    if (j < H) v = (float)fmin(__dmul_rn(__dsub_rn(0.0, mean[j]), inv[j]), max_value);
+    if (j < H) v = (float)fmax(fmin(__dmul_rn(__dsub_rn(0.0, mean[j]), inv[j]), max_value), min_value);
     else if (j == ones_col) v = 1.0f;
     zsm[j] = v;
   }
@@ -1031,7 +1033,7 @@ scale_dense_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
         if (!((q.valid >> k) & 1u)) continue;
         const int j = s_slot[q.g[k]];
         if (j >= 0)
-          zr[j] = (float)fmin(__dmul_rn(__dsub_rn((double)q.x[k], s_mean[j]), s_inv[j]), max_value);
+          zr[j] = (float)fmax(fmin(__dmul_rn(__dsub_rn((double)q.x[k], s_mean[j]), s_inv[j]), max_value), min_value);
       }
     });
     __syncwarp();
@@ -1280,7 +1282,7 @@ extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int3
 }
 
 extern "C" int scb_hvg_select(scb_ctx* ctx, const uint64_t* sums, int32_t n_cols, int64_t n_cells,
-                              int32_t n_top, int32_t n_bins, double* means, double* vars, double* disp,
+                              int32_t n_top, int32_t n_bins, int32_t ties, double* means, double* vars, double* disp,
                               double* dnorm, int32_t* mbin, uint8_t* mask, int32_t* hvg_index,
                               int32_t* n_selected, void* stream) {
   SCB_REQUIRE(ctx && sums && means && vars && disp && dnorm && mbin && mask && hvg_index && n_selected,
@@ -1288,12 +1290,13 @@ extern "C" int scb_hvg_select(scb_ctx* ctx, const uint64_t* sums, int32_t n_cols
   SCB_REQUIRE(n_bins >= 1 && n_bins <= kMaxBins, SCB_ERR_ARG, "scb_hvg_select: n_bins must be in [1, %d]",
               kMaxBins);
   SCB_REQUIRE(n_cells >= 2 && n_cols >= 1 && n_top >= 0, SCB_ERR_ARG, "scb_hvg_select: bad sizes");
+  SCB_REQUIRE(ties == 0 || ties == 1, SCB_ERR_ARG, "scb_hvg_select: ties must be 0 (exactly n_top) or 1 (Scanpy >= cutoff)");
   cudaStream_t s = (cudaStream_t)stream;
   void* ws;
   SCB_TRY(ws_get(ctx, 2, (size_t)n_cols * 8, &ws, s));
   hvg_select_kernel<<<1, kSelThreads, 0, s>>>((const unsigned long long*)sums, n_cols, n_cells, n_top, n_bins,
                                               means, vars, disp, dnorm, mbin, mask, hvg_index, n_selected,
-                                              (double*)ws);
+                                              (double*)ws, ties);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
@@ -1328,7 +1331,7 @@ extern "C" int scb_scale_finalize(scb_ctx* ctx, const uint64_t* sums, int32_t n_
 extern "C" int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
                                const float* ldata, int64_t n_rows, int32_t n_cols, const int32_t* slot,
                                int32_t n_slots, const double* mean, const double* inv_std, double max_value,
-                               float* Z, int64_t ldz, int32_t ones_col, void* stream) {
+                               double min_value, float* Z, int64_t ldz, int32_t ones_col, void* stream) {
   SCB_REQUIRE(ctx && indptr && indices && ldata && slot && mean && inv_std && Z, SCB_ERR_ARG,
               "scb_scale_dense: null argument");
   SCB_REQUIRE(ldz % 4 == 0 && ldz >= n_slots && ones_col < ldz, SCB_ERR_ARG,
@@ -1341,7 +1344,7 @@ extern "C" int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_
   SCB_CUDA(cudaFuncSetAttribute(scale_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int per_sm = std::max(1, std::min(4, (int)(kSmemLimit / (smem + 1024))));
   scale_dense_kernel<<<grid_for(ctx, per_sm), kRowThreads, smem, (cudaStream_t)stream>>>(
-      indptr, indices, ldata, n_rows, n_cols, slot, n_slots, mean, inv_std, max_value, Z, ldz, ones_col);
+      indptr, indices, ldata, n_rows, n_cols, slot, n_slots, mean, inv_std, max_value, min_value, Z, ldz, ones_col);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }

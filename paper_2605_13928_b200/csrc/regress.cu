@@ -15,7 +15,7 @@
 //   xty        Σ l, Σ a1 l, Σ a2 l, Σ l² per gene: per-CTA fp64 column partials over row
 //              blocks (deterministic), reduced in a fixed order            -- reads 4·N·ld B
 //   finalize   beta = G^-1 (Aᵀl), rss = Σl² - betaᵀ(Aᵀl), inv_std = 1/sqrt(rss/(N-1))
-//   apply      z = min((l - beta0 - a1 beta1 - a2 beta2) * inv_std, max_value) in place (fp32)
+//   apply      z = clip((l - beta0 - a1 beta1 - a2 beta2) * inv_std, min_value, max_value) in place (fp32)
 //                                                                         -- 8·N·ld B
 // The residual mean is zero by construction (intercept), so scale's centring is the
 // identity here; the oracle (oracle/pipeline.py: regress_out_scale) uses the same
@@ -178,16 +178,18 @@ __global__ void regress_finalize_kernel(const double* __restrict__ xty, const do
   inv_std[g] = 1.0 / sd;
 }
 
-// in place over columns [0, H) of every row: z = min((l - b0 - a1 b1 - a2 b2) * inv, max).
+// in place over columns [0, H) of every row: z = clip((l - b0 - a1 b1 - a2 b2) * inv, min, max).
 // Thread j of a CTA owns float4 column group j (+ k * blockDim) and keeps its 4 columns'
 // (b0, b1, b2, inv) in registers (fp32: the fit is O(l), its rounding is ~1e-7 of l); CTAs
 // stride over rows, four rows' loads in flight per thread.
 constexpr int kApplyThreads = 512;
 __global__ void __launch_bounds__(kApplyThreads)
 regress_apply_kernel(float* __restrict__ Z, int64_t n_rows, int64_t ld, int32_t H, const double* __restrict__ a,
-                     const double* __restrict__ beta, const double* __restrict__ inv_std, double max_value) {
+                     const double* __restrict__ beta, const double* __restrict__ inv_std, double max_value,
+                     double min_value) {
   const int h4 = (H + 3) >> 2;
   const float mx = (float)fmin(max_value, 3.0e38);
+  const float mn = (float)fmax(min_value, -3.0e38);
   for (int j = threadIdx.x; j < h4; j += blockDim.x) {
     const int c0 = 4 * j;
     float b0[4], b1[4], b2[4], iv[4];
@@ -205,7 +207,7 @@ regress_apply_kernel(float* __restrict__ Z, int64_t n_rows, int64_t ld, int32_t 
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float fit = fmaf(x2, b2[k], fmaf(x1, b1[k], b0[k]));
-        if (k < nk) o[k] = fminf((o[k] - fit) * iv[k], mx);
+        if (k < nk) o[k] = fmaxf(fminf((o[k] - fit) * iv[k], mx), mn);
       }
       v.x = o[0]; v.y = o[1]; v.z = o[2]; v.w = o[3];
     };
@@ -296,13 +298,14 @@ extern "C" int scb_regress_finalize(scb_ctx* ctx, const double* xty, const doubl
 }
 
 extern "C" int scb_regress_apply(scb_ctx* ctx, float* Z, int64_t n_rows, int64_t ld, int32_t H, const double* design,
-                                 const double* beta, const double* inv_std, double max_value, void* stream) {
+                                 const double* beta, const double* inv_std, double max_value, double min_value,
+                                 void* stream) {
   SCB_REQUIRE(ctx && Z && design && beta && inv_std, SCB_ERR_ARG, "scb_regress_apply: null argument");
   SCB_REQUIRE(ld % 4 == 0 && H <= ld && ((uintptr_t)Z & 15) == 0, SCB_ERR_ARG,
               "scb_regress_apply: ld % 4 == 0, H <= ld, 16-byte aligned Z required");
   if (n_rows == 0 || H == 0) return SCB_OK;
   regress_apply_kernel<<<ctx->num_sms * 4, kApplyThreads, 0, (cudaStream_t)stream>>>(Z, n_rows, ld, H, design, beta,
-                                                                                   inv_std, max_value);
+                                                                                   inv_std, max_value, min_value);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }

@@ -35,7 +35,9 @@ class Params:
     target_sum: float = 1e4
     n_top_genes: int = 2000
     n_bins: int = 20
+    hvg_ties: str = "cutoff"  # Scanpy's ">= n-th largest" rule; "rank" = exactly n_top_genes
     max_value: float = 10.0
+    clip: str = "symmetric"  # [-max_value, max_value] (Scanpy >= 1.10, rapids-singlecell); "upper" = Scanpy <= 1.9
     n_comps: int = 50
     n_neighbors: int = 15
     regress_out: bool = False  # sc.pp.regress_out(["total_counts", "pct_counts_mt"]) before scale
@@ -113,7 +115,8 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
     if comm is not None:
         comm.allreduce_(qc["n_cells_by_counts"])
         comm.allreduce_(qc["gene_total_counts"])
-    cm, gm, (nk_local, gk) = pp.filter_masks(qc, p.min_genes, p.max_genes, p.max_pct_mt, p.min_cells)
+    cm, gm, (nk_local, gk) = pp.filter_masks(qc, min_genes=p.min_genes, max_genes=p.max_genes,
+                                             max_pct_mt=p.max_pct_mt, min_cells=p.min_cells)
     n_total = nk_local if comm is None else comm.allreduce_int(nk_local)
 
     # ------------------------------------------------------------------ norm_hvg
@@ -128,7 +131,7 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
                             row_splits=qc["hvg_row_splits"])
     if comm is not None:
         comm.allreduce_(sums)
-    hvg_mask, hvg_index, st = pp.hvg_select(sums, n_total, p.n_top_genes, p.n_bins)
+    hvg_mask, hvg_index, st = pp.hvg_select(sums, n_total, p.n_top_genes, p.n_bins, p.hvg_ties)
     H = int(hvg_index.numel())
     slot = pp.gene_slots(hvg_index, gk)
     ssum = None
@@ -149,14 +152,14 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
         if comm is not None:
             comm.allreduce_(xty)
         beta, inv = pp.regress_finalize(xty, s6)
-        sc = pp.regress_apply(sc, design, beta, inv, p.max_value)
+        sc = pp.regress_apply(sc, design, beta, inv, p.max_value, p.clip)
     else:
         if ssum is None:
             ssum = pp.scale_gene_sums(X_log, slot, H)
         if comm is not None:
             comm.allreduce_(ssum)
         mean, inv = pp.scale_finalize(ssum, n_total)
-        sc = pp.scale_dense(X_log, slot, H, mean, inv, p.max_value)
+        sc = pp.scale_dense(X_log, slot, H, mean, inv, p.max_value, clip=p.clip)
 
     # ------------------------------------------------------------------ pca
     tm.step("pca")

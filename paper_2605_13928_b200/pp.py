@@ -100,9 +100,25 @@ def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor, row_splits: bool =
     return out
 
 
-def filter_masks(qc, min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3):
+def qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor):
+    """SURVEY §8(b2) form of calculate_qc_metrics: returns (cell, gene) -- Scanpy's obs / var
+    metric tables as dicts of device tensors."""
+    q = calculate_qc_metrics(X, mt_mask)
+    cell = {k: q[k] for k in ("n_genes_by_counts", "total_counts", "total_counts_mt", "pct_counts_mt")}
+    gene = {"n_cells_by_counts": q["n_cells_by_counts"], "total_counts": q["gene_total_counts"]}
+    return cell, gene
+
+
+def filter_masks(cell, gene=None, *, min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3):
     """sc.pp.filter_cells(min_genes, max_genes) & pct_counts_mt < max_pct_mt; sc.pp.filter_genes(min_cells).
+    ``filter_masks(cell, gene, ...)`` takes the two tables of ``qc_metrics``; with ``gene`` omitted,
+    ``cell`` is the combined dict of ``calculate_qc_metrics``.
     Returns (cell_mask u8[N], gene_mask u8[G], (n_kept_cells, n_kept_genes))."""
+    if gene is not None:
+        qc = {"n_genes_by_counts": cell["n_genes_by_counts"], "pct_counts_mt": cell["pct_counts_mt"],
+              "n_cells_by_counts": gene["n_cells_by_counts"]}
+    else:
+        qc = cell
     ng = qc["n_genes_by_counts"]
     dev = ng.device
     N, G = ng.numel(), qc["n_cells_by_counts"].numel()
@@ -223,7 +239,14 @@ def hvg_gene_sums(X: DeviceCSR, counts=None, row_scale=None, gene_remap=None, n_
     return sums
 
 
-def hvg_select(sums, n_cells: int, n_top_genes: int, n_bins: int = 20):
+HVG_TIES = {"rank": 0, "cutoff": 1}
+
+
+def hvg_select(sums, n_cells: int, n_top_genes: int, n_bins: int = 20, ties: str = "cutoff"):
+    """Seurat selection from the (all-reduced) gene sums.  ``ties="cutoff"`` is Scanpy's rule
+    (every gene with dispersions_norm >= the n-th largest); ``"rank"`` returns exactly n."""
+    if ties not in HVG_TIES:
+        raise ValueError(f"ties must be one of {sorted(HVG_TIES)}")
     dev = sums.device
     G = sums.shape[-1]
     st = dict(means=torch.empty(G, dtype=torch.float64, device=dev),
@@ -232,9 +255,9 @@ def hvg_select(sums, n_cells: int, n_top_genes: int, n_bins: int = 20):
               dispersions_norm=torch.empty(G, dtype=torch.float64, device=dev),
               mean_bin=torch.empty(G, dtype=torch.int32, device=dev))
     mask = torch.empty(G, dtype=torch.uint8, device=dev)
-    index = torch.empty(max(1, n_top_genes), dtype=torch.int32, device=dev)
+    index = torch.empty(max(1, G), dtype=torch.int32, device=dev)
     nsel = torch.empty(1, dtype=torch.int32, device=dev)
-    _lib.call("scb_hvg_select", _ctx(sums), _p(sums), G, int(n_cells), int(n_top_genes), int(n_bins),
+    _lib.call("scb_hvg_select", _ctx(sums), _p(sums), G, int(n_cells), int(n_top_genes), int(n_bins), HVG_TIES[ties],
               _p(st["means"]), _p(st["variances"]), _p(st["dispersions"]), _p(st["dispersions_norm"]),
               _p(st["mean_bin"]), _p(mask), _p(index), _p(nsel), _stream(dev))
     n = int(nsel.item())
@@ -242,11 +265,16 @@ def hvg_select(sums, n_cells: int, n_top_genes: int, n_bins: int = 20):
     return mask, index[:n], st
 
 
-def highly_variable_genes(X_log: DeviceCSR, n_top_genes: int = 2000, n_bins: int = 20):
+def highly_variable_genes(X_log: DeviceCSR, n_top_genes: int = 2000, n_bins: int = 20, flavor: str = "seurat",
+                          ties: str = "cutoff"):
     """sc.pp.highly_variable_genes(flavor='seurat', n_top_genes, n_bins) on normalize_log1p output.
+    Only the seurat flavour is implemented (cell_ranger / seurat_v3 need a loess fit or the raw
+    counts' median dispersion; they are not on the north-star path).
     Returns (hvg_mask u8[G], hvg_index i32[H] sorted, stats dict)."""
+    if flavor != "seurat":
+        raise NotImplementedError(f"highly_variable_genes: flavor={flavor!r} (only 'seurat' is implemented)")
     sums = hvg_gene_sums(X_log)
-    return hvg_select(sums, X_log.n_rows, n_top_genes, n_bins)
+    return hvg_select(sums, X_log.n_rows, n_top_genes, n_bins, ties)
 
 
 # ----------------------------------------------------------------------------- regress (scale)
@@ -297,24 +325,45 @@ def scale_finalize(sums, n_cells: int):
     return mean, inv
 
 
-def scale_dense(X_log: DeviceCSR, slot, H, mean, inv, max_value=10.0, out=None) -> Scaled:
+CLIPS = ("symmetric", "upper")
+
+
+def clip_min(max_value: float, clip: str) -> float:
+    """Lower clip bound: -max_value for Scanpy >= 1.10 / rapids-singlecell (zero_center=True),
+    -inf for Scanpy <= 1.9 (upper clip only)."""
+    if clip not in CLIPS:
+        raise ValueError(f"clip must be one of {CLIPS}")
+    return -float(max_value) if clip == "symmetric" else float("-inf")
+
+
+def scale_dense(X_log: DeviceCSR, slot, H, mean, inv, max_value=10.0, out=None, clip: str = "symmetric") -> Scaled:
     """Dense clipped z-scores Z[N][ld] (float32) of the HVG columns, plus the ones column."""
     ld = padded_width(H)
     dev = X_log.device
     Z = out if out is not None else torch.empty((X_log.n_rows, ld), dtype=torch.float32, device=dev)
     _lib.call("scb_scale_dense", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
-              X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value), _p(Z), ld, H,
-              _stream(dev))
+              X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value),
+              clip_min(max_value, clip), _p(Z), ld, H, _stream(dev))
     return Scaled(Z, H, H, mean, inv)
 
 
-def scale(X_log: DeviceCSR, hvg_index: torch.Tensor, max_value: float = 10.0) -> Scaled:
-    """sc.pp.scale(adata[:, hvg], max_value) -> dense float32 (zero-centred, unit variance, clipped)."""
+def _hvg_index(X_log: DeviceCSR, hvg: torch.Tensor) -> torch.Tensor:
+    """Accept the HVG mask (bool/uint8 [n_cols]) or the sorted index list."""
+    if hvg.dtype in (torch.bool, torch.uint8) and hvg.numel() == X_log.n_cols:
+        return torch.nonzero(hvg.to(torch.bool)).view(-1).to(torch.int32)
+    return hvg.to(torch.int32)
+
+
+def scale(X_log: DeviceCSR, hvg_mask: torch.Tensor, max_value: float = 10.0, clip: str = "symmetric") -> Scaled:
+    """sc.pp.scale(adata[:, hvg], max_value, zero_center=True) -> dense float32 (zero-centred, unit
+    variance, clipped to [-max_value, max_value]; ``clip="upper"``: Scanpy <= 1.9's upper clip).
+    ``hvg_mask``: uint8/bool mask over the columns (or the sorted HVG index list)."""
+    hvg_index = _hvg_index(X_log, hvg_mask)
     H = int(hvg_index.numel())
     slot = gene_slots(hvg_index, X_log.n_cols)
     sums = scale_gene_sums(X_log, slot, H)
     mean, inv = scale_finalize(sums, X_log.n_rows)
-    return scale_dense(X_log, slot, H, mean, inv, max_value)
+    return scale_dense(X_log, slot, H, mean, inv, max_value, clip=clip)
 
 
 # ----------------------------------------------------------------------------- regress_out
@@ -340,7 +389,7 @@ def regress_dense_log(X_log: DeviceCSR, slot, H: int) -> Scaled:
     dev = X_log.device
     zeros = torch.zeros(H, dtype=torch.float64, device=dev)
     ones = torch.ones(H, dtype=torch.float64, device=dev)
-    return scale_dense(X_log, slot, H, zeros, ones, float("inf"))
+    return scale_dense(X_log, slot, H, zeros, ones, float("inf"), clip="upper")
 
 
 def regress_xty(L: Scaled, design: torch.Tensor, xty=None) -> torch.Tensor:
@@ -359,28 +408,29 @@ def regress_finalize(xty: torch.Tensor, sums6: torch.Tensor):
     return beta, inv
 
 
-def regress_apply(L: Scaled, design, beta, inv, max_value: float = 10.0) -> Scaled:
-    """In place: Z[:, :H] = min((l - fit) * inv_std, max_value); returns the Scaled view
-    (mean 0 -- the residual mean is zero by construction)."""
+def regress_apply(L: Scaled, design, beta, inv, max_value: float = 10.0, clip: str = "symmetric") -> Scaled:
+    """In place: Z[:, :H] = clip((l - fit) * inv_std, -max_value | -inf, max_value); returns the Scaled
+    view (mean 0 -- the residual mean is zero by construction)."""
     _lib.call("scb_regress_apply", _ctx(L.Z), _p(L.Z), L.Z.shape[0], L.ld, L.H, _p(design), _p(beta), _p(inv),
-              float(max_value), _stream(L.Z.device))
+              float(max_value), clip_min(max_value, clip), _stream(L.Z.device))
     L.mean = torch.zeros(L.H, dtype=torch.float64, device=L.Z.device)
     L.inv_std = inv
     return L
 
 
 def regress_out_scale(X_log: DeviceCSR, hvg_index: torch.Tensor, qc: dict, cell_mask: torch.Tensor,
-                      max_value: float = 10.0) -> Scaled:
+                      max_value: float = 10.0, clip: str = "symmetric") -> Scaled:
     """sc.pp.regress_out(adata[:, hvg], ["total_counts", "pct_counts_mt"]) + sc.pp.scale(max_value)
     (paper Table 1 step 4).  ``qc``/``cell_mask`` are the QC metrics and cell mask of the ORIGINAL
     rows; X_log holds the kept rows in order."""
+    hvg_index = _hvg_index(X_log, hvg_index)
     H = int(hvg_index.numel())
     slot = gene_slots(hvg_index, X_log.n_cols)
     s6 = regress_cov_sums(qc, cell_mask)
     design = regress_design(qc, cell_mask, s6, X_log.n_rows)
     L = regress_dense_log(X_log, slot, H)
     beta, inv = regress_finalize(regress_xty(L, design), s6)
-    return regress_apply(L, design, beta, inv, max_value)
+    return regress_apply(L, design, beta, inv, max_value, clip)
 
 
 # ----------------------------------------------------------------------------- pca

@@ -4,9 +4,10 @@ Same model and counter-based randomness as ``oracle/synth.py`` (SURVEY.md §8(d)
 log-means N(-4.1, 1.7) (13 mitochondrial genes raised), cell size factors LogNormal(0, 0.5),
 planted low-rank log-fold-changes (cell types + decaying continuous factors) and NB(theta=0.5)
 counts drawn by inverse CDF from one splitmix64 uniform per (cell, gene).  The per-gene and
-per-cell tables are a few MB and built on the host with numpy; the O(N*G) sampling is the
-``scb_synth_rows`` kernel, and the rank-64 factor term U B is a plain cuBLAS GEMM (torch) per
-row chunk.  Generation is input synthesis, never part of a timed region.
+per-cell tables are a few MB and built on the host with numpy; the O(N*G) work is two kernels
+per row chunk: ``scb_synth_logmean`` (fixed-order fp64 log means, including the rank-64 factor
+term) and ``scb_synth_rows`` (sampling).  Generator v2: bit-identical to oracle/synth.py
+(tests/test_gpu_synth.py).  Generation is input synthesis, never part of a timed region.
 """
 from __future__ import annotations
 
@@ -100,7 +101,7 @@ def generate_rows(spec: Spec, r0: int, r1: int, device="cuda", chunk: int = 1638
     log_mu, A, B, cum = gene_tables(spec)
     d_log_mu = torch.as_tensor(log_mu, device=dev)
     d_A = torch.as_tensor(A, device=dev).contiguous()
-    d_B = torch.as_tensor(B, dtype=torch.float32, device=dev)
+    d_B = torch.as_tensor(B, device=dev).contiguous()
     ctx, s = _ctx(d_log_mu), _stream(dev)
     n = r1 - r0
     nnz = torch.empty(n, dtype=torch.int64, device=dev)
@@ -109,18 +110,25 @@ def generate_rows(spec: Spec, r0: int, r1: int, device="cuda", chunk: int = 1638
         c1 = min(r1, c0 + chunk)
         ct, ls, U = cell_tables(spec, c0, c1, cum)
         tables.append((c0, c1, torch.as_tensor(ct, device=dev), torch.as_tensor(ls, device=dev),
-                       torch.as_tensor(U, dtype=torch.float32, device=dev)))
+                       torch.as_tensor(U, device=dev).contiguous()))
+    xbuf = torch.empty((min(chunk, max(n, 1)), G), dtype=torch.float64, device=dev)
+
+    def logmean(c0, c1, ct, ls, U):
+        _lib.call("scb_synth_logmean", ctx, c1 - c0, G, spec.n_factors, _p(d_log_mu), _p(d_A), _p(ct), _p(ls), _p(U),
+                  _p(d_B), _p(xbuf), s)
+        return xbuf
+
     for (c0, c1, ct, ls, U) in tables:
-        Lf = (U @ d_B).contiguous()
-        _lib.call("scb_synth_rows", ctx, spec.seed, c0, c1 - c0, G, _p(d_log_mu), _p(d_A), _p(ct), _p(ls), _p(Lf), 0,
-                  _p(nnz[c0 - r0:c1 - r0]), 0, 0, s)
+        x = logmean(c0, c1, ct, ls, U)
+        _lib.call("scb_synth_rows", ctx, spec.seed, c0, c1 - c0, G, _p(x), 0, _p(nnz[c0 - r0:c1 - r0]), 0, 0, s)
     indptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     torch.cumsum(nnz, 0, out=indptr[1:])
     Z = int(indptr[-1].item())
     indices = torch.empty(Z, dtype=torch.int32, device=dev)
     data = torch.empty(Z, dtype=torch.float32, device=dev)
     for (c0, c1, ct, ls, U) in tables:
-        Lf = (U @ d_B).contiguous()
-        _lib.call("scb_synth_rows", ctx, spec.seed, c0, c1 - c0, G, _p(d_log_mu), _p(d_A), _p(ct), _p(ls), _p(Lf),
-                  _p(indptr[c0 - r0:c1 - r0]), 0, _p(indices), _p(data), s)
+        x = logmean(c0, c1, ct, ls, U)
+        _lib.call("scb_synth_rows", ctx, spec.seed, c0, c1 - c0, G, _p(x), _p(indptr[c0 - r0:c1 - r0]), 0,
+                  _p(indices), _p(data), s)
+    del xbuf
     return DeviceCSR(indptr, indices, data, G)

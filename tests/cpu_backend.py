@@ -32,7 +32,7 @@ def calculate_qc_metrics(X, mt_mask, row_splits=False):
     return out
 
 
-def filter_masks(qc, min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3):
+def filter_masks(qc, gene=None, *, min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3):
     p = op.Params(min_genes=min_genes, max_genes=max_genes, max_pct_mt=max_pct_mt, min_cells=min_cells)
     cm, gm = op.filter_masks({k: _np(v) for k, v in qc.items() if v is not None}, p)
     return torch.as_tensor(cm), torch.as_tensor(gm), (int(cm.sum()), int(gm.sum()))
@@ -102,9 +102,9 @@ def hvg_gene_sums(X, counts=None, row_scale=None, gene_remap=None, n_out=None, s
     return _limbs(g[keep], y32, n_out, op.FX1, op.FX2)
 
 
-def hvg_select(sums, n_cells, n_top_genes, n_bins=20):
+def hvg_select(sums, n_cells, n_top_genes, n_bins=20, ties="cutoff"):
     s1, s2 = _limb_values(sums, op.FX1, op.FX2)
-    mask, st = op.hvg_seurat_from_sums(s1, s2, n_cells, n_top_genes, n_bins)
+    mask, st = op.hvg_seurat_from_sums(s1, s2, n_cells, n_top_genes, n_bins, ties)
     idx = np.nonzero(mask)[0].astype(np.int32)
     st = {k: torch.as_tensor(v) for k, v in st.items()}
     st["n_selected"] = len(idx)
@@ -127,17 +127,18 @@ def scale_finalize(sums, n_cells):
     return torch.as_tensor(mean), torch.as_tensor(1.0 / std)
 
 
-def scale_dense(X_log, slot, H, mean, inv, max_value=10.0, out=None):
+def scale_dense(X_log, slot, H, mean, inv, max_value=10.0, out=None, clip="symmetric"):
     A = _csr(X_log)
     ld = padded_width(H)
     m, iv = _np(mean), _np(inv)
     Z = np.zeros((A.n_rows, ld), np.float32)
-    Z[:, :H] = np.minimum((0.0 - m) * iv, max_value).astype(np.float32)[None, :]
+    Z[:, :H] = op.clip_z((0.0 - m) * iv, max_value, clip).astype(np.float32)[None, :]
     Z[:, H] = 1.0
     rows = A.row_ids()
     j = _np(slot)[A.indices]
     k = j >= 0
-    Z[rows[k], j[k]] = np.minimum((A.data[k].astype(np.float64) - m[j[k]]) * iv[j[k]], max_value).astype(np.float32)
+    Z[rows[k], j[k]] = op.clip_z((A.data[k].astype(np.float64) - m[j[k]]) * iv[j[k]], max_value,
+                                 clip).astype(np.float32)
     return Scaled(torch.as_tensor(Z), H, H, mean, inv)
 
 
@@ -155,7 +156,7 @@ def regress_design(qc, cell_mask, sums6, n_kept):
 
 def regress_dense_log(X_log, slot, H):
     return scale_dense(X_log, slot, H, torch.zeros(H, dtype=torch.float64), torch.ones(H, dtype=torch.float64),
-                       float("inf"))
+                       float("inf"), clip="upper")
 
 
 def regress_xty(L, design, xty=None):
@@ -182,11 +183,11 @@ def regress_finalize(xty, sums6):
     return torch.as_tensor(np.stack([b0, b1, b2])), torch.as_tensor(1.0 / std)
 
 
-def regress_apply(L, design, beta, inv, max_value=10.0):
+def regress_apply(L, design, beta, inv, max_value=10.0, clip="symmetric"):
     Z = _np(L.Z).copy()
     a, b, iv = _np(design), _np(beta), _np(inv)
     fit = b[0][None, :] + a[0][:, None] * b[1][None, :] + a[1][:, None] * b[2][None, :]
-    Z[:, :L.H] = np.minimum((Z[:, :L.H].astype(np.float64) - fit) * iv[None, :], max_value).astype(np.float32)
+    Z[:, :L.H] = op.clip_z((Z[:, :L.H].astype(np.float64) - fit) * iv[None, :], max_value, clip).astype(np.float32)
     return Scaled(torch.as_tensor(Z), L.H, L.ones_col, torch.zeros(L.H, dtype=torch.float64), inv)
 
 

@@ -19,7 +19,7 @@ def dev_state():
     p = C1["params"]
     Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, X.n_cols)
     qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
-    cm, gm, kept = scb.filter_masks(qc, p.min_genes, p.max_genes, p.max_pct_mt, p.min_cells)
+    cm, gm, kept = scb.filter_masks(qc, min_genes=p.min_genes, max_genes=p.max_genes, max_pct_mt=p.max_pct_mt, min_cells=p.min_cells)
     Xs = scb.subset(Xd, cm, gm, kept)
     Xl = scb.normalize_log1p(Xs, p.target_sum)
     hvg_mask, hvg_index, st = scb.highly_variable_genes(Xl, p.n_top_genes, p.n_bins)
@@ -123,7 +123,7 @@ def test_cpm_normalization_hvg_and_scale_exact():
     o = op.run(X, mt, p, with_knn=False)
     Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, X.n_cols)
     qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
-    cm, gm, kept = scb.filter_masks(qc, p.min_genes, p.max_genes, p.max_pct_mt, p.min_cells)
+    cm, gm, kept = scb.filter_masks(qc, min_genes=p.min_genes, max_genes=p.max_genes, max_pct_mt=p.max_pct_mt, min_cells=p.min_cells)
     Xl = scb.normalize_log1p(scb.subset(Xd, cm, gm, kept), p.target_sum)
     hvg_mask, hvg_index, st = scb.highly_variable_genes(Xl, p.n_top_genes, p.n_bins)
     np.testing.assert_array_equal(hvg_mask.cpu().numpy(), o["hvg_mask"])
@@ -206,7 +206,7 @@ def test_fused_fill_scale_sums_equal_separate_pass():
     p = C1["params"]
     Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, X.n_cols)
     qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
-    cm, gm, kept = scb.filter_masks(qc, p.min_genes, p.max_genes, p.max_pct_mt, p.min_cells)
+    cm, gm, kept = scb.filter_masks(qc, min_genes=p.min_genes, max_genes=p.max_genes, max_pct_mt=p.max_pct_mt, min_cells=p.min_cells)
     _, hvg_index, _ = scb.highly_variable_genes(scb.normalize_log1p(scb.subset(Xd, cm, gm, kept), p.target_sum),
                                                 p.n_top_genes, p.n_bins)
     remap, nip, rs, rso, nnz = pp.subset_count_scale(Xd, cm, gm, kept, p.target_sum)
@@ -227,3 +227,55 @@ def test_fused_fill_scale_sums_equal_separate_pass():
     m1, i1 = pp.scale_finalize(sums, n)
     m2, i2 = pp.scale_finalize(sep, n)
     assert torch.equal(m1, m2) and torch.equal(i1, i2)
+
+
+def test_hvg_tie_rules_gpu_match_oracle():
+    """Both selection rules on the device equal the oracle's, on sums with planted exact ties
+    (every gene has a twin, so the cutoff falls on a tie)."""
+    import torch
+    from oracle import pipeline as op
+    from paper_2605_13928_b200 import pp
+    rng = np.random.default_rng(3)
+    G, N = 600, 1000
+    y = rng.gamma(0.5, 2.0, (N, G // 2)).astype(np.float32) * (rng.random((N, G // 2)) < 0.3)
+    y = np.concatenate([y, y], axis=1)                     # exact twins -> tied statistics
+    import scipy.sparse as sp
+    A = sp.csr_matrix(y)
+    q1 = np.rint(A.data.astype(np.float64) * 2.0 ** op.FX1).astype(np.uint64)
+    q2 = np.rint(A.data.astype(np.float64) ** 2 * 2.0 ** op.FX2).astype(np.uint64)
+    lo1, hi1 = op._fx_sum(A.indices, q1, G)
+    lo2, hi2 = op._fx_sum(A.indices, q2, G)
+    sums = torch.as_tensor(np.stack([np.stack([lo1, hi1]), np.stack([lo2, hi2])]).view(np.int64)).cuda()
+    s1, s2 = op.fx_gene_sums(A.indices, A.data, G)
+    _, st = op.hvg_seurat_from_sums(s1, s2, N, 10)
+    key = np.sort(np.where(np.isnan(st["dispersions_norm"]), -np.inf, st["dispersions_norm"]))[::-1]
+    n = int(np.nonzero(key[:-1] == key[1:])[0][3]) + 1
+    for ties in ("cutoff", "rank"):
+        ref, _ = op.hvg_seurat_from_sums(s1, s2, N, n, ties=ties)
+        mask, idx, dst = pp.hvg_select(sums, N, n, 20, ties)
+        np.testing.assert_array_equal(mask.cpu().numpy(), ref, err_msg=ties)
+        assert dst["n_selected"] == int(ref.sum()) == idx.numel()
+        np.testing.assert_array_equal(idx.cpu().numpy(), np.nonzero(ref)[0])
+    assert int(op.hvg_seurat_from_sums(s1, s2, N, n, ties="cutoff")[0].sum()) > n
+
+
+@pytest.mark.parametrize("clip", ["symmetric", "upper"])
+def test_scale_clip_modes_gpu(dev_state, clip):
+    """scale_dense with both clip modes vs the oracle, at a max_value (2.0) that clips both sides."""
+    import torch
+    from oracle import pipeline as op
+    from paper_2605_13928_b200 import pp
+    o = c1_oracle(False)
+    Xl = dev_state["Xl"]
+    sc = pp.scale(Xl, dev_state["hvg"], 2.0, clip=clip)
+    torch.cuda.synchronize()
+    oXl = o["X_log"]
+    ref, mean, inv = op.scale(oXl, o["hvg_mask"], 2.0, clip=clip)
+    Z = sc.values().cpu().numpy()
+    mag = np.maximum(np.abs(ref), np.abs(mean * inv)[None, :])
+    assert (np.abs(Z - ref) / np.maximum(mag, 1e-30)).max() < 1e-5
+    assert Z.max() <= 2.0
+    if clip == "symmetric":
+        assert Z.min() >= -2.0
+    else:
+        assert Z.min() < -2.0

@@ -18,7 +18,7 @@ def test_rank_genes_groups_matches_oracle():
     P = C1["params"]
     Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, X.n_cols)
     qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
-    cm, gm, kept = scb.filter_masks(qc, P.min_genes, P.max_genes, P.max_pct_mt, P.min_cells)
+    cm, gm, kept = scb.filter_masks(qc, min_genes=P.min_genes, max_genes=P.max_genes, max_pct_mt=P.max_pct_mt, min_cells=P.min_cells)
     Xl = scb.normalize_log1p(scb.subset(Xd, cm, gm, kept), P.target_sum)
     rng = np.random.default_rng(0)
     labels = rng.integers(0, 5, Xl.n_rows).astype(np.int32)

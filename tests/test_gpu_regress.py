@@ -48,7 +48,7 @@ def test_regress_out_scale_step_api_matches_pipeline():
     P = C1["params"]
     Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, X.n_cols)
     qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
-    cm, gm, kept = scb.filter_masks(qc, P.min_genes, P.max_genes, P.max_pct_mt, P.min_cells)
+    cm, gm, kept = scb.filter_masks(qc, min_genes=P.min_genes, max_genes=P.max_genes, max_pct_mt=P.max_pct_mt, min_cells=P.min_cells)
     Xl = scb.normalize_log1p(scb.subset(Xd, cm, gm, kept), P.target_sum)
     _, hvg_index, _ = scb.highly_variable_genes(Xl, P.n_top_genes, P.n_bins)
     sc = scb.regress_out_scale(Xl, hvg_index, qc, cm, P.max_value)

@@ -355,3 +355,81 @@ def test_leiden_oracle_quality_and_connectivity():
     for c in range(nc):
         idx = np.nonzero(labels == c)[0]
         assert cg.connected_components(C[idx][:, idx], directed=False)[0] == 1
+
+
+# ----------------------------------------------------------------------------- Scanpy float pin
+def _c1_scanpy_vs_fixed_point(spec, n_top, min_genes, max_pct_mt):
+    from oracle import scanpy_float as sf
+    ip, ix, d = generate_csr(spec, threads=8)
+    X = op.CSR(ip, ix, d, spec.n_genes)
+    p = op.Params(min_genes=min_genes, max_pct_mt=max_pct_mt, n_top_genes=n_top)
+    o = op.run(X, mt_mask(spec), p, with_knn=False)
+    Xl = o["X_log"]
+    sel, dn = sf.hvg_seurat_expm1(Xl.indices, Xl.data, Xl.n_rows, Xl.n_cols, n_top)
+    return o, sel, dn
+
+
+def test_hvg_fixed_point_set_equals_scanpy_float64_expm1_c1():
+    """The fixed-point HVG statistics (device arithmetic) select exactly the gene set that
+    Scanpy's float64 mean/var of expm1(X_log) selects, at C1 (10k x 2k, H = 1000)."""
+    o, sel, dn = _c1_scanpy_vs_fixed_point(SynthSpec(10000, 2000, seed=1), 1000, 50, 15.0)
+    flips = np.nonzero(o["hvg_mask"].astype(bool) != sel)[0]
+    assert flips.size == 0, f"HVG set differs from Scanpy's float path at genes {flips.tolist()}"
+    # the normalised dispersions agree to ~1e-6 relative (expm1(log1p(y)) vs y rounding)
+    st = o["hvg_stats"]["dispersions_norm"]
+    ok = ~np.isnan(st)
+    np.testing.assert_allclose(st[ok], dn[ok], rtol=1e-5, atol=1e-6)
+
+
+def test_hvg_tie_rules():
+    """'cutoff' (Scanpy) keeps every gene tied at the n-th value; 'rank' keeps exactly n by index."""
+    rng = np.random.default_rng(3)
+    G = 400
+    mean = rng.uniform(0.1, 2.0, G)
+    var = mean * np.exp(rng.normal(0, 0.5, G))
+    s1, s2 = mean * 1000.0, (var * 999.0 / 1000.0 + mean * mean) * 1000.0
+    s1[200:], s2[200:] = s1[:200], s2[:200]          # every gene has an exact twin
+    _, st = op.hvg_seurat_from_sums(s1, s2, 1000, 10)
+    key = np.where(np.isnan(st["dispersions_norm"]), -np.inf, st["dispersions_norm"])
+    srt = np.sort(key)[::-1]
+    i = int(np.nonzero(srt[:-1] == srt[1:])[0][5])     # a tie inside the ranking
+    n = i + 1                                           # n-th largest value is tied with the (n+1)-th
+    m_cut, _ = op.hvg_seurat_from_sums(s1, s2, 1000, n, ties="cutoff")
+    m_rank, _ = op.hvg_seurat_from_sums(s1, s2, 1000, n, ties="rank")
+    assert m_rank.sum() == n
+    assert m_cut.sum() == int((key >= srt[n - 1]).sum()) > n
+    assert np.all(m_cut >= m_rank)
+    tied = np.nonzero(key == srt[n - 1])[0]
+    assert m_rank[tied].sum() == n - int((key > srt[n - 1]).sum()) and m_rank[tied.min()]
+
+
+def test_scale_clip_modes():
+    ip = np.array([0, 2, 3, 3], np.int64)
+    ix = np.array([0, 1, 0], np.int32)
+    l = np.array([5.0, 0.1, 0.2], np.float32)
+    Xl = op.CSR(ip, ix, l, 2)
+    mask = np.array([1, 1], np.uint8)
+    Zs, mean, inv = op.scale(Xl, mask, max_value=0.5, clip="symmetric")
+    Zu, _, _ = op.scale(Xl, mask, max_value=0.5, clip="upper")
+    assert Zs.max() <= 0.5 and Zs.min() >= -0.5
+    assert Zu.max() <= 0.5 and Zu.min() < -0.5
+    np.testing.assert_array_equal(Zs, np.maximum(Zu, np.float32(-0.5)))
+
+
+def test_chunked_oracle_equals_unchunked():
+    """oracle/chunked.py (row chunks in forked workers, 128-bit limb sums) reproduces
+    pipeline.run stage by stage: the driver of the full-size (C3) parity test."""
+    from oracle import chunked
+    spec = SynthSpec(3000, 800, seed=9)
+    ip, ix, d = generate_csr(spec)
+    p = op.Params(min_genes=20, max_pct_mt=15.0, n_top_genes=300, n_comps=20, n_neighbors=10)
+    ref = op.run(op.CSR(ip, ix, d, spec.n_genes), mt_mask(spec), p)
+    q = np.arange(0, ref["X_pca"].shape[0], 7)
+    got = chunked.run(ip, ix, d, spec.n_genes, mt_mask(spec), p, workers=3, chunk_rows=700, knn_queries=q)
+    for k, v in ref["qc"].items():
+        np.testing.assert_array_equal(got["qc"][k], v, err_msg=k)
+    for k in ("cell_mask", "gene_mask", "hvg_mask", "scale_mean", "scale_inv_std"):
+        np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+    assert op.subspace_angle(got["components"], ref["components"]) < 1e-7
+    np.testing.assert_allclose(got["variance"], ref["variance"], rtol=1e-10)
+    np.testing.assert_array_equal(got["knn_idx"], ref["knn_idx"][q])
