@@ -10,6 +10,7 @@
 // term is <= 2^-16 relative) at the BF16 tensor rate (twice TF32's), accumulating in TMEM.
 // Only tiles touching the upper triangle are computed; split-K over cells fills the 148 SMs,
 // and a deterministic reduce kernel sums the K-slices in fp64 and mirrors the result.
+#include <cstdlib>
 #include <vector>
 #include <cuda_bf16.h>
 #include "tc_common.cuh"
@@ -213,10 +214,19 @@ split_bf16_kernel(const float4* __restrict__ Z, int64_t n4, uint2* __restrict__ 
   }
 }
 
-// ---- variant fed by pre-split BF16 planes (written by scb_scale_dense_split): no converter
-// warps and no fp32 staging -- TMA brings the hi and lo boxes straight into the MN-major
+// ---- variant fed by pre-split BF16 planes (written by scb_split_bf16): no converter warps
+// and no fp32 staging -- TMA brings the hi and lo boxes straight into the MN-major
 // 128-byte-swizzled operand layout, so shared memory carries only the TMA writes and the MMA
 // operand reads (the fp32 variant is bound by the converter's extra smem traffic).
+//
+// Accumulation precision: tcgen05's FP32 accumulate truncates (~2.4 ulp lost per MMA,
+// measured), a bias that grows with the number of MMAs folded into one accumulator -- with
+// 4096 cells per accumulator it was the whole PCA error (C2 subspace angle 2.2e-4; an fp64
+// Gram of the same Z gives 4.7e-8, tools/pca_precision.py).  So each accumulator restarts
+// every kDrainStages stages (256 cells, 48 MMAs): eight epilogue warps drain it (tcgen05.ld)
+// into round-to-nearest fp32 running sums held in registers (each thread one row x 128
+// columns) while the other accumulator keeps the tensor pipe busy, and only the running sums
+// of a long K-slice are written out.
 template <int BN>
 struct GramSplitCfg {
   static constexpr int BM = 128;
@@ -227,8 +237,11 @@ struct GramSplitCfg {
   static constexpr int STAGES = 4;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
   static constexpr uint32_t IDESC = tc::idesc_bf16(BM, BN, true, true);
+  static constexpr int EPI_WARPS = 8;                 // 2 per TMEM lane quarter, BN/2 columns each
+  static constexpr int COLS = BN / 2;
 };
-constexpr int kGramSplitThreads = 32 * 7;  // warp0 TMA, warps 1-2 MMA, warps 3..6 epilogue
+constexpr int kDrainStages = 8;            // stages per accumulator between drains (256 cells)
+constexpr int kGramSplitThreads = 32 * 11;  // warp0 TMA, warps 1-2 MMA, warps 3..10 epilogue
 
 template <int BN>
 __global__ void __launch_bounds__(kGramSplitThreads, 1)
@@ -240,8 +253,9 @@ gram_split_kernel(const __grid_constant__ CUtensorMap thi, const __grid_constant
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* done = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* acc_full = empty + C::STAGES;   // [2]: sub-slice complete in accumulator p
+  uint64_t* acc_empty = acc_full + 2;       // [2]: accumulator p drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = warp_id(), lane = lane_id();
   const int tile = blockIdx.x % n_tiles;
@@ -260,7 +274,10 @@ gram_split_kernel(const __grid_constant__ CUtensorMap thi, const __grid_constant
         tc::mbar_init(&full[s], 1);
         tc::mbar_init(&empty[s], 1);
       }
-      tc::mbar_init(done, 2);
+      for (int p = 0; p < 2; ++p) {
+        tc::mbar_init(&acc_full[p], 1);
+        tc::mbar_init(&acc_empty[p], C::EPI_WARPS);
+      }
       tc::fence_barrier_init();
     }
     __syncwarp();
@@ -293,10 +310,18 @@ gram_split_kernel(const __grid_constant__ CUtensorMap thi, const __grid_constant
       }
     }
   } else if (warp <= 2) {
-    const int p = warp - 1;  // stage parity: two issuers into two accumulators (see gram_kernel)
+    // issuer p feeds accumulator p with the stages of parity p (a tcgen05.commit stalls its
+    // issuing thread until the pipe drains, so two issuers keep the tensor pipe busy)
+    const int p = warp - 1;
     if (lane == 0) {
       const uint32_t acc = tmem + p * BN;
-      for (int it = p; it < num_kb; it += 2) {
+      const int n_mine = (num_kb - p + 1) / 2;
+      for (int j = 0; j < n_mine; ++j) {
+        const int it = p + 2 * j;
+        const int u = j / kDrainStages;          // sub-slice of this accumulator
+        const bool first = (j % kDrainStages) == 0;
+        const bool last = (j % kDrainStages) == kDrainStages - 1 || j == n_mine - 1;
+        if (first) tc::mbar_wait(&acc_empty[p], (u & 1) ^ 1);
         const int s = it % C::STAGES;
         tc::mbar_wait(&full[s], (it / C::STAGES) & 1);
         tc::tc_fence_after();
@@ -311,34 +336,45 @@ gram_split_kernel(const __grid_constant__ CUtensorMap thi, const __grid_constant
           const uint64_t dbh = tc::smem_desc_sw128(bh + ko, C::BOX, 1024);
           const uint64_t dal = tc::smem_desc_sw128(al + ko, C::BOX, 1024);
           const uint64_t dbl = tc::smem_desc_sw128(bl + ko, C::BOX, 1024);
-          tc::mma_f16(acc, dah, dbh, C::IDESC, (it > p || kk > 0) ? 1u : 0u);
+          tc::mma_f16(acc, dah, dbh, C::IDESC, (first && kk == 0) ? 0u : 1u);
           tc::mma_f16(acc, dah, dbl, C::IDESC, 1u);
           tc::mma_f16(acc, dal, dbh, C::IDESC, 1u);
         }
         tc::mma_commit(&empty[s]);
+        if (last) tc::mma_commit(&acc_full[p]);
       }
-      tc::mma_commit(done);
     }
   } else {
-    tc::mbar_wait(done, 0);
-    tc::tc_fence_after();
-    const int q = warp & 3;
+    const int e = warp - 3;        // 0..7
+    const int q = warp & 3;        // TMEM lane quarter this warp may access
+    const int h = e >> 2;          // column half
     const int row = i0 + 32 * q + lane;
-    float* out = partial + (size_t)slice * hp * hp + (size_t)row * hp + j0;
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      uint32_t r0[32], r1[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + c * 32, r0);
-      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + BN + c * 32, r1);
-      tc::tmem_ld_wait();
-      float v[32];
+    float sum[C::COLS];
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        v[j] = (num_kb > 0 ? __uint_as_float(r0[j]) : 0.0f) + (num_kb > 1 ? __uint_as_float(r1[j]) : 0.0f);
-      float4* o4 = reinterpret_cast<float4*>(out + c * 32);
+    for (int j = 0; j < C::COLS; ++j) sum[j] = 0.0f;
+    const int n_sub[2] = {((num_kb + 1) / 2 + kDrainStages - 1) / kDrainStages,
+                          (num_kb / 2 + kDrainStages - 1) / kDrainStages};
+    const int n_drain = n_sub[0] + n_sub[1];
+    for (int d = 0; d < n_drain; ++d) {
+      const int p = d & 1, u = d >> 1;   // accumulators finish alternately: 0, 1, 0, 1, ...
+      tc::mbar_wait(&acc_full[p], u & 1);
+      tc::tc_fence_after();
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + p * BN + h * C::COLS;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      for (int c = 0; c < C::COLS / 32; ++c) {
+        uint32_t r[32];
+        tc::tmem_ld32(ta + c * 32, r);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum[c * 32 + j] += __uint_as_float(r[j]);
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&acc_empty[p]);
     }
+    float4* o4 = reinterpret_cast<float4*>(partial + (size_t)slice * hp * hp + (size_t)row * hp + j0 + h * C::COLS);
+#pragma unroll
+    for (int j = 0; j < C::COLS / 4; ++j) o4[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -362,6 +398,7 @@ __global__ void gram_reduce_kernel(const float* __restrict__ partial, int slices
 // 2.2e-4, scratch/gram_precision.py).  The slices are summed in fp64; 8k cells costs ~2 GB of
 // partials at 1M cells and no measurable time.
 constexpr int64_t kSliceCells = 8192;
+constexpr int64_t kSplitSliceCells = 32768;
 
 template <int BN>
 static int launch_gram(scb_ctx* ctx, const float* Z, const uint16_t* Zhi, const uint16_t* Zlo, int64_t n_rows, int hp,
@@ -383,9 +420,24 @@ static int launch_gram(scb_ctx* ctx, const float* Z, const uint16_t* Zhi, const 
     for (int bj = 0; bj < hp / BN; ++bj)
       if (bj * BN + BN - 1 >= bi * BM) tl.push_back(make_int2(bi, bj));
   const int n_tiles = (int)tl.size();
-  // K-slices: fill the SMs and keep each fp32 TMEM accumulation <= kSliceCells cells
+  // K-slices: fill the SMs; the fp32-input variant keeps each TMEM accumulation <= kSliceCells
+  // cells, the planes variant drains its accumulators every kDrainStages stages and takes long
+  // slices (<= kSplitSliceCells), with the slice count chosen to end on a full wave of CTAs
   const int64_t kbs = (n_rows + KB - 1) / KB;
-  int64_t sl = std::max<int64_t>((ctx->num_sms + n_tiles - 1) / n_tiles, (n_rows + kSliceCells - 1) / kSliceCells);
+  int64_t slice_cells = split ? kSplitSliceCells : kSliceCells;
+  if (const char* e = getenv("SCB_GRAM_SLICE_CELLS")) slice_cells = std::max<int64_t>(KB, atoll(e));  // experiments
+  int64_t sl = std::max<int64_t>((ctx->num_sms + n_tiles - 1) / n_tiles, (n_rows + slice_cells - 1) / slice_cells);
+  if (split) {  // least tail: smallest s in [sl, 2 sl) maximising the filled fraction of the last wave
+    int64_t best = sl;
+    double best_fill = -1.0;
+    for (int64_t c = sl; c < 2 * sl && c <= kbs; ++c) {
+      const int64_t ctas = c * n_tiles, waves = (ctas + ctx->num_sms - 1) / ctx->num_sms;
+      const double fill = (double)ctas / (double)(waves * ctx->num_sms);
+      if (fill > best_fill + 1e-9) { best_fill = fill; best = c; }
+      if (fill > 0.999) break;
+    }
+    sl = best;
+  }
   const int slices = (int)std::max<int64_t>(1, std::min<int64_t>(sl, kbs));
   const int64_t rows_per_slice = ((kbs + slices - 1) / slices) * KB;
   const size_t part_bytes = (size_t)slices * hp * hp * 4;

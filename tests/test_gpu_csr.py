@@ -261,21 +261,21 @@ def test_hvg_tie_rules_gpu_match_oracle():
 
 @pytest.mark.parametrize("clip", ["symmetric", "upper"])
 def test_scale_clip_modes_gpu(dev_state, clip):
-    """scale_dense with both clip modes vs the oracle, at a max_value (2.0) that clips both sides."""
+    """scale_dense with both clip modes vs the oracle, at a max_value (1.0) that clips both sides."""
     import torch
     from oracle import pipeline as op
     from paper_2605_13928_b200 import pp
     o = c1_oracle(False)
     Xl = dev_state["Xl"]
-    sc = pp.scale(Xl, dev_state["hvg"], 2.0, clip=clip)
+    sc = pp.scale(Xl, dev_state["hvg"], 1.0, clip=clip)
     torch.cuda.synchronize()
     oXl = o["X_log"]
-    ref, mean, inv = op.scale(oXl, o["hvg_mask"], 2.0, clip=clip)
+    ref, mean, inv = op.scale(oXl, o["hvg_mask"], 1.0, clip=clip)
     Z = sc.values().cpu().numpy()
     mag = np.maximum(np.abs(ref), np.abs(mean * inv)[None, :])
     assert (np.abs(Z - ref) / np.maximum(mag, 1e-30)).max() < 1e-5
-    assert Z.max() <= 2.0
+    assert Z.max() <= 1.0
     if clip == "symmetric":
-        assert Z.min() >= -2.0
+        assert Z.min() >= -1.0
     else:
-        assert Z.min() < -2.0
+        assert Z.min() < -1.0
