@@ -74,8 +74,9 @@ def test_pca_matches_oracle():
 @pytest.mark.parametrize("n,h", [(3001, 200), (20011, 1000)])
 def test_gram_split_planes_match_converter_path(n, h):
     """scb_split_bf16's planes are bit-exact round-to-nearest BF16 (hi) and BF16(Z - hi) (lo); fed
-    to gram_split_kernel they give the operands and MMA sequence of the in-kernel-converter path,
-    so the two Grams agree to rounding of the fp64 slice sums."""
+    to gram_split_kernel they give the operands of the in-kernel-converter path.  The planes
+    kernel restarts its TMEM accumulators every 256 cells (fp32 running sums), so it is at least
+    as close to the fp64 Gram as the converter path (8k-cell accumulations), and both agree."""
     import torch
     from paper_2605_13928_b200 import pp
     rng = np.random.default_rng(n + h)
@@ -88,4 +89,10 @@ def test_gram_split_planes_match_converter_path(n, h):
     assert torch.equal(sc.Z_hi.view(torch.int16), hi.view(torch.int16))
     assert torch.equal(sc.Z_lo.view(torch.int16), lo.view(torch.int16))
     scale = np.sqrt(np.outer(np.diag(C1), np.diag(C1)))
-    assert (np.abs(C1 - C2) / np.maximum(scale, 1e-30)).max() < 1e-6
+    Z64 = Z.astype(np.float64)
+    C64 = Z64.T @ Z64
+    e1 = (np.abs(C1[:h, :h] - C64) / np.maximum(scale[:h, :h], 1e-30)).max()
+    e2 = (np.abs(C2[:h, :h] - C64) / np.maximum(scale[:h, :h], 1e-30)).max()
+    assert e2 <= e1 * 1.01 + 1e-7, (e1, e2)
+    assert e2 < 2e-6, e2
+    assert (np.abs(C1 - C2) / np.maximum(scale, 1e-30)).max() < 2e-5
