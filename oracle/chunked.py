@@ -221,3 +221,16 @@ def run(indptr, indices, data, n_cols: int, mt_mask, p: op.Params, workers: Opti
         out["knn_queries"] = q
     _G.clear()
     return out
+
+
+def knn_queries(E, k: int, queries, workers: Optional[int] = None, block: int = 64):
+    """Exact kNN (pipeline.knn, float64 brute force) of ``queries`` against all rows of E, query
+    blocks spread over forked workers.  Returns (idx, dist)."""
+    workers = workers or max(1, min(32, len(os.sched_getaffinity(0))))
+    q = np.asarray(queries)
+    _G.update(E=E, k=k)
+    blocks = [q[i:i + block] for i in range(0, len(q), block)]
+    with _pool(workers) as pool:
+        res = pool.map(_w_knn, blocks)
+    _G.clear()
+    return np.concatenate([r[1][0] for r in res]), np.concatenate([r[1][1] for r in res])

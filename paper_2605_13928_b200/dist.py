@@ -1,6 +1,7 @@
 """Cell-sharded multi-GPU plumbing over torch.distributed (NCCL on B200s, gloo in CPU tests).
 
-Rows (cells) are split into contiguous blocks; every collective of the path is one of
+Rows (cells) are split into contiguous blocks balanced by nonzeros (``shard_rows_by_nnz``);
+every collective of the path is one of
 (SURVEY.md §8(e)): SUM all-reduce of per-gene integer sums / counts and of the partial
 Gram matrix, a broadcast of the rank-0 eigenvectors, and a row all-gather of the PCA
 embedding for the kNN keys.  Integer fixed-point gene sums make the HVG set and the scale
@@ -13,10 +14,37 @@ import torch.distributed as td
 
 
 def shard_rows(n: int, rank: int, world: int):
-    """Contiguous, balanced [begin, end) row range of ``rank``."""
+    """Contiguous [begin, end) row range of ``rank`` with balanced row counts."""
     base, rem = divmod(n, world)
     b = rank * base + min(rank, rem)
     return b, b + base + (1 if rank < rem else 0)
+
+
+def shard_rows_by_nnz(indptr, rank: int, world: int):
+    """Contiguous [begin, end) row range of ``rank`` balanced by nonzeros: the
+    cut before shard r is the first row boundary with indptr >= Z * r / world.  ``indptr`` is the
+    host (numpy or CPU tensor) int64 row-pointer array of the whole matrix."""
+    import numpy as np
+    ip = np.asarray(indptr, dtype=np.int64)
+    n, Z = len(ip) - 1, int(ip[-1])
+    if Z == 0:
+        return shard_rows(n, rank, world)
+
+    def cut(r):
+        if r <= 0:
+            return 0
+        if r >= world:
+            return n
+        return int(min(n, np.searchsorted(ip, (Z * r + world - 1) // world, side="left")))
+    return cut(rank), cut(rank + 1)
+
+
+def row_shards_from_counts(row_nnz, world: int):
+    """All ranks' nnz-balanced [begin, end) ranges from per-row nonzero counts."""
+    import numpy as np
+    ip = np.zeros(len(row_nnz) + 1, dtype=np.int64)
+    np.cumsum(np.asarray(row_nnz, dtype=np.int64), out=ip[1:])
+    return [shard_rows_by_nnz(ip, r, world) for r in range(world)]
 
 
 class Comm:

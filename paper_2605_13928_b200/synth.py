@@ -12,6 +12,7 @@ term) and ``scb_synth_rows`` (sampling).  Generator v2: bit-identical to oracle/
 from __future__ import annotations
 
 import dataclasses
+from typing import Optional
 
 import numpy as np
 import torch
@@ -87,6 +88,30 @@ def mt_mask(spec: Spec, device="cuda"):
     m = torch.zeros(spec.n_genes, dtype=torch.uint8, device=device)
     m[: spec.n_mt] = 1
     return m
+
+
+def row_nnz(spec: Spec, r0: int = 0, r1: Optional[int] = None, device="cuda", chunk: int = 16384) -> torch.Tensor:
+    """Nonzeros per row of rows [r0, r1) (the generator's count pass only; e.g. to cut
+    nnz-balanced cell shards before generating them)."""
+    r1 = spec.n_cells if r1 is None else r1
+    dev = torch.device(device)
+    G = spec.n_genes
+    log_mu, A, B, cum = gene_tables(spec)
+    d_log_mu = torch.as_tensor(log_mu, device=dev)
+    d_A = torch.as_tensor(A, device=dev).contiguous()
+    d_B = torch.as_tensor(B, device=dev).contiguous()
+    ctx, s = _ctx(d_log_mu), _stream(dev)
+    nnz = torch.empty(r1 - r0, dtype=torch.int64, device=dev)
+    xbuf = torch.empty((min(chunk, max(r1 - r0, 1)), G), dtype=torch.float64, device=dev)
+    for c0 in range(r0, r1, chunk):
+        c1 = min(r1, c0 + chunk)
+        ct, ls, U = cell_tables(spec, c0, c1, cum)
+        ct, ls, U = (torch.as_tensor(ct, device=dev), torch.as_tensor(ls, device=dev),
+                     torch.as_tensor(U, device=dev).contiguous())
+        _lib.call("scb_synth_logmean", ctx, c1 - c0, G, spec.n_factors, _p(d_log_mu), _p(d_A), _p(ct), _p(ls), _p(U),
+                  _p(d_B), _p(xbuf), s)
+        _lib.call("scb_synth_rows", ctx, spec.seed, c0, c1 - c0, G, _p(xbuf), 0, _p(nnz[c0 - r0:c1 - r0]), 0, 0, s)
+    return nnz
 
 
 def generate(spec: Spec, device="cuda", chunk: int = 16384) -> DeviceCSR:

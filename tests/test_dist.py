@@ -33,7 +33,7 @@ def _params(regress_out=False):
 def _run(rank, world, port, out_dir, regress_out=False):
     import tests.cpu_backend as cb
     from paper_2605_13928_b200 import pipeline
-    from paper_2605_13928_b200.dist import Comm, shard_rows
+    from paper_2605_13928_b200.dist import Comm, shard_rows_by_nnz
     from paper_2605_13928_b200.pp import DeviceCSR
     pipeline.pp = cb  # test-only substitution of the device step functions
     comm = None
@@ -42,7 +42,7 @@ def _run(rank, world, port, out_dir, regress_out=False):
         td.init_process_group("gloo", rank=rank, world_size=world)
         comm = Comm()
     g = np.load("tests/golden/g600x300.npz")
-    r0, r1 = shard_rows(len(g["indptr"]) - 1, rank, world)
+    r0, r1 = shard_rows_by_nnz(g["indptr"], rank, world)
     ip = g["indptr"][r0:r1 + 1] - g["indptr"][r0]
     sl = slice(int(g["indptr"][r0]), int(g["indptr"][r1]))
     X = DeviceCSR(torch.as_tensor(ip), torch.as_tensor(g["indices"][sl]), torch.as_tensor(g["data"][sl]), 300)
@@ -98,3 +98,19 @@ def test_two_rank_gloo_regress_out_matches_single_process_and_oracle(tmp_path):
     o = op.run(X, g["mt_mask"], dataclasses.replace(P, regress_out=True), with_knn=False)
     np.testing.assert_allclose(one["Z"], o["Z"], rtol=1e-5, atol=1e-5)
     np.testing.assert_allclose(one["inv"], o["scale_inv_std"], rtol=1e-10)
+
+
+def test_shard_rows_by_nnz_balances_nonzeros():
+    from paper_2605_13928_b200.dist import row_shards_from_counts, shard_rows_by_nnz
+    rng = np.random.default_rng(0)
+    nnz = rng.integers(0, 500, 10001)
+    nnz[:100] = 5000  # a dense head: equal row counts would unbalance the shards
+    ip = np.r_[0, np.cumsum(nnz)]
+    for world in (1, 2, 3, 8):
+        sh = row_shards_from_counts(nnz, world)
+        assert sh[0][0] == 0 and sh[-1][1] == len(nnz)
+        assert all(a[1] == b[0] for a, b in zip(sh, sh[1:]))
+        z = [int(ip[e] - ip[b]) for b, e in sh]
+        assert max(z) - min(z) <= 2 * 5000
+        assert sh == [shard_rows_by_nnz(ip, r, world) for r in range(world)]
+    assert shard_rows_by_nnz(np.zeros(5, np.int64), 1, 2) == (2, 4)  # no nonzeros: balanced row counts

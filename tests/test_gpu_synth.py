@@ -40,6 +40,20 @@ def test_synth_c3_window_identical():
     assert 0.05 < z / (16384 * 25000) < 0.12
 
 
+def test_synth_c3_windows_identical_to_c_oracle():
+    """Four more 16k-row windows spread over the C3 matrix (first, last and two inside) against
+    the C restatement of the generator (oracle/csynth.c, itself == numpy in test_oracle.py)."""
+    import subprocess
+    from oracle import synth as osynth
+    if osynth.native_lib() is None:
+        subprocess.run(["make", "-C", "oracle"], check=True, capture_output=True)
+    spec = SynthSpec(1_000_000, 25_000, seed=0)
+    for r0 in (0, 250_000, 750_000, 1_000_000 - 16384):
+        ip, ix, d = _device_rows(1_000_000, 25_000, 0, r0, r0 + 16384)
+        oip, oix, od = osynth.generate_csr_native(spec, rows=(r0, r0 + 16384))
+        assert np.array_equal(ip, oip) and np.array_equal(ix, oix) and np.array_equal(d, od), r0
+
+
 def test_synth_row_windows_compose():
     """Shards generated separately concatenate to the whole matrix (cell sharding)."""
     from paper_2605_13928_b200 import synth

@@ -433,3 +433,21 @@ def test_chunked_oracle_equals_unchunked():
     assert op.subspace_angle(got["components"], ref["components"]) < 1e-7
     np.testing.assert_allclose(got["variance"], ref["variance"], rtol=1e-10)
     np.testing.assert_array_equal(got["knn_idx"], ref["knn_idx"][q])
+
+
+def _oracle_native():
+    import subprocess
+    from oracle import synth as osynth
+    if osynth.native_lib() is None:
+        subprocess.run(["make", "-C", "oracle"], check=True, capture_output=True)
+    return osynth
+
+
+def test_c_generator_equals_numpy_generator():
+    """oracle/csynth.c (pthreads) reproduces oracle/synth.py bit for bit (row windows, two specs)."""
+    osynth = _oracle_native()
+    for spec, rows in ((SynthSpec(3000, 700, seed=5), None), (SynthSpec(1_000_000, 25_000, seed=0), (123_456, 123_800))):
+        a = generate_csr(spec, rows=rows)
+        b = osynth.generate_csr_native(spec, rows=rows, threads=4)
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
