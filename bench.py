@@ -354,6 +354,25 @@ def main():
     gram_flops = float(N_sub_loc) * H * (H + 1)
     stages["pca"]["gram_flop_unique"] = gram_flops
 
+    # ---- CPU baseline (before the e2e leg allocates ~15 GB of pinned host buffers: forked oracle
+    # workers of a process holding them start slowly)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # the same C3 matrix (device generator == oracle/synth.py, tests/test_gpu_synth.py): its
+        # first --cpu-sample rows for the stages, and this run's own 1M-row embedding as kNN keys
+        import numpy as np
+        ns = min(args.cpu_sample, N)
+        Xs = synth.generate_rows(spec, 0, ns)
+        host = Xs.to_host()
+        del Xs
+        keys = res.pca.X_pca[:, :p.n_comps].float().cpu().numpy()
+        qsel = np.sort(np.random.default_rng(args.seed).choice(len(keys), min(args.cpu_queries, len(keys)),
+                                                               replace=False))
+        cores = len(os.sched_getaffinity(0))
+        est = cpu_c3_estimate(host, mt.cpu().numpy(), N, keys, qsel, args, cores)
+        cpu = _cpu_line(est, cores, N, G, args.k, len(keys))
+
+
     # ---- e2e through the public API with host buffers (H2D of the CSR + D2H of the graph)
     e2e = None
     if not args.no_e2e:
@@ -416,22 +435,6 @@ def main():
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
                "overlap": "pinned H2D of step i+1 on a copy stream overlaps the compute of step i "
                           "(2 device input buffers); first copy and last compute are not overlapped"}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # the same C3 matrix (device generator == oracle/synth.py, tests/test_gpu_synth.py): its
-        # first --cpu-sample rows for the stages, and this run's own 1M-row embedding as kNN keys
-        import numpy as np
-        ns = min(args.cpu_sample, N)
-        Xs = synth.generate_rows(spec, 0, ns)
-        host = Xs.to_host()
-        del Xs
-        keys = res.pca.X_pca[:, :p.n_comps].float().cpu().numpy()
-        qsel = np.sort(np.random.default_rng(args.seed).choice(len(keys), min(args.cpu_queries, len(keys)),
-                                                               replace=False))
-        cores = len(os.sched_getaffinity(0))
-        est = cpu_c3_estimate(host, mt.cpu().numpy(), N, keys, qsel, args, cores)
-        cpu = _cpu_line(est, cores, N, G, args.k, len(keys))
 
     if rank == 0:
         line = {

@@ -85,7 +85,8 @@ def test_two_ranks_real_kernels_match_single_rank(tmp_path):
         np.testing.assert_array_equal(p["hvg"], one["hvg"])
         np.testing.assert_array_equal(p["mean"], one["mean"])
         np.testing.assert_array_equal(p["inv"], one["inv"])
-        np.testing.assert_allclose(p["var"], one["var"], rtol=1e-9)
+        # the Gram is fp32-accumulated per shard (different partial-sum boundaries): ~1e-7 relative
+        np.testing.assert_allclose(p["var"], one["var"], rtol=1e-6)
         c = np.abs(np.sum(p["comps"].astype(np.float64) * one["comps"], axis=1))
         assert c.min() > 1 - 1e-6, c.min()
     np.testing.assert_array_equal(np.concatenate([p["Z"] for p in parts]), one["Z"])  # row-local kernel
