@@ -112,11 +112,12 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def _step_bytes(Z_in, N, G, Z_sub, N_sub, H, ld, regress_out=False):
-    """Algorithmic HBM bytes per step."""
+def _step_bytes(Z_in, N, G, Z_sub, N_sub, H, ld, regress_out=False, bpn=8):
+    """Algorithmic HBM bytes per step; ``bpn`` = bytes per input nonzero (8 for the
+    int32/float32 CSR, 4 for the compact u16 CSR)."""
     return {
-        "qc": 8 * Z_in + 8 * (N + 1),
-        "norm_hvg": 8 * Z_in + (8 * Z_in + 8 * Z_sub) + 8 * Z_in + 4 * N,  # count, fill, hvg sums
+        "qc": bpn * Z_in + 8 * (N + 1),
+        "norm_hvg": bpn * Z_in + (bpn * Z_in + 8 * Z_sub) + bpn * Z_in + 4 * N,  # count, fill, hvg sums
         # scale: dense scale (its gene sums are fused into the subset fill pass of norm_hvg);
         # regress_out: dense log (8Z' + 4N ld), Aᵀl read (4N ld), in-place residual scaling (8N ld)
         "regress": (8 * Z_sub + 16 * N_sub * ld) if regress_out else (8 * Z_sub + 4 * N_sub * ld),
@@ -230,6 +231,8 @@ def main():
     ap.add_argument("--cpu-queries", type=int, default=1000, help="kNN queries of the cpu_baseline sample")
     ap.add_argument("--ref-sample", type=int, default=100000, help="cells of the reference arm's stage sample")
     ap.add_argument("--ref-queries", type=int, default=1000, help="kNN queries per reference-arm step")
+    ap.add_argument("--input", default="u16", choices=["u16", "f32"],
+                    help="device/host CSR layout: compact u16 indices+counts (lossless here) or int32/float32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", action="store_true",
@@ -275,6 +278,8 @@ def main():
     # ---- input synthesis (untimed): this rank's rows of the global matrix
     t0 = time.time()
     X = synth.generate_rows(spec, r0, r1)
+    if args.input == "u16":
+        X = X.to_u16()  # lossless (25k genes, counts < 65536; to_u16 refuses otherwise)
     mt = synth.mt_mask(spec)
     torch.cuda.synchronize()
     gen_s = time.time() - t0
@@ -333,7 +338,8 @@ def main():
     f16_peak = bf16_sus  # dense FP16 == dense BF16 tensor rate; sustained: the kernel runs inside a long step loop
     flops_knn = 2.0 * N_sub_loc * n_keys * p.n_comps
     achieved = flops_knn / (knn_ms / 1e3) / 1e12
-    sb = _step_bytes(Z_in, X.n_rows, G, Z_sub, N_sub_loc, H, ld, args.regress_out)
+    bpn = X.indices.element_size() + X.data.element_size()
+    sb = _step_bytes(Z_in, X.n_rows, G, Z_sub, N_sub_loc, H, ld, args.regress_out, bpn)
     stages = {}
     for kk in ("qc", "norm_hvg", "regress"):
         if kk in step_ms and step_ms[kk] > 0:
@@ -429,7 +435,8 @@ def main():
         e_ms = e0.elapsed_time(e1) / args.steps
         if comm is not None:
             e_ms = comm.allreduce_max(e_ms)
-        h2d_bytes = h_indptr.numel() * 8 + h_ind.numel() * 4 + h_dat.numel() * 4
+        h2d_bytes = (h_indptr.numel() * h_indptr.element_size() + h_ind.numel() * h_ind.element_size()
+                     + h_dat.numel() * h_dat.element_size())
         d2h_bytes = o_i.numel() * 4 + o_d.numel() * 4
         e2e = {"value": N / (e_ms / 1e3), "unit": "cells/s", "ms_per_step": round(e_ms, 3),
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
@@ -451,7 +458,11 @@ def main():
                                    f"log1p->HVG(seurat,{args.hvg})->{'regress_out+' if args.regress_out else ''}scale->PCA(50)->"
                                    f"kNN(k={args.k}, {KNN_LABEL}){'+umap graph' if args.graph or args.umap or args.cluster or args.de else ''}{'+umap layout' if args.umap else ''}{'+leiden' if args.cluster or args.de else ''}{'+rank_genes_groups' if args.de else ''}",
                        "cells": N, "genes": G, "nnz": int(Z_total), "kept_cells": int(n_keys), "hvg": H,
-                       "parallelism": f"cells sharded x{world}", "l2": "inputs (14 GB) >> L2 (126 MB); no flush needed",
+                       "input_format": ("CSR int64 indptr + uint16 gene indices + uint16 counts (lossless: G <= 65536, "
+                                        "counts <= 65535, checked by DeviceCSR.to_u16)") if bpn == 4 else
+                                       "CSR int64 indptr + int32 gene indices + float32 counts",
+                       "parallelism": f"cells sharded x{world}, nnz-balanced",
+                       "l2": f"inputs ({(bpn * Z_in + 8 * N) / 1e9:.1f} GB) >> L2 (126 MB); no flush needed",
                        "gen_seconds": round(gen_s, 1)},
             "step_ms": {kk: round(v, 3) for kk, v in step_ms.items()},
             "stages": stages,

@@ -85,10 +85,10 @@ __device__ __forceinline__ void red_shared_add(uint32_t a, uint32_t v) {
 // CTAs also write the per-cell metrics and, for the HVG pass, the per-row positions where
 // the original gene index crosses each HVG tile boundary (splits[r][t-1] = #entries with
 // gene < t*split_w, relative to the row start).
-template <int NSPLIT, bool SINGLE_TILE>
+template <typename IT, typename VT, int NSPLIT, bool SINGLE_TILE>
 __global__ void __launch_bounds__(kQcThreads)
-qc_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-          const float* __restrict__ data, int64_t n_rows, int32_t n_cols,
+qc_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
+          const VT* __restrict__ data, int64_t n_rows, int32_t n_cols,
           const uint8_t* __restrict__ mt_mask, int32_t tile_w, int32_t n_split, int32_t split_w,
           int32_t* __restrict__ splits, int32_t* __restrict__ n_genes, double* __restrict__ total,
           double* __restrict__ total_mt, double* __restrict__ pct, uint32_t* __restrict__ g_cells,
@@ -297,10 +297,10 @@ __global__ void gene_remap_kernel(const uint8_t* gmask, int32_t n, int32_t* rema
 
 // Count kept entries (and kept total) per original row; writes counts into
 // cnt[kept_row] where kept_row = row_pos[r] (exclusive scan of cell_mask).
-template <bool SMALL>
+template <typename IT, typename VT, bool SMALL>
 __global__ void __launch_bounds__(kRowThreads)
-subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                    const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
+subset_count_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
+                    const VT* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
                     const int32_t* __restrict__ remap, int32_t n_cols, const int64_t* __restrict__ row_pos,
                     int64_t* __restrict__ cnt, double target_sum, float* __restrict__ row_scale,
                     float* __restrict__ row_scale_orig) {
@@ -344,10 +344,10 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
 // exclusive scan so the output stays in row order.  The (up to 128) kept elements of a warp
 // step are staged in shared memory and written back 32 consecutive elements per instruction
 // (full 128-byte lines instead of four lane-strided partial-sector stores per quad).
-template <bool SMALL>
+template <typename IT, typename VT, bool SMALL>
 __global__ void __launch_bounds__(kRowThreads)
-subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                   const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
+subset_fill_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
+                   const VT* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
                    const int32_t* __restrict__ remap, int32_t n_cols, const int64_t* __restrict__ row_pos,
                    const int64_t* __restrict__ new_indptr, const float* __restrict__ row_scale,
                    int32_t* __restrict__ out_idx, float* __restrict__ out_val) {
@@ -405,9 +405,10 @@ subset_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
 // smem: int32 per original gene = new index | (slot + 1) << 16 (-1: dropped; slot -1: not an HVG),
 // 4 u32 words per HVG.  Requires n_cols <= 32767.
 constexpr int kFillSumsThreads = 1024;
+template <typename IT, typename VT>
 __global__ void __launch_bounds__(kFillSumsThreads)
-subset_fill_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                        const float* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
+subset_fill_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
+                        const VT* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
                         const int32_t* __restrict__ remap, int32_t n_cols, const int32_t* __restrict__ slot_new,
                         int32_t n_slots, const int64_t* __restrict__ row_pos, const int64_t* __restrict__ new_indptr,
                         const float* __restrict__ row_scale, int64_t rows_per_block, int32_t* __restrict__ out_idx,
@@ -529,9 +530,10 @@ normalize_log1p_kernel(const int64_t* __restrict__ indptr, const float* __restri
 // so each nonzero is read exactly once; without them every tile CTA filters whole rows.
 __device__ __forceinline__ uint64_t fx_round(double v) { return (uint64_t)__double2ull_rn(v); }
 
+template <typename IT, typename VT>
 __global__ void __launch_bounds__(kHvgThreads)
-hvg_sums_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                const float* __restrict__ data, const float* __restrict__ row_scale, int64_t n_rows,
+hvg_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
+                const VT* __restrict__ data, const float* __restrict__ row_scale, int64_t n_rows,
                 int32_t n_cols, const int32_t* __restrict__ remap, int32_t n_out, int32_t tile_w,
                 int32_t n_tiles, const int32_t* __restrict__ splits, int64_t rows_per_block,
                 unsigned long long* __restrict__ sums, int* __restrict__ order_flag) {
@@ -1050,8 +1052,9 @@ extern "C" int32_t scb_hvg_tiles(int32_t n_cols) { return n_cols <= 0 ? 1 : (n_c
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                              const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
+template <typename IT, typename VT>
+static int qc_metrics_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indices,
+                              const VT* data, int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
                               int32_t* n_genes, double* total, double* total_mt, double* pct,
                               int32_t* n_cells, double* gene_total, int32_t* hvg_row_splits, void* stream) {
   SCB_REQUIRE(ctx && indptr && mt_mask && n_genes && total && total_mt && pct && n_cells && gene_total,
@@ -1088,17 +1091,17 @@ extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t
     static_assert(kMaxSplit == 3, "qc_kernel is instantiated for 0..3 row splits");
     if (n_tiles == 1) {
       switch (n_split) {
-        case 0: SCB_TRY(launch(qc_kernel<0, true>)); break;
-        case 1: SCB_TRY(launch(qc_kernel<1, true>)); break;
-        case 2: SCB_TRY(launch(qc_kernel<2, true>)); break;
-        default: SCB_TRY(launch(qc_kernel<3, true>)); break;
+        case 0: SCB_TRY(launch(qc_kernel<IT, VT, 0, true>)); break;
+        case 1: SCB_TRY(launch(qc_kernel<IT, VT, 1, true>)); break;
+        case 2: SCB_TRY(launch(qc_kernel<IT, VT, 2, true>)); break;
+        default: SCB_TRY(launch(qc_kernel<IT, VT, 3, true>)); break;
       }
     } else {
       switch (n_split) {
-        case 0: SCB_TRY(launch(qc_kernel<0, false>)); break;
-        case 1: SCB_TRY(launch(qc_kernel<1, false>)); break;
-        case 2: SCB_TRY(launch(qc_kernel<2, false>)); break;
-        default: SCB_TRY(launch(qc_kernel<3, false>)); break;
+        case 0: SCB_TRY(launch(qc_kernel<IT, VT, 0, false>)); break;
+        case 1: SCB_TRY(launch(qc_kernel<IT, VT, 1, false>)); break;
+        case 2: SCB_TRY(launch(qc_kernel<IT, VT, 2, false>)); break;
+        default: SCB_TRY(launch(qc_kernel<IT, VT, 3, false>)); break;
       }
     }
     SCB_LAUNCH_CHECK();
@@ -1111,6 +1114,20 @@ extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t
   SCB_REQUIRE(flag == 0, SCB_ERR_DATA,
               "scb_qc_metrics: counts must be non-negative integers < 2^24 with column indices in range");
   return SCB_OK;
+}
+
+extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                              const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
+                              int32_t* n_genes, double* total, double* total_mt, double* pct,
+                              int32_t* n_cells, double* gene_total, int32_t* hvg_row_splits, void* stream) {
+  return qc_metrics_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, mt_mask, n_genes, total, total_mt, pct, n_cells, gene_total, hvg_row_splits, stream);
+}
+
+extern "C" int scb_qc_metrics_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
+                              const uint16_t* data, int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
+                              int32_t* n_genes, double* total, double* total_mt, double* pct,
+                              int32_t* n_cells, double* gene_total, int32_t* hvg_row_splits, void* stream) {
+  return qc_metrics_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, mt_mask, n_genes, total, total_mt, pct, n_cells, gene_total, hvg_row_splits, stream);
 }
 
 extern "C" int scb_filter_masks(scb_ctx* ctx, const int32_t* ng, const double* pct, int64_t n_rows,
@@ -1131,8 +1148,9 @@ extern "C" int scb_filter_masks(scb_ctx* ctx, const int32_t* ng, const double* p
   return SCB_OK;
 }
 
-extern "C" int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                                const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+template <typename IT, typename VT>
+static int subset_count_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indices,
+                                const VT* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                 const uint8_t* gmask, int32_t* remap, int64_t* new_indptr,
                                 double target_sum, float* row_scale, float* row_scale_orig, void* stream) {
   SCB_REQUIRE(ctx && indptr && indices && cmask && gmask && remap && new_indptr, SCB_ERR_ARG,
@@ -1152,7 +1170,7 @@ extern "C" int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32
     const bool small = n_cols <= 32767;
     const size_t map_bytes = small ? (size_t)((n_cols + 7) & ~7) * 2 : (size_t)((n_cols + 31) / 32) * 8;
     SCB_REQUIRE(map_bytes <= 64 * 1024, SCB_ERR_UNSUPPORTED, "scb_subset_count: too many genes");
-    auto kern = small ? subset_count_kernel<true> : subset_count_kernel<false>;
+    auto kern = small ? subset_count_kernel<IT, VT, true> : subset_count_kernel<IT, VT, false>;
     SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_bytes));
     kern<<<grid_for(ctx, 4), kRowThreads, map_bytes, s>>>(indptr, indices, data, n_rows, cmask, remap, n_cols,
                                                           row_pos, cnt, target_sum, row_scale, row_scale_orig);
@@ -1163,8 +1181,23 @@ extern "C" int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32
   return SCB_OK;
 }
 
-extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                               const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+extern "C" int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                                const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+                                const uint8_t* gmask, int32_t* remap, int64_t* new_indptr,
+                                double target_sum, float* row_scale, float* row_scale_orig, void* stream) {
+  return subset_count_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, cmask, gmask, remap, new_indptr, target_sum, row_scale, row_scale_orig, stream);
+}
+
+extern "C" int scb_subset_count_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
+                                const uint16_t* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+                                const uint8_t* gmask, int32_t* remap, int64_t* new_indptr,
+                                double target_sum, float* row_scale, float* row_scale_orig, void* stream) {
+  return subset_count_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, cmask, gmask, remap, new_indptr, target_sum, row_scale, row_scale_orig, stream);
+}
+
+template <typename IT, typename VT>
+static int subset_fill_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indices,
+                               const VT* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
                                int32_t* new_indices, float* new_data, void* stream) {
   SCB_REQUIRE(ctx && indptr && indices && data && cmask && remap && new_indptr && new_indices && new_data,
@@ -1179,7 +1212,7 @@ extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_
     const bool small = n_cols <= 32767;
     const size_t map_bytes = small ? (size_t)((n_cols + 7) & ~7) * 2 : (size_t)((n_cols + 31) / 32) * 8;
     SCB_REQUIRE(map_bytes <= 64 * 1024, SCB_ERR_UNSUPPORTED, "scb_subset_fill: too many genes");
-    auto kern = small ? subset_fill_kernel<true> : subset_fill_kernel<false>;
+    auto kern = small ? subset_fill_kernel<IT, VT, true> : subset_fill_kernel<IT, VT, false>;
     SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_bytes));
     kern<<<grid_for(ctx, 4), kRowThreads, map_bytes, s>>>(indptr, indices, data, n_rows, cmask, remap, n_cols,
                                                           row_pos, new_indptr, row_scale, new_indices, new_data);
@@ -1188,8 +1221,23 @@ extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_
   return SCB_OK;
 }
 
-extern "C" int scb_subset_fill_scale_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                                          const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                               const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+                               const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
+                               int32_t* new_indices, float* new_data, void* stream) {
+  return subset_fill_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, new_indices, new_data, stream);
+}
+
+extern "C" int scb_subset_fill_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
+                               const uint16_t* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+                               const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
+                               int32_t* new_indices, float* new_data, void* stream) {
+  return subset_fill_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, new_indices, new_data, stream);
+}
+
+template <typename IT, typename VT>
+static int subset_fill_scale_sums_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indices,
+                                          const VT* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                           const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
                                           const int32_t* slot, int32_t n_slots, int32_t* new_indices,
                                           float* new_data, uint64_t* sums, void* stream) {
@@ -1208,12 +1256,28 @@ extern "C" int scb_subset_fill_scale_sums(scb_ctx* ctx, const int64_t* indptr, c
   SCB_TRY(scan_u8_to_i64(ctx, cmask, n_rows, row_pos, s));
   if (n_rows == 0) return SCB_OK;
   const int64_t rpb = 1024;  // carry-free fixed point
-  SCB_CUDA(cudaFuncSetAttribute(subset_fill_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  subset_fill_sums_kernel<<<(unsigned)((n_rows + rpb - 1) / rpb), kFillSumsThreads, smem, s>>>(
+  SCB_CUDA(cudaFuncSetAttribute(subset_fill_sums_kernel<IT, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  subset_fill_sums_kernel<IT, VT><<<(unsigned)((n_rows + rpb - 1) / rpb), kFillSumsThreads, smem, s>>>(
       indptr, indices, data, n_rows, cmask, remap, n_cols, slot, n_slots, row_pos, new_indptr, row_scale, rpb,
       new_indices, new_data, (unsigned long long*)sums);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
+}
+
+extern "C" int scb_subset_fill_scale_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                                          const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+                                          const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
+                                          const int32_t* slot, int32_t n_slots, int32_t* new_indices,
+                                          float* new_data, uint64_t* sums, void* stream) {
+  return subset_fill_scale_sums_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, slot, n_slots, new_indices, new_data, sums, stream);
+}
+
+extern "C" int scb_subset_fill_scale_sums_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
+                                          const uint16_t* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
+                                          const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
+                                          const int32_t* slot, int32_t n_slots, int32_t* new_indices,
+                                          float* new_data, uint64_t* sums, void* stream) {
+  return subset_fill_scale_sums_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, slot, n_slots, new_indices, new_data, sums, stream);
 }
 
 extern "C" int scb_normalize_log1p(scb_ctx* ctx, const int64_t* indptr, const float* data, int64_t n_rows,
@@ -1227,8 +1291,9 @@ extern "C" int scb_normalize_log1p(scb_ctx* ctx, const int64_t* indptr, const fl
   return SCB_OK;
 }
 
-extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                                 const float* data, const float* row_scale, int64_t n_rows, int32_t n_cols,
+template <typename IT, typename VT>
+static int hvg_gene_sums_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indices,
+                                 const VT* data, const float* row_scale, int64_t n_rows, int32_t n_cols,
                                  const int32_t* remap, int32_t n_out, const int32_t* row_splits, uint64_t* sums,
                                  void* stream) {
   SCB_REQUIRE(ctx && indptr && indices && data && row_scale && sums, SCB_ERR_ARG,
@@ -1242,11 +1307,11 @@ extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int3
   // row blocks of <= 1024 rows: the 22-bit low words cannot overflow (1024 * 2^22 = 2^32)
   int64_t rows_per_block = std::max<int64_t>(64, std::min<int64_t>(1024, n_rows / (2 * ctx->num_sms) + 1));
   const int64_t n_blocks = (n_rows + rows_per_block - 1) / rows_per_block;
-  SCB_CUDA(cudaFuncSetAttribute(hvg_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SCB_CUDA(cudaFuncSetAttribute(hvg_sums_kernel<IT, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaStream_t s = (cudaStream_t)stream;
   const bool split = row_splits && n_tiles > 1;
   if (!split) {
-    hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
+    hvg_sums_kernel<IT, VT><<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
         indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, nullptr,
         rows_per_block, (unsigned long long*)sums, ctx->d_flag + 1);
     SCB_LAUNCH_CHECK();
@@ -1262,7 +1327,7 @@ extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int3
   int* order_flag = ctx->d_flag + 1;
   SCB_CUDA(cudaMemsetAsync(tmp, 0, sbytes, s));
   SCB_CUDA(cudaMemsetAsync(order_flag, 0, sizeof(int), s));
-  hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
+  hvg_sums_kernel<IT, VT><<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
       indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, row_splits,
       rows_per_block, tmp, order_flag);
   SCB_LAUNCH_CHECK();
@@ -1271,7 +1336,7 @@ extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int3
   SCB_CUDA(cudaStreamSynchronize(s));
   if (flag) {
     SCB_CUDA(cudaMemsetAsync(tmp, 0, sbytes, s));
-    hvg_sums_kernel<<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
+    hvg_sums_kernel<IT, VT><<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
         indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, nullptr,
         rows_per_block, tmp, order_flag);
     SCB_LAUNCH_CHECK();
@@ -1279,6 +1344,20 @@ extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int3
   add_u64_kernel<<<ceil_div(4 * n_out, 256), 256, 0, s>>>(tmp, (unsigned long long*)sums, (int64_t)4 * n_out);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
+}
+
+extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                                 const float* data, const float* row_scale, int64_t n_rows, int32_t n_cols,
+                                 const int32_t* remap, int32_t n_out, const int32_t* row_splits, uint64_t* sums,
+                                 void* stream) {
+  return hvg_gene_sums_impl<int32_t, float>(ctx, indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, row_splits, sums, stream);
+}
+
+extern "C" int scb_hvg_gene_sums_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
+                                 const uint16_t* data, const float* row_scale, int64_t n_rows, int32_t n_cols,
+                                 const int32_t* remap, int32_t n_out, const int32_t* row_splits, uint64_t* sums,
+                                 void* stream) {
+  return hvg_gene_sums_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, row_splits, sums, stream);
 }
 
 extern "C" int scb_hvg_select(scb_ctx* ctx, const uint64_t* sums, int32_t n_cols, int64_t n_cells,

@@ -3,6 +3,9 @@
 // A warp walks the row [b, e) in windows of 128 elements: lane l owns the 4 consecutive
 // elements at base + 128*u + 4*l (u < U windows in flight), loaded with one 16-byte
 // ld.global.nc per array, so every warp keeps U x 1 KB of index+value bytes in flight.
+// Compact inputs: uint16_t column indices and/or uint16_t counts (the lossless "u16" CSR
+// wire format, G <= 65536 and counts <= 65535) are loaded 8 bytes per lane-quad and widened
+// in registers -- half the HBM bytes per nonzero, the same Quad for the consumer.
 // Elements outside [b, e) are masked (the vector start is rounded down to a multiple of 4;
 // the arrays must be 16-byte aligned).  The tail vector that would cross the end of the
 // arrays is read with scalar loads.
@@ -26,6 +29,28 @@ __device__ __forceinline__ float4 ld_nc_v4(const float* p) {
   return r;
 }
 
+__device__ __forceinline__ uint2 ld_nc_v2(const uint16_t* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void ld4(const int* p, int (&o)[4]) {
+  const int4 v = ld_nc_v4(p);
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+__device__ __forceinline__ void ld4(const float* p, float (&o)[4]) {
+  const float4 v = ld_nc_v4(p);
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+__device__ __forceinline__ void ld4(const uint16_t* p, int (&o)[4]) {
+  const uint2 v = ld_nc_v2(p);
+  o[0] = (int)(v.x & 0xffffu); o[1] = (int)(v.x >> 16); o[2] = (int)(v.y & 0xffffu); o[3] = (int)(v.y >> 16);
+}
+__device__ __forceinline__ void ld4(const uint16_t* p, float (&o)[4]) {
+  const uint2 v = ld_nc_v2(p);
+  o[0] = (float)(v.x & 0xffffu); o[1] = (float)(v.x >> 16); o[2] = (float)(v.y & 0xffffu); o[3] = (float)(v.y >> 16);
+}
+
 struct Quad {
   int64_t p;   // position of element 0
   int g[4];    // column indices
@@ -34,8 +59,8 @@ struct Quad {
 };
 
 // one window of U quads starting at `base` (lane l: elements base + 128u + 4l .. +3)
-template <int U>
-__device__ __forceinline__ void load_window(const int* __restrict__ idx, const float* __restrict__ val, int64_t base,
+template <int U, typename IT, typename VT>
+__device__ __forceinline__ void load_window(const IT* __restrict__ idx, const VT* __restrict__ val, int64_t base,
                                             int64_t b, int64_t e, int64_t nnz, Quad (&q)[U]) {
   const int lane = lane_id();
 #pragma unroll
@@ -45,17 +70,13 @@ __device__ __forceinline__ void load_window(const int* __restrict__ idx, const f
     q[u].valid = 0;
     if (p < e) {
       if (p + 4 <= nnz) {
-        const int4 iv = ld_nc_v4(idx + p);
-        q[u].g[0] = iv.x; q[u].g[1] = iv.y; q[u].g[2] = iv.z; q[u].g[3] = iv.w;
-        if (val) {
-          const float4 dv = ld_nc_v4(val + p);
-          q[u].x[0] = dv.x; q[u].x[1] = dv.y; q[u].x[2] = dv.z; q[u].x[3] = dv.w;
-        }
+        ld4(idx + p, q[u].g);
+        if (val) ld4(val + p, q[u].x);
       } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          q[u].g[k] = (p + k < nnz) ? idx[p + k] : 0;
-          if (val) q[u].x[k] = (p + k < nnz) ? val[p + k] : 0.0f;
+          q[u].g[k] = (p + k < nnz) ? (int)idx[p + k] : 0;
+          if (val) q[u].x[k] = (p + k < nnz) ? (float)val[p + k] : 0.0f;
         }
       }
       if (!val) {
@@ -71,8 +92,8 @@ __device__ __forceinline__ void load_window(const int* __restrict__ idx, const f
   }
 }
 
-template <int U, typename F>
-__device__ __forceinline__ void stream_row(const int* __restrict__ idx, const float* __restrict__ val, int64_t b,
+template <int U, typename IT, typename VT, typename F>
+__device__ __forceinline__ void stream_row(const IT* __restrict__ idx, const VT* __restrict__ val, int64_t b,
                                            int64_t e, int64_t nnz, F&& f) {
   for (int64_t base = b & ~int64_t(3); base < e; base += 128 * U) {
     Quad q[U];
@@ -85,8 +106,8 @@ __device__ __forceinline__ void stream_row(const int* __restrict__ idx, const fl
 // Software-pipelined variant: the next window's loads are issued before the current window
 // is processed, so a warp always has U x 1 KB in flight while it computes (for kernels whose
 // per-element work is long enough to expose the load latency).
-template <int U, typename F>
-__device__ __forceinline__ void stream_row_pipe(const int* __restrict__ idx, const float* __restrict__ val, int64_t b,
+template <int U, typename IT, typename VT, typename F>
+__device__ __forceinline__ void stream_row_pipe(const IT* __restrict__ idx, const VT* __restrict__ val, int64_t b,
                                                 int64_t e, int64_t nnz, F&& f) {
   int64_t base = b & ~int64_t(3);
   if (base >= e) return;

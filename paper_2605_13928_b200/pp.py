@@ -36,9 +36,25 @@ def _ctx(t: torch.Tensor):
     return _lib.context(t.device.index if t.device.index is not None else torch.cuda.current_device())
 
 
+_U16 = (torch.uint16, torch.int16)
+
+
+def _fmt(indices: torch.Tensor, data: torch.Tensor) -> str:
+    """C-ABI suffix of a raw-matrix entry point for these array types: "" for the 32-bit CSR
+    (int32 indices, float32 counts), "_u16" for the compact u16 CSR (uint16 indices and counts)."""
+    if indices.dtype == torch.int32 and data.dtype == torch.float32:
+        return ""
+    if indices.dtype in _U16 and data.dtype in _U16:
+        return "_u16"
+    raise TypeError(f"unsupported CSR array types {indices.dtype}/{data.dtype}: use int32/float32 or the compact "
+                    "uint16/uint16 format (DeviceCSR.to_u16)")
+
+
 @dataclasses.dataclass
 class DeviceCSR:
-    """CSR count matrix resident in HBM: indptr int64[N+1], indices int32[nnz], data float32[nnz]."""
+    """CSR count matrix resident in HBM: indptr int64[N+1], indices int32[nnz], data float32[nnz]
+    -- or the lossless compact form (``to_u16``): uint16 indices and uint16 counts, accepted by
+    every step that reads the raw matrix (half the bytes per nonzero)."""
 
     indptr: torch.Tensor
     indices: torch.Tensor
@@ -69,6 +85,31 @@ class DeviceCSR:
     def to_host(self):
         return (self.indptr.cpu().numpy(), self.indices.cpu().numpy(), self.data.cpu().numpy(), self.n_cols)
 
+    @property
+    def is_u16(self) -> bool:
+        return self.indices.dtype in _U16
+
+    def to_u16(self) -> "DeviceCSR":
+        """The compact u16 form (n_cols <= 65536 and every count an integer in [0, 65535];
+        raises ValueError otherwise -- the conversion is lossless or refused)."""
+        if self.is_u16:
+            return self
+        if self.n_cols > 65536:
+            raise ValueError(f"u16 CSR needs n_cols <= 65536 (got {self.n_cols})")
+        d = self.data
+        if d.numel():
+            ok = torch.stack([(d < 0).any(), (d > 65535).any(), (d != torch.round(d)).any()]).cpu()
+            if bool(ok.any()):
+                raise ValueError("u16 CSR needs integer counts in [0, 65535]")
+        return DeviceCSR(self.indptr, self.indices.to(torch.uint16), d.to(torch.int32).to(torch.uint16), self.n_cols)
+
+    def to_f32(self) -> "DeviceCSR":
+        """The 32-bit form (int32 indices, float32 counts)."""
+        if not self.is_u16:
+            return self
+        return DeviceCSR(self.indptr, self.indices.to(torch.int32), self.data.to(torch.int32).to(torch.float32),
+                         self.n_cols)
+
 
 # ----------------------------------------------------------------------------- qc
 def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor, row_splits: bool = False):
@@ -92,7 +133,8 @@ def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor, row_splits: bool =
         T = int(_lib.call("scb_hvg_tiles", G))
         if T > 1:
             splits = torch.empty((N, T - 1), dtype=torch.int32, device=dev)
-    _lib.call("scb_qc_metrics", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), N, G, _p(mt),
+    _lib.call("scb_qc_metrics" + _fmt(X.indices, X.data), _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), N, G,
+              _p(mt),
               _p(out["n_genes_by_counts"]), _p(out["total_counts"]), _p(out["total_counts_mt"]),
               _p(out["pct_counts_mt"]), _p(out["n_cells_by_counts"]), _p(out["gene_total_counts"]),
               _p(splits), _stream(dev))
@@ -146,14 +188,15 @@ def subset(X: DeviceCSR, cell_mask, gene_mask, n_kept=None, target_sum=None):
     new_indptr = torch.empty(nk + 1, dtype=torch.int64, device=dev)
     row_scale = torch.empty(nk, dtype=torch.float32, device=dev) if target_sum is not None else None
     ctx, s = _ctx(X.data), _stream(dev)
-    _lib.call("scb_subset_count", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols,
+    fmt = _fmt(X.indices, X.data)
+    _lib.call("scb_subset_count" + fmt, ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols,
               _p(cell_mask), _p(gene_mask), _p(remap), _p(new_indptr), float(target_sum or 0.0),
               _p(row_scale), 0, s)
     nnz = int(new_indptr[nk].item())
     ind = torch.empty(nnz, dtype=torch.int32, device=dev)
     dat = torch.empty(nnz, dtype=torch.float32, device=dev)
-    _lib.call("scb_subset_fill", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols, _p(cell_mask),
-              _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(dat), s)
+    _lib.call("scb_subset_fill" + fmt, ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols,
+              _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(dat), s)
     out = DeviceCSR(new_indptr, ind, dat, gk)
     out.row_scale = row_scale
     return out
@@ -169,8 +212,9 @@ def subset_count_scale(X: DeviceCSR, cell_mask, gene_mask, n_kept, target_sum: f
     row_scale = torch.empty(nk, dtype=torch.float32, device=dev)
     row_scale_orig = torch.empty(X.n_rows, dtype=torch.float32, device=dev)
     ctx, s = _ctx(X.data), _stream(dev)
-    _lib.call("scb_subset_count", ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols, _p(cell_mask),
-              _p(gene_mask), _p(remap), _p(new_indptr), float(target_sum), _p(row_scale), _p(row_scale_orig), s)
+    _lib.call("scb_subset_count" + _fmt(X.indices, X.data), ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows,
+              X.n_cols, _p(cell_mask), _p(gene_mask), _p(remap), _p(new_indptr), float(target_sum), _p(row_scale),
+              _p(row_scale_orig), s)
     nnz = int(new_indptr[nk].item())
     return remap, new_indptr, row_scale, row_scale_orig, nnz
 
@@ -180,8 +224,9 @@ def subset_fill_log(X: DeviceCSR, cell_mask, remap, new_indptr, row_scale, nnz: 
     dev = X.device
     ind = torch.empty(nnz, dtype=torch.int32, device=dev)
     logv = torch.empty(nnz, dtype=torch.float32, device=dev)
-    _lib.call("scb_subset_fill", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols,
-              _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(logv), _stream(dev))
+    _lib.call("scb_subset_fill" + _fmt(X.indices, X.data), _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data),
+              X.n_rows, X.n_cols, _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(logv),
+              _stream(dev))
     return DeviceCSR(new_indptr, ind, logv, n_genes_kept, row_scale=row_scale)
 
 
@@ -206,9 +251,9 @@ def subset_fill_log_scale_sums(X: DeviceCSR, cell_mask, remap, new_indptr, row_s
     logv = torch.empty(nnz, dtype=torch.float32, device=dev)
     if sums is None:
         sums = torch.zeros((2, 2, H), dtype=torch.int64, device=dev)
-    _lib.call("scb_subset_fill_scale_sums", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols,
-              _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(slot), H, _p(ind), _p(logv), _p(sums),
-              _stream(dev))
+    _lib.call("scb_subset_fill_scale_sums" + _fmt(X.indices, X.data), _ctx(X.data), _p(X.indptr), _p(X.indices),
+              _p(X.data), X.n_rows, X.n_cols, _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(slot), H,
+              _p(ind), _p(logv), _p(sums), _stream(dev))
     return DeviceCSR(new_indptr, ind, logv, n_genes_kept, row_scale=row_scale), sums
 
 
@@ -216,6 +261,7 @@ def subset_fill_log_scale_sums(X: DeviceCSR, cell_mask, remap, new_indptr, row_s
 def normalize_log1p(X: DeviceCSR, target_sum: float = 1e4) -> DeviceCSR:
     """sc.pp.normalize_total(target_sum) followed by sc.pp.log1p (out of place).  The result
     keeps a reference to the raw counts and the per-row factor for highly_variable_genes."""
+    X = X.to_f32()  # the standalone (unfused) step writes float values in the input's layout
     dev = X.device
     out = torch.empty_like(X.data)
     scale = torch.empty(X.n_rows, dtype=torch.float32, device=dev)
@@ -234,8 +280,8 @@ def hvg_gene_sums(X: DeviceCSR, counts=None, row_scale=None, gene_remap=None, n_
     n_out = X.n_cols if n_out is None else n_out
     if sums is None:
         sums = torch.zeros((2, 2, n_out), dtype=torch.int64, device=X.device)
-    _lib.call("scb_hvg_gene_sums", _ctx(X.data), _p(X.indptr), _p(X.indices), _p(counts), _p(row_scale),
-              X.n_rows, X.n_cols, _p(gene_remap), n_out, _p(row_splits), _p(sums), _stream(X.device))
+    _lib.call("scb_hvg_gene_sums" + _fmt(X.indices, counts), _ctx(X.data), _p(X.indptr), _p(X.indices), _p(counts),
+              _p(row_scale), X.n_rows, X.n_cols, _p(gene_remap), n_out, _p(row_splits), _p(sums), _stream(X.device))
     return sums
 
 
