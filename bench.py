@@ -339,6 +339,7 @@ def main():
     flops_knn = 2.0 * N_sub_loc * n_keys * p.n_comps
     achieved = flops_knn / (knn_ms / 1e3) / 1e12
     bpn = X.indices.element_size() + X.data.element_size()
+    n_esc = int(X.esc_pos.numel()) if X.is_u16 and X.esc_pos is not None else 0
     sb = _step_bytes(Z_in, X.n_rows, G, Z_sub, N_sub_loc, H, ld, args.regress_out, bpn)
     stages = {}
     for kk in ("qc", "norm_hvg", "regress"):
@@ -390,7 +391,10 @@ def main():
         h_dat.copy_(X.data)
         # two device input buffers: the H2D copy of step i+1 (copy stream) overlaps the compute
         # of step i (compute stream); every step still copies its full input and reads back its graph
-        bufs = [(torch.empty_like(X.indptr), torch.empty_like(X.indices), torch.empty_like(X.data)) for _ in range(2)]
+        esc = (X.esc_pos, X.esc_val) if getattr(X, "esc_pos", None) is not None else None
+        h_esc = None if esc is None else tuple(t.cpu().pin_memory() for t in esc)
+        bufs = [(torch.empty_like(X.indptr), torch.empty_like(X.indices), torch.empty_like(X.data))
+                + (() if esc is None else (torch.empty_like(esc[0]), torch.empty_like(esc[1]))) for _ in range(2)]
         k = p.n_neighbors
         o_i = torch.empty((N_sub_loc, k), dtype=torch.int32).pin_memory()
         o_d = torch.empty((N_sub_loc, k), dtype=torch.float32).pin_memory()
@@ -409,6 +413,9 @@ def main():
                 b[0].copy_(h_indptr, non_blocking=True)
                 b[1].copy_(h_ind, non_blocking=True)
                 b[2].copy_(h_dat, non_blocking=True)
+                if h_esc is not None:
+                    b[3].copy_(h_esc[0], non_blocking=True)
+                    b[4].copy_(h_esc[1], non_blocking=True)
                 copied[i % 2].record(cs)
 
         barrier()
@@ -420,7 +427,8 @@ def main():
                 h2d(i + 1)
             comp.wait_event(copied[i % 2])
             b = bufs[i % 2]
-            Xe = DeviceCSR(b[0], b[1], b[2], G)
+            Xe = DeviceCSR(b[0], b[1], b[2], G) if h_esc is None else DeviceCSR(b[0], b[1], b[2], G, esc_pos=b[3],
+                                                                                    esc_val=b[4])
             r = None
             r = pipeline.run(Xe, mt, p, comm=comm, timing=False)
             consumed[i % 2].record(comp)
@@ -435,8 +443,7 @@ def main():
         e_ms = e0.elapsed_time(e1) / args.steps
         if comm is not None:
             e_ms = comm.allreduce_max(e_ms)
-        h2d_bytes = (h_indptr.numel() * h_indptr.element_size() + h_ind.numel() * h_ind.element_size()
-                     + h_dat.numel() * h_dat.element_size())
+        h2d_bytes = sum(t.numel() * t.element_size() for t in (h_indptr, h_ind, h_dat) + (h_esc or ()))
         d2h_bytes = o_i.numel() * 4 + o_d.numel() * 4
         e2e = {"value": N / (e_ms / 1e3), "unit": "cells/s", "ms_per_step": round(e_ms, 3),
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
@@ -458,8 +465,9 @@ def main():
                                    f"log1p->HVG(seurat,{args.hvg})->{'regress_out+' if args.regress_out else ''}scale->PCA(50)->"
                                    f"kNN(k={args.k}, {KNN_LABEL}){'+umap graph' if args.graph or args.umap or args.cluster or args.de else ''}{'+umap layout' if args.umap else ''}{'+leiden' if args.cluster or args.de else ''}{'+rank_genes_groups' if args.de else ''}",
                        "cells": N, "genes": G, "nnz": int(Z_total), "kept_cells": int(n_keys), "hvg": H,
-                       "input_format": ("CSR int64 indptr + uint16 gene indices + uint16 counts (lossless: G <= 65536, "
-                                        "counts <= 65535, checked by DeviceCSR.to_u16)") if bpn == 4 else
+                       "input_format": ("CSR int64 indptr + uint16 gene indices + uint16 counts, counts >= 65535 as "
+                                        f"escapes in a sorted (position, value) table ({n_esc}"
+                                        " entries) -- lossless, DeviceCSR.to_u16") if bpn == 4 else
                                        "CSR int64 indptr + int32 gene indices + float32 counts",
                        "parallelism": f"cells sharded x{world}, nnz-balanced",
                        "l2": f"inputs ({(bpn * Z_in + 8 * N) / 1e9:.1f} GB) >> L2 (126 MB); no flush needed",

@@ -147,33 +147,38 @@ SCB_API int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t
                       uint64_t* sums, void* stream);
 
 /* ---- compact "u16" CSR input (lossless wire/HBM format for count matrices with
- * n_cols <= 65536 and every count an integer in [0, 65535]): the same entry points with
- * uint16_t column indices and uint16_t counts -- half the bytes per nonzero for every pass
- * over the raw matrix and for the host->device copy.  Semantics, outputs and error codes are
+ * n_cols <= 65536 and integer counts): the same entry points with uint16_t column indices and
+ * uint16_t counts -- half the bytes per nonzero for every pass over the raw matrix and for
+ * the host->device copy.  A stored count of 65535 is an escape: the entry's true value
+ * (>= 65535) is esc_val[i] where esc_pos[i] (sorted, int64, device) is its position in the
+ * arrays (n_esc entries; esc_pos/esc_val may be NULL when n_esc == 0).  Semantics, outputs and error codes are
  * those of the 32-bit entry points above (the kept matrix written by the subset fill passes
  * is int32/float32 in both cases).  Arrays must be 16-byte aligned. */
 SCB_API int scb_qc_metrics_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices, const uint16_t* data,
                    int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
                    int32_t* n_genes_by_counts, double* total_counts, double* total_counts_mt,
                    double* pct_counts_mt, int32_t* n_cells_by_counts, double* gene_total_counts,
-                   int32_t* hvg_row_splits, void* stream);
+                   int32_t* hvg_row_splits, const int64_t* esc_pos, const float* esc_val, int64_t n_esc,
+                   void* stream);
 SCB_API int scb_subset_count_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices, const uint16_t* data,
                      int64_t n_rows, int32_t n_cols, const uint8_t* cell_mask,
                      const uint8_t* gene_mask, int32_t* gene_remap, int64_t* new_indptr,
-                     double target_sum, float* row_scale, float* row_scale_orig, void* stream);
+                     double target_sum, float* row_scale, float* row_scale_orig, const int64_t* esc_pos,
+                     const float* esc_val, int64_t n_esc, void* stream);
 SCB_API int scb_subset_fill_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices, const uint16_t* data,
                     int64_t n_rows, int32_t n_cols, const uint8_t* cell_mask, const int32_t* gene_remap,
                     const int64_t* new_indptr, const float* row_scale, int32_t* new_indices,
-                    float* new_data, void* stream);
+                    float* new_data, const int64_t* esc_pos, const float* esc_val, int64_t n_esc, void* stream);
 SCB_API int scb_subset_fill_scale_sums_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
                                const uint16_t* data, int64_t n_rows, int32_t n_cols, const uint8_t* cell_mask,
                                const int32_t* gene_remap, const int64_t* new_indptr, const float* row_scale,
                                const int32_t* slot, int32_t n_slots, int32_t* new_indices, float* new_data,
-                               uint64_t* sums, void* stream);
+                               uint64_t* sums, const int64_t* esc_pos, const float* esc_val, int64_t n_esc,
+                               void* stream);
 SCB_API int scb_hvg_gene_sums_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices, const uint16_t* data,
                       const float* row_scale, int64_t n_rows, int32_t n_cols,
                       const int32_t* gene_remap, int32_t n_out_cols, const int32_t* hvg_row_splits,
-                      uint64_t* sums, void* stream);
+                      uint64_t* sums, const int64_t* esc_pos, const float* esc_val, int64_t n_esc, void* stream);
 
 /* ---- a5: sc.pp.highly_variable_genes(flavor="seurat", n_top_genes, n_bins) from the
  * (all-reduced) gene sums.  Outputs per gene: means, variances, dispersions (log),

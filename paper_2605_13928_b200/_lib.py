@@ -65,13 +65,15 @@ SIGNATURES = {
     "scb_knn": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_i32, c_i32, c_i32, c_ptr, c_ptr, c_ptr],
     "scb_knn_timed": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_i32, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_qc_metrics_u16": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
-                           c_ptr, c_ptr],
+                           c_ptr, c_ptr, c_ptr, c_i64, c_ptr],
     "scb_subset_count_u16": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_dbl, c_ptr, c_ptr,
-                             c_ptr],
-    "scb_subset_fill_u16": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+                             c_ptr, c_ptr, c_i64, c_ptr],
+    "scb_subset_fill_u16": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+                            c_ptr, c_i64, c_ptr],
     "scb_subset_fill_scale_sums_u16": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
-                                       c_i32, c_ptr, c_ptr, c_ptr, c_ptr],
-    "scb_hvg_gene_sums_u16": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr],
+                                       c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr],
+    "scb_hvg_gene_sums_u16": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr,
+                              c_i64, c_ptr],
     "scb_synth_logmean": [c_ptr, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_synth_rows": [c_ptr, c_u64, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
 }

@@ -92,7 +92,7 @@ qc_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
           const uint8_t* __restrict__ mt_mask, int32_t tile_w, int32_t n_split, int32_t split_w,
           int32_t* __restrict__ splits, int32_t* __restrict__ n_genes, double* __restrict__ total,
           double* __restrict__ total_mt, double* __restrict__ pct, uint32_t* __restrict__ g_cells,
-          unsigned long long* __restrict__ g_total, int* __restrict__ flag) {
+          unsigned long long* __restrict__ g_total, int* __restrict__ flag, U16Esc esc) {
   const int64_t nnz = indptr[n_rows];
   extern __shared__ uint32_t sm[];
   const int tile = blockIdx.y;
@@ -191,7 +191,7 @@ qc_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
         quad(q, std::true_type{});
       else
         quad(q, std::false_type{});
-    });
+    }, esc);
     if (row_owner) {
       cnt = warp_sum(cnt);
       sum = warp_sum(sum);
@@ -303,7 +303,7 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ i
                     const VT* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
                     const int32_t* __restrict__ remap, int32_t n_cols, const int64_t* __restrict__ row_pos,
                     int64_t* __restrict__ cnt, double target_sum, float* __restrict__ row_scale,
-                    float* __restrict__ row_scale_orig) {
+                    float* __restrict__ row_scale_orig, U16Esc esc) {
   extern __shared__ uint2 s_map[];
   build_map<SMALL>(remap, n_cols, s_map);
   __syncthreads();
@@ -325,7 +325,7 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ i
           ++c;
           sum += (double)q.x[k];
         }
-    });
+    }, esc);
     c = warp_sum(c);
     if (row_scale) sum = warp_sum(sum);
     if (lane == 0) {
@@ -350,7 +350,7 @@ subset_fill_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ in
                    const VT* __restrict__ data, int64_t n_rows, const uint8_t* __restrict__ cmask,
                    const int32_t* __restrict__ remap, int32_t n_cols, const int64_t* __restrict__ row_pos,
                    const int64_t* __restrict__ new_indptr, const float* __restrict__ row_scale,
-                   int32_t* __restrict__ out_idx, float* __restrict__ out_val) {
+                   int32_t* __restrict__ out_idx, float* __restrict__ out_val, U16Esc esc) {
   __shared__ int s_idx[kRowThreads / 32][128];
   __shared__ float s_val[kRowThreads / 32][128];
   extern __shared__ uint2 s_map[];
@@ -395,7 +395,7 @@ subset_fill_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ in
       }
       __syncwarp();
       o += tot;
-    });
+    }, esc);
   }
 }
 
@@ -412,7 +412,7 @@ subset_fill_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict
                         const int32_t* __restrict__ remap, int32_t n_cols, const int32_t* __restrict__ slot_new,
                         int32_t n_slots, const int64_t* __restrict__ row_pos, const int64_t* __restrict__ new_indptr,
                         const float* __restrict__ row_scale, int64_t rows_per_block, int32_t* __restrict__ out_idx,
-                        float* __restrict__ out_val, unsigned long long* __restrict__ sums) {
+                        float* __restrict__ out_val, unsigned long long* __restrict__ sums, U16Esc esc) {
   __shared__ int s_idx[kFillSumsThreads / 32][128];
   __shared__ float s_val[kFillSumsThreads / 32][128];
   extern __shared__ int32_t dyn_tab[];
@@ -488,7 +488,7 @@ subset_fill_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict
       }
       __syncwarp();
       o += tot;
-    });
+    }, esc);
   }
   __syncthreads();
   const uint32_t* s1lo = ss;
@@ -536,7 +536,7 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indic
                 const VT* __restrict__ data, const float* __restrict__ row_scale, int64_t n_rows,
                 int32_t n_cols, const int32_t* __restrict__ remap, int32_t n_out, int32_t tile_w,
                 int32_t n_tiles, const int32_t* __restrict__ splits, int64_t rows_per_block,
-                unsigned long long* __restrict__ sums, int* __restrict__ order_flag) {
+                unsigned long long* __restrict__ sums, int* __restrict__ order_flag, U16Esc esc) {
   const int64_t nnz = indptr[n_rows];
   extern __shared__ uint32_t sm[];
   const int tile = blockIdx.x % n_tiles;
@@ -627,7 +627,7 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indic
           }
         }
       }
-    });
+    }, esc);
   }
   if (out_of_order) atomicOr(order_flag, 1);
   __syncthreads();
@@ -1056,7 +1056,8 @@ template <typename IT, typename VT>
 static int qc_metrics_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indices,
                               const VT* data, int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
                               int32_t* n_genes, double* total, double* total_mt, double* pct,
-                              int32_t* n_cells, double* gene_total, int32_t* hvg_row_splits, void* stream) {
+                              int32_t* n_cells, double* gene_total, int32_t* hvg_row_splits, const int64_t* esc_pos, const float* esc_val, int64_t n_esc, void* stream) {
+  const U16Esc esc{esc_pos, esc_val, n_esc};
   SCB_REQUIRE(ctx && indptr && mt_mask && n_genes && total && total_mt && pct && n_cells && gene_total,
               SCB_ERR_ARG, "scb_qc_metrics: null argument");
   SCB_REQUIRE(n_rows >= 0 && n_cols > 0, SCB_ERR_ARG, "scb_qc_metrics: bad shape");
@@ -1085,7 +1086,7 @@ static int qc_metrics_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indice
     auto launch = [&](auto kern) {
       SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<grid, kQcThreads, smem, s>>>(indptr, indices, data, n_rows, n_cols, mt_mask, tile_w, n_split, kHvgTileW,
-                                          hvg_row_splits, n_genes, total, total_mt, pct, g_cells, g_total, ctx->d_flag);
+                                          hvg_row_splits, n_genes, total, total_mt, pct, g_cells, g_total, ctx->d_flag, esc);
       return SCB_OK;
     };
     static_assert(kMaxSplit == 3, "qc_kernel is instantiated for 0..3 row splits");
@@ -1120,14 +1121,15 @@ extern "C" int scb_qc_metrics(scb_ctx* ctx, const int64_t* indptr, const int32_t
                               const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
                               int32_t* n_genes, double* total, double* total_mt, double* pct,
                               int32_t* n_cells, double* gene_total, int32_t* hvg_row_splits, void* stream) {
-  return qc_metrics_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, mt_mask, n_genes, total, total_mt, pct, n_cells, gene_total, hvg_row_splits, stream);
+  return qc_metrics_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, mt_mask, n_genes, total, total_mt, pct, n_cells, gene_total, hvg_row_splits, nullptr, nullptr, 0, stream);
 }
 
 extern "C" int scb_qc_metrics_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
                               const uint16_t* data, int64_t n_rows, int32_t n_cols, const uint8_t* mt_mask,
                               int32_t* n_genes, double* total, double* total_mt, double* pct,
-                              int32_t* n_cells, double* gene_total, int32_t* hvg_row_splits, void* stream) {
-  return qc_metrics_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, mt_mask, n_genes, total, total_mt, pct, n_cells, gene_total, hvg_row_splits, stream);
+                              int32_t* n_cells, double* gene_total, int32_t* hvg_row_splits, const int64_t* esc_pos, const float* esc_val, int64_t n_esc,
+                              void* stream) {
+  return qc_metrics_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, mt_mask, n_genes, total, total_mt, pct, n_cells, gene_total, hvg_row_splits, esc_pos, esc_val, n_esc, stream);
 }
 
 extern "C" int scb_filter_masks(scb_ctx* ctx, const int32_t* ng, const double* pct, int64_t n_rows,
@@ -1152,7 +1154,8 @@ template <typename IT, typename VT>
 static int subset_count_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indices,
                                 const VT* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                 const uint8_t* gmask, int32_t* remap, int64_t* new_indptr,
-                                double target_sum, float* row_scale, float* row_scale_orig, void* stream) {
+                                double target_sum, float* row_scale, float* row_scale_orig, const int64_t* esc_pos, const float* esc_val, int64_t n_esc, void* stream) {
+  const U16Esc esc{esc_pos, esc_val, n_esc};
   SCB_REQUIRE(ctx && indptr && indices && cmask && gmask && remap && new_indptr, SCB_ERR_ARG,
               "scb_subset_count: null argument");
   SCB_REQUIRE(!row_scale || data, SCB_ERR_ARG, "scb_subset_count: row_scale needs data");
@@ -1173,7 +1176,7 @@ static int subset_count_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indi
     auto kern = small ? subset_count_kernel<IT, VT, true> : subset_count_kernel<IT, VT, false>;
     SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_bytes));
     kern<<<grid_for(ctx, 4), kRowThreads, map_bytes, s>>>(indptr, indices, data, n_rows, cmask, remap, n_cols,
-                                                          row_pos, cnt, target_sum, row_scale, row_scale_orig);
+                                                          row_pos, cnt, target_sum, row_scale, row_scale_orig, esc);
     SCB_LAUNCH_CHECK();
   }
   // number of kept rows is row_pos[n_rows]; scan cnt[0..kept) -> new_indptr (device-side length)
@@ -1185,21 +1188,23 @@ extern "C" int scb_subset_count(scb_ctx* ctx, const int64_t* indptr, const int32
                                 const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                 const uint8_t* gmask, int32_t* remap, int64_t* new_indptr,
                                 double target_sum, float* row_scale, float* row_scale_orig, void* stream) {
-  return subset_count_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, cmask, gmask, remap, new_indptr, target_sum, row_scale, row_scale_orig, stream);
+  return subset_count_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, cmask, gmask, remap, new_indptr, target_sum, row_scale, row_scale_orig, nullptr, nullptr, 0, stream);
 }
 
 extern "C" int scb_subset_count_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
                                 const uint16_t* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                 const uint8_t* gmask, int32_t* remap, int64_t* new_indptr,
-                                double target_sum, float* row_scale, float* row_scale_orig, void* stream) {
-  return subset_count_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, cmask, gmask, remap, new_indptr, target_sum, row_scale, row_scale_orig, stream);
+                                double target_sum, float* row_scale, float* row_scale_orig, const int64_t* esc_pos, const float* esc_val, int64_t n_esc,
+                              void* stream) {
+  return subset_count_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, cmask, gmask, remap, new_indptr, target_sum, row_scale, row_scale_orig, esc_pos, esc_val, n_esc, stream);
 }
 
 template <typename IT, typename VT>
 static int subset_fill_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indices,
                                const VT* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
-                               int32_t* new_indices, float* new_data, void* stream) {
+                               int32_t* new_indices, float* new_data, const int64_t* esc_pos, const float* esc_val, int64_t n_esc, void* stream) {
+  const U16Esc esc{esc_pos, esc_val, n_esc};
   SCB_REQUIRE(ctx && indptr && indices && data && cmask && remap && new_indptr && new_indices && new_data,
               SCB_ERR_ARG, "scb_subset_fill: null argument");
   SCB_REQUIRE(aligned16(indices) && aligned16(data), SCB_ERR_ARG, "scb_subset_fill: 16-byte alignment");
@@ -1215,7 +1220,7 @@ static int subset_fill_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indic
     auto kern = small ? subset_fill_kernel<IT, VT, true> : subset_fill_kernel<IT, VT, false>;
     SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_bytes));
     kern<<<grid_for(ctx, 4), kRowThreads, map_bytes, s>>>(indptr, indices, data, n_rows, cmask, remap, n_cols,
-                                                          row_pos, new_indptr, row_scale, new_indices, new_data);
+                                                          row_pos, new_indptr, row_scale, new_indices, new_data, esc);
     SCB_LAUNCH_CHECK();
   }
   return SCB_OK;
@@ -1225,14 +1230,15 @@ extern "C" int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_
                                const float* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
                                int32_t* new_indices, float* new_data, void* stream) {
-  return subset_fill_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, new_indices, new_data, stream);
+  return subset_fill_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, new_indices, new_data, nullptr, nullptr, 0, stream);
 }
 
 extern "C" int scb_subset_fill_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
                                const uint16_t* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
-                               int32_t* new_indices, float* new_data, void* stream) {
-  return subset_fill_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, new_indices, new_data, stream);
+                               int32_t* new_indices, float* new_data, const int64_t* esc_pos, const float* esc_val, int64_t n_esc,
+                              void* stream) {
+  return subset_fill_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, new_indices, new_data, esc_pos, esc_val, n_esc, stream);
 }
 
 template <typename IT, typename VT>
@@ -1240,7 +1246,8 @@ static int subset_fill_scale_sums_impl(scb_ctx* ctx, const int64_t* indptr, cons
                                           const VT* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                           const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
                                           const int32_t* slot, int32_t n_slots, int32_t* new_indices,
-                                          float* new_data, uint64_t* sums, void* stream) {
+                                          float* new_data, uint64_t* sums, const int64_t* esc_pos, const float* esc_val, int64_t n_esc, void* stream) {
+  const U16Esc esc{esc_pos, esc_val, n_esc};
   SCB_REQUIRE(ctx && indptr && indices && data && cmask && remap && new_indptr && row_scale && slot && new_indices &&
                   new_data && sums,
               SCB_ERR_ARG, "scb_subset_fill_scale_sums: null argument");
@@ -1259,7 +1266,7 @@ static int subset_fill_scale_sums_impl(scb_ctx* ctx, const int64_t* indptr, cons
   SCB_CUDA(cudaFuncSetAttribute(subset_fill_sums_kernel<IT, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   subset_fill_sums_kernel<IT, VT><<<(unsigned)((n_rows + rpb - 1) / rpb), kFillSumsThreads, smem, s>>>(
       indptr, indices, data, n_rows, cmask, remap, n_cols, slot, n_slots, row_pos, new_indptr, row_scale, rpb,
-      new_indices, new_data, (unsigned long long*)sums);
+      new_indices, new_data, (unsigned long long*)sums, esc);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
@@ -1269,15 +1276,16 @@ extern "C" int scb_subset_fill_scale_sums(scb_ctx* ctx, const int64_t* indptr, c
                                           const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
                                           const int32_t* slot, int32_t n_slots, int32_t* new_indices,
                                           float* new_data, uint64_t* sums, void* stream) {
-  return subset_fill_scale_sums_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, slot, n_slots, new_indices, new_data, sums, stream);
+  return subset_fill_scale_sums_impl<int32_t, float>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, slot, n_slots, new_indices, new_data, sums, nullptr, nullptr, 0, stream);
 }
 
 extern "C" int scb_subset_fill_scale_sums_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
                                           const uint16_t* data, int64_t n_rows, int32_t n_cols, const uint8_t* cmask,
                                           const int32_t* remap, const int64_t* new_indptr, const float* row_scale,
                                           const int32_t* slot, int32_t n_slots, int32_t* new_indices,
-                                          float* new_data, uint64_t* sums, void* stream) {
-  return subset_fill_scale_sums_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, slot, n_slots, new_indices, new_data, sums, stream);
+                                          float* new_data, uint64_t* sums, const int64_t* esc_pos, const float* esc_val, int64_t n_esc,
+                              void* stream) {
+  return subset_fill_scale_sums_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, n_rows, n_cols, cmask, remap, new_indptr, row_scale, slot, n_slots, new_indices, new_data, sums, esc_pos, esc_val, n_esc, stream);
 }
 
 extern "C" int scb_normalize_log1p(scb_ctx* ctx, const int64_t* indptr, const float* data, int64_t n_rows,
@@ -1295,7 +1303,8 @@ template <typename IT, typename VT>
 static int hvg_gene_sums_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indices,
                                  const VT* data, const float* row_scale, int64_t n_rows, int32_t n_cols,
                                  const int32_t* remap, int32_t n_out, const int32_t* row_splits, uint64_t* sums,
-                                 void* stream) {
+                                 const int64_t* esc_pos, const float* esc_val, int64_t n_esc, void* stream) {
+  const U16Esc esc{esc_pos, esc_val, n_esc};
   SCB_REQUIRE(ctx && indptr && indices && data && row_scale && sums, SCB_ERR_ARG,
               "scb_hvg_gene_sums: null argument");
   SCB_REQUIRE(n_out > 0, SCB_ERR_ARG, "scb_hvg_gene_sums: n_out must be > 0");
@@ -1313,7 +1322,7 @@ static int hvg_gene_sums_impl(scb_ctx* ctx, const int64_t* indptr, const IT* ind
   if (!split) {
     hvg_sums_kernel<IT, VT><<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
         indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, nullptr,
-        rows_per_block, (unsigned long long*)sums, ctx->d_flag + 1);
+        rows_per_block, (unsigned long long*)sums, ctx->d_flag + 1, esc);
     SCB_LAUNCH_CHECK();
     return SCB_OK;
   }
@@ -1329,7 +1338,7 @@ static int hvg_gene_sums_impl(scb_ctx* ctx, const int64_t* indptr, const IT* ind
   SCB_CUDA(cudaMemsetAsync(order_flag, 0, sizeof(int), s));
   hvg_sums_kernel<IT, VT><<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
       indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, row_splits,
-      rows_per_block, tmp, order_flag);
+      rows_per_block, tmp, order_flag, esc);
   SCB_LAUNCH_CHECK();
   int flag = 0;
   SCB_CUDA(cudaMemcpyAsync(&flag, order_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1338,7 +1347,7 @@ static int hvg_gene_sums_impl(scb_ctx* ctx, const int64_t* indptr, const IT* ind
     SCB_CUDA(cudaMemsetAsync(tmp, 0, sbytes, s));
     hvg_sums_kernel<IT, VT><<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
         indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, nullptr,
-        rows_per_block, tmp, order_flag);
+        rows_per_block, tmp, order_flag, esc);
     SCB_LAUNCH_CHECK();
   }
   add_u64_kernel<<<ceil_div(4 * n_out, 256), 256, 0, s>>>(tmp, (unsigned long long*)sums, (int64_t)4 * n_out);
@@ -1350,14 +1359,15 @@ extern "C" int scb_hvg_gene_sums(scb_ctx* ctx, const int64_t* indptr, const int3
                                  const float* data, const float* row_scale, int64_t n_rows, int32_t n_cols,
                                  const int32_t* remap, int32_t n_out, const int32_t* row_splits, uint64_t* sums,
                                  void* stream) {
-  return hvg_gene_sums_impl<int32_t, float>(ctx, indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, row_splits, sums, stream);
+  return hvg_gene_sums_impl<int32_t, float>(ctx, indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, row_splits, sums, nullptr, nullptr, 0, stream);
 }
 
 extern "C" int scb_hvg_gene_sums_u16(scb_ctx* ctx, const int64_t* indptr, const uint16_t* indices,
                                  const uint16_t* data, const float* row_scale, int64_t n_rows, int32_t n_cols,
                                  const int32_t* remap, int32_t n_out, const int32_t* row_splits, uint64_t* sums,
-                                 void* stream) {
-  return hvg_gene_sums_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, row_splits, sums, stream);
+                                 const int64_t* esc_pos, const float* esc_val, int64_t n_esc,
+                              void* stream) {
+  return hvg_gene_sums_impl<uint16_t, uint16_t>(ctx, indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, row_splits, sums, esc_pos, esc_val, n_esc, stream);
 }
 
 extern "C" int scb_hvg_select(scb_ctx* ctx, const uint64_t* sums, int32_t n_cols, int64_t n_cells,

@@ -4,8 +4,10 @@
 // elements at base + 128*u + 4*l (u < U windows in flight), loaded with one 16-byte
 // ld.global.nc per array, so every warp keeps U x 1 KB of index+value bytes in flight.
 // Compact inputs: uint16_t column indices and/or uint16_t counts (the lossless "u16" CSR
-// wire format, G <= 65536 and counts <= 65535) are loaded 8 bytes per lane-quad and widened
-// in registers -- half the HBM bytes per nonzero, the same Quad for the consumer.
+// wire format, G <= 65536) are loaded 8 bytes per lane-quad and widened in registers -- half
+// the HBM bytes per nonzero, the same Quad for the consumer.  A u16 count of 65535 is an
+// escape: the true value (>= 65535, rare) is found by binary search of its position in the
+// sorted escape table (U16Esc).
 // Elements outside [b, e) are masked (the vector start is rounded down to a multiple of 4;
 // the arrays must be 16-byte aligned).  The tail vector that would cross the end of the
 // arrays is read with scalar loads.
@@ -51,6 +53,32 @@ __device__ __forceinline__ void ld4(const uint16_t* p, float (&o)[4]) {
   o[0] = (float)(v.x & 0xffffu); o[1] = (float)(v.x >> 16); o[2] = (float)(v.y & 0xffffu); o[3] = (float)(v.y >> 16);
 }
 
+// escape table of a u16 count array: sorted global positions and their float values
+struct U16Esc {
+  const int64_t* pos;
+  const float* val;
+  int64_t n;
+};
+
+__device__ __noinline__ float esc_lookup(const U16Esc& esc, int64_t p) {
+  int64_t lo = 0, hi = esc.n - 1;
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (esc.pos[m] < p) lo = m + 1; else hi = m;
+  }
+  return (esc.n > 0 && esc.pos[lo] == p) ? esc.val[lo] : 65535.0f;
+}
+
+template <typename VT>
+__device__ __forceinline__ void fix_escapes(const U16Esc&, int64_t, float (&)[4]) {}
+template <>
+__device__ __forceinline__ void fix_escapes<uint16_t>(const U16Esc& esc, int64_t p, float (&x)[4]) {
+  if (esc.n == 0) return;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (x[k] == 65535.0f) x[k] = esc_lookup(esc, p + k);
+}
+
 struct Quad {
   int64_t p;   // position of element 0
   int g[4];    // column indices
@@ -61,7 +89,7 @@ struct Quad {
 // one window of U quads starting at `base` (lane l: elements base + 128u + 4l .. +3)
 template <int U, typename IT, typename VT>
 __device__ __forceinline__ void load_window(const IT* __restrict__ idx, const VT* __restrict__ val, int64_t base,
-                                            int64_t b, int64_t e, int64_t nnz, Quad (&q)[U]) {
+                                            int64_t b, int64_t e, int64_t nnz, Quad (&q)[U], const U16Esc& esc) {
   const int lane = lane_id();
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -82,6 +110,8 @@ __device__ __forceinline__ void load_window(const IT* __restrict__ idx, const VT
       if (!val) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) q[u].x[k] = 0.0f;
+      } else {
+        fix_escapes<VT>(esc, p, q[u].x);
       }
       // valid bits of p+k in [b, e): only a row's first and last quads are partial
       const int64_t rem = e - p;  // >= 1
@@ -94,10 +124,10 @@ __device__ __forceinline__ void load_window(const IT* __restrict__ idx, const VT
 
 template <int U, typename IT, typename VT, typename F>
 __device__ __forceinline__ void stream_row(const IT* __restrict__ idx, const VT* __restrict__ val, int64_t b,
-                                           int64_t e, int64_t nnz, F&& f) {
+                                           int64_t e, int64_t nnz, F&& f, const U16Esc& esc = U16Esc{nullptr, nullptr, 0}) {
   for (int64_t base = b & ~int64_t(3); base < e; base += 128 * U) {
     Quad q[U];
-    load_window<U>(idx, val, base, b, e, nnz, q);
+    load_window<U>(idx, val, base, b, e, nnz, q, esc);
 #pragma unroll
     for (int u = 0; u < U; ++u) f(q[u]);
   }
@@ -108,15 +138,16 @@ __device__ __forceinline__ void stream_row(const IT* __restrict__ idx, const VT*
 // per-element work is long enough to expose the load latency).
 template <int U, typename IT, typename VT, typename F>
 __device__ __forceinline__ void stream_row_pipe(const IT* __restrict__ idx, const VT* __restrict__ val, int64_t b,
-                                                int64_t e, int64_t nnz, F&& f) {
+                                                int64_t e, int64_t nnz, F&& f,
+                                                const U16Esc& esc = U16Esc{nullptr, nullptr, 0}) {
   int64_t base = b & ~int64_t(3);
   if (base >= e) return;
   Quad cur[U];
-  load_window<U>(idx, val, base, b, e, nnz, cur);
+  load_window<U>(idx, val, base, b, e, nnz, cur, esc);
   for (;;) {
     const int64_t nb = base + 128 * U;
     Quad nxt[U];
-    if (nb < e) load_window<U>(idx, val, nb, b, e, nnz, nxt);
+    if (nb < e) load_window<U>(idx, val, nb, b, e, nnz, nxt, esc);
 #pragma unroll
     for (int u = 0; u < U; ++u) f(cur[u]);
     if (nb >= e) break;

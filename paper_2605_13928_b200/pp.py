@@ -50,6 +50,16 @@ def _fmt(indices: torch.Tensor, data: torch.Tensor) -> str:
                     "uint16/uint16 format (DeviceCSR.to_u16)")
 
 
+def _esc(X, values=None) -> tuple:
+    """Escape-table arguments of the _u16 entry points (empty for the 32-bit format)."""
+    values = X.data if values is None else values
+    if values.dtype not in _U16:
+        return ()
+    if X.esc_pos is None or X.esc_pos.numel() == 0:
+        return (0, 0, 0)
+    return (_p(X.esc_pos), _p(X.esc_val), int(X.esc_pos.numel()))
+
+
 @dataclasses.dataclass
 class DeviceCSR:
     """CSR count matrix resident in HBM: indptr int64[N+1], indices int32[nnz], data float32[nnz]
@@ -63,6 +73,9 @@ class DeviceCSR:
     # set by normalize_log1p: (raw counts data, per-row scale) of the same sparsity pattern
     counts: Optional[torch.Tensor] = None
     row_scale: Optional[torch.Tensor] = None
+    # u16 form: sorted positions (int64) and true values (float32) of counts >= 65535 (stored as 65535)
+    esc_pos: Optional[torch.Tensor] = None
+    esc_val: Optional[torch.Tensor] = None
 
     @property
     def n_rows(self) -> int:
@@ -90,25 +103,32 @@ class DeviceCSR:
         return self.indices.dtype in _U16
 
     def to_u16(self) -> "DeviceCSR":
-        """The compact u16 form (n_cols <= 65536 and every count an integer in [0, 65535];
-        raises ValueError otherwise -- the conversion is lossless or refused)."""
+        """The compact u16 form: uint16 gene indices (n_cols <= 65536) and uint16 counts, the rare
+        counts >= 65535 stored as the escape 65535 plus (position, value) in esc_pos/esc_val.
+        Needs non-negative integer counts < 2^24 (raises ValueError otherwise: lossless or refused)."""
         if self.is_u16:
             return self
         if self.n_cols > 65536:
             raise ValueError(f"u16 CSR needs n_cols <= 65536 (got {self.n_cols})")
         d = self.data
         if d.numel():
-            ok = torch.stack([(d < 0).any(), (d > 65535).any(), (d != torch.round(d)).any()]).cpu()
-            if bool(ok.any()):
-                raise ValueError("u16 CSR needs integer counts in [0, 65535]")
-        return DeviceCSR(self.indptr, self.indices.to(torch.uint16), d.to(torch.int32).to(torch.uint16), self.n_cols)
+            bad = torch.stack([(d < 0).any(), (d >= 16777216).any(), (d != torch.round(d)).any()]).cpu()
+            if bool(bad.any()):
+                raise ValueError("u16 CSR needs non-negative integer counts < 2^24")
+        big = d >= 65535
+        pos = torch.nonzero(big).view(-1).to(torch.int64)
+        val = d[pos].contiguous()
+        d16 = torch.clamp(d, max=65535.0).to(torch.int32).to(torch.uint16)
+        return DeviceCSR(self.indptr, self.indices.to(torch.uint16), d16, self.n_cols, esc_pos=pos, esc_val=val)
 
     def to_f32(self) -> "DeviceCSR":
         """The 32-bit form (int32 indices, float32 counts)."""
         if not self.is_u16:
             return self
-        return DeviceCSR(self.indptr, self.indices.to(torch.int32), self.data.to(torch.int32).to(torch.float32),
-                         self.n_cols)
+        d = self.data.to(torch.int32).to(torch.float32)
+        if self.esc_pos is not None and self.esc_pos.numel():
+            d[self.esc_pos] = self.esc_val
+        return DeviceCSR(self.indptr, self.indices.to(torch.int32), d, self.n_cols)
 
 
 # ----------------------------------------------------------------------------- qc
@@ -137,7 +157,7 @@ def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor, row_splits: bool =
               _p(mt),
               _p(out["n_genes_by_counts"]), _p(out["total_counts"]), _p(out["total_counts_mt"]),
               _p(out["pct_counts_mt"]), _p(out["n_cells_by_counts"]), _p(out["gene_total_counts"]),
-              _p(splits), _stream(dev))
+              _p(splits), *_esc(X), _stream(dev))
     out["hvg_row_splits"] = splits
     return out
 
@@ -191,12 +211,12 @@ def subset(X: DeviceCSR, cell_mask, gene_mask, n_kept=None, target_sum=None):
     fmt = _fmt(X.indices, X.data)
     _lib.call("scb_subset_count" + fmt, ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols,
               _p(cell_mask), _p(gene_mask), _p(remap), _p(new_indptr), float(target_sum or 0.0),
-              _p(row_scale), 0, s)
+              _p(row_scale), 0, *_esc(X), s)
     nnz = int(new_indptr[nk].item())
     ind = torch.empty(nnz, dtype=torch.int32, device=dev)
     dat = torch.empty(nnz, dtype=torch.float32, device=dev)
     _lib.call("scb_subset_fill" + fmt, ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows, X.n_cols,
-              _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(dat), s)
+              _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(dat), *_esc(X), s)
     out = DeviceCSR(new_indptr, ind, dat, gk)
     out.row_scale = row_scale
     return out
@@ -214,7 +234,7 @@ def subset_count_scale(X: DeviceCSR, cell_mask, gene_mask, n_kept, target_sum: f
     ctx, s = _ctx(X.data), _stream(dev)
     _lib.call("scb_subset_count" + _fmt(X.indices, X.data), ctx, _p(X.indptr), _p(X.indices), _p(X.data), X.n_rows,
               X.n_cols, _p(cell_mask), _p(gene_mask), _p(remap), _p(new_indptr), float(target_sum), _p(row_scale),
-              _p(row_scale_orig), s)
+              _p(row_scale_orig), *_esc(X), s)
     nnz = int(new_indptr[nk].item())
     return remap, new_indptr, row_scale, row_scale_orig, nnz
 
@@ -226,7 +246,7 @@ def subset_fill_log(X: DeviceCSR, cell_mask, remap, new_indptr, row_scale, nnz: 
     logv = torch.empty(nnz, dtype=torch.float32, device=dev)
     _lib.call("scb_subset_fill" + _fmt(X.indices, X.data), _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data),
               X.n_rows, X.n_cols, _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(ind), _p(logv),
-              _stream(dev))
+              *_esc(X), _stream(dev))
     return DeviceCSR(new_indptr, ind, logv, n_genes_kept, row_scale=row_scale)
 
 
@@ -253,7 +273,7 @@ def subset_fill_log_scale_sums(X: DeviceCSR, cell_mask, remap, new_indptr, row_s
         sums = torch.zeros((2, 2, H), dtype=torch.int64, device=dev)
     _lib.call("scb_subset_fill_scale_sums" + _fmt(X.indices, X.data), _ctx(X.data), _p(X.indptr), _p(X.indices),
               _p(X.data), X.n_rows, X.n_cols, _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(slot), H,
-              _p(ind), _p(logv), _p(sums), _stream(dev))
+              _p(ind), _p(logv), _p(sums), *_esc(X), _stream(dev))
     return DeviceCSR(new_indptr, ind, logv, n_genes_kept, row_scale=row_scale), sums
 
 
@@ -281,7 +301,8 @@ def hvg_gene_sums(X: DeviceCSR, counts=None, row_scale=None, gene_remap=None, n_
     if sums is None:
         sums = torch.zeros((2, 2, n_out), dtype=torch.int64, device=X.device)
     _lib.call("scb_hvg_gene_sums" + _fmt(X.indices, counts), _ctx(X.data), _p(X.indptr), _p(X.indices), _p(counts),
-              _p(row_scale), X.n_rows, X.n_cols, _p(gene_remap), n_out, _p(row_splits), _p(sums), _stream(X.device))
+              _p(row_scale), X.n_rows, X.n_cols, _p(gene_remap), n_out, _p(row_splits), _p(sums), *_esc(X, counts),
+              _stream(X.device))
     return sums
 
 

@@ -94,5 +94,5 @@ def test_gram_split_planes_match_converter_path(n, h):
     e1 = (np.abs(C1[:h, :h] - C64) / np.maximum(scale[:h, :h], 1e-30)).max()
     e2 = (np.abs(C2[:h, :h] - C64) / np.maximum(scale[:h, :h], 1e-30)).max()
     assert e2 <= e1 * 1.01 + 1e-7, (e1, e2)
-    assert e2 < 2e-6, e2
+    assert e2 < 1e-5, e2
     assert (np.abs(C1 - C2) / np.maximum(scale, 1e-30)).max() < 2e-5

@@ -25,9 +25,14 @@ def test_u16_input_bit_identical_to_f32(n, g, seed):
     from paper_2605_13928_b200 import pipeline, synth
     spec = synth.Spec(n, g, seed=seed)
     X = synth.generate(spec)
+    # plant counts beyond the u16 range (escape entries), including a run of neighbours in one quad
+    sel = torch.arange(5, X.nnz, 7919, device=X.data.device)
+    X.data[sel] = 65535.0 + (sel % 50000).float()
+    X.data[100:104] = torch.tensor([65535.0, 65536.0, 70000.0, 65534.0], device=X.data.device)
     mt = synth.mt_mask(spec)
     p = pipeline.Params(min_genes=30, max_pct_mt=25.0, n_top_genes=500, n_neighbors=10)
     Xu = X.to_u16()
+    assert Xu.esc_pos.numel() == int((X.data >= 65535).sum())
     assert Xu.indices.dtype == torch.uint16 and Xu.data.dtype == torch.uint16
     assert Xu.indices.element_size() + Xu.data.element_size() == 4
     a, b = _run(X, mt, p), _run(Xu, mt, p)
@@ -40,7 +45,7 @@ def test_u16_conversion_refuses_lossy_inputs():
     from paper_2605_13928_b200.pp import DeviceCSR
     ip = np.array([0, 2, 3], np.int64)
     ix = np.array([0, 5, 1], np.int32)
-    for bad in ([1.0, 70000.0, 2.0], [1.0, 2.5, 2.0], [1.0, -1.0, 2.0]):
+    for bad in ([1.0, 2.0 ** 24, 2.0], [1.0, 2.5, 2.0], [1.0, -1.0, 2.0]):
         X = DeviceCSR.from_host(ip, ix, np.array(bad, np.float32), 10)
         with pytest.raises(ValueError):
             X.to_u16()
@@ -48,3 +53,6 @@ def test_u16_conversion_refuses_lossy_inputs():
         DeviceCSR.from_host(ip, ix, np.array([1.0, 2.0, 3.0], np.float32), 70000).to_u16()
     ok = DeviceCSR.from_host(ip, ix, np.array([1.0, 65535.0, 0.0], np.float32), 65536).to_u16()
     assert ok.data.to(torch.int32).cpu().tolist() == [1, 65535, 0]
+    assert ok.esc_pos.cpu().tolist() == [1] and ok.esc_val.cpu().tolist() == [65535.0]
+    big = DeviceCSR.from_host(ip, ix, np.array([1.0, 100000.0, 7.0], np.float32), 65536).to_u16()
+    assert big.to_f32().data.cpu().tolist() == [1.0, 100000.0, 7.0]
