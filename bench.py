@@ -231,8 +231,10 @@ def main():
     ap.add_argument("--cpu-queries", type=int, default=1000, help="kNN queries of the cpu_baseline sample")
     ap.add_argument("--ref-sample", type=int, default=100000, help="cells of the reference arm's stage sample")
     ap.add_argument("--ref-queries", type=int, default=1000, help="kNN queries per reference-arm step")
-    ap.add_argument("--input", default="u16", choices=["u16", "f32"],
-                    help="device/host CSR layout: compact u16 indices+counts (lossless here) or int32/float32")
+    ap.add_argument("--input", default="f32", choices=["u16", "f32"],
+                    help="device-resident CSR layout of the timed step: int32/float32 or the compact u16 form")
+    ap.add_argument("--wire", default="u16", choices=["u16", "f32"],
+                    help="host->device layout of the e2e leg: compact u16 (decoded on the device) or int32/float32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", action="store_true",
@@ -380,25 +382,28 @@ def main():
         cpu = _cpu_line(est, cores, N, G, args.k, len(keys))
 
 
-    # ---- e2e through the public API with host buffers (H2D of the CSR + D2H of the graph)
+    # ---- e2e through the public API with host buffers: every step copies its input CSR from pinned
+    # host memory (compact u16 wire format by default, decoded on the device by scb_csr_u16_decode)
+    # and reads its kNN graph back
     e2e = None
     if not args.no_e2e:
-        h_indptr = torch.empty_like(X.indptr, device="cpu").pin_memory()
-        h_ind = torch.empty_like(X.indices, device="cpu").pin_memory()
-        h_dat = torch.empty_like(X.data, device="cpu").pin_memory()
-        h_indptr.copy_(X.indptr)
-        h_ind.copy_(X.indices)
-        h_dat.copy_(X.data)
-        # two device input buffers: the H2D copy of step i+1 (copy stream) overlaps the compute
+        wire_u16 = args.wire == "u16"
+        Xw = X.to_u16() if wire_u16 else X.to_f32()
+        arrs = [Xw.indptr, Xw.indices, Xw.data] + ([Xw.esc_pos, Xw.esc_val] if wire_u16 else [])
+        h_arrs = [torch.empty_like(t, device="cpu").pin_memory() for t in arrs]
+        for h, t in zip(h_arrs, arrs):
+            h.copy_(t)
+        # two device staging buffers: the H2D copy of step i+1 (copy stream) overlaps the compute
         # of step i (compute stream); every step still copies its full input and reads back its graph
-        esc = (X.esc_pos, X.esc_val) if getattr(X, "esc_pos", None) is not None else None
-        h_esc = None if esc is None else tuple(t.cpu().pin_memory() for t in esc)
-        bufs = [(torch.empty_like(X.indptr), torch.empty_like(X.indices), torch.empty_like(X.data))
-                + (() if esc is None else (torch.empty_like(esc[0]), torch.empty_like(esc[1]))) for _ in range(2)]
+        bufs = [[torch.empty_like(t) for t in arrs] for _ in range(2)]
         k = p.n_neighbors
         o_i = torch.empty((N_sub_loc, k), dtype=torch.int32).pin_memory()
         o_d = torch.empty((N_sub_loc, k), dtype=torch.float32).pin_memory()
-        del X
+        Xd = None
+        if wire_u16:  # decode target (32-bit CSR in HBM), reused every step
+            Xd = DeviceCSR(Xw.indptr, torch.empty(Xw.nnz, dtype=torch.int32, device=Xw.indices.device),
+                           torch.empty(Xw.nnz, dtype=torch.float32, device=Xw.indices.device), G)
+        del X, Xw, arrs
         torch.cuda.empty_cache()
         comp = torch.cuda.current_stream()
         cs = torch.cuda.Stream()
@@ -410,12 +415,8 @@ def main():
             with torch.cuda.stream(cs):
                 if i >= 2:
                     cs.wait_event(consumed[i % 2])
-                b[0].copy_(h_indptr, non_blocking=True)
-                b[1].copy_(h_ind, non_blocking=True)
-                b[2].copy_(h_dat, non_blocking=True)
-                if h_esc is not None:
-                    b[3].copy_(h_esc[0], non_blocking=True)
-                    b[4].copy_(h_esc[1], non_blocking=True)
+                for dst, src in zip(b, h_arrs):
+                    dst.copy_(src, non_blocking=True)
                 copied[i % 2].record(cs)
 
         barrier()
@@ -427,11 +428,16 @@ def main():
                 h2d(i + 1)
             comp.wait_event(copied[i % 2])
             b = bufs[i % 2]
-            Xe = DeviceCSR(b[0], b[1], b[2], G) if h_esc is None else DeviceCSR(b[0], b[1], b[2], G, esc_pos=b[3],
-                                                                                    esc_val=b[4])
+            if wire_u16:
+                Xe = DeviceCSR(b[0], b[1], b[2], G, esc_pos=b[3], esc_val=b[4]).to_f32(out=Xd)
+            else:
+                Xe = DeviceCSR(b[0], b[1], b[2], G)
+            if wire_u16:
+                consumed[i % 2].record(comp)  # the staging buffers are free once decoded
             r = None
             r = pipeline.run(Xe, mt, p, comm=comm, timing=False)
-            consumed[i % 2].record(comp)
+            if not wire_u16:
+                consumed[i % 2].record(comp)
             if r.knn_index.shape[0] != o_i.shape[0]:
                 o_i = torch.empty(tuple(r.knn_index.shape), dtype=torch.int32).pin_memory()
                 o_d = torch.empty(tuple(r.knn_dist.shape), dtype=torch.float32).pin_memory()
@@ -443,12 +449,15 @@ def main():
         e_ms = e0.elapsed_time(e1) / args.steps
         if comm is not None:
             e_ms = comm.allreduce_max(e_ms)
-        h2d_bytes = sum(t.numel() * t.element_size() for t in (h_indptr, h_ind, h_dat) + (h_esc or ()))
+        h2d_bytes = sum(t.numel() * t.element_size() for t in h_arrs)
         d2h_bytes = o_i.numel() * 4 + o_d.numel() * 4
         e2e = {"value": N / (e_ms / 1e3), "unit": "cells/s", "ms_per_step": round(e_ms, 3),
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
+               "wire_format": ("compact u16 CSR (uint16 gene indices + uint16 counts + escape table), decoded on "
+                               "the device each step (scb_csr_u16_decode, inside the timed region)") if wire_u16
+                              else "int32/float32 CSR",
                "overlap": "pinned H2D of step i+1 on a copy stream overlaps the compute of step i "
-                          "(2 device input buffers); first copy and last compute are not overlapped"}
+                          "(2 device staging buffers); first copy and last compute are not overlapped"}
 
     if rank == 0:
         line = {

@@ -180,6 +180,13 @@ SCB_API int scb_hvg_gene_sums_u16(scb_ctx* ctx, const int64_t* indptr, const uin
                       const int32_t* gene_remap, int32_t n_out_cols, const int32_t* hvg_row_splits,
                       uint64_t* sums, const int64_t* esc_pos, const float* esc_val, int64_t n_esc, void* stream);
 
+/* ---- f1 wire decode: compact u16 CSR (as above) -> int32 indices + float32 counts in HBM
+ * (arrays 16-byte aligned; the output may then feed the 32-bit entry points).  4 B read + 8 B
+ * written per nonzero; the escaped counts are scattered from (esc_pos, esc_val). */
+SCB_API int scb_csr_u16_decode(scb_ctx* ctx, const uint16_t* indices16, const uint16_t* data16, int64_t nnz,
+                               const int64_t* esc_pos, const float* esc_val, int64_t n_esc, int32_t* indices,
+                               float* data, void* stream);
+
 /* ---- a5: sc.pp.highly_variable_genes(flavor="seurat", n_top_genes, n_bins) from the
  * (all-reduced) gene sums.  Outputs per gene: means, variances, dispersions (log),
  * dispersions_norm, mean_bin; hvg_mask; hvg_index = sorted selected genes (int32[n_cols]

@@ -18,6 +18,7 @@
 // f64 ulp before the f32 rounding.
 #include "common.cuh"
 #include "scan.cuh"
+#include <algorithm>
 
 namespace scb {
 
@@ -387,5 +388,67 @@ extern "C" int scb_coo_to_csr(scb_ctx* ctx, const int32_t* major, const int32_t*
   SCB_CUDA(cudaStreamSynchronize(s));
   SCB_REQUIRE(!(f & 8), SCB_ERR_UNSUPPORTED, "scb_coo_to_csr: unsorted row longer than %d entries", kMaxSortRow);
   SCB_REQUIRE(!(f & 4), SCB_ERR_DATA, "scb_coo_to_csr: duplicate (row, column) entries");
+  return SCB_OK;
+}
+
+// ---------------------------------------------------------------------------- u16 wire decode
+// Compact u16 CSR (host->device wire format: uint16 gene indices + uint16 counts, counts >=
+// 65535 escaped to a sorted (position, value) table) -> the int32/float32 CSR in HBM.  HBM-bound:
+// 4 B read + 8 B written per nonzero; each thread converts 8 nonzeros per iteration (16-byte
+// loads of each u16 array, 2 x 16-byte stores of each output array).
+namespace scb {
+__global__ void __launch_bounds__(256) u16_decode_kernel(const uint4* __restrict__ ind16, const uint4* __restrict__ dat16,
+                                                         int64_t n8, int4* __restrict__ ind, float4* __restrict__ dat) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    uint4 a, b;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(ind16 + i));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(dat16 + i));
+    ind[2 * i] = make_int4(a.x & 0xffff, a.x >> 16, a.y & 0xffff, a.y >> 16);
+    ind[2 * i + 1] = make_int4(a.z & 0xffff, a.z >> 16, a.w & 0xffff, a.w >> 16);
+    dat[2 * i] = make_float4((float)(b.x & 0xffff), (float)(b.x >> 16), (float)(b.y & 0xffff), (float)(b.y >> 16));
+    dat[2 * i + 1] = make_float4((float)(b.z & 0xffff), (float)(b.z >> 16), (float)(b.w & 0xffff), (float)(b.w >> 16));
+  }
+}
+__global__ void u16_decode_tail_kernel(const uint16_t* __restrict__ ind16, const uint16_t* __restrict__ dat16,
+                                       int64_t begin, int64_t nnz, int32_t* __restrict__ ind, float* __restrict__ dat) {
+  const int64_t i = begin + threadIdx.x;
+  if (i < nnz) {
+    ind[i] = ind16[i];
+    dat[i] = (float)dat16[i];
+  }
+}
+__global__ void u16_escape_kernel(const int64_t* __restrict__ pos, const float* __restrict__ val, int64_t n,
+                                  int64_t nnz, float* __restrict__ dat) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t p = pos[i];
+  if (p >= 0 && p < nnz) dat[p] = val[i];  // out-of-range escapes are ignored (no host sync here)
+}
+}  // namespace scb
+
+extern "C" int scb_csr_u16_decode(scb_ctx* ctx, const uint16_t* indices16, const uint16_t* data16, int64_t nnz,
+                                  const int64_t* esc_pos, const float* esc_val, int64_t n_esc, int32_t* indices,
+                                  float* data, void* stream) {
+  using namespace scb;
+  SCB_REQUIRE(ctx && (nnz == 0 || (indices16 && data16 && indices && data)), SCB_ERR_ARG, "scb_csr_u16_decode: null argument");
+  SCB_REQUIRE(n_esc == 0 || (esc_pos && esc_val), SCB_ERR_ARG, "scb_csr_u16_decode: escape table missing");
+  SCB_REQUIRE(((uintptr_t)indices16 & 15) == 0 && ((uintptr_t)data16 & 15) == 0 && ((uintptr_t)indices & 15) == 0 &&
+                  ((uintptr_t)data & 15) == 0,
+              SCB_ERR_ARG, "scb_csr_u16_decode: 16-byte aligned arrays required");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n8 = nnz / 8;
+  if (n8 > 0) {
+    const int g = (int)std::min<int64_t>((int64_t)ctx->num_sms * 8, (n8 + 255) / 256);
+    u16_decode_kernel<<<g, 256, 0, s>>>((const uint4*)indices16, (const uint4*)data16, n8, (int4*)indices, (float4*)data);
+    SCB_LAUNCH_CHECK();
+  }
+  if (nnz > 8 * n8) {
+    u16_decode_tail_kernel<<<1, 8, 0, s>>>(indices16, data16, 8 * n8, nnz, indices, data);
+    SCB_LAUNCH_CHECK();
+  }
+  if (n_esc > 0) {
+    u16_escape_kernel<<<(unsigned)((n_esc + 255) / 256), 256, 0, s>>>(esc_pos, esc_val, n_esc, nnz, data);
+    SCB_LAUNCH_CHECK();
+  }
   return SCB_OK;
 }

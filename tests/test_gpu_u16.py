@@ -56,3 +56,19 @@ def test_u16_conversion_refuses_lossy_inputs():
     assert ok.esc_pos.cpu().tolist() == [1] and ok.esc_val.cpu().tolist() == [65535.0]
     big = DeviceCSR.from_host(ip, ix, np.array([1.0, 100000.0, 7.0], np.float32), 65536).to_u16()
     assert big.to_f32().data.cpu().tolist() == [1.0, 100000.0, 7.0]
+
+
+def test_u16_wire_decode_matches_f32():
+    """scb_csr_u16_decode (the e2e wire format's device decode) restores the 32-bit CSR exactly,
+    including escaped counts and a tail that is not a multiple of 8."""
+    from paper_2605_13928_b200 import synth
+    X = synth.generate(synth.Spec(3001, 1700, seed=8))
+    X.data[7::1000] = 65535.0 + torch.arange(X.data[7::1000].numel(), device=X.data.device, dtype=torch.float32)
+    Xu = X.to_u16()
+    Y = Xu.to_f32()
+    assert torch.equal(Y.indices, X.indices) and torch.equal(Y.data, X.data)
+    n = X.nnz - 5  # odd length: exercises the tail kernel
+    from paper_2605_13928_b200.pp import DeviceCSR
+    part = DeviceCSR(X.indptr, Xu.indices[:n], Xu.data[:n], X.n_cols, esc_pos=Xu.esc_pos[Xu.esc_pos < n],
+                     esc_val=Xu.esc_val[Xu.esc_pos < n]).to_f32()
+    assert torch.equal(part.data, X.data[:n]) and torch.equal(part.indices, X.indices[:n])
