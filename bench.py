@@ -112,12 +112,14 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def _step_bytes(Z_in, N, G, Z_sub, N_sub, H, ld, regress_out=False, bpn=8):
+def _step_bytes(Z_in, N, G, Z_sub, N_sub, H, ld, regress_out=False, bpn=8, all_genes=False):
     """Algorithmic HBM bytes per step; ``bpn`` = bytes per input nonzero (8 for the
-    int32/float32 CSR, 4 for the compact u16 CSR)."""
+    int32/float32 CSR, 4 for the compact u16 CSR).  ``all_genes``: every gene kept, so the subset
+    count pass is replaced by an O(N) pass over the row metadata (no read of the nonzeros)."""
+    count = 24 * N if all_genes else bpn * Z_in
     return {
         "qc": bpn * Z_in + 8 * (N + 1),
-        "norm_hvg": bpn * Z_in + (bpn * Z_in + 8 * Z_sub) + bpn * Z_in + 4 * N,  # count, fill, hvg sums
+        "norm_hvg": count + (bpn * Z_in + 8 * Z_sub) + bpn * Z_in + 4 * N,  # count, fill, hvg sums
         # scale: dense scale (its gene sums are fused into the subset fill pass of norm_hvg);
         # regress_out: dense log (8Z' + 4N ld), Aᵀl read (4N ld), in-place residual scaling (8N ld)
         "regress": (8 * Z_sub + 16 * N_sub * ld) if regress_out else (8 * Z_sub + 4 * N_sub * ld),
@@ -342,7 +344,8 @@ def main():
     achieved = flops_knn / (knn_ms / 1e3) / 1e12
     bpn = X.indices.element_size() + X.data.element_size()
     n_esc = int(X.esc_pos.numel()) if X.is_u16 and X.esc_pos is not None else 0
-    sb = _step_bytes(Z_in, X.n_rows, G, Z_sub, N_sub_loc, H, ld, args.regress_out, bpn)
+    all_genes = bool(res.gene_mask.all().item())
+    sb = _step_bytes(Z_in, X.n_rows, G, Z_sub, N_sub_loc, H, ld, args.regress_out, bpn, all_genes)
     stages = {}
     for kk in ("qc", "norm_hvg", "regress"):
         if kk in step_ms and step_ms[kk] > 0:

@@ -61,6 +61,9 @@ SCB_API const char* scb_last_error(void);
 SCB_API unsigned long long scb_launch_count(void);
 SCB_API int scb_ctx_create(int device, scb_ctx** out);
 SCB_API int scb_ctx_destroy(scb_ctx* ctx);
+/* on != 0: scb_qc_metrics no longer waits for its data-validity check (one host round trip);
+ * the flag is returned in n_kept[3] of the next scb_filter_masks instead. */
+SCB_API int scb_ctx_set_deferred_checks(scb_ctx* ctx, int32_t on);
 
 /* ---- f1 ingest (sc.read_10x_mtx / sc.read_mtx): MatrixMarket coordinate data lines -> COO
  * on the device.  text holds the whole file (16-byte aligned, readable up to
@@ -100,11 +103,22 @@ SCB_API int32_t scb_hvg_tiles(int32_t n_cols);
 
 /* ---- a2: sc.pp.filter_cells(min_genes, max_genes) + pct_counts_mt < max_pct_mt, and
  * sc.pp.filter_genes(min_cells).  max_genes < 0 disables the upper bound.
- * n_kept (device int64[2]) receives {kept cells, kept genes}. */
+ * n_kept (device int64[4]) receives {kept cells, kept genes, nonzeros of the kept rows (if
+ * indptr != NULL, else 0), the QC data-error flag (nonzero: scb_qc_metrics saw invalid counts
+ * or column indices while the ctx defers checks, see scb_ctx_set_deferred_checks)}. */
 SCB_API int scb_filter_masks(scb_ctx* ctx, const int32_t* n_genes_by_counts, const double* pct_counts_mt,
                      int64_t n_rows, const int32_t* n_cells_by_counts, int32_t n_cols,
                      int32_t min_genes, int32_t max_genes, double max_pct_mt, int32_t min_cells,
-                     uint8_t* cell_mask, uint8_t* gene_mask, int64_t* n_kept, void* stream);
+                     const int64_t* indptr, uint8_t* cell_mask, uint8_t* gene_mask, int64_t* n_kept, void* stream);
+
+/* ---- a2 pass 1 when EVERY gene is kept (n_kept[1] == n_cols): no pass over the nonzeros --
+ * gene_remap = identity, new_indptr from the kept rows' lengths, row_scale / row_scale_orig =
+ * float32(target_sum / total_counts) (QC's exact totals; 1 for empty rows), i.e. exactly what
+ * scb_subset_count computes in that case. */
+SCB_API int scb_subset_rows_all_genes(scb_ctx* ctx, const int64_t* indptr, int64_t n_rows, int32_t n_cols,
+                              const uint8_t* cell_mask, const double* total_counts, double target_sum,
+                              int32_t* gene_remap, int64_t* new_indptr, float* row_scale, float* row_scale_orig,
+                              void* stream);
 
 /* ---- a2: adata[cell_mask, gene_mask] -- pass 1.  Builds gene_remap (new column or -1),
  * new_indptr (int64[n_kept_cells+1]; new_indptr[n_kept] = kept nnz) and, if

@@ -217,6 +217,12 @@ qc_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
   }
 }
 
+__global__ void zero_if_flag_kernel(unsigned long long* __restrict__ a, int64_t n, const int* __restrict__ flag) {
+  if (*flag == 0) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = 0ull;
+}
+
 __global__ void add_u64_kernel(const unsigned long long* __restrict__ a, unsigned long long* __restrict__ b,
                                int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -339,6 +345,44 @@ subset_count_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ i
     }
   }
 }
+
+// Pass 1 when every gene is kept (the usual case at scale: min_cells = 3 over 1M cells): the
+// kept-row lengths are the row lengths and the normalisation totals are QC's exact row totals,
+// so no pass over the nonzeros is needed (same float32(target_sum / total) as subset_count).
+__global__ void rows_all_genes_kernel(const int64_t* __restrict__ indptr, const uint8_t* __restrict__ cmask,
+                                      const int64_t* __restrict__ row_pos, const double* __restrict__ total,
+                                      int64_t n_rows, double target_sum, int64_t* __restrict__ cnt,
+                                      float* __restrict__ row_scale, float* __restrict__ row_scale_orig) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+    if (!cmask[r]) {
+      if (row_scale_orig) row_scale_orig[r] = 0.0f;
+      continue;
+    }
+    const int64_t kr = row_pos[r];
+    cnt[kr] = indptr[r + 1] - indptr[r];
+    const double t = total[r];
+    const float sc = (t > 0.0) ? (float)__ddiv_rn(target_sum, t) : 1.0f;
+    row_scale[kr] = sc;
+    if (row_scale_orig) row_scale_orig[r] = sc;
+  }
+}
+
+__global__ void identity_remap_kernel(int32_t n, int32_t* remap) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) remap[i] = i;
+}
+
+// kept-row nonzeros (for allocation without an extra host round trip)
+__global__ void kept_nnz_kernel(const int64_t* __restrict__ indptr, const uint8_t* __restrict__ cmask, int64_t n,
+                                unsigned long long* __restrict__ out) {
+  unsigned long long acc = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    if (cmask[r]) acc += (unsigned long long)(indptr[r + 1] - indptr[r]);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane_id() == 0 && acc) atomicAdd(out, acc);
+}
+
+__global__ void copy_flag_kernel(const int* __restrict__ flag, long long* __restrict__ out) { *out = *flag; }
 
 // Compacting copy: each lane's 4-element quad contributes its kept count to a warp-wide
 // exclusive scan so the output stays in row order.  The (up to 128) kept elements of a warp
@@ -536,7 +580,9 @@ hvg_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indic
                 const VT* __restrict__ data, const float* __restrict__ row_scale, int64_t n_rows,
                 int32_t n_cols, const int32_t* __restrict__ remap, int32_t n_out, int32_t tile_w,
                 int32_t n_tiles, const int32_t* __restrict__ splits, int64_t rows_per_block,
-                unsigned long long* __restrict__ sums, int* __restrict__ order_flag, U16Esc esc) {
+                unsigned long long* __restrict__ sums, int* __restrict__ order_flag, U16Esc esc,
+                const int* __restrict__ run_if = nullptr) {
+  if (run_if && *run_if == 0) return;  // conditional fallback launch (no host round trip)
   const int64_t nnz = indptr[n_rows];
   extern __shared__ uint32_t sm[];
   const int tile = blockIdx.x % n_tiles;
@@ -1109,6 +1155,7 @@ static int qc_metrics_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indice
   }
   qc_finalize<<<ceil_div(n_cols, 256), 256, 0, s>>>(g_cells, g_total, n_cols, n_cells, gene_total);
   SCB_LAUNCH_CHECK();
+  if (ctx->defer_checks) return SCB_OK;  // the flag is reported by scb_filter_masks (n_kept[3])
   int flag = 0;
   SCB_CUDA(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   SCB_CUDA(cudaStreamSynchronize(s));
@@ -1134,11 +1181,11 @@ extern "C" int scb_qc_metrics_u16(scb_ctx* ctx, const int64_t* indptr, const uin
 
 extern "C" int scb_filter_masks(scb_ctx* ctx, const int32_t* ng, const double* pct, int64_t n_rows,
                                 const int32_t* nc, int32_t n_cols, int32_t min_genes, int32_t max_genes,
-                                double max_pct, int32_t min_cells, uint8_t* cmask, uint8_t* gmask,
-                                int64_t* n_kept, void* stream) {
+                                double max_pct, int32_t min_cells, const int64_t* indptr, uint8_t* cmask,
+                                uint8_t* gmask, int64_t* n_kept, void* stream) {
   SCB_REQUIRE(ctx && ng && pct && nc && cmask && gmask && n_kept, SCB_ERR_ARG, "scb_filter_masks: null argument");
   cudaStream_t s = (cudaStream_t)stream;
-  SCB_CUDA(cudaMemsetAsync(n_kept, 0, 2 * sizeof(int64_t), s));
+  SCB_CUDA(cudaMemsetAsync(n_kept, 0, 4 * sizeof(int64_t), s));
   if (n_rows > 0) {
     cell_mask_kernel<<<ceil_div(n_rows, 256), 256, 0, s>>>(ng, pct, n_rows, min_genes, max_genes, max_pct,
                                                            cmask, (unsigned long long*)n_kept);
@@ -1147,6 +1194,35 @@ extern "C" int scb_filter_masks(scb_ctx* ctx, const int32_t* ng, const double* p
   gene_mask_kernel<<<ceil_div(n_cols, 256), 256, 0, s>>>(nc, n_cols, min_cells, gmask,
                                                          (unsigned long long*)n_kept);
   SCB_LAUNCH_CHECK();
+  if (indptr && n_rows > 0) {
+    kept_nnz_kernel<<<grid_for(ctx, 2), 256, 0, s>>>(indptr, cmask, n_rows, (unsigned long long*)(n_kept + 2));
+    SCB_LAUNCH_CHECK();
+  }
+  copy_flag_kernel<<<1, 1, 0, s>>>(ctx->d_flag, (long long*)(n_kept + 3));
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}
+
+extern "C" int scb_subset_rows_all_genes(scb_ctx* ctx, const int64_t* indptr, int64_t n_rows, int32_t n_cols,
+                                         const uint8_t* cmask, const double* total_counts, double target_sum,
+                                         int32_t* remap, int64_t* new_indptr, float* row_scale,
+                                         float* row_scale_orig, void* stream) {
+  SCB_REQUIRE(ctx && indptr && cmask && total_counts && remap && new_indptr && row_scale, SCB_ERR_ARG,
+              "scb_subset_rows_all_genes: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  identity_remap_kernel<<<ceil_div(n_cols, 256), 256, 0, s>>>(n_cols, remap);
+  SCB_LAUNCH_CHECK();
+  void* ws;
+  SCB_TRY(ws_get(ctx, 1, (size_t)(n_rows + 1) * 8 * 2, &ws, s));
+  int64_t* row_pos = (int64_t*)ws;
+  int64_t* cnt = row_pos + (n_rows + 1);
+  SCB_TRY(scan_u8_to_i64(ctx, cmask, n_rows, row_pos, s));
+  if (n_rows > 0) {
+    rows_all_genes_kernel<<<grid_for(ctx, 8), 256, 0, s>>>(indptr, cmask, row_pos, total_counts, n_rows, target_sum,
+                                                           cnt, row_scale, row_scale_orig);
+    SCB_LAUNCH_CHECK();
+  }
+  SCB_TRY(scan_i64_dev_len(ctx, cnt, row_pos + n_rows, n_rows, new_indptr, s));
   return SCB_OK;
 }
 
@@ -1340,16 +1416,14 @@ static int hvg_gene_sums_impl(scb_ctx* ctx, const int64_t* indptr, const IT* ind
       indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, row_splits,
       rows_per_block, tmp, order_flag, esc);
   SCB_LAUNCH_CHECK();
-  int flag = 0;
-  SCB_CUDA(cudaMemcpyAsync(&flag, order_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SCB_CUDA(cudaStreamSynchronize(s));
-  if (flag) {
-    SCB_CUDA(cudaMemsetAsync(tmp, 0, sbytes, s));
-    hvg_sums_kernel<IT, VT><<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
-        indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, nullptr,
-        rows_per_block, tmp, order_flag, esc);
-    SCB_LAUNCH_CHECK();
-  }
+  // unsorted rows seen: redo without splits -- launched unconditionally, both kernels exit at
+  // once unless the device-side flag is set (no host round trip)
+  zero_if_flag_kernel<<<ceil_div(4 * n_out, 256), 256, 0, s>>>(tmp, (int64_t)4 * n_out, order_flag);
+  SCB_LAUNCH_CHECK();
+  hvg_sums_kernel<IT, VT><<<(unsigned)(n_blocks * n_tiles), kHvgThreads, smem, s>>>(
+      indptr, indices, data, row_scale, n_rows, n_cols, remap, n_out, std::min(tile_w, n_cols), n_tiles, nullptr,
+      rows_per_block, tmp, ctx->d_flag + 3, esc, order_flag);
+  SCB_LAUNCH_CHECK();
   add_u64_kernel<<<ceil_div(4 * n_out, 256), 256, 0, s>>>(tmp, (unsigned long long*)sums, (int64_t)4 * n_out);
   SCB_LAUNCH_CHECK();
   return SCB_OK;

@@ -17,6 +17,21 @@
 
 namespace scb {
 
+// t-th tile (row-major order) of the upper-triangle tile list: block row bi holds the column
+// blocks bj with bj*BN + BN - 1 >= bi*BM.  Computed per CTA (a few iterations), so no host-built
+// list has to be uploaded (and kept alive) per launch.
+__device__ __forceinline__ int2 upper_tile(int t, int hp, int BM, int BN) {
+  const int n_bi = hp / BM, n_bj = hp / BN;
+  for (int bi = 0; bi < n_bi; ++bi) {
+    const int lo = bi * BM - BN + 1;
+    const int bj0 = lo <= 0 ? 0 : (lo + BN - 1) / BN;
+    const int cnt = n_bj - bj0;
+    if (t < cnt) return make_int2(bi, bj0 + t);
+    t -= cnt;
+  }
+  return make_int2(0, 0);
+}
+
 constexpr int kConvWarps = 12;
 constexpr int kConv0 = 3;                                   // first converter warp
 constexpr int kGemmThreads = 32 * (kConv0 + kConvWarps);   // warp0 TMA, warps 1-2 MMA, converters (3..6 also epilogue)
@@ -54,7 +69,7 @@ gram_kernel(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ t
   const int warp = warp_id(), lane = lane_id();
   const int tile = blockIdx.x % n_tiles;
   const int slice = blockIdx.x / n_tiles;
-  const int2 t = tiles[tile];
+  const int2 t = tiles ? tiles[tile] : upper_tile(tile, hp, C::BM, BN);
   const int i0 = t.x * C::BM, j0 = t.y * BN;
   const int64_t k_begin = (int64_t)slice * rows_per_slice;
   const int64_t k_end = min(n_rows, k_begin + rows_per_slice);
@@ -260,7 +275,7 @@ gram_split_kernel(const __grid_constant__ CUtensorMap thi, const __grid_constant
   const int warp = warp_id(), lane = lane_id();
   const int tile = blockIdx.x % n_tiles;
   const int slice = blockIdx.x / n_tiles;
-  const int2 t = tiles[tile];
+  const int2 t = tiles ? tiles[tile] : upper_tile(tile, hp, C::BM, BN);
   const int i0 = t.x * C::BM, j0 = t.y * BN;
   const int64_t k_begin = (int64_t)slice * rows_per_slice;
   const int64_t k_end = min(n_rows, k_begin + rows_per_slice);
@@ -442,10 +457,9 @@ static int launch_gram(scb_ctx* ctx, const float* Z, const uint16_t* Zhi, const 
   const int64_t rows_per_slice = ((kbs + slices - 1) / slices) * KB;
   const size_t part_bytes = (size_t)slices * hp * hp * 4;
   void* ws;
-  SCB_TRY(ws_get(ctx, 0, part_bytes + n_tiles * sizeof(int2) + 256, &ws, s));
+  SCB_TRY(ws_get(ctx, 0, part_bytes + 256, &ws, s));
   float* partial = (float*)ws;
-  int2* d_tiles = (int2*)((char*)ws + ((part_bytes + 255) / 256) * 256);
-  SCB_CUDA(cudaMemcpyAsync(d_tiles, tl.data(), n_tiles * sizeof(int2), cudaMemcpyHostToDevice, s));
+  const int2* d_tiles = nullptr;  // enumerated on the device (upper_tile), same order as tl
   if (split) {
     using Cfg = GramSplitCfg<BN>;
     auto kern = gram_split_kernel<BN>;
@@ -463,7 +477,6 @@ static int launch_gram(scb_ctx* ctx, const float* Z, const uint16_t* Zhi, const 
   dim3 g((hp + 255) / 256, hp);
   gram_reduce_kernel<<<g, 256, 0, s>>>(partial, slices, hp, C);
   SCB_LAUNCH_CHECK();
-  SCB_CUDA(cudaStreamSynchronize(s));  // keeps the host tile list alive for the async copy
   return SCB_OK;
 }
 

@@ -72,6 +72,12 @@ extern "C" int scb_ctx_create(int device, scb_ctx** out) {
   return SCB_OK;
 }
 
+extern "C" int scb_ctx_set_deferred_checks(scb_ctx* ctx, int32_t on) {
+  SCB_REQUIRE(ctx, SCB_ERR_ARG, "scb_ctx_set_deferred_checks: null ctx");
+  ctx->defer_checks = on ? 1 : 0;
+  return SCB_OK;
+}
+
 extern "C" int scb_ctx_destroy(scb_ctx* ctx) {
   if (!ctx) return SCB_OK;
   cudaSetDevice(ctx->device);

@@ -111,12 +111,14 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
 
     # ------------------------------------------------------------------ qc
     tm.step("qc")
-    qc = pp.calculate_qc_metrics(X, mt_mask, row_splits=True)
+    qc = pp.calculate_qc_metrics(X, mt_mask, row_splits=True, defer_check=True)
     if comm is not None:
         comm.allreduce_(qc["n_cells_by_counts"])
         comm.allreduce_(qc["gene_total_counts"])
-    cm, gm, (nk_local, gk) = pp.filter_masks(qc, min_genes=p.min_genes, max_genes=p.max_genes,
-                                             max_pct_mt=p.max_pct_mt, min_cells=p.min_cells)
+    # one host round trip: kept counts, kept-row nonzeros and QC's deferred data check
+    cm, gm, (nk_local, gk), kept_nnz = pp.filter_masks_ex(qc, min_genes=p.min_genes, max_genes=p.max_genes,
+                                                          max_pct_mt=p.max_pct_mt, min_cells=p.min_cells,
+                                                          indptr=X.indptr)
     n_total = nk_local if comm is None else comm.allreduce_int(nk_local)
 
     # ------------------------------------------------------------------ norm_hvg
@@ -125,8 +127,13 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
     # from the raw matrix (remapped genes, per-original-row factors); pass 2 writes the kept
     # log1p matrix and, for the plain scale path, accumulates the scale step's gene sums of
     # the selected HVG columns on the way (no second read of the kept matrix)
-    remap, new_indptr, row_scale, row_scale_orig, nnz = pp.subset_count_scale(X, cm, gm, (nk_local, gk),
-                                                                             p.target_sum)
+    if gk == X.n_cols:  # every gene kept: row factors from QC's totals, no count pass (no host sync)
+        remap, new_indptr, row_scale, row_scale_orig = pp.subset_rows_all_genes(X, cm, qc["total_counts"], nk_local,
+                                                                                p.target_sum)
+        nnz = kept_nnz
+    else:
+        remap, new_indptr, row_scale, row_scale_orig, nnz = pp.subset_count_scale(X, cm, gm, (nk_local, gk),
+                                                                                 p.target_sum)
     sums = pp.hvg_gene_sums(X, counts=X.data, row_scale=row_scale_orig, gene_remap=remap, n_out=gk,
                             row_splits=qc["hvg_row_splits"])
     if comm is not None:

@@ -136,11 +136,13 @@ class DeviceCSR:
 
 
 # ----------------------------------------------------------------------------- qc
-def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor, row_splits: bool = False):
+def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor, row_splits: bool = False, defer_check: bool = False):
     """sc.pp.calculate_qc_metrics(qc_vars=['mt'], percent_top=None, log1p=False).
 
     With ``row_splits`` the result also holds ``hvg_row_splits`` (per-row gene-tile split
-    counts that let the HVG column pass read every nonzero exactly once)."""
+    counts that let the HVG column pass read every nonzero exactly once).  With ``defer_check``
+    the data-validity check (non-negative integer counts < 2^24, column indices in range) does
+    not wait for the device: ``filter_masks_ex`` raises it instead (one host round trip fewer)."""
     dev = X.device
     N, G = X.n_rows, X.n_cols
     out = dict(
@@ -157,11 +159,14 @@ def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor, row_splits: bool =
         T = int(_lib.call("scb_hvg_tiles", G))
         if T > 1:
             splits = torch.empty((N, T - 1), dtype=torch.int32, device=dev)
-    _lib.call("scb_qc_metrics" + _fmt(X.indices, X.data), _ctx(X.data), _p(X.indptr), _p(X.indices), _p(X.data), N, G,
+    ctx = _ctx(X.data)
+    _lib.call("scb_ctx_set_deferred_checks", ctx, 1 if defer_check else 0)
+    _lib.call("scb_qc_metrics" + _fmt(X.indices, X.data), ctx, _p(X.indptr), _p(X.indices), _p(X.data), N, G,
               _p(mt),
               _p(out["n_genes_by_counts"]), _p(out["total_counts"]), _p(out["total_counts_mt"]),
               _p(out["pct_counts_mt"]), _p(out["n_cells_by_counts"]), _p(out["gene_total_counts"]),
               _p(splits), *_esc(X), _stream(dev))
+    _lib.call("scb_ctx_set_deferred_checks", ctx, 0)
     out["hvg_row_splits"] = splits
     return out
 
@@ -175,11 +180,10 @@ def qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor):
     return cell, gene
 
 
-def filter_masks(cell, gene=None, *, min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3):
-    """sc.pp.filter_cells(min_genes, max_genes) & pct_counts_mt < max_pct_mt; sc.pp.filter_genes(min_cells).
-    ``filter_masks(cell, gene, ...)`` takes the two tables of ``qc_metrics``; with ``gene`` omitted,
-    ``cell`` is the combined dict of ``calculate_qc_metrics``.
-    Returns (cell_mask u8[N], gene_mask u8[G], (n_kept_cells, n_kept_genes))."""
+def filter_masks_ex(cell, gene=None, *, min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3, indptr=None):
+    """filter_masks plus, in the same host round trip, the nonzeros of the kept rows (when the
+    raw ``indptr`` is given; else 0).  Raises ScbError if a deferred QC data check failed.
+    Returns (cell_mask, gene_mask, (n_kept_cells, n_kept_genes), kept_row_nnz)."""
     if gene is not None:
         qc = {"n_genes_by_counts": cell["n_genes_by_counts"], "pct_counts_mt": cell["pct_counts_mt"],
               "n_cells_by_counts": gene["n_cells_by_counts"]}
@@ -190,12 +194,25 @@ def filter_masks(cell, gene=None, *, min_genes=200, max_genes=None, max_pct_mt=2
     N, G = ng.numel(), qc["n_cells_by_counts"].numel()
     cm = torch.empty(N, dtype=torch.uint8, device=dev)
     gm = torch.empty(G, dtype=torch.uint8, device=dev)
-    kept = torch.empty(2, dtype=torch.int64, device=dev)
+    kept = torch.empty(4, dtype=torch.int64, device=dev)
     _lib.call("scb_filter_masks", _ctx(ng), _p(ng), _p(qc["pct_counts_mt"]), N, _p(qc["n_cells_by_counts"]), G,
               int(min_genes), -1 if max_genes is None else int(max_genes), float(max_pct_mt), int(min_cells),
-              _p(cm), _p(gm), _p(kept), _stream(dev))
+              _p(indptr), _p(cm), _p(gm), _p(kept), _stream(dev))
     k = kept.cpu().tolist()
-    return cm, gm, (int(k[0]), int(k[1]))
+    if k[3]:
+        raise _lib.ScbError("scb_qc_metrics", -4, "counts must be non-negative integers < 2^24 with column indices "
+                                                  "in range (deferred check)")
+    return cm, gm, (int(k[0]), int(k[1])), int(k[2])
+
+
+def filter_masks(cell, gene=None, *, min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3):
+    """sc.pp.filter_cells(min_genes, max_genes) & pct_counts_mt < max_pct_mt; sc.pp.filter_genes(min_cells).
+    ``filter_masks(cell, gene, ...)`` takes the two tables of ``qc_metrics``; with ``gene`` omitted,
+    ``cell`` is the combined dict of ``calculate_qc_metrics``.
+    Returns (cell_mask u8[N], gene_mask u8[G], (n_kept_cells, n_kept_genes))."""
+    cm, gm, kept, _ = filter_masks_ex(cell, gene, min_genes=min_genes, max_genes=max_genes, max_pct_mt=max_pct_mt,
+                                      min_cells=min_cells)
+    return cm, gm, kept
 
 
 def subset(X: DeviceCSR, cell_mask, gene_mask, n_kept=None, target_sum=None):
@@ -241,6 +258,20 @@ def subset_count_scale(X: DeviceCSR, cell_mask, gene_mask, n_kept, target_sum: f
               _p(row_scale_orig), *_esc(X), s)
     nnz = int(new_indptr[nk].item())
     return remap, new_indptr, row_scale, row_scale_orig, nnz
+
+
+def subset_rows_all_genes(X: DeviceCSR, cell_mask, total_counts, n_kept: int, target_sum: float = 1e4):
+    """subset_count_scale when every gene is kept: the same (remap, new_indptr, row_scale,
+    row_scale_orig) from the row lengths and QC's exact totals, without reading the nonzeros."""
+    dev = X.device
+    remap = torch.empty(X.n_cols, dtype=torch.int32, device=dev)
+    new_indptr = torch.empty(n_kept + 1, dtype=torch.int64, device=dev)
+    row_scale = torch.empty(n_kept, dtype=torch.float32, device=dev)
+    row_scale_orig = torch.empty(X.n_rows, dtype=torch.float32, device=dev)
+    _lib.call("scb_subset_rows_all_genes", _ctx(X.indptr), _p(X.indptr), X.n_rows, X.n_cols, _p(cell_mask),
+              _p(total_counts), float(target_sum), _p(remap), _p(new_indptr), _p(row_scale), _p(row_scale_orig),
+              _stream(dev))
+    return remap, new_indptr, row_scale, row_scale_orig
 
 
 def subset_fill_log(X: DeviceCSR, cell_mask, remap, new_indptr, row_scale, nnz: int, n_genes_kept: int) -> DeviceCSR:

@@ -25,7 +25,7 @@ def _csr(X):
     return op.CSR(_np(X.indptr), _np(X.indices), _np(X.data), X.n_cols)
 
 
-def calculate_qc_metrics(X, mt_mask, row_splits=False):
+def calculate_qc_metrics(X, mt_mask, row_splits=False, defer_check=False):
     q = op.qc_metrics(_csr(X), _np(mt_mask))
     out = {k: torch.as_tensor(v) for k, v in q.items()}
     out["hvg_row_splits"] = None
@@ -36,6 +36,22 @@ def filter_masks(qc, gene=None, *, min_genes=200, max_genes=None, max_pct_mt=20.
     p = op.Params(min_genes=min_genes, max_genes=max_genes, max_pct_mt=max_pct_mt, min_cells=min_cells)
     cm, gm = op.filter_masks({k: _np(v) for k, v in qc.items() if v is not None}, p)
     return torch.as_tensor(cm), torch.as_tensor(gm), (int(cm.sum()), int(gm.sum()))
+
+
+def filter_masks_ex(qc, gene=None, *, min_genes=200, max_genes=None, max_pct_mt=20.0, min_cells=3, indptr=None):
+    cm, gm, kept = filter_masks(qc, min_genes=min_genes, max_genes=max_genes, max_pct_mt=max_pct_mt,
+                                min_cells=min_cells)
+    nnz = 0
+    if indptr is not None:
+        ip = _np(indptr)
+        nnz = int(np.diff(ip)[_np(cm).astype(bool)].sum())
+    return cm, gm, kept, nnz
+
+
+def subset_rows_all_genes(X, cm, total_counts, n_kept, target_sum=1e4):
+    gm = torch.ones(X.n_cols, dtype=torch.uint8)
+    remap, new_indptr, row_scale, rso, _ = subset_count_scale(X, cm, gm, (n_kept, X.n_cols), target_sum)
+    return remap, new_indptr, row_scale, rso
 
 
 def subset_normalize(X, cm, gm, n_kept, target_sum=1e4):
