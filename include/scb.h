@@ -355,6 +355,12 @@ SCB_API int scb_knn_timed(scb_ctx* ctx, const float* queries, int64_t n_queries,
                           int32_t d, int32_t ld, int32_t k, int32_t k_cand, int32_t* knn_index, float* knn_dist,
                           void* stream, void* ev_start, void* ev_end);
 
+/* ---- a9 with a caller-chosen scan order (queries == keys = x): order_key[i] (16-bit bucket)
+ * replaces the built-in Morton bucket of row i; rows are scanned outward in bucket order. */
+SCB_API int scb_knn_ordered(scb_ctx* ctx, const float* x, int64_t n, int32_t d, int32_t ld, int32_t k,
+                            const uint16_t* order_key, int32_t* knn_index, float* knn_dist, void* stream,
+                            void* ev_start, void* ev_end);
+
 /* ---- synthetic negative-binomial counts (oracle/synth.py specification, generator v2), on
  * device; bit-identical to the CPU generator (fixed-order correctly rounded fp64 only).
  * scb_synth_logmean: logmean[c][g] = (log_s[c] + log_mu[g]) + L, L = A[cell_type[c]][g], then

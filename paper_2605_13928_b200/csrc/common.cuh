@@ -74,8 +74,6 @@ struct scb_ctx {
   scb::Workspace ws[4];  // independent scratch slots (grown on demand, stream-ordered use)
   int* d_flag = nullptr; // device error flag (non-integral counts etc.)
   int defer_checks = 0;  // 1: data checks that need a host round trip are reported later (see scb.h)
-  void* blas = nullptr;   // cublasHandle_t for the eigensolver's plain fp64 GEMMs (created on first use)
-  void* solver = nullptr; // cusolverDnHandle_t, only for the rank-deficient eigensolver fallback
 };
 
 namespace scb {

@@ -8,8 +8,6 @@
 // continue until it falls below 1e-10 (or an iteration cap).  Sign rule: the
 // largest-|loading| entry of every component is positive (first index on ties).
 #include <cstdlib>
-#include <cublas_v2.h>
-#include <cusolverDn.h>
 #include "common.cuh"
 
 namespace scb {
@@ -18,88 +16,194 @@ constexpr int kB = 96;   // subspace block size (n_comps + oversampling)
 constexpr int kLd = kB + 1;
 
 // ------------------------------------------------------------------ small fp64 GEMM
-// Cm[M][N] (ldc) = alpha * op(A) * op(B) + beta * Cm ; row-major operands.
-// opA: 0 -> A[M][K] (lda), 1 -> A^T where A is [K][M]; opB: 0 -> B[K][N], 1 -> B^T ([N][K]).
-// 64x64 tiles, 256 threads, 4x4 per thread, K chunk 16; split-K over blockIdx.z with
-// atomicAdd when gridDim.z > 1 (caller zeroes Cm and passes beta = 0).
-// Plain fp64 GEMMs of the eigensolver (Cov x block, block^T x block, block x small) go to
-// cuBLAS: row-major C[M][N] = op(A) op(B) is column-major C^T = op(B)^T op(A)^T.
+// Cm[M][N] (ldc) = op(A) * op(B), row-major operands, fp64 on the CUDA cores (the eigensolver's
+// GEMMs are 2000 x 96 x 2000 at most, ~0.8 GFLOP each).  opA: 0 -> A[M][K] (lda), 1 -> A^T with
+// A stored [K][M]; opB: 0 -> B[K][N] (ldb), 1 -> B^T with B stored [N][K].  64x64 tiles, K chunk
+// 16, 256 threads with 4x4 outputs each.  Split-K over blockIdx.z writes per-slice partials
+// that a second kernel sums in slice order (deterministic).  Every kernel of the eigensolver
+// takes the device `done` flag and exits at once when it is set, so the host can enqueue a
+// batch of outer iterations without a round trip per iteration.
+constexpr int kGT = 64, kGK = 16;
+__global__ void __launch_bounds__(256) dgemm_kernel(int M, int N, int K, const double* __restrict__ A, int lda,
+                                                    int opA, const double* __restrict__ B, int ldb, int opB,
+                                                    double* __restrict__ Cm, int ldc, int k_per_slice,
+                                                    double* __restrict__ partial, const int* __restrict__ done) {
+  if (done && *done) return;
+  __shared__ double As[kGK][kGT + 1];
+  __shared__ double Bs[kGK][kGT + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * kGT, n0 = blockIdx.x * kGT;
+  const int kb = blockIdx.z * k_per_slice, ke = min(K, kb + k_per_slice);
+  double acc[4][4] = {};
+  for (int k0 = kb; k0 < ke; k0 += kGK) {
+    for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
+      int kk, mm;
+      if (opA) { kk = e / kGT; mm = e % kGT; } else { mm = e / kGK; kk = e % kGK; }
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < ke) ? (opA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk]) : 0.0;
+      int kn, nn;
+      if (opB) { nn = e / kGK; kn = e % kGK; } else { kn = e / kGT; nn = e % kGT; }
+      const int gn = n0 + nn, gk2 = k0 + kn;
+      Bs[kn][nn] = (gn < N && gk2 < ke) ? (opB ? B[(size_t)gn * ldb + gk2] : B[(size_t)gk2 * ldb + gn]) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kGK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  double* out = partial ? partial + (size_t)blockIdx.z * M * N : Cm;
+  const int ld = partial ? N : ldc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+      if (m < M && n < N) out[(size_t)m * ld + n] = acc[i][j];
+    }
+}
+
+__global__ void splitk_reduce_kernel(const double* __restrict__ partial, int slices, int M, int N,
+                                     double* __restrict__ Cm, int ldc, const int* __restrict__ done) {
+  if (done && *done) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)M * N) return;
+  double s = 0.0;
+  for (int z = 0; z < slices; ++z) s += partial[(size_t)z * M * N + e];
+  Cm[(size_t)(e / N) * ldc + e % N] = s;
+}
+
 static int dgemm(scb_ctx* ctx, int M, int N, int K, const double* A, int lda, int opA, const double* B, int ldb,
-                 int opB, double* Cm, int ldc, cudaStream_t s) {
-  if (!ctx->blas) {
-    cublasHandle_t h;
-    SCB_REQUIRE(cublasCreate(&h) == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasCreate failed");
-    ctx->blas = h;
+                 int opB, double* Cm, int ldc, cudaStream_t s, const int* done = nullptr) {
+  const int tiles = ((M + kGT - 1) / kGT) * ((N + kGT - 1) / kGT);
+  int slices = std::max(1, std::min((ctx->num_sms + tiles - 1) / tiles, K / 128));
+  const int kps = ((K + slices - 1) / slices + kGK - 1) / kGK * kGK;
+  slices = (K + kps - 1) / kps;
+  double* partial = nullptr;
+  if (slices > 1) {
+    void* ws;
+    SCB_TRY(ws_get(ctx, 3, (size_t)slices * M * N * sizeof(double), &ws, s));
+    partial = (double*)ws;
   }
-  cublasHandle_t h = (cublasHandle_t)ctx->blas;
-  SCB_REQUIRE(cublasSetStream(h, s) == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasSetStream failed");
-  const double one = 1.0, zero = 0.0;
-  const cublasStatus_t st = cublasDgemm(h, opB ? CUBLAS_OP_T : CUBLAS_OP_N, opA ? CUBLAS_OP_T : CUBLAS_OP_N, N, M, K,
-                                        &one, B, ldb, A, lda, &zero, Cm, ldc);
-  SCB_REQUIRE(st == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasDgemm failed (%d)", (int)st);
+  dim3 g((N + kGT - 1) / kGT, (M + kGT - 1) / kGT, slices);
+  dgemm_kernel<<<g, 256, 0, s>>>(M, N, K, A, lda, opA, B, ldb, opB, Cm, ldc, kps, partial, done);
+  SCB_LAUNCH_CHECK();
+  if (slices > 1) {
+    splitk_reduce_kernel<<<(unsigned)(((int64_t)M * N + 255) / 256), 256, 0, s>>>(partial, slices, M, N, Cm, ldc, done);
+    SCB_LAUNCH_CHECK();
+  }
   return SCB_OK;
 }
 
-// M[h][kB] (row-major) := M R^{-1} with R upper triangular [kB][kB] (row-major): column-major
-// this is M^T := R^{-T} M^T, a left solve with the lower-triangular column-major view of R.
-static int trsm_right_upper(scb_ctx* ctx, int h, const double* R, double* M, cudaStream_t s) {
-  cublasHandle_t hd = (cublasHandle_t)ctx->blas;
-  SCB_REQUIRE(cublasSetStream(hd, s) == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasSetStream failed");
-  const double one = 1.0;
-  const cublasStatus_t st = cublasDtrsm(hd, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
-                                        CUBLAS_DIAG_NON_UNIT, kB, h, &one, R, kB, M, kB);
-  SCB_REQUIRE(st == CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cublasDtrsm failed (%d)", (int)st);
+// M[h][kB] (row-major) := M R^{-1}, R upper triangular [kB][kB]: each warp solves one row
+// x R = m by forward substitution (lane l owns columns l, l+32, l+64), R staged in smem.
+__global__ void __launch_bounds__(256) trsm_rows_kernel(const double* __restrict__ R, double* __restrict__ M, int h,
+                                                        const int* __restrict__ done) {
+  if (done && *done) return;
+  extern __shared__ double rdyn[];
+  double (*r)[kB + 1] = reinterpret_cast<double (*)[kB + 1]>(rdyn);
+  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) r[e / kB][e % kB] = R[e];
+  __syncthreads();
+  const int lane = lane_id();
+  for (int row = blockIdx.x * 8 + warp_id(); row < h; row += gridDim.x * 8) {
+    double m[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) m[t] = M[(size_t)row * kB + lane + 32 * t];
+    for (int j = 0; j < kB; ++j) {
+      const int owner = j & 31, slot = j >> 5;
+      double mj = 0.0;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) if (t == slot) mj = m[t];
+      const double xj = __shfl_sync(0xffffffffu, mj, owner) / r[j][j];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const int c = lane + 32 * t;
+        if (c == j) m[t] = xj;
+        else if (c > j) m[t] -= xj * r[j][c];
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t) M[(size_t)row * kB + lane + 32 * t] = m[t];
+  }
+}
+
+static int trsm_right_upper(scb_ctx* ctx, int h, const double* R, double* M, cudaStream_t s, const int* done) {
+  const int smem = kB * (kB + 1) * 8;
+  SCB_CUDA(cudaFuncSetAttribute(trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  trsm_rows_kernel<<<std::max(1, std::min(ctx->num_sms * 2, (h + 7) / 8)), 256, smem, s>>>(R, M, h, done);
+  SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
 
-// M[h][kB] (row-major) := an orthonormal basis of its column space by Householder QR
-// (cuSOLVER geqrf + orgqr on the column-major transpose, via cublasDgeam); robust to rank
-// deficiency.  tmp: h * kB doubles.  Used only when CholQR breaks down.
-static int householder_orth(scb_ctx* ctx, int h, double* M, double* tmp, cudaStream_t s) {
-  if (!ctx->solver) {
-    cusolverDnHandle_t sh;
-    SCB_REQUIRE(cusolverDnCreate(&sh) == CUSOLVER_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: cusolverDnCreate failed");
-    ctx->solver = sh;
+// M[h][kB] (row-major) := an orthonormal basis by classical Gram-Schmidt with
+// re-orthogonalisation (CGS2) in one CTA; a column that vanishes (rank deficiency) is replaced
+// by a deterministic pseudo-random vector and re-orthogonalised, completing the basis.  Used
+// only when Cholesky-QR breaks down (fewer than kB + 1 distinct cells).
+constexpr int kOrthThreads = 1024;
+__device__ __forceinline__ double hash_unit(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+__device__ double block_sum(double v, double* sb) {
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane_id() == 0) sb[warp_id()] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sb[w];
+  return t;
+}
+__global__ void __launch_bounds__(kOrthThreads) cgs2_kernel(double* __restrict__ Mq, int h,
+                                                            const int* __restrict__ done) {
+  if (done && *done) return;
+  __shared__ double coef[kB];
+  __shared__ double sb[32];
+  for (int j = 0; j < kB; ++j) {
+    for (int attempt = 0; attempt < 4; ++attempt) {
+      double n0 = 0.0;
+      for (int i = threadIdx.x; i < h; i += blockDim.x) n0 += Mq[(size_t)i * kB + j] * Mq[(size_t)i * kB + j];
+      n0 = sqrt(block_sum(n0, sb));
+      for (int pass = 0; pass < 2; ++pass) {
+        // coef[c] = <q_c, m_j> for c < j: warp w takes columns w, w+32, ...
+        for (int c = warp_id(); c < j; c += blockDim.x >> 5) {
+          double d = 0.0;
+          for (int i = lane_id(); i < h; i += 32) d += Mq[(size_t)i * kB + c] * Mq[(size_t)i * kB + j];
+          d = warp_sum(d);
+          if (lane_id() == 0) coef[c] = d;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < h; i += blockDim.x) {
+          double v = Mq[(size_t)i * kB + j];
+          for (int c = 0; c < j; ++c) v -= coef[c] * Mq[(size_t)i * kB + c];
+          Mq[(size_t)i * kB + j] = v;
+        }
+        __syncthreads();
+      }
+      double nn = 0.0;
+      for (int i = threadIdx.x; i < h; i += blockDim.x) nn += Mq[(size_t)i * kB + j] * Mq[(size_t)i * kB + j];
+      nn = sqrt(block_sum(nn, sb));
+      if (nn > 1e-10 * fmax(n0, 1e-300) && nn > 1e-300) {
+        for (int i = threadIdx.x; i < h; i += blockDim.x) Mq[(size_t)i * kB + j] /= nn;
+        __syncthreads();
+        break;
+      }
+      for (int i = threadIdx.x; i < h; i += blockDim.x)  // dependent column: restart from a random vector
+        Mq[(size_t)i * kB + j] = hash_unit(((uint64_t)(attempt + 1) << 40) ^ ((uint64_t)j << 20) ^ (uint64_t)i);
+      __syncthreads();
+    }
   }
-  cusolverDnHandle_t sh = (cusolverDnHandle_t)ctx->solver;
-  cublasHandle_t bh = (cublasHandle_t)ctx->blas;
-  SCB_REQUIRE(cusolverDnSetStream(sh, s) == CUSOLVER_STATUS_SUCCESS && cublasSetStream(bh, s) == CUBLAS_STATUS_SUCCESS,
-              SCB_ERR_CUDA, "scb_pca_eig: set stream failed");
-  const double one = 1.0, zero = 0.0;
-  // row-major M[h][kB] is column-major kB x h; tmp := its transpose (column-major h x kB)
-  SCB_REQUIRE(cublasDgeam(bh, CUBLAS_OP_T, CUBLAS_OP_N, h, kB, &one, M, kB, &zero, tmp, h, tmp, h) ==
-                  CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: geam failed");
-  int lw1 = 0, lw2 = 0;
-  SCB_REQUIRE(cusolverDnDgeqrf_bufferSize(sh, h, kB, tmp, h, &lw1) == CUSOLVER_STATUS_SUCCESS, SCB_ERR_CUDA,
-              "scb_pca_eig: geqrf_bufferSize failed");
-  void* ws;
-  const size_t need = (size_t)(kB + std::max(lw1, 1)) * 8 + 64;
-  SCB_TRY(ws_get(ctx, 3, need, &ws, s));
-  double* tau = (double*)ws;
-  double* work = tau + kB;
-  int* info = (int*)((char*)ws + need - 16);
-  SCB_REQUIRE(cusolverDnDgeqrf(sh, h, kB, tmp, h, tau, work, lw1, info) == CUSOLVER_STATUS_SUCCESS, SCB_ERR_CUDA,
-              "scb_pca_eig: geqrf failed");
-  SCB_REQUIRE(cusolverDnDorgqr_bufferSize(sh, h, kB, kB, tmp, h, tau, &lw2) == CUSOLVER_STATUS_SUCCESS, SCB_ERR_CUDA,
-              "scb_pca_eig: orgqr_bufferSize failed");
-  if (lw2 > lw1) {
-    const size_t need2 = (size_t)(kB + lw2) * 8 + 64;
-    SCB_TRY(ws_get(ctx, 3, need2, &ws, s));
-    tau = (double*)ws;  // tau must survive: recompute geqrf into the larger buffer
-    work = tau + kB;
-    info = (int*)((char*)ws + need2 - 16);
-    SCB_REQUIRE(cublasDgeam(bh, CUBLAS_OP_T, CUBLAS_OP_N, h, kB, &one, M, kB, &zero, tmp, h, tmp, h) ==
-                    CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: geam failed");
-    SCB_REQUIRE(cusolverDnDgeqrf(sh, h, kB, tmp, h, tau, work, lw2, info) == CUSOLVER_STATUS_SUCCESS, SCB_ERR_CUDA,
-                "scb_pca_eig: geqrf failed");
-    lw1 = lw2;
-  }
-  SCB_REQUIRE(cusolverDnDorgqr(sh, h, kB, kB, tmp, h, tau, work, std::max(lw1, lw2), info) == CUSOLVER_STATUS_SUCCESS,
-              SCB_ERR_CUDA, "scb_pca_eig: orgqr failed");
-  // back to row-major M[h][kB]: column-major kB x h = transpose of tmp
-  SCB_REQUIRE(cublasDgeam(bh, CUBLAS_OP_T, CUBLAS_OP_N, kB, h, &one, tmp, h, &zero, M, kB, M, kB) ==
-                  CUBLAS_STATUS_SUCCESS, SCB_ERR_CUDA, "scb_pca_eig: geam failed");
-  return SCB_OK;
 }
 
 // ------------------------------------------------------------------ covariance
@@ -143,7 +247,9 @@ __global__ void init_block_kernel(double* __restrict__ Q, int h) {
 // ------------------------------------------------------------------ Cholesky QR
 // In place Cholesky of the kB x kB Gram S = Q^T Q (one CTA), S -> R (upper, row-major).
 constexpr int kCholThreads = 1024;  // 32 x 32 thread grid over the trailing matrix
-__global__ void __launch_bounds__(kCholThreads) chol_kernel(double* __restrict__ S, int* __restrict__ fail) {
+__global__ void __launch_bounds__(kCholThreads) chol_kernel(double* __restrict__ S, int* __restrict__ fail,
+                                                             const int* __restrict__ done) {
+  if (*done) return;
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) a[e / kB][e % kB] = S[e];
@@ -188,7 +294,21 @@ __device__ int g_jacobi_sweeps;  // debug: sweeps used by the last call
 // element of A belongs to exactly one 2x2 block (rows of pair k, columns of pair l), updated
 // in a single pass as R_k^T B R_l by one thread (the k > l block is the mirror), so a round
 // is two barriers and one read + one write of A and W.
-__global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict__ T, double* __restrict__ W, int sweeps) {
+// device-side solver state (no host round trip per outer step)
+struct EigState {
+  double cheb_b;      // top of the damped interval of the Chebyshev filter (smallest Ritz value)
+  double prev_worst;  // relative residual of the previous outer step
+  double worst;       // max_j ||Cov v_j - l_j v_j|| / l_1 of the wanted pairs, last executed step
+  int done;           // converged: every later kernel of the solve exits at once
+  int iters;          // outer steps executed
+};
+
+__global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict__ T, double* __restrict__ W,
+                                                              const EigState* __restrict__ st) {
+  if (st->done) return;
+  // far from convergence the Rayleigh-Ritz step only has to supply the filter bound and a
+  // reasonable rotation (every rotation is exactly orthogonal): 2 sweeps; near it, to completion
+  const int sweeps = st->prev_worst > 1e-4 ? 2 : 30;
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
   double (*w)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn + kB * kLd);
@@ -282,7 +402,9 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
 }
 
 // order eigenpairs by eigenvalue (desc), top k; eigenvalues from diag(T)
-__global__ void select_kernel(const double* __restrict__ T, int k, int* __restrict__ order, double* __restrict__ lam) {
+__global__ void select_kernel(const double* __restrict__ T, int k, int* __restrict__ order, double* __restrict__ lam,
+                              const int* __restrict__ done) {
+  if (*done) return;
   __shared__ double d[kB];
   if (threadIdx.x < kB) d[threadIdx.x] = T[threadIdx.x * kB + threadIdx.x];
   __syncthreads();
@@ -299,14 +421,17 @@ __global__ void select_kernel(const double* __restrict__ T, int k, int* __restri
 
 // V[h][k] = Q[h][kB] * W[:, order]
 __global__ void gather_cols_kernel(const double* __restrict__ W, const int* __restrict__ order, int k,
-                                   double* __restrict__ Wk) {
+                                   double* __restrict__ Wk, const int* __restrict__ done) {
+  if (*done) return;
   const int i = blockIdx.x, j = threadIdx.x;
   if (j < k) Wk[(size_t)i * k + j] = W[(size_t)i * kB + order[j]];
 }
 
 // residual r_j = ||Cov v_j - l_j v_j||, components sign fix and output
 __global__ void residual_kernel(const double* __restrict__ CV, const double* __restrict__ V, const double* __restrict__ lam,
-                                int h, int k, double* __restrict__ res) {  // k = leading dimension of CV / V
+                                int h, int k, double* __restrict__ res,
+                                const int* __restrict__ done) {  // k = leading dimension of CV / V
+  if (*done) return;
   const int j = blockIdx.x;
   __shared__ double sb[32];
   double s = 0.0;
@@ -349,12 +474,36 @@ __global__ void gather_first_cols_kernel(const double* __restrict__ Q, int ld, i
   if (j < k) V[(size_t)i * k + j] = Q[(size_t)i * ld + j];
 }
 
-// Chebyshev three-term step: out = alpha * CY + beta * Y + gamma * Yold (element-wise)
+// Chebyshev three-term step: out = (alpha_mult * 2 / b) * CY + beta * Y + gamma * Yold (element-wise),
+// b = st->cheb_b read on the device
 __global__ void cheb_combine_kernel(const double* __restrict__ CY, const double* __restrict__ Y,
-                                    const double* __restrict__ Yold, int64_t n, double alpha, double beta, double gamma,
-                                    double* __restrict__ out) {
+                                    const double* __restrict__ Yold, int64_t n, double alpha_mult, double beta,
+                                    double gamma, double* __restrict__ out, const EigState* __restrict__ st) {
+  if (st->done) return;
+  const double alpha = alpha_mult * (2.0 / st->cheb_b);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = alpha * CY[i] + beta * Y[i] + (Yold ? gamma * Yold[i] : 0.0);
+}
+
+__global__ void copy_gated_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t n,
+                                  const int* __restrict__ done) {
+  if (*done) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[i];
+}
+
+// after the residuals of an outer step: filter bound, convergence, iteration count
+__global__ void eig_state_kernel(const double* __restrict__ res, const double* __restrict__ lam_all, int n_comps,
+                                 EigState* __restrict__ st) {
+  if (st->done) return;
+  const double lam0 = lam_all[0], lamb = lam_all[kB - 1];
+  double worst = 0.0;
+  for (int j = 0; j < n_comps; ++j) worst = fmax(worst, res[j]);
+  st->cheb_b = fmax(lamb, 1e-12 * lam0);
+  st->prev_worst = worst / fmax(lam0, 1e-300);
+  st->worst = st->prev_worst;
+  st->iters += 1;
+  if (worst <= 1e-9 * fmax(lam0, 1e-300)) st->done = 1;
 }
 
 __global__ void fill_zero_rows(float* __restrict__ comp_t, int k, int kpad, int hp) {
@@ -374,7 +523,7 @@ using namespace scb;
 
 static int pca_eig_impl(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, int32_t ones_col, int64_t n_cells,
                         int32_t n_comps, int32_t n_comps_pad, double* eigenvalues, float* components_t,
-                        float* col_mean, double* trace, void* stream, bool use_qr, bool* broke) {
+                        float* col_mean, double* trace, void* stream, bool use_qr, bool* broke, double* final_res) {
   *broke = false;
   SCB_REQUIRE(ctx && C && eigenvalues && components_t && col_mean && trace, SCB_ERR_ARG, "scb_pca_eig: null argument");
   SCB_REQUIRE(n_comps >= 1 && n_comps <= kB - 16 && n_comps <= h && n_comps_pad >= n_comps, SCB_ERR_ARG,
@@ -385,140 +534,122 @@ static int pca_eig_impl(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, in
   const int kSmemKB = kB * kLd * 8;
   SCB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemKB));
   SCB_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSmemKB));
-  // workspace: cov h*h, Q h*kB, Y h*kB, S kB*kB, W kB*kB, Wk kB*n, V h*n, CV h*n, mean h, misc
-  const size_t nd = (size_t)h * h + 2 * (size_t)h * kB + 3 * kB * kB + (size_t)kB * kB + 2 * (size_t)h * kB +
-                    h + 4 * kB + 64;
+  // workspace: cov h*h, Qf/Q/Y/Yold/V h*kB each, S 2*kB*kB, W kB*kB, Wk kB*kB, mean h, res, lam, order, flags
+  const size_t nd = (size_t)h * h + 5 * (size_t)h * kB + 4 * (size_t)kB * kB + h + 4 * kB + 64;
   void* ws;
   SCB_TRY(ws_get(ctx, 2, nd * 8 + 4096, &ws, s));
   double* cov = (double*)ws;
-  double* Q = cov + (size_t)h * h;
+  double* Qf = cov + (size_t)h * h;   // the iterate between outer steps (fixed buffer)
+  double* Q = Qf + (size_t)h * kB;
   double* Y = Q + (size_t)h * kB;
-  double* S = Y + (size_t)h * kB;
+  double* Yold = Y + (size_t)h * kB;
+  double* V = Yold + (size_t)h * kB;
+  double* S = V + (size_t)h * kB;
   double* W = S + 2 * kB * kB;
   double* Wk = W + kB * kB;
-  double* V = Wk + (size_t)kB * kB;
-  double* CV = V + (size_t)h * kB;
-  double* mean = CV + (size_t)h * kB;
+  double* mean = Wk + (size_t)kB * kB;
   double* res = mean + h;
   double* lam_all = res + kB;
   int* order = (int*)(lam_all + kB);
   int* fail = order + kB;
+  EigState* st = (EigState*)(((uintptr_t)(fail + 4) + 15) & ~(uintptr_t)15);
+  const int* done = &st->done;
 
   dim3 gc((h + 255) / 256, h);
   cov_build_kernel<<<gc, 256, 0, s>>>(C, hp, h, ones_col, n_cells, cov, mean);
   SCB_LAUNCH_CHECK();
   trace_kernel<<<1, 1024, 0, s>>>(cov, h, trace);
   SCB_LAUNCH_CHECK();
-  init_block_kernel<<<h, kB, 0, s>>>(Q, h);
+  init_block_kernel<<<h, kB, 0, s>>>(Qf, h);
   SCB_LAUNCH_CHECK();
   SCB_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
-  auto orth = [&](double*& M, int reps) -> int {
-    if (use_qr) return householder_orth(ctx, h, M, Y, s);  // rank-deficient fallback
-    for (int rep = 0; rep < reps; ++rep) {  // CholQR(reps): M := M R^{-1}
-      SCB_TRY(dgemm(ctx, kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s));
-      chol_kernel<<<1, kCholThreads, kSmemKB, s>>>(S, fail);
+  SCB_CUDA(cudaMemsetAsync(st, 0, sizeof(EigState), s));
+  auto orth = [&](double* M, int reps) -> int {
+    if (use_qr) {  // rank-deficient fallback
+      cgs2_kernel<<<1, kOrthThreads, 0, s>>>(M, h, done);
       SCB_LAUNCH_CHECK();
-      SCB_TRY(trsm_right_upper(ctx, h, S, M, s));  // M := M R^{-1} in place
+      return SCB_OK;
+    }
+    for (int rep = 0; rep < reps; ++rep) {  // CholQR(reps): M := M R^{-1}
+      SCB_TRY(dgemm(ctx, kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s, done));
+      chol_kernel<<<1, kCholThreads, kSmemKB, s>>>(S, fail, done);
+      SCB_LAUNCH_CHECK();
+      SCB_TRY(trsm_right_upper(ctx, h, S, M, s, done));  // M := M R^{-1} in place
     }
     return SCB_OK;
   };
-  SCB_TRY(orth(Q, 2));
+  SCB_TRY(orth(Qf, 2));
   // filter degree: 6 converges the synthetic C3 spectrum in 3 outer steps (3 -> 5 steps, 8 -> 3 steps
   // but slower ones; >= 12 overflows CholQR's conditioning), scratch/prof_eig_real.py
-  const int kPower = 6, kMaxOuter = 60;
-  double host_res[kB];
-  int outer = 0;
+  const int kPower = 6, kMaxOuter = 60, kBatch = 4;
+  const int64_t nel = (int64_t)h * kB;
+  const int eb = (int)((nel + 255) / 256);
   const bool verbose = getenv("SCB_EIG_VERBOSE") != nullptr;
-  cudaEvent_t ev0, ev1;
-  if (verbose) {
-    cudaEventCreate(&ev0);
-    cudaEventCreate(&ev1);
-    cudaEventRecord(ev0, s);
-  }
-  double prev_worst = 1.0;  // relative residual of the previous outer step
-  double cheb_b = 0.0;  // top of the damped interval [0, b] (smallest Ritz value of the block)
-  double* Yold = CV;      // h x kB scratch for the three-term recurrence (CV reused below)
-  for (; outer < kMaxOuter; ++outer) {
-    if (cheb_b <= 0.0) {
-      // plain power steps until Ritz values are known
-      for (int pw = 0; pw < kPower; ++pw) {
-        SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s));
-        std::swap(Q, Y);
-      }
-    } else {
-      // Chebyshev filter T_kPower(sigma), sigma = (2/b) Cov - I: damps [0, b], amplifies > b
-      const int64_t nel = (int64_t)h * kB;
-      const int eb = (int)((nel + 255) / 256);
-      const double a2 = 2.0 / cheb_b;
-      // Y1 = sigma Q  -> stored in Y
-      SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, V, kB, s));
-      cheb_combine_kernel<<<eb, 256, 0, s>>>(V, Q, nullptr, nel, a2, -1.0, 0.0, Y);
-      SCB_LAUNCH_CHECK();
-      std::swap(Q, Yold);  // Yold = Y0
-      for (int k = 1; k < kPower; ++k) {  // Y_{k+1} = 2 sigma Y_k - Y_{k-1}
-        SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Y, kB, 0, V, kB, s));
-        cheb_combine_kernel<<<eb, 256, 0, s>>>(V, Y, Yold, nel, 2.0 * a2, -2.0, -1.0, Q);
+  EigState hs{};
+  int outer = 0;
+  // Outer steps are enqueued kBatch at a time; every kernel exits at once after convergence
+  // (device flag), so a converged solve costs one host round trip per batch.
+  while (outer < kMaxOuter) {
+    for (int b = 0; b < kBatch && outer < kMaxOuter; ++b, ++outer) {
+      SCB_CUDA(cudaMemcpyAsync(Q, Qf, nel * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      if (outer == 0) {  // plain power steps until Ritz values are known
+        for (int pw = 0; pw < kPower; ++pw) {
+          SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, done));
+          std::swap(Q, Y);
+        }
+      } else {
+        // Chebyshev filter T_kPower(sigma), sigma = (2/b) Cov - I: damps [0, b], amplifies > b
+        SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, V, kB, s, done));
+        cheb_combine_kernel<<<eb, 256, 0, s>>>(V, Q, nullptr, nel, 1.0, -1.0, 0.0, Y, st);  // Y1 = sigma Q
         SCB_LAUNCH_CHECK();
-        std::swap(Yold, Y);  // Yold = Y_k
-        std::swap(Y, Q);     // Y = Y_{k+1}
+        std::swap(Q, Yold);  // Yold = Y0
+        for (int k = 1; k < kPower; ++k) {  // Y_{k+1} = 2 sigma Y_k - Y_{k-1}
+          SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Y, kB, 0, V, kB, s, done));
+          cheb_combine_kernel<<<eb, 256, 0, s>>>(V, Y, Yold, nel, 2.0, -2.0, -1.0, Q, st);
+          SCB_LAUNCH_CHECK();
+          std::swap(Yold, Y);  // Yold = Y_k
+          std::swap(Y, Q);     // Y = Y_{k+1}
+        }
+        std::swap(Q, Y);  // Q = last iterate
       }
-      std::swap(Q, Y);  // Q = last iterate
+      SCB_TRY(orth(Q, 2));
+      // Rayleigh-Ritz: T = Q^T Cov Q, T = W diag W^T; rotate Q := Q W (sorted descending)
+      SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, done));        // Y = Cov Q
+      SCB_TRY(dgemm(ctx, kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s, done));        // T = Q^T Y
+      jacobi_kernel<<<1, kJacThreads, 2 * kSmemKB, s>>>(S, W, st);
+      SCB_LAUNCH_CHECK();
+      select_kernel<<<1, kB, 0, s>>>(S, kB, order, lam_all, done);
+      SCB_LAUNCH_CHECK();
+      gather_cols_kernel<<<kB, kB, 0, s>>>(W, order, kB, Wk, done);
+      SCB_LAUNCH_CHECK();
+      SCB_TRY(dgemm(ctx, h, kB, kB, Q, kB, 0, Wk, kB, 0, Yold, kB, s, done));   // Ritz vectors
+      SCB_TRY(dgemm(ctx, h, kB, kB, Y, kB, 0, Wk, kB, 0, V, kB, s, done));      // Cov * Ritz vectors
+      residual_kernel<<<n_comps, 256, 0, s>>>(V, Yold, lam_all, h, kB, res, done);
+      SCB_LAUNCH_CHECK();
+      copy_gated_kernel<<<eb, 256, 0, s>>>(Yold, Qf, nel, done);                 // next iterate
+      SCB_LAUNCH_CHECK();
+      eig_state_kernel<<<1, 1, 0, s>>>(res, lam_all, n_comps, st);
+      SCB_LAUNCH_CHECK();
     }
-    SCB_TRY(orth(Q, 2));
-    // Rayleigh-Ritz: T = Q^T Cov Q, T = W diag W^T; rotate Q := Q W (sorted descending)
-    SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s));        // Y = Cov Q
-    SCB_TRY(dgemm(ctx, kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s));   // T = Q^T Y
-    // Far from convergence the Rayleigh-Ritz step only has to supply the filter bound and a
-    // reasonable rotation (every Jacobi rotation is exactly orthogonal, so a partial sweep
-    // count never damages the subspace): 2 sweeps.  Near convergence it runs to completion.
-    jacobi_kernel<<<1, kJacThreads, 2 * kSmemKB, s>>>(S, W, prev_worst > 1e-4 ? 2 : 30);
-    SCB_LAUNCH_CHECK();
-    select_kernel<<<1, kB, 0, s>>>(S, kB, order, lam_all);
-    SCB_LAUNCH_CHECK();
-    gather_cols_kernel<<<kB, kB, 0, s>>>(W, order, kB, Wk);
-    SCB_LAUNCH_CHECK();
-    SCB_TRY(dgemm(ctx, h, kB, kB, Q, kB, 0, Wk, kB, 0, Yold, kB, s));        // Ritz vectors (spare buffer)
-    SCB_TRY(dgemm(ctx, h, kB, kB, Y, kB, 0, Wk, kB, 0, V, kB, s));           // Cov * Ritz vectors
-    std::swap(Q, Yold);
-    residual_kernel<<<n_comps, 256, 0, s>>>(V, Q, lam_all, h, kB, res);
-    SCB_LAUNCH_CHECK();
-    double lam0 = 0.0, lamb = 0.0;
-    SCB_CUDA(cudaMemcpyAsync(host_res, res, sizeof(double) * n_comps, cudaMemcpyDeviceToHost, s));
-    SCB_CUDA(cudaMemcpyAsync(&lam0, lam_all, sizeof(double), cudaMemcpyDeviceToHost, s));
-    SCB_CUDA(cudaMemcpyAsync(&lamb, lam_all + kB - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
     int hfail_now = 0;
+    SCB_CUDA(cudaMemcpyAsync(&hs, st, sizeof(EigState), cudaMemcpyDeviceToHost, s));
     SCB_CUDA(cudaMemcpyAsync(&hfail_now, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
     SCB_CUDA(cudaStreamSynchronize(s));
-    if (hfail_now) {  // Cholesky-QR broke down (block rank-deficient): caller retries with QR
+    if (verbose)
+      fprintf(stderr, "[scb_pca_eig] after %d enqueued outer steps: executed %d, residual %.3e, done %d\n", outer,
+              hs.iters, hs.worst, hs.done);
+    if (hfail_now) {  // Cholesky-QR broke down (block rank-deficient): caller retries with CGS2
       *broke = true;
       return SCB_OK;
     }
-    cheb_b = std::max(lamb, 1e-12 * lam0);
-    double worst = 0.0;  // max residual / lambda_1 of the wanted Ritz pairs
-    for (int j = 0; j < n_comps; ++j) worst = std::max(worst, host_res[j]);
-    if (verbose) {
-      cudaEventRecord(ev1, s);
-      cudaEventSynchronize(ev1);
-      float ms = 0;
-      cudaEventElapsedTime(&ms, ev0, ev1);
-      int sweeps = 0;
-      cudaMemcpyFromSymbol(&sweeps, g_jacobi_sweeps, sizeof(int));
-      fprintf(stderr, "[scb_pca_eig] outer %d residual %.3e (lam0 %.4e) jacobi sweeps %d elapsed %.2f ms\n", outer + 1,
-              worst, lam0, sweeps, ms);
-    }
-    prev_worst = worst / std::max(lam0, 1e-300);
-    if (worst <= 1e-9 * std::max(lam0, 1e-300)) break;
+    if (hs.done) break;
   }
-  // V := the n_comps leading Ritz vectors (columns 0..n_comps-1 of Q, already sorted)
-  gather_first_cols_kernel<<<h, kB, 0, s>>>(Q, kB, n_comps, V);
+  *final_res = hs.worst;
+  SCB_REQUIRE(hs.done, SCB_ERR_DATA, "scb_pca_eig: not converged after %d outer steps (relative residual %.3e)",
+              kMaxOuter, hs.worst);
+  // V := the n_comps leading Ritz vectors (columns 0..n_comps-1 of Qf, already sorted)
+  gather_first_cols_kernel<<<h, kB, 0, s>>>(Qf, kB, n_comps, V);
   SCB_LAUNCH_CHECK();
-  int hfail = 0;
-  SCB_CUDA(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SCB_CUDA(cudaStreamSynchronize(s));
-  if (hfail) {
-    *broke = true;
-    return SCB_OK;
-  }
   SCB_CUDA(cudaMemcpyAsync(eigenvalues, lam_all, sizeof(double) * n_comps, cudaMemcpyDeviceToDevice, s));
   finalize_components_kernel<<<n_comps, 256, 0, s>>>(V, h, n_comps, hp, n_comps_pad, components_t);
   SCB_LAUNCH_CHECK();
@@ -535,14 +666,15 @@ extern "C" int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp,
                            int32_t n_comps, int32_t n_comps_pad, double* eigenvalues, float* components_t,
                            float* col_mean, double* trace, void* stream) {
   // CholQR2 orthonormalisation; if the block turns rank-deficient (fewer than kB + 1 cells, or
-  // duplicated cells: the covariance has rank < kB) the solve is redone with Householder QR,
-  // which completes the basis with arbitrary orthonormal directions
+  // duplicated cells: the covariance has rank < kB) the solve is redone with CGS2, which
+  // completes the basis with pseudo-random orthonormal directions
   bool broke = false;
+  double res = 0.0;
   SCB_TRY(pca_eig_impl(ctx, C, h, hp, ones_col, n_cells, n_comps, n_comps_pad, eigenvalues, components_t, col_mean,
-                       trace, stream, false, &broke));
+                       trace, stream, false, &broke, &res));
   if (!broke) return SCB_OK;
   SCB_TRY(pca_eig_impl(ctx, C, h, hp, ones_col, n_cells, n_comps, n_comps_pad, eigenvalues, components_t, col_mean,
-                       trace, stream, true, &broke));
+                       trace, stream, true, &broke, &res));
   SCB_REQUIRE(!broke, SCB_ERR_DATA, "scb_pca_eig: orthonormalisation breakdown");
   return SCB_OK;
 }

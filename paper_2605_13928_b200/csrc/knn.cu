@@ -123,9 +123,9 @@ __device__ __forceinline__ int order_bucket(const float* x, int d, const int* om
 }
 
 __global__ void bucket_hist_kernel(const float* __restrict__ X, int64_t n, int d, int ld, const int* omin,
-                                   const int* omax, int* __restrict__ hist) {
+                                   const int* omax, const uint16_t* __restrict__ ext, int* __restrict__ hist) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&hist[order_bucket(X + r * ld, d, omin, omax)], 1);
+    atomicAdd(&hist[ext ? (int)ext[r] : order_bucket(X + r * ld, d, omin, omax)], 1);
 }
 
 // single CTA exclusive scan of the bucket histogram (in place)
@@ -164,10 +164,10 @@ __global__ void bucket_scan_kernel(int* __restrict__ hist) {
 
 // scatter rows into curve order; key_sorted[pos] = bucket id (non-decreasing, for start search)
 __global__ void bucket_scatter_kernel(const float* __restrict__ X, int64_t n, int d, int ld, const int* omin,
-                                      const int* omax, int* __restrict__ cursor, int* __restrict__ perm,
-                                      float* __restrict__ key_sorted) {
+                                      const int* omax, const uint16_t* __restrict__ ext, int* __restrict__ cursor,
+                                      int* __restrict__ perm, float* __restrict__ key_sorted) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-    const int b = order_bucket(X + r * ld, d, omin, omax);
+    const int b = ext ? (int)ext[r] : order_bucket(X + r * ld, d, omin, omax);
     const int pos = atomicAdd(&cursor[b], 1);
     perm[pos] = (int)r;
     key_sorted[pos] = (float)b;
@@ -586,21 +586,22 @@ __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __re
 
 // ------------------------------------------------------------------ host orchestration
 static int sort_by_pc1(const float* X, int64_t n, int d, int ld, const int* omin, const int* omax, int* hist, int* perm,
-                       float* pc1_sorted, cudaStream_t s) {
+                       float* pc1_sorted, cudaStream_t s, const uint16_t* ext = nullptr) {
   SCB_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * kBuckets, s));
   const int g = std::max(1, std::min(1184, ceil_div(n, 256)));
-  bucket_hist_kernel<<<g, 256, 0, s>>>(X, n, d, ld, omin, omax, hist);
+  bucket_hist_kernel<<<g, 256, 0, s>>>(X, n, d, ld, omin, omax, ext, hist);
   SCB_LAUNCH_CHECK();
   bucket_scan_kernel<<<1, 1024, 0, s>>>(hist);
   SCB_LAUNCH_CHECK();
-  bucket_scatter_kernel<<<g, 256, 0, s>>>(X, n, d, ld, omin, omax, hist, perm, pc1_sorted);
+  bucket_scatter_kernel<<<g, 256, 0, s>>>(X, n, d, ld, omin, omax, ext, hist, perm, pc1_sorted);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
 
 template <int KC, int HALVES>
 static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* Kx, int64_t n_k, int d, int ld, int k,
-                      int* out_i, float* out_d, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+                      int* out_i, float* out_d, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                      const uint16_t* ext_key = nullptr) {
   using Cfg = KnnCfg<KC, HALVES>;
   constexpr int KCT = Cfg::KCT;
   const bool same = (Qx == Kx && n_q == n_k);
@@ -634,7 +635,7 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   const int g = std::max(1, std::min(1184, ceil_div(n_k, 256)));
   range_kernel<<<g, 256, 0, s>>>(Kx, n_k, d, ld, amax, omin, omax);
   SCB_LAUNCH_CHECK();
-  SCB_TRY(sort_by_pc1(Kx, n_k, d, ld, omin, omax, hist, perm_k, pc1_k, s));
+  SCB_TRY(sort_by_pc1(Kx, n_k, d, ld, omin, omax, hist, perm_k, pc1_k, s, same ? ext_key : nullptr));
   if (same) {
     perm_q = perm_k;
     pc1_q = pc1_k;
@@ -691,6 +692,17 @@ extern "C" int scb_knn_timed(scb_ctx* ctx, const float* queries, int64_t n_queri
   if (k_cand == 32) return launch_knn<16, 2>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
   if (k <= 32) return launch_knn<48, 1>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
   return launch_knn<64, 1>(ctx, queries, n_queries, keys, n_keys, d, ld, k, knn_index, knn_dist, s, e0, e1);
+}
+
+// experiment hook: caller-supplied 16-bit scan-order bucket per row (queries == keys only)
+extern "C" int scb_knn_ordered(scb_ctx* ctx, const float* x, int64_t n, int32_t d, int32_t ld, int32_t k,
+                               const uint16_t* order_key, int32_t* knn_index, float* knn_dist, void* stream,
+                               void* ev_start, void* ev_end) {
+  SCB_REQUIRE(ctx && x && knn_index && knn_dist, SCB_ERR_ARG, "scb_knn_ordered: null argument");
+  SCB_REQUIRE(d >= 1 && d <= kD - 2 && ld >= d && k >= 1 && k <= 16 && k <= n, SCB_ERR_ARG, "scb_knn_ordered: bad args");
+  if (n == 0) return SCB_OK;
+  return launch_knn<16, 2>(ctx, x, n, x, n, d, ld, k, knn_index, knn_dist, (cudaStream_t)stream, (cudaEvent_t)ev_start,
+                           (cudaEvent_t)ev_end, order_key);
 }
 
 extern "C" int scb_knn(scb_ctx* ctx, const float* queries, int64_t n_queries, const float* keys, int64_t n_keys,

@@ -1,6 +1,4 @@
 // Context, scratch arena and error reporting behind the C ABI.
-#include <cublas_v2.h>
-#include <cusolverDn.h>
 #include "common.cuh"
 #include <algorithm>
 #include <atomic>
@@ -85,8 +83,6 @@ extern "C" int scb_ctx_destroy(scb_ctx* ctx) {
   for (auto& w : ctx->ws)
     if (w.ptr) cudaFree(w.ptr);
   if (ctx->d_flag) cudaFree(ctx->d_flag);
-  if (ctx->blas) cublasDestroy((cublasHandle_t)ctx->blas);
-  if (ctx->solver) cusolverDnDestroy((cusolverDnHandle_t)ctx->solver);
   delete ctx;
   return SCB_OK;
 }
