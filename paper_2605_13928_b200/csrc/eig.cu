@@ -248,7 +248,7 @@ __global__ void init_block_kernel(double* __restrict__ Q, int h) {
 // In place Cholesky of the kB x kB Gram S = Q^T Q (one CTA), S -> R (upper, row-major).
 constexpr int kCholThreads = 1024;  // 32 x 32 thread grid over the trailing matrix
 __global__ void __launch_bounds__(kCholThreads) chol_kernel(double* __restrict__ S, int* __restrict__ fail,
-                                                             const int* __restrict__ done) {
+                                                             int* __restrict__ done) {
   if (*done) return;
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
@@ -262,7 +262,10 @@ __global__ void __launch_bounds__(kCholThreads) chol_kernel(double* __restrict__
     const double r = sqrt(d), inv = 1.0 / r;
     __syncthreads();  // all pivots read before row k is rescaled
     if (threadIdx.x == 0) {
-      if (!(a[k][k] > 0.0)) *fail = 1;
+      if (!(a[k][k] > 0.0)) {
+        *fail = 1;
+        *done = 1;  // stop the enqueued outer steps; the host redoes the solve with CGS2
+      }
       a[k][k] = r;
     }
     for (int j = k + 1 + threadIdx.x; j < kB; j += blockDim.x) a[k][j] *= inv;
@@ -406,7 +409,10 @@ __global__ void select_kernel(const double* __restrict__ T, int k, int* __restri
                               const int* __restrict__ done) {
   if (*done) return;
   __shared__ double d[kB];
-  if (threadIdx.x < kB) d[threadIdx.x] = T[threadIdx.x * kB + threadIdx.x];
+  if (threadIdx.x < kB) {
+    const double v = T[threadIdx.x * kB + threadIdx.x];
+    d[threadIdx.x] = isnan(v) ? -INFINITY : v;  // ranks stay a permutation
+  }
   __syncthreads();
   if (threadIdx.x < kB) {
     const int i = threadIdx.x;
@@ -572,7 +578,7 @@ static int pca_eig_impl(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, in
     }
     for (int rep = 0; rep < reps; ++rep) {  // CholQR(reps): M := M R^{-1}
       SCB_TRY(dgemm(ctx, kB, kB, h, M, kB, 1, M, kB, 0, S, kB, s, done));
-      chol_kernel<<<1, kCholThreads, kSmemKB, s>>>(S, fail, done);
+      chol_kernel<<<1, kCholThreads, kSmemKB, s>>>(S, fail, &st->done);
       SCB_LAUNCH_CHECK();
       SCB_TRY(trsm_right_upper(ctx, h, S, M, s, done));  // M := M R^{-1} in place
     }

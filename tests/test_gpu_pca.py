@@ -96,3 +96,23 @@ def test_gram_split_planes_match_converter_path(n, h):
     assert e2 <= e1 * 1.01 + 1e-7, (e1, e2)
     assert e2 < 1e-5, e2
     assert (np.abs(C1 - C2) / np.maximum(scale, 1e-30)).max() < 2e-5
+
+
+def test_pca_rank_deficient_uses_cgs2_fallback():
+    """60 distinct cells repeated (covariance rank <= 59 < the 96-wide block): Cholesky-QR breaks
+    down and the solve is redone with CGS2; the leading components still match numpy's eigh."""
+    import torch
+    from oracle import pipeline as op
+    from paper_2605_13928_b200 import pp
+    rng = np.random.default_rng(2)
+    base = rng.standard_normal((60, 200)) * np.linspace(3.0, 0.2, 200)[None, :]
+    Z = np.repeat(base, 50, axis=0).astype(np.float32)
+    sc = _scaled_from_host(Z, 200)
+    r = pp.pca(sc, n_comps=10)
+    torch.cuda.synchronize()
+    C, m = op.covariance(Z)
+    w, V = np.linalg.eigh(C)
+    V = V[:, np.argsort(w)[::-1][:10]]
+    got = r.components.cpu().numpy().T.astype(np.float64)
+    assert op.subspace_angle(got, V) < 1e-4  # 3xBF16 Gram (fp32 accumulation) vs an fp64 covariance
+    np.testing.assert_allclose(r.variance.cpu().numpy(), np.sort(w)[::-1][:10], rtol=1e-5)
