@@ -16,48 +16,76 @@ constexpr int kB = 96;   // subspace block size (n_comps + oversampling)
 constexpr int kLd = kB + 1;
 
 // ------------------------------------------------------------------ small fp64 GEMM
-// Cm[M][N] (ldc) = op(A) * op(B), row-major operands, fp64 on the CUDA cores (the eigensolver's
-// GEMMs are 2000 x 96 x 2000 at most, ~0.8 GFLOP each).  opA: 0 -> A[M][K] (lda), 1 -> A^T with
-// A stored [K][M]; opB: 0 -> B[K][N] (ldb), 1 -> B^T with B stored [N][K].  64x64 tiles, K chunk
-// 16, 256 threads with 4x4 outputs each.  Split-K over blockIdx.z writes per-slice partials
+// Cm[M][N] (ldc) = op(A) * op(B), row-major operands, fp64 on the FP64 tensor path (DMMA; the
+// eigensolver's GEMMs are 2000 x 96 x 2000 at most, ~0.8 GFLOP each).  opA: 0 -> A[M][K] (lda),
+// 1 -> A^T with A stored [K][M]; opB: 0 -> B[K][N] (ldb), 1 -> B^T with B stored [N][K].  64x64
+// tiles, K chunk 16.  Split-K over blockIdx.z writes per-slice partials
 // that a second kernel sums in slice order (deterministic).  Every kernel of the eigensolver
 // takes the device `done` flag and exits at once when it is set, so the host can enqueue a
 // batch of outer iterations without a round trip per iteration.
-constexpr int kGT = 64, kGK = 16;
-__global__ void __launch_bounds__(256) dgemm_kernel(int M, int N, int K, const double* __restrict__ A, int lda,
+constexpr int kGT = 64, kGK = 32;
+// DMMA (mma.sync m8n8k4 f64) tile GEMM: CTA 64x64 of C, 4 warps of 32x32 (4x4 MMA tiles of 8x8),
+// K staged through shared memory 32 at a time with the next chunk's global loads issued into
+// registers before the current chunk's MMAs.  Fragments (m8n8k4, row.col): lane = 4 g + t;
+// A[g][t], B[t][g], C[g][2t .. 2t+1].
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+constexpr int kGLoads = kGK * kGT / 128;  // elements of A (and of B) per thread per chunk
+__global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, const double* __restrict__ A, int lda,
                                                     int opA, const double* __restrict__ B, int ldb, int opB,
                                                     double* __restrict__ Cm, int ldc, int k_per_slice,
                                                     double* __restrict__ partial, const int* __restrict__ done) {
   if (done && *done) return;
-  __shared__ double As[kGK][kGT + 1];
-  __shared__ double Bs[kGK][kGT + 1];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  __shared__ double As[kGT][kGK + 1];   // [m][k]
+  __shared__ double Bs[kGK][kGT + 1];   // [k][n]
+  const int warp = warp_id(), lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int m0 = blockIdx.y * kGT, n0 = blockIdx.x * kGT;
   const int kb = blockIdx.z * k_per_slice, ke = min(K, kb + k_per_slice);
-  double acc[4][4] = {};
-  for (int k0 = kb; k0 < ke; k0 += kGK) {
-    for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
+  double acc[4][4][2] = {};
+  double ra[kGLoads], rb[kGLoads];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < kGLoads; ++u) {
+      const int e = threadIdx.x + 128 * u;
       int kk, mm;
       if (opA) { kk = e / kGT; mm = e % kGT; } else { mm = e / kGK; kk = e % kGK; }
       const int gm = m0 + mm, gk = k0 + kk;
-      As[kk][mm] = (gm < M && gk < ke) ? (opA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk]) : 0.0;
+      ra[u] = (gm < M && gk < ke) ? (opA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk]) : 0.0;
       int kn, nn;
       if (opB) { nn = e / kGK; kn = e % kGK; } else { kn = e / kGT; nn = e % kGT; }
       const int gn = n0 + nn, gk2 = k0 + kn;
-      Bs[kn][nn] = (gn < N && gk2 < ke) ? (opB ? B[(size_t)gn * ldb + gk2] : B[(size_t)gk2 * ldb + gn]) : 0.0;
+      rb[u] = (gn < N && gk2 < ke) ? (opB ? B[(size_t)gn * ldb + gk2] : B[(size_t)gk2 * ldb + gn]) : 0.0;
     }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int u = 0; u < kGLoads; ++u) {
+      const int e = threadIdx.x + 128 * u;
+      if (opA) As[e % kGT][e / kGT] = ra[u]; else As[e / kGK][e % kGK] = ra[u];
+      if (opB) Bs[e % kGK][e / kGK] = rb[u]; else Bs[e / kGT][e % kGT] = rb[u];
+    }
+  };
+  if (kb < ke) fetch(kb);
+  for (int k0 = kb; k0 < ke; k0 += kGK) {
+    stash();
     __syncthreads();
+    if (k0 + kGK < ke) fetch(k0 + kGK);  // next chunk in flight during this chunk's MMAs
 #pragma unroll
-    for (int kk = 0; kk < kGK; ++kk) {
-      double a[4], b[4];
+    for (int kk = 0; kk < kGK; kk += 4) {
+      double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+      for (int i = 0; i < 4; ++i) af[i] = As[wm + 8 * i + g][kk + t];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[kk + t][wn + 8 * j + g];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
     __syncthreads();
   }
@@ -66,10 +94,12 @@ __global__ void __launch_bounds__(256) dgemm_kernel(int M, int N, int K, const d
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
-      if (m < M && n < N) out[(size_t)m * ld + n] = acc[i][j];
-    }
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int m = m0 + wm + 8 * i + g, n = n0 + wn + 8 * j + 2 * t + c;
+        if (m < M && n < N) out[(size_t)m * ld + n] = acc[i][j][c];
+      }
 }
 
 __global__ void splitk_reduce_kernel(const double* __restrict__ partial, int slices, int M, int N,
@@ -95,7 +125,7 @@ static int dgemm(scb_ctx* ctx, int M, int N, int K, const double* A, int lda, in
     partial = (double*)ws;
   }
   dim3 g((N + kGT - 1) / kGT, (M + kGT - 1) / kGT, slices);
-  dgemm_kernel<<<g, 256, 0, s>>>(M, N, K, A, lda, opA, B, ldb, opB, Cm, ldc, kps, partial, done);
+  dgemm_kernel<<<g, 128, 0, s>>>(M, N, K, A, lda, opA, B, ldb, opB, Cm, ldc, kps, partial, done);
   SCB_LAUNCH_CHECK();
   if (slices > 1) {
     splitk_reduce_kernel<<<(unsigned)(((int64_t)M * N + 255) / 256), 256, 0, s>>>(partial, slices, M, N, Cm, ldc, done);
@@ -491,6 +521,14 @@ __global__ void cheb_combine_kernel(const double* __restrict__ CY, const double*
   if (i < n) out[i] = alpha * CY[i] + beta * Y[i] + (Yold ? gamma * Yold[i] : 0.0);
 }
 
+__global__ void eig_state_init_kernel(EigState* st) {
+  st->cheb_b = 0.0;
+  st->prev_worst = 1.0;  // first Rayleigh-Ritz step: far from convergence (2 Jacobi sweeps)
+  st->worst = 1.0;
+  st->done = 0;
+  st->iters = 0;
+}
+
 __global__ void copy_gated_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t n,
                                   const int* __restrict__ done) {
   if (*done) return;
@@ -569,7 +607,8 @@ static int pca_eig_impl(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, in
   init_block_kernel<<<h, kB, 0, s>>>(Qf, h);
   SCB_LAUNCH_CHECK();
   SCB_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
-  SCB_CUDA(cudaMemsetAsync(st, 0, sizeof(EigState), s));
+  eig_state_init_kernel<<<1, 1, 0, s>>>(st);
+  SCB_LAUNCH_CHECK();
   auto orth = [&](double* M, int reps) -> int {
     if (use_qr) {  // rank-deficient fallback
       cgs2_kernel<<<1, kOrthThreads, 0, s>>>(M, h, done);
@@ -641,9 +680,12 @@ static int pca_eig_impl(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, in
     SCB_CUDA(cudaMemcpyAsync(&hs, st, sizeof(EigState), cudaMemcpyDeviceToHost, s));
     SCB_CUDA(cudaMemcpyAsync(&hfail_now, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
     SCB_CUDA(cudaStreamSynchronize(s));
-    if (verbose)
-      fprintf(stderr, "[scb_pca_eig] after %d enqueued outer steps: executed %d, residual %.3e, done %d\n", outer,
-              hs.iters, hs.worst, hs.done);
+    if (verbose) {
+      int sweeps = 0;
+      cudaMemcpyFromSymbol(&sweeps, g_jacobi_sweeps, sizeof(int));
+      fprintf(stderr, "[scb_pca_eig] after %d enqueued outer steps: executed %d, residual %.3e, done %d, last jacobi "
+              "sweeps %d\n", outer, hs.iters, hs.worst, hs.done, sweeps);
+    }
     if (hfail_now) {  // Cholesky-QR broke down (block rank-deficient): caller retries with CGS2
       *broke = true;
       return SCB_OK;
