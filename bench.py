@@ -270,9 +270,14 @@ def main():
         backend = os.environ.get("SCB_DIST_BACKEND", "nccl")
         if backend == "nccl":
             td.init_process_group("nccl", device_id=torch.device("cuda", local))
+            comm = Comm()
+        elif backend == "scb":  # the C ABI's own NCCL communicator (scb_ctx_create_comm); gloo for the id + barriers
+            from paper_2605_13928_b200.dist import NcclComm
+            td.init_process_group("gloo")
+            comm = NcclComm.from_torch_distributed(local)
         else:
             td.init_process_group(backend)
-        comm = Comm()
+            comm = Comm()
     p = _params(args)
     N, G = args.cells, args.genes
     spec = synth.Spec(N, G, seed=args.seed)

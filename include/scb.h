@@ -65,6 +65,22 @@ SCB_API int scb_ctx_destroy(scb_ctx* ctx);
  * the flag is returned in n_kept[3] of the next scb_filter_masks instead. */
 SCB_API int scb_ctx_set_deferred_checks(scb_ctx* ctx, int32_t on);
 
+/* ---- multi-GPU: a ctx that owns an NCCL communicator over `world`
+ * ranks (one process per GPU).  Rank 0 makes the 128-byte id with scb_nccl_unique_id and
+ * shares it (e.g. through the torch.distributed store); every rank then calls
+ * scb_ctx_create_comm(its device, id, rank, world).  libnccl.so.2 is loaded on first use
+ * (SCB_ERR_UNSUPPORTED without it).  The collectives are stream-ordered and in place:
+ *   scb_comm_allreduce: dtype 0 int64, 1 float64, 2 float32, 3 int32; op 0 sum, 1 max;
+ *   scb_comm_broadcast: `bytes` from `root`;
+ *   scb_comm_allgather: recv[r * bytes_per_rank ...] = rank r's send buffer.
+ * On a ctx without a communicator they are the world-size-1 identities. */
+SCB_API int scb_nccl_unique_id(uint8_t* id_out);
+SCB_API int scb_ctx_create_comm(int device, const uint8_t* nccl_id, int32_t rank, int32_t world, scb_ctx** out);
+SCB_API int scb_comm_info(scb_ctx* ctx, int32_t* rank, int32_t* world);
+SCB_API int scb_comm_allreduce(scb_ctx* ctx, void* buf, int64_t count, int32_t dtype, int32_t op, void* stream);
+SCB_API int scb_comm_broadcast(scb_ctx* ctx, void* buf, int64_t bytes, int32_t root, void* stream);
+SCB_API int scb_comm_allgather(scb_ctx* ctx, const void* send, void* recv, int64_t bytes_per_rank, void* stream);
+
 /* ---- f1 ingest (sc.read_10x_mtx / sc.read_mtx): MatrixMarket coordinate data lines -> COO
  * on the device.  text holds the whole file (16-byte aligned, readable up to
  * roundup(n_bytes, 16)); data_offset = first data line (the host parses the banner, comments

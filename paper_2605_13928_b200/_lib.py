@@ -22,6 +22,12 @@ SIGNATURES = {
     "scb_launch_count": [],
     "scb_ctx_create": [ctypes.c_int, ctypes.POINTER(c_ptr)],
     "scb_ctx_destroy": [c_ptr],
+    "scb_nccl_unique_id": [c_ptr],
+    "scb_ctx_create_comm": [ctypes.c_int, c_ptr, c_i32, c_i32, ctypes.POINTER(c_ptr)],
+    "scb_comm_info": [c_ptr, c_ptr, c_ptr],
+    "scb_comm_allreduce": [c_ptr, c_ptr, c_i64, c_i32, c_i32, c_ptr],
+    "scb_comm_broadcast": [c_ptr, c_ptr, c_i64, c_i32, c_ptr],
+    "scb_comm_allgather": [c_ptr, c_ptr, c_ptr, c_i64, c_ptr],
     "scb_qc_metrics": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
                        c_ptr],
     "scb_hvg_tiles": [c_i32],
@@ -149,15 +155,29 @@ def context(device: int):
     return c
 
 
+def install_context(device: int, ptr: int):
+    """Make ``ptr`` (e.g. a ctx that owns an NCCL communicator) the device's ctx for every step
+    call; a previously created ctx of that device is destroyed at exit."""
+    with _lock:
+        old = _ctx.get(device)
+        _ctx[device] = ptr
+        if old is not None and old != ptr:
+            _retired.append(old)
+
+
+_retired = []
+
+
 def _destroy_all():
     if _lib is None:
         return
-    for c in list(_ctx.values()):
+    for c in list(_ctx.values()) + _retired:
         try:
             _lib.scb_ctx_destroy(c)
         except Exception:  # pragma: no cover - interpreter shutdown
             pass
     _ctx.clear()
+    _retired.clear()
 
 
 import atexit  # noqa: E402

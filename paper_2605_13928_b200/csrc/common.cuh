@@ -73,7 +73,9 @@ struct scb_ctx {
   size_t smem_optin = 0;
   scb::Workspace ws[4];  // independent scratch slots (grown on demand, stream-ordered use)
   int* d_flag = nullptr; // device error flag (non-integral counts etc.)
-  int defer_checks = 0;  // 1: data checks that need a host round trip are reported later (see scb.h)
+  int defer_checks = 0;
+  void* comm = nullptr;   // ncclComm_t (scb_ctx_create_comm), else nullptr (world 1)
+  int rank = 0, world = 1;  // 1: data checks that need a host round trip are reported later (see scb.h)
 };
 
 namespace scb {
