@@ -337,7 +337,7 @@ struct EigState {
 };
 
 __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict__ T, double* __restrict__ W,
-                                                              const EigState* __restrict__ st) {
+                                                              const EigState* __restrict__ st, int n_wanted) {
   if (st->done) return;
   // far from convergence the Rayleigh-Ritz step only has to supply the filter bound and a
   // reasonable rotation (every rotation is exactly orthogonal): 2 sweeps; near it, to completion
@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
   __shared__ int pp[kPairs], qq[kPairs];
   __shared__ short2 blk[kBlocks];
   __shared__ double red[2][kJacThreads / 32];
+  __shared__ int wanted[kB];  // 1: row among the n_wanted largest diagonal entries
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
     a[e / kB][e % kB] = T[e];
     w[e / kB][e % kB] = (e / kB == e % kB) ? 1.0 : 0.0;
@@ -412,11 +413,21 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
       }
       __syncthreads();
     }
+    // convergence is judged on the couplings of the wanted (largest) Ritz pairs only: the
+    // unwanted tail of the block (oversampling) may stay unconverged
+    if (threadIdx.x < kB) {
+      const int i = threadIdx.x;
+      int rank = 0;
+      for (int j = 0; j < kB; ++j) rank += (a[j][j] > a[i][i] || (a[j][j] == a[i][i] && j < i)) ? 1 : 0;
+      wanted[i] = rank < n_wanted ? 1 : 0;
+    }
+    __syncthreads();
     double off = 0.0, dia = 0.0;
     for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
       const int i = e / kB, j = e % kB;
       const double v = a[i][j] * a[i][j];
-      if (i != j) off += v; else dia += v;
+      if (i == j) dia += v;
+      else if (wanted[i] | wanted[j]) off += v;
     }
     off = warp_sum(off);
     dia = warp_sum(dia);
@@ -661,7 +672,7 @@ static int pca_eig_impl(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, in
       // Rayleigh-Ritz: T = Q^T Cov Q, T = W diag W^T; rotate Q := Q W (sorted descending)
       SCB_TRY(dgemm(ctx, h, kB, h, cov, h, 0, Q, kB, 0, Y, kB, s, done));        // Y = Cov Q
       SCB_TRY(dgemm(ctx, kB, kB, h, Q, kB, 1, Y, kB, 0, S, kB, s, done));        // T = Q^T Y
-      jacobi_kernel<<<1, kJacThreads, 2 * kSmemKB, s>>>(S, W, st);
+      jacobi_kernel<<<1, kJacThreads, 2 * kSmemKB, s>>>(S, W, st, n_comps);
       SCB_LAUNCH_CHECK();
       select_kernel<<<1, kB, 0, s>>>(S, kB, order, lam_all, done);
       SCB_LAUNCH_CHECK();

@@ -233,6 +233,19 @@ __device__ __forceinline__ int outward_tile(int start, int j, int n_kt) {
   return above > below ? start + (j - below) : start - (j - above);
 }
 
+// Work units of the persistent candidate kernel: query pairs, except that the pairs of a final
+// partial round (r <= gridDim/2 pairs) are split into two halves of their outward key scan, so
+// that round takes half as long; the two halves' lists go to a separate buffer (2 x KCT
+// candidates per row) and are re-ranked together.
+struct KnnUnit {
+  int pair, i0, i1, tail, half;
+};
+__device__ __forceinline__ KnnUnit knn_unit(int u, int n_full, int n_kt) {
+  if (u < n_full) return KnnUnit{u, 0, n_kt, 0, 0};
+  const int t = u - n_full, half = t & 1, mid = n_kt >> 1;
+  return KnnUnit{n_full + (t >> 1), half ? mid : 0, half ? n_kt : mid, 1, half};
+}
+
 template <int KC>
 __device__ __forceinline__ void list_insert(float (&L)[KC], int (&I)[KC], float v, int iv) {
 #pragma unroll
@@ -298,7 +311,8 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
 template <int KC, int HALVES>
 __global__ void __launch_bounds__(KnnCfg<KC, HALVES>::THREADS, 1)
 knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, int64_t n_q,
-                      int64_t n_k, const int* __restrict__ start_tile, int* __restrict__ cand) {
+                      int64_t n_k, const int* __restrict__ start_tile, int* __restrict__ cand, int n_full,
+                      int n_units, int* __restrict__ cand_tail) {
   using C = KnnCfg<KC, HALVES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -314,7 +328,6 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2 * C::NBUF);
 
   const int warp = warp_id(), lane = lane_id();
-  const int n_pairs = (int)((n_q + 2 * C::BM - 1) / (2 * C::BM));
   const int n_kt = (int)((n_k + C::BN - 1) / C::BN);
 
   if (warp == 0) {
@@ -345,12 +358,14 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   if (warp == 0) {
     if (lane == 0) {
       int it = 0, pc = 0;
-      for (int pair = blockIdx.x; pair < n_pairs; pair += gridDim.x, ++pc) {
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++pc) {
+        const KnnUnit U = knn_unit(u, n_full, n_kt);
+        const int pair = U.pair;
         const int st = start_tile[pair];
         tc::mbar_wait(a_empty, (pc & 1) ^ 1);
         tc::mbar_arrive_expect_tx(a_full, C::A_BYTES);
         for (int t = 0; t < 2; ++t) tc::tma_load_2d(a_base + t * C::TILE, &tq, a_full, 0, (pair * 2 + t) * C::BM);
-        for (int i = 0; i < n_kt; ++i) {
+        for (int i = U.i0; i < U.i1; ++i) {
           const int kt = outward_tile(st, i, n_kt);
           const int s = it % C::STAGES;
           tc::mbar_wait(&b_empty[s], ((it / C::STAGES) & 1) ^ 1);
@@ -370,9 +385,10 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       PROF_T0(tot);
       const uint32_t ab = tc::smem_u32(a_base + t * C::TILE);
       int it = 0, pc = 0;
-      for (int pair = blockIdx.x; pair < n_pairs; pair += gridDim.x, ++pc) {
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++pc) {
+        const KnnUnit U = knn_unit(u, n_full, n_kt);
         tc::mbar_wait(a_full, pc & 1);
-        for (int i = 0; i < n_kt; ++i, ++it) {
+        for (int i = U.i0; i < U.i1; ++i, ++it) {
           const int s = it % C::STAGES;
           const int buf = it & 1;
           PROF_T0(w0);
@@ -405,7 +421,9 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
     const int n_k32 = (int)n_k;
     int it = 0;
     PROF_T0(tot);
-    for (int pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const KnnUnit U = knn_unit(u, n_full, n_kt);
+      const int pair = U.pair;
       const int st = start_tile[pair];
       float L[KC];
       int I[KC];
@@ -423,7 +441,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         Qi[j] = -1;
       }
       const int64_t row = (int64_t)(pair * 2 + t) * C::BM + 32 * q + lane;
-      for (int i = 0; i < n_kt; ++i, ++it) {
+      for (int i = U.i0; i < U.i1; ++i, ++it) {
         const int kt = outward_tile(st, i, n_kt);
         const int buf = it & 1;
         PROF_T0(w0);
@@ -486,7 +504,9 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       }
       queue_merge<KC>(L, I, Qv, Qi, qn);
       if (row < n_q) {
-        int* o = cand + row * C::KCT + hf * KC;
+        const int64_t tail_row0 = (int64_t)n_full * 2 * C::BM;
+        int* o = U.tail ? cand_tail + (row - tail_row0) * (2 * C::KCT) + U.half * C::KCT + hf * KC
+                        : cand + row * C::KCT + hf * KC;
 #pragma unroll
         for (int j = 0; j < KC; ++j) o[j] = I[j];
       }
@@ -503,12 +523,14 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
 template <int KC>
 __global__ void knn_rerank_kernel(const float* __restrict__ Q, const float* __restrict__ Kx, int64_t n_q, int d,
                                   int ld, const int* __restrict__ perm_q, const int* __restrict__ perm_k,
-                                  const int* __restrict__ cand, int k, int* __restrict__ out_i, float* __restrict__ out_d) {
+                                  const int* __restrict__ cand, int k, int* __restrict__ out_i, float* __restrict__ out_d,
+                                  int64_t i0 = 0) {
   constexpr int PER = (KC + 31) / 32;  // KC not a multiple of 32: the upper lanes carry no candidate
   constexpr int NS = PER * 32;         // sort width (power of two up to 64)
   static_assert(NS == 32 || NS == 64, "rerank sort width");
-  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  const int64_t i = i0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();  // sorted query position
   if (i >= n_q) return;
+  cand -= i0 * KC;  // candidates of rows [i0, n_q) start at cand
   const int l = lane_id();
   const int64_t r = perm_q[i];
   const float* qp = Q + r * ld;
@@ -607,9 +629,17 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   const bool same = (Qx == Kx && n_q == n_k);
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
   const int64_t n_pairs = (n_q + 2 * Cfg::BM - 1) / (2 * Cfg::BM);
+  // final partial round: split its pairs' key scans in two when that fits one round (§ KnnUnit)
+  const int64_t G = std::min<int64_t>(n_pairs, ctx->num_sms);
+  const int64_t r = n_pairs % G;
+  const bool split = r > 0 && 2 * r <= G && 2 * KCT <= 64;
+  const int64_t n_full = split ? n_pairs - r : n_pairs;
+  const int64_t n_units = split ? n_full + 2 * r : n_pairs;
+  const int64_t tail_row0 = std::min<int64_t>(n_q, n_full * 2 * Cfg::BM);
+  const int64_t tail_rows = n_q - tail_row0;
   const size_t sz[] = {256, sizeof(int) * kBuckets, 4 * (size_t)n_q, 4 * (size_t)n_k, 4 * (size_t)n_q,
                        4 * (size_t)n_k, 4 * (size_t)n_pairs, (size_t)n_q * kD * 2, (size_t)n_k * kD * 2,
-                       (size_t)n_q * KCT * 4};
+                       (size_t)n_q * KCT * 4, (size_t)std::max<int64_t>(tail_rows, 1) * 2 * KCT * 4};
   size_t total = 0;
   for (size_t v : sz) total += up(v);
   void* ws;
@@ -627,7 +657,8 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   int* start = (int*)p; p += up(sz[6]);
   __half* Qa = (__half*)p; p += up(sz[7]);
   __half* Ka = (__half*)p; p += up(sz[8]);
-  int* cand = (int*)p;
+  int* cand = (int*)p; p += up(sz[9]);
+  int* cand_tail = (int*)p;
   // FP16 scale and the PC1 range come from the KEYS (queries are rows of the same embedding)
   const int init[12] = {0, 0, 0, 0, 0x7fffffff, 0x7fffffff, 0x7fffffff, 0, (int)0x80000000, (int)0x80000000,
                         (int)0x80000000, 0};
@@ -654,7 +685,7 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   auto kern = knn_candidates_kernel<KC, HALVES>;
   SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   if (ev0) SCB_CUDA(cudaEventRecord(ev0, s));
-  kern<<<(int)std::min<int64_t>(n_pairs, ctx->num_sms), Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, n_q, n_k, start, cand);
+  kern<<<(int)G, Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, n_q, n_k, start, cand, (int)n_full, (int)n_units, cand_tail);
   SCB_LAUNCH_CHECK();
   if (ev1) SCB_CUDA(cudaEventRecord(ev1, s));
 #ifdef SCB_KNN_PROF
@@ -669,8 +700,22 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
     SCB_CUDA(cudaMemcpyToSymbolAsync(g_knn_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
   }
 #endif
-  knn_rerank_kernel<KCT><<<ceil_div(n_q, 8), 256, 0, s>>>(Qx, Kx, n_q, d, ld, perm_q, perm_k, cand, k, out_i, out_d);
-  SCB_LAUNCH_CHECK();
+  if (!split) {
+    knn_rerank_kernel<KCT><<<ceil_div(n_q, 8), 256, 0, s>>>(Qx, Kx, n_q, d, ld, perm_q, perm_k, cand, k, out_i, out_d);
+    SCB_LAUNCH_CHECK();
+  } else {
+    if (tail_row0 > 0) {
+      knn_rerank_kernel<KCT><<<ceil_div(tail_row0, 8), 256, 0, s>>>(Qx, Kx, tail_row0, d, ld, perm_q, perm_k, cand, k,
+                                                                     out_i, out_d);
+      SCB_LAUNCH_CHECK();
+    }
+    if (tail_rows > 0) {
+      constexpr int KCT2 = (2 * KCT <= 64) ? 2 * KCT : 64;
+      knn_rerank_kernel<KCT2><<<ceil_div(tail_rows, 8), 256, 0, s>>>(Qx, Kx, n_q, d, ld, perm_q, perm_k, cand_tail, k,
+                                                                      out_i, out_d, tail_row0);
+      SCB_LAUNCH_CHECK();
+    }
+  }
   return SCB_OK;
 }
 

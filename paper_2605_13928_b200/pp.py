@@ -609,7 +609,10 @@ def pca(sc: Scaled, n_comps: int = 50) -> PCAResult:
 # ----------------------------------------------------------------------------- knn
 def neighbors(X_pca: torch.Tensor, n_neighbors: int = 15, n_comps: Optional[int] = None,
               keys: Optional[torch.Tensor] = None, timer=None):
-    """sc.pp.neighbors(n_neighbors, method='exact' brute force, metric='euclidean'):
+    """sc.pp.neighbors(n_neighbors, metric='euclidean') by brute force over every key: FP16
+    tensor-core candidate scores (32 candidates per query for k <= 16) and an exact FP32 re-rank.
+    Recall-checked (>= 0.999 against exact float64 neighbours in the tests), not certified exact:
+    a true neighbour whose FP16 score misses the candidate lists is not reported.  Output:
     (indices int32 [Nq][k], distances float32 [Nq][k]) ordered by (distance, index), self
     included.  ``keys`` (default: X_pca itself) is the full embedding when the queries are a
     shard (multi-GPU); returned indices index ``keys``.  ``timer`` = (start, end) CUDA events
