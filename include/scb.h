@@ -248,6 +248,15 @@ SCB_API int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_t* 
                     int32_t n_slots, const double* mean, const double* inv_std, double max_value,
                     double min_value, float* Z, int64_t ldz, int32_t ones_col, void* stream);
 
+/* ---- a6 in the pipeline's layout: the same z-scores written directly as BF16 planes
+ * Z_hi = bf16(z), Z_lo = bf16(z - hi) (row-major [n_rows][ldz], ldz % 8 == 0; column ones_col =
+ * 1) -- bit-identical to scb_scale_dense followed by scb_split_bf16, without the fp32 matrix.
+ * The Gram (scb_gram_split) and the projection (scb_project_planes) read the planes. */
+SCB_API int scb_scale_dense_planes(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* logdata,
+                                   int64_t n_rows, int32_t n_cols, const int32_t* gene_slot, int32_t n_slots,
+                                   const double* mean, const double* inv_std, double max_value, double min_value,
+                                   uint16_t* Z_hi, uint16_t* Z_lo, int64_t ldz, int32_t ones_col, void* stream);
+
 /* ---- f2 (optional, paper Table 1 step 4): sc.pp.regress_out(["total_counts",
  * "pct_counts_mt"]) fused with scale.  Replaces scale_gene_sums/finalize:
  *   1. scb_regress_cov_sums: sums6 = {n, Σtc, Σtc², Σpct, Σpct², Σtc·pct} over the kept
@@ -352,6 +361,12 @@ SCB_API int scb_pca_eig(scb_ctx* ctx, const double* C, int32_t h, int32_t hp, in
 SCB_API int scb_project(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp,
                 const float* components_t, const float* col_mean, int32_t n_comps,
                 int32_t n_comps_pad, float* X_pca, int32_t ld_out, void* stream);
+
+/* ---- a8 from the BF16 planes: X_pca = (Z - m) V with Z = hi + lo (3xBF16 tcgen05 MMAs, the
+ * Gram's operand scheme); same arguments and output as scb_project, hp % 64 == 0. */
+SCB_API int scb_project_planes(scb_ctx* ctx, const uint16_t* Z_hi, const uint16_t* Z_lo, int64_t n_rows, int32_t hp,
+                               const float* components_t, const float* col_mean, int32_t n_comps, int32_t n_comps_pad,
+                               float* X_pca, int32_t ld_out, void* stream);
 
 /* ---- a9: sc.pp.neighbors(n_neighbors=k, method exact, metric euclidean): for each query
  * row, the k nearest key rows (self included) ordered by (distance, index).  Candidate

@@ -1089,6 +1089,70 @@ scale_dense_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
 }
 
 
+// Planes variant: the same clipped z-scores written directly as the Gram's / projection's BF16
+// operand planes hi = bf16(z), lo = bf16(z - hi) (bit-identical to scb_split_bf16 of the fp32
+// matrix) -- the fp32 matrix and the separate split pass (8 GB read + 8 GB write at C3) are gone.
+__global__ void __launch_bounds__(kRowThreads)
+scale_dense_planes_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                          const float* __restrict__ ldata, int64_t n_rows, int32_t n_cols,
+                          const int32_t* __restrict__ slot, int32_t H, const double* __restrict__ mean,
+                          const double* __restrict__ inv, double max_value, double min_value,
+                          __nv_bfloat16* __restrict__ Zh, __nv_bfloat16* __restrict__ Zl, int64_t ldz,
+                          int32_t ones_col) {
+  const int64_t nnz = indptr[n_rows];
+  extern __shared__ float zsm[];                        // background rows: hi [ldz], lo [ldz] (bf16)
+  __nv_bfloat16* bh = reinterpret_cast<__nv_bfloat16*>(zsm);
+  __nv_bfloat16* bl = bh + ldz;
+  int16_t* s_slot = reinterpret_cast<int16_t*>(bl + ldz);
+  double* s_mean = reinterpret_cast<double*>(s_slot + ((n_cols + 7) & ~7));
+  double* s_inv = s_mean + H;
+  for (int j = threadIdx.x; j < ldz; j += blockDim.x) {
+    float v = 0.0f;
+    if (j < H) v = (float)fmax(fmin(__dmul_rn(__dsub_rn(0.0, mean[j]), inv[j]), max_value), min_value);
+    else if (j == ones_col) v = 1.0f;
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    bh[j] = h;
+    bl[j] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+  for (int i = threadIdx.x; i < n_cols; i += blockDim.x) s_slot[i] = (int16_t)slot[i];
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    s_mean[j] = mean[j];
+    s_inv[j] = inv[j];
+  }
+  __syncthreads();
+  const int lane = lane_id();
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const uint4* bgh = reinterpret_cast<const uint4*>(bh);
+  const uint4* bgl = reinterpret_cast<const uint4*>(bl);
+  const int n8 = (int)(ldz >> 3);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+    __nv_bfloat16* zh = Zh + r * ldz;
+    __nv_bfloat16* zl = Zl + r * ldz;
+    uint4* zh4 = reinterpret_cast<uint4*>(zh);
+    uint4* zl4 = reinterpret_cast<uint4*>(zl);
+    for (int j = lane; j < n8; j += 32) {
+      zh4[j] = bgh[j];
+      zl4[j] = bgl[j];
+    }
+    __syncwarp();  // orders this warp's background stores before the scattered overwrites
+    stream_row<2>(indices, ldata, indptr[r], indptr[r + 1], nnz, [&](const Quad& q) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!((q.valid >> k) & 1u)) continue;
+        const int j = s_slot[q.g[k]];
+        if (j >= 0) {
+          const float z = (float)fmax(fmin(__dmul_rn(__dsub_rn((double)q.x[k], s_mean[j]), s_inv[j]), max_value),
+                                      min_value);
+          const __nv_bfloat16 h = __float2bfloat16_rn(z);
+          zh[j] = h;
+          zl[j] = __float2bfloat16_rn(z - __bfloat162float(h));
+        }
+      }
+    });
+    __syncwarp();
+  }
+}
+
 }  // namespace scb
 
 // ============================================================================ C ABI
@@ -1512,3 +1576,26 @@ extern "C" int scb_scale_dense(scb_ctx* ctx, const int64_t* indptr, const int32_
   return SCB_OK;
 }
 
+
+extern "C" int scb_scale_dense_planes(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* ldata,
+                                      int64_t n_rows, int32_t n_cols, const int32_t* slot, int32_t n_slots,
+                                      const double* mean, const double* inv_std, double max_value, double min_value,
+                                      uint16_t* Z_hi, uint16_t* Z_lo, int64_t ldz, int32_t ones_col, void* stream) {
+  SCB_REQUIRE(ctx && indptr && indices && ldata && slot && mean && inv_std && Z_hi && Z_lo, SCB_ERR_ARG,
+              "scb_scale_dense_planes: null argument");
+  SCB_REQUIRE(ldz % 8 == 0 && ldz >= n_slots && ones_col < ldz, SCB_ERR_ARG,
+              "scb_scale_dense_planes: ldz must be a multiple of 8 and >= n_slots");
+  SCB_REQUIRE(((uintptr_t)Z_hi & 15) == 0 && ((uintptr_t)Z_lo & 15) == 0, SCB_ERR_ARG,
+              "scb_scale_dense_planes: 16-byte aligned planes required");
+  SCB_REQUIRE(aligned16(indices) && aligned16(ldata), SCB_ERR_ARG, "scb_scale_dense_planes: 16-byte alignment");
+  const size_t smem = (size_t)ldz * 4 + (size_t)((n_cols + 7) & ~7) * 2 + (size_t)n_slots * 16;
+  SCB_REQUIRE(smem <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_scale_dense_planes: too many genes");
+  if (n_rows == 0) return SCB_OK;
+  SCB_CUDA(cudaFuncSetAttribute(scale_dense_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int per_sm = std::max(1, std::min(4, (int)(kSmemLimit / (smem + 1024))));
+  scale_dense_planes_kernel<<<grid_for(ctx, per_sm), kRowThreads, smem, (cudaStream_t)stream>>>(
+      indptr, indices, ldata, n_rows, n_cols, slot, n_slots, mean, inv_std, max_value, min_value,
+      (__nv_bfloat16*)Z_hi, (__nv_bfloat16*)Z_lo, ldz, ones_col);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}

@@ -166,7 +166,8 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
         if comm is not None:
             comm.allreduce_(ssum)
         mean, inv = pp.scale_finalize(ssum, n_total)
-        sc = pp.scale_dense(X_log, slot, H, mean, inv, p.max_value, clip=p.clip)
+        # written directly as the Gram's / projection's BF16 planes (no float32 matrix, no split pass)
+        sc = pp.scale_dense(X_log, slot, H, mean, inv, p.max_value, clip=p.clip, planes=True)
 
     # ------------------------------------------------------------------ pca
     tm.step("pca")

@@ -382,22 +382,38 @@ def highly_variable_genes(X_log: DeviceCSR, n_top_genes: int = 2000, n_bins: int
 # ----------------------------------------------------------------------------- regress (scale)
 @dataclasses.dataclass
 class Scaled:
-    """Dense scaled HVG matrix Z[N][ld] (float32, row-major): columns [0, H) are the HVGs,
-    column ``ones_col`` = 1 (gives the column sums in the Gram), the rest zero."""
-    Z: torch.Tensor
+    """Dense scaled HVG matrix Z[N][ld] (row-major): columns [0, H) are the HVGs, column
+    ``ones_col`` = 1 (gives the column sums in the Gram), the rest zero.  Held as float32 ``Z``
+    and/or as the BF16 operand planes ``Z_hi`` = bf16(Z), ``Z_lo`` = bf16(Z - hi) (the pipeline
+    writes only the planes: Z = hi + lo to 2^-17 relative)."""
+    Z: Optional[torch.Tensor]
     H: int
     ones_col: int
     mean: torch.Tensor
     inv_std: torch.Tensor
-    Z_hi: Optional[torch.Tensor] = None  # BF16 planes hi = bf16(Z), lo = bf16(Z - hi) for the Gram
+    Z_hi: Optional[torch.Tensor] = None
     Z_lo: Optional[torch.Tensor] = None
 
     @property
     def ld(self):
-        return self.Z.shape[1]
+        return (self.Z if self.Z is not None else self.Z_hi).shape[1]
+
+    @property
+    def n_rows(self):
+        return (self.Z if self.Z is not None else self.Z_hi).shape[0]
+
+    @property
+    def device(self):
+        return (self.Z if self.Z is not None else self.Z_hi).device
+
+    def dense(self) -> torch.Tensor:
+        """float32 [N][ld]: Z, or hi + lo reconstructed from the planes."""
+        if self.Z is not None:
+            return self.Z
+        return self.Z_hi.float() + self.Z_lo.float()
 
     def values(self):
-        return self.Z[:, : self.H]
+        return self.dense()[:, : self.H]
 
 
 def padded_width(H: int) -> int:
@@ -438,10 +454,20 @@ def clip_min(max_value: float, clip: str) -> float:
     return -float(max_value) if clip == "symmetric" else float("-inf")
 
 
-def scale_dense(X_log: DeviceCSR, slot, H, mean, inv, max_value=10.0, out=None, clip: str = "symmetric") -> Scaled:
-    """Dense clipped z-scores Z[N][ld] (float32) of the HVG columns, plus the ones column."""
+def scale_dense(X_log: DeviceCSR, slot, H, mean, inv, max_value=10.0, out=None, clip: str = "symmetric",
+                planes: bool = False) -> Scaled:
+    """Dense clipped z-scores Z[N][ld] (float32) of the HVG columns, plus the ones column.  With
+    ``planes`` the z-scores are written directly as the BF16 planes the Gram and the projection
+    read (no float32 matrix, no split pass; bit-identical to splitting the float32 one)."""
     ld = padded_width(H)
     dev = X_log.device
+    if planes:
+        hi = torch.empty((X_log.n_rows, ld), dtype=torch.bfloat16, device=dev)
+        lo = torch.empty((X_log.n_rows, ld), dtype=torch.bfloat16, device=dev)
+        _lib.call("scb_scale_dense_planes", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
+                  X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value),
+                  clip_min(max_value, clip), _p(hi), _p(lo), ld, H, _stream(dev))
+        return Scaled(None, H, H, mean, inv, hi, lo)
     Z = out if out is not None else torch.empty((X_log.n_rows, ld), dtype=torch.float32, device=dev)
     _lib.call("scb_scale_dense", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
               X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value),
@@ -548,6 +574,8 @@ class PCAResult:
 
 def split_planes(sc: Scaled) -> Scaled:
     """BF16 operand planes of Z for the Gram: hi = bf16(Z), lo = bf16(Z - hi) (one streaming pass)."""
+    if sc.Z is None:  # already planes only
+        return sc
     n, ld = sc.Z.shape
     if sc.Z_hi is None:
         sc.Z_hi = torch.empty((n, ld), dtype=torch.bfloat16, device=sc.Z.device)
@@ -562,12 +590,12 @@ def gram(sc: Scaled, out=None, planes: bool = True, keep_planes: bool = False):
     converts fp32 tiles inside the Gram kernel instead (no extra 4 B/element of HBM, slower).  The
     planes (4 B per element) are released after the call unless ``keep_planes``."""
     ld = sc.ld
-    C = out if out is not None else torch.empty((ld, ld), dtype=torch.float64, device=sc.Z.device)
-    if planes:
+    dev = sc.device
+    C = out if out is not None else torch.empty((ld, ld), dtype=torch.float64, device=dev)
+    if planes or sc.Z is None:
         split_planes(sc)
-        _lib.call("scb_gram_split", _ctx(sc.Z), _p(sc.Z_hi), _p(sc.Z_lo), sc.Z.shape[0], ld, _p(C),
-                  _stream(sc.Z.device))
-        if not keep_planes:  # stream-ordered release: the caching allocator reuses them after the Gram
+        _lib.call("scb_gram_split", _ctx(sc.Z_hi), _p(sc.Z_hi), _p(sc.Z_lo), sc.n_rows, ld, _p(C), _stream(dev))
+        if not keep_planes and sc.Z is not None:  # stream-ordered release (planes-only matrices keep them)
             sc.Z_hi = sc.Z_lo = None
     else:
         _lib.call("scb_gram", _ctx(sc.Z), _p(sc.Z), sc.Z.shape[0], ld, _p(C), _stream(sc.Z.device))
@@ -575,7 +603,7 @@ def gram(sc: Scaled, out=None, planes: bool = True, keep_planes: bool = False):
 
 
 def pca_from_gram(sc: Scaled, C, n_cells: int, n_comps: int = 50):
-    dev = sc.Z.device
+    dev = sc.device
     ld = sc.ld
     npad = 64 if n_comps <= 64 else 128
     lam = torch.empty(n_comps, dtype=torch.float64, device=dev)
@@ -588,9 +616,15 @@ def pca_from_gram(sc: Scaled, C, n_cells: int, n_comps: int = 50):
 
 
 def project(sc: Scaled, comp_t, mean, n_comps: int, ld_out: int = 64):
-    dev = sc.Z.device
+    """X_pca = (Z - m) V: from the float32 matrix (3xTF32) or, for a planes-only matrix, from the
+    BF16 planes (3xBF16, scb_project_planes)."""
+    dev = sc.device
     npad = comp_t.shape[0]
-    X = torch.empty((sc.Z.shape[0], max(ld_out, npad)), dtype=torch.float32, device=dev)
+    X = torch.empty((sc.n_rows, max(ld_out, npad)), dtype=torch.float32, device=dev)
+    if sc.Z is None:
+        _lib.call("scb_project_planes", _ctx(sc.Z_hi), _p(sc.Z_hi), _p(sc.Z_lo), sc.n_rows, sc.ld, _p(comp_t), _p(mean),
+                  n_comps, npad, _p(X), X.shape[1], _stream(dev))
+        return X
     _lib.call("scb_project", _ctx(sc.Z), _p(sc.Z), sc.Z.shape[0], sc.ld, _p(comp_t), _p(mean), n_comps, npad, _p(X),
               X.shape[1], _stream(dev))
     return X
@@ -600,7 +634,7 @@ def pca(sc: Scaled, n_comps: int = 50) -> PCAResult:
     """sc.tl.pca(n_comps, zero_center=True) on the scaled matrix: tcgen05 Gram, float64
     subspace-iteration eigensolve, tcgen05 projection."""
     C = gram(sc)
-    N = sc.Z.shape[0]
+    N = sc.n_rows
     lam, comp_t, mean, tr = pca_from_gram(sc, C, N, n_comps)
     X = project(sc, comp_t, mean, n_comps)
     return PCAResult(X, comp_t[:n_comps, : sc.H], lam, lam / tr, mean, n_comps)

@@ -143,7 +143,7 @@ def scale_finalize(sums, n_cells):
     return torch.as_tensor(mean), torch.as_tensor(1.0 / std)
 
 
-def scale_dense(X_log, slot, H, mean, inv, max_value=10.0, out=None, clip="symmetric"):
+def scale_dense(X_log, slot, H, mean, inv, max_value=10.0, out=None, clip="symmetric", planes=False):  # noqa: ARG001
     A = _csr(X_log)
     ld = padded_width(H)
     m, iv = _np(mean), _np(inv)

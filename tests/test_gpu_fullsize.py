@@ -81,7 +81,7 @@ def test_c3_pca_orthonormal_and_projection(c3):
     g = torch.Generator(device="cpu").manual_seed(3)
     rows = torch.randint(0, r.pca.X_pca.shape[0], (2048,), generator=g).to(V.device)
     H = r.scaled.H
-    Zs = r.scaled.Z[rows, :H].double() - r.pca.col_mean[:H].double()
+    Zs = r.scaled.dense()[rows, :H].double() - r.pca.col_mean[:H].double()
     ref = Zs @ V.T
     got = r.pca.X_pca[rows, : r.pca.n_comps].double()
     scale = ref.abs().max().item()

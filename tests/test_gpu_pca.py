@@ -116,3 +116,37 @@ def test_pca_rank_deficient_uses_cgs2_fallback():
     got = r.components.cpu().numpy().T.astype(np.float64)
     assert op.subspace_angle(got, V) < 1e-4  # 3xBF16 Gram (fp32 accumulation) vs an fp64 covariance
     np.testing.assert_allclose(r.variance.cpu().numpy(), np.sort(w)[::-1][:10], rtol=1e-5)
+
+
+def test_scale_planes_bit_identical_to_split_and_projection_close():
+    """scale_dense(planes=True) writes exactly split_bf16(scale_dense fp32); the planes projection
+    (3xBF16) matches the fp32 (3xTF32) projection to ~1e-5 of the embedding's scale."""
+    import torch
+    from paper_2605_13928_b200 import pipeline, pp, synth
+    spec = synth.Spec(6000, 2000, seed=12)
+    X = synth.generate(spec)
+    r = pipeline.run(X, synth.mt_mask(spec), pipeline.Params(min_genes=30, n_top_genes=600), timing=False,
+                     with_knn=False)
+    Xl = r.X_log
+    slot = pp.gene_slots(r.hvg_index, Xl.n_cols)
+    H = int(r.hvg_index.numel())
+    mean, inv = r.scaled.mean, r.scaled.inv_std
+    f32 = pp.scale_dense(Xl, slot, H, mean, inv, 10.0)
+    pl = pp.scale_dense(Xl, slot, H, mean, inv, 10.0, planes=True)
+    pp.split_planes(f32)
+    torch.cuda.synchronize()
+    assert pl.Z is None
+    assert torch.equal(pl.Z_hi.view(torch.int16), f32.Z_hi.view(torch.int16))
+    assert torch.equal(pl.Z_lo.view(torch.int16), f32.Z_lo.view(torch.int16))
+    rel = ((pl.dense() - f32.Z).abs() / f32.Z.abs().clamp_min(1e-3)).max().item()
+    assert rel < 2e-5
+    comp_t, cmean = r.pca.components, r.pca.col_mean
+    npad = 64
+    ct = torch.zeros((npad, pl.ld), dtype=torch.float32, device="cuda")
+    ct[: comp_t.shape[0], : comp_t.shape[1]] = comp_t
+    a = pp.project(f32, ct, cmean, 50)
+    b = pp.project(pl, ct, cmean, 50)
+    torch.cuda.synchronize()
+    err = (a - b).abs().max().item() / a.abs().max().item()
+    assert err < 1e-4, err
+    assert torch.all(b[:, 50:] == 0)

@@ -15,7 +15,7 @@ def _run(X, mt, p):
     out = {k: v.cpu().numpy() for k, v in r.qc.items() if v is not None}
     out.update(cell_mask=r.cell_mask.cpu().numpy(), gene_mask=r.gene_mask.cpu().numpy(),
                hvg=r.hvg_mask.cpu().numpy(), log_ip=r.X_log.indptr.cpu().numpy(), log_ix=r.X_log.indices.cpu().numpy(),
-               log=r.X_log.data.cpu().numpy(), Z=r.scaled.Z.cpu().numpy(), mean=r.scaled.mean.cpu().numpy(),
+               log=r.X_log.data.cpu().numpy(), Z=r.scaled.dense().cpu().numpy(), mean=r.scaled.mean.cpu().numpy(),
                xpca=r.pca.X_pca.cpu().numpy(), knn=r.knn_index.cpu().numpy(), dist=r.knn_dist.cpu().numpy())
     return out
 

@@ -29,7 +29,8 @@ o = chunked.run(*host, mt.cpu().numpy(), op.Params(), workers=16)
 V = o["components"]
 sc = r.scaled
 H = sc.H
-N = sc.Z.shape[0]
+N = sc.n_rows
+sc = pp.Scaled(sc.dense().contiguous(), sc.H, sc.ones_col, sc.mean, sc.inv_std)  # fp32 copy for the experiments
 out = {"cells": n, "genes": g, "slice_cells": os.environ.get("SCB_GRAM_SLICE_CELLS", "default")}
 out["angle_shipped"] = op.subspace_angle(r.pca.components.cpu().numpy().T.astype(np.float64), V)
 for planes in (True, False):

@@ -13,7 +13,7 @@ X = synth.generate(spec)
 r = pipeline.run(X, synth.mt_mask(spec), pipeline.Params(), with_knn=False, timing=False)
 del X
 sc = r.scaled
-N = sc.Z.shape[0]
+N = sc.n_rows
 out = {}
 for rep in range(3):
     ev = [torch.cuda.Event(True) for _ in range(5)]
@@ -23,7 +23,7 @@ for rep in range(3):
     C = torch.empty((sc.ld, sc.ld), dtype=torch.float64, device="cuda")
     from paper_2605_13928_b200 import _lib
     from paper_2605_13928_b200.pp import _ctx, _p, _stream
-    _lib.call("scb_gram_split", _ctx(sc.Z), _p(sc.Z_hi), _p(sc.Z_lo), N, sc.ld, _p(C), _stream())
+    _lib.call("scb_gram_split", _ctx(sc.Z_hi), _p(sc.Z_hi), _p(sc.Z_lo), N, sc.ld, _p(C), _stream())
     ev[2].record()
     lam, comp_t, mean, tr = pp.pca_from_gram(sc, C, N, 50)
     ev[3].record()
