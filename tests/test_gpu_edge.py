@@ -80,3 +80,20 @@ def test_k_close_to_cell_count():
     p = op.Params(min_genes=10, max_pct_mt=100.0, min_cells=1, n_top_genes=200, n_comps=20, n_neighbors=60)
     o = op.run(X, mt, p)
     _check(_run(X, mt, p), o, 60)
+
+
+def test_pipeline_reports_invalid_counts_through_deferred_qc_check():
+    """pipeline.run defers QC's data-validity check to the filter round trip: non-integral
+    counts still raise (SCB_ERR_DATA), and the ctx is back in synchronous-check mode after."""
+    import numpy as np
+    import pytest
+    import torch
+    from paper_2605_13928_b200 import _lib, pipeline, pp
+    ip = np.array([0, 2, 4, 6], np.int64)
+    ix = np.array([0, 1, 1, 2, 0, 2], np.int32)
+    d = np.array([1.0, 2.5, 3.0, 1.0, 4.0, 2.0], np.float32)
+    X = pp.DeviceCSR.from_host(ip, ix, d, 3)
+    with pytest.raises(_lib.ScbError, match="deferred"):
+        pipeline.run(X, torch.zeros(3, dtype=torch.uint8), pipeline.Params(min_genes=0, min_cells=0), timing=False)
+    with pytest.raises(_lib.ScbError):
+        pp.calculate_qc_metrics(X, torch.zeros(3, dtype=torch.uint8))
