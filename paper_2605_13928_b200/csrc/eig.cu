@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
   if (st->done) return;
   // far from convergence the Rayleigh-Ritz step only has to supply the filter bound and a
   // reasonable rotation (every rotation is exactly orthogonal): 2 sweeps; near it, to completion
-  const int sweeps = st->prev_worst > 1e-4 ? 2 : 30;
+  const int sweeps = st->prev_worst > 1e-2 ? 1 : (st->prev_worst > 1e-4 ? 2 : 30);
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
   double (*w)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn + kB * kLd);
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
     for (int w2 = 0; w2 < kJacThreads / 32; ++w2) { o += red[0][w2]; d += red[1][w2]; }
     __syncthreads();
     if (threadIdx.x == 0) g_jacobi_sweeps = sw + 1;
-    if (o <= 1e-26 * d) break;
+    if (o <= 1e-22 * d) break;  // wanted couplings <= 1e-11 of the diagonal (residual target 1e-9)
   }
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
     T[e] = a[e / kB][e % kB];
