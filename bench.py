@@ -429,8 +429,10 @@ def main():
 
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
         e0.record(cs)
         h2d(0)
+        c1.record(cs)  # the first copy runs alone: its time gives the host link's bandwidth
         for i in range(args.steps):
             if i + 1 < args.steps:
                 h2d(i + 1)
@@ -458,9 +460,11 @@ def main():
         if comm is not None:
             e_ms = comm.allreduce_max(e_ms)
         h2d_bytes = sum(t.numel() * t.element_size() for t in h_arrs)
+        first_copy_ms = e0.elapsed_time(c1)
         d2h_bytes = o_i.numel() * 4 + o_d.numel() * 4
         e2e = {"value": N / (e_ms / 1e3), "unit": "cells/s", "ms_per_step": round(e_ms, 3),
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
+               "h2d_GBps_measured": round(h2d_bytes / (first_copy_ms / 1e3) / 1e9, 1),
                "wire_format": ("compact u16 CSR (uint16 gene indices + uint16 counts + escape table), decoded on "
                                "the device each step (scb_csr_u16_decode, inside the timed region)") if wire_u16
                               else "int32/float32 CSR",
