@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
   if (st->done) return;
   // far from convergence the Rayleigh-Ritz step only has to supply the filter bound and a
   // reasonable rotation (every rotation is exactly orthogonal): 2 sweeps; near it, to completion
-  const int sweeps = st->prev_worst > 1e-2 ? 1 : (st->prev_worst > 1e-4 ? 2 : 30);
+  const int sweeps = st->prev_worst > 1e-4 ? 2 : 30;  // (1 sweep far from convergence costs an extra outer step)
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
   double (*w)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn + kB * kLd);
