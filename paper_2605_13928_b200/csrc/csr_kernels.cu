@@ -25,6 +25,14 @@ constexpr size_t kSmemLimit = 227 * 1024;  // opt-in dynamic shared memory per C
 
 static int grid_for(scb_ctx* ctx, int ctas_per_sm) { return ctx->num_sms * ctas_per_sm; }
 
+// log1p of a normalised count y >= 0.  For y >= 0.25 the MUFU logarithm of (1 + y) is used
+// (__logf: <= 2^-21.4 absolute error on [1.25, 2], <= 3 ulp above; the rounding of 1 + y adds
+// <= 2^-24 absolute) -- relative error <= 2e-6, inside the 1e-5 tolerance of the log values
+// (numpy's own float32 log1p is not correctly rounded either); below 0.25, where 1 + y would
+// cancel, the accurate log1pf.  About 4 instructions instead of ~25 for almost every nonzero
+// (y = count * 1e4 / total is >= 1 for most entries).
+__device__ __forceinline__ float log1p_count(float y) { return y >= 0.25f ? __logf(1.0f + y) : log1pf(y); }
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -429,7 +437,7 @@ subset_fill_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ in
       for (int k = 0; k < 4; ++k)
         if (ng[k] >= 0) {
           s_idx[w][pos] = ng[k];
-          s_val[w][pos] = row_scale ? log1pf(__fmul_rn(q.x[k], s)) : q.x[k];
+          s_val[w][pos] = row_scale ? log1p_count(__fmul_rn(q.x[k], s)) : q.x[k];
           ++pos;
         }
       __syncwarp();
@@ -503,7 +511,7 @@ subset_fill_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (ng[k] >= 0) {
-          const float l = log1pf(__fmul_rn(q.x[k], s));
+          const float l = log1p_count(__fmul_rn(q.x[k], s));
           s_idx[w][pos] = ng[k];
           s_val[w][pos] = l;
           ++pos;
@@ -563,7 +571,7 @@ normalize_log1p_kernel(const int64_t* __restrict__ indptr, const float* __restri
     sum = warp_sum(sum);
     const float s = (sum > 0.0) ? (float)__ddiv_rn(target_sum, sum) : 1.0f;
     if (lane == 0) row_scale[r] = s;
-    for (int64_t p = b + lane; p < e; p += 32) out[p] = log1pf(__fmul_rn(data[p], s));
+    for (int64_t p = b + lane; p < e; p += 32) out[p] = log1p_count(__fmul_rn(data[p], s));
   }
 }
 
