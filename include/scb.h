@@ -64,6 +64,9 @@ SCB_API int scb_ctx_destroy(scb_ctx* ctx);
 /* on != 0: scb_qc_metrics no longer waits for its data-validity check (one host round trip);
  * the flag is returned in n_kept[3] of the next scb_filter_masks instead. */
 SCB_API int scb_ctx_set_deferred_checks(scb_ctx* ctx, int32_t on);
+/* stream-ordered copy of the ctx's current data-error flag (set by a deferred scb_qc_metrics) to
+ * a device int32 -- e.g. to keep each chunk's check when QC runs chunk by chunk. */
+SCB_API int scb_ctx_copy_data_flag(scb_ctx* ctx, int32_t* dst, void* stream);
 
 /* ---- multi-GPU: a ctx that owns an NCCL communicator over `world`
  * ranks (one process per GPU).  Rank 0 makes the 128-byte id with scb_nccl_unique_id and

@@ -35,6 +35,7 @@ SIGNATURES = {
                          c_ptr],
     "scb_subset_rows_all_genes": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_ctx_set_deferred_checks": [c_ptr, c_i32],
+    "scb_ctx_copy_data_flag": [c_ptr, c_ptr, c_ptr],
     "scb_subset_count": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr],
     "scb_subset_fill": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_normalize_log1p": [c_ptr, c_ptr, c_ptr, c_i64, c_dbl, c_ptr, c_ptr, c_ptr],

@@ -77,6 +77,12 @@ extern "C" int scb_ctx_set_deferred_checks(scb_ctx* ctx, int32_t on) {
   return SCB_OK;
 }
 
+extern "C" int scb_ctx_copy_data_flag(scb_ctx* ctx, int32_t* dst, void* stream) {
+  SCB_REQUIRE(ctx && dst, SCB_ERR_ARG, "scb_ctx_copy_data_flag: null argument");
+  SCB_CUDA(cudaMemcpyAsync(dst, ctx->d_flag, sizeof(int32_t), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return SCB_OK;
+}
+
 static void scb_comm_release(scb_ctx* ctx);
 
 extern "C" int scb_ctx_destroy(scb_ctx* ctx) {

@@ -103,15 +103,17 @@ class _Timer:
 
 def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, comm=None,
         mark: Optional[Callable[[str], None]] = None, timing: bool = True, with_knn: bool = True,
-        knn_timer=None) -> Result:
-    """Run the whole hot path on the device-resident count matrix ``X`` (this rank's rows)."""
+        knn_timer=None, qc: Optional[dict] = None) -> Result:
+    """Run the whole hot path on the device-resident count matrix ``X`` (this rank's rows).
+    ``qc``: QC metrics already computed while the matrix was uploaded (``ingest.upload_qc``)."""
     p = params
     tm = _Timer(timing, mark)
     dev = X.device
 
     # ------------------------------------------------------------------ qc
     tm.step("qc")
-    qc = pp.calculate_qc_metrics(X, mt_mask, row_splits=True, defer_check=True)
+    if qc is None:
+        qc = pp.calculate_qc_metrics(X, mt_mask, row_splits=True, defer_check=True)
     if comm is not None:
         comm.allreduce_(qc["n_cells_by_counts"])
         comm.allreduce_(qc["gene_total_counts"])
