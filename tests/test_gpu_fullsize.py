@@ -1,6 +1,7 @@
 """Full-size (C3: 1M cells x 25k genes, BASELINE.json's headline config) checks of the whole
-path through size-independent properties -- the oracle cannot run at this size, so each stage is
-checked against an identity that holds at any size:
+path through size-independent properties (the stage-by-stage comparison with the CPU oracle at
+this size is tests/test_gpu_parity_scale.py); each stage is checked against an identity that
+holds at any size:
 
 * QC: checksum of checksums -- sum over cells of total_counts == sum over genes of total_counts ==
   sum of the stored counts, and likewise for the nonzero counts (exact: integer counts in f64);
@@ -10,7 +11,10 @@ checked against an identity that holds at any size:
 * PCA: orthonormal components, non-increasing variances, X_pca == (Z - mean) V^T on sampled rows
   (float64 recomputation);
 * kNN: self at distance 0 first, distances non-decreasing, and 512 random queries against an
-  exact float64 brute force over all 1M rows (recall >= 0.999, distances within 1e-4).
+  exact float64 brute force over all 1M rows (recall >= 0.999, distances within 1e-4);
+* the compact u16 input at full size: every stage bit-identical to the 32-bit input;
+* kNN with k = 30 (config C5's k) on the C3 embedding: recall >= 0.999 on 1000 random queries
+  against the CPU oracle's exact float64 neighbours.
 """
 import numpy as np
 import pytest
@@ -32,8 +36,9 @@ def c3():
     p = pipeline.Params()
     r = pipeline.run(X, mt, p)
     torch.cuda.synchronize()
+    Xu = X.to_u16()
     del X
-    return dict(r=r, p=p, data_sum=data_sum, nnz_pos=nnz_pos)
+    return dict(r=r, p=p, data_sum=data_sum, nnz_pos=nnz_pos, Xu=Xu, mt=mt)
 
 
 def test_c3_qc_checksums_and_masks(c3):
@@ -105,3 +110,37 @@ def test_c3_knn_sampled_exact(c3):
     hits = sum(len(set(a.tolist()) & set(b.tolist())) for a, b in zip(got.cpu(), ref_i.cpu()))
     assert hits / (512 * k) >= 0.999
     np.testing.assert_allclose(dist[q].double().cpu().numpy(), ref_d.sqrt().cpu().numpy(), rtol=1e-4, atol=1e-4)
+
+
+def test_c3_u16_input_bit_identical(c3):
+    """The compact u16 CSR (292 escaped counts >= 65535 at C3) through every raw-matrix pass
+    gives exactly the 32-bit input's results at full size."""
+    import torch
+    from paper_2605_13928_b200 import pipeline
+    r, Xu = c3["r"], c3["Xu"]
+    assert Xu.esc_pos.numel() > 0
+    ru = pipeline.run(Xu, c3["mt"], c3["p"], timing=False)
+    torch.cuda.synchronize()
+    for k in ("n_genes_by_counts", "total_counts", "n_cells_by_counts", "gene_total_counts"):
+        assert torch.equal(ru.qc[k], r.qc[k]), k
+    assert torch.equal(ru.cell_mask, r.cell_mask) and torch.equal(ru.hvg_mask, r.hvg_mask)
+    assert torch.equal(ru.X_log.data, r.X_log.data)
+    assert torch.equal(ru.scaled.Z_hi, r.scaled.Z_hi) and torch.equal(ru.scaled.Z_lo, r.scaled.Z_lo)
+    assert torch.equal(ru.pca.X_pca, r.pca.X_pca) and torch.equal(ru.knn_index, r.knn_index)
+
+
+def test_c3_knn_k30_recall_vs_oracle(c3):
+    """k = 30 (config C5) on the C3 embedding against the CPU oracle's float64 brute force."""
+    import os
+    import torch
+    from oracle import chunked
+    from oracle import pipeline as op
+    from paper_2605_13928_b200 import pp
+    E = c3["r"].pca.X_pca[:, :50].contiguous()
+    idx, dist = pp.neighbors(E, 30)
+    torch.cuda.synchronize()
+    q = np.sort(np.random.default_rng(7).choice(E.shape[0], 1000, replace=False))
+    ref_i, ref_d = chunked.knn_queries(E.cpu().numpy(), 30, q, workers=max(1, min(32, len(os.sched_getaffinity(0)))))
+    got = idx.cpu().numpy()[q]
+    assert op.knn_recall(got, ref_i) >= 0.999
+    np.testing.assert_allclose(dist.cpu().numpy()[q][:, -1], ref_d[:, -1], rtol=1e-4, atol=1e-5)

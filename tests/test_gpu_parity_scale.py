@@ -125,3 +125,23 @@ def test_c3_sample_scanpy_float_hvg():
     got = r.hvg_mask.cpu().numpy().astype(bool)
     flips = np.nonzero(sel != got)[0]
     assert flips.size == 0, f"device HVG set differs from Scanpy's float64 set at {flips.tolist()}"
+
+
+def test_c2_regress_out_parity():
+    """regress_out + scale (paper Table 1 step 4) at C2 vs the oracle's OLS restatement."""
+    import torch
+    from paper_2605_13928_b200 import pipeline, synth
+    p = pipeline.Params(regress_out=True)
+    spec = synth.Spec(100_000, 20_000, seed=0)
+    X = synth.generate(spec)
+    r = pipeline.run(X, synth.mt_mask(spec), p, timing=False, with_knn=False)
+    torch.cuda.synchronize()
+    ip, ix, d, G = X.to_host()
+    o = op.run(op.CSR(ip, ix, d, G), synth.mt_mask(spec).cpu().numpy(),
+               op.Params(regress_out=True, hvg_ties=p.hvg_ties, clip=p.clip), with_knn=False)
+    np.testing.assert_array_equal(r.hvg_mask.cpu().numpy(), o["hvg_mask"])
+    Z = r.scaled.values().cpu().numpy()
+    np.testing.assert_allclose(Z, o["Z"], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(r.scaled.inv_std.cpu().numpy(), o["scale_inv_std"], rtol=1e-7)
+    ang = op.subspace_angle(r.pca.components.cpu().numpy().T.astype(np.float64), o["components"])
+    assert ang < 2e-4, ang
