@@ -33,41 +33,53 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
-constexpr int kGLoads = kGK * kGT / 128;  // elements of A (and of B) per thread per chunk
-__global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, const double* __restrict__ A, int lda,
+// CTA tile TM x TN, WARPS_M x WARPS_N warps of (TM/WARPS_M) x (TN/WARPS_N) (MI x NJ MMA tiles)
+template <int TM, int TN, int WARPS_M, int WARPS_N, int MIN_CTAS>
+__global__ void __launch_bounds__(128, MIN_CTAS) dgemm_kernel(int M, int N, int K, const double* __restrict__ A, int lda,
                                                     int opA, const double* __restrict__ B, int ldb, int opB,
                                                     double* __restrict__ Cm, int ldc, int k_per_slice,
                                                     double* __restrict__ partial, const int* __restrict__ done) {
+  static_assert(WARPS_M * WARPS_N == 4, "4 warps");
+  constexpr int WTM = TM / WARPS_M, WTN = TN / WARPS_N, MI = WTM / 8, NJ = WTN / 8;
+  constexpr int LA = kGK * TM / 128, LB = kGK * TN / 128;  // elements of A / B per thread per chunk
   if (done && *done) return;
-  __shared__ double As[kGT][kGK + 1];   // [m][k]
-  __shared__ double Bs[kGK][kGT + 1];   // [k][n]
+  __shared__ double As[TM][kGK + 1];   // [m][k]
+  __shared__ double Bs[kGK][TN + 1];   // [k][n]
   const int warp = warp_id(), lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  const int m0 = blockIdx.y * kGT, n0 = blockIdx.x * kGT;
+  const int wm = (warp / WARPS_N) * WTM, wn = (warp % WARPS_N) * WTN;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   const int kb = blockIdx.z * k_per_slice, ke = min(K, kb + k_per_slice);
-  double acc[4][4][2] = {};
-  double ra[kGLoads], rb[kGLoads];
+  double acc[MI][NJ][2] = {};
+  double ra[LA], rb[LB];
   auto fetch = [&](int k0) {
 #pragma unroll
-    for (int u = 0; u < kGLoads; ++u) {
+    for (int u = 0; u < LA; ++u) {
       const int e = threadIdx.x + 128 * u;
       int kk, mm;
-      if (opA) { kk = e / kGT; mm = e % kGT; } else { mm = e / kGK; kk = e % kGK; }
+      if (opA) { kk = e / TM; mm = e % TM; } else { mm = e / kGK; kk = e % kGK; }
       const int gm = m0 + mm, gk = k0 + kk;
       ra[u] = (gm < M && gk < ke) ? (opA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int e = threadIdx.x + 128 * u;
       int kn, nn;
-      if (opB) { nn = e / kGK; kn = e % kGK; } else { kn = e / kGT; nn = e % kGT; }
+      if (opB) { nn = e / kGK; kn = e % kGK; } else { kn = e / TN; nn = e % TN; }
       const int gn = n0 + nn, gk2 = k0 + kn;
       rb[u] = (gn < N && gk2 < ke) ? (opB ? B[(size_t)gn * ldb + gk2] : B[(size_t)gk2 * ldb + gn]) : 0.0;
     }
   };
   auto stash = [&]() {
 #pragma unroll
-    for (int u = 0; u < kGLoads; ++u) {
+    for (int u = 0; u < LA; ++u) {
       const int e = threadIdx.x + 128 * u;
-      if (opA) As[e % kGT][e / kGT] = ra[u]; else As[e / kGK][e % kGK] = ra[u];
-      if (opB) Bs[e % kGK][e / kGK] = rb[u]; else Bs[e / kGT][e % kGT] = rb[u];
+      if (opA) As[e % TM][e / TM] = ra[u]; else As[e / kGK][e % kGK] = ra[u];
+    }
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int e = threadIdx.x + 128 * u;
+      if (opB) Bs[e % kGK][e / kGK] = rb[u]; else Bs[e / TN][e % TN] = rb[u];
     }
   };
   if (kb < ke) fetch(kb);
@@ -77,24 +89,24 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, const d
     if (k0 + kGK < ke) fetch(k0 + kGK);  // next chunk in flight during this chunk's MMAs
 #pragma unroll
     for (int kk = 0; kk < kGK; kk += 4) {
-      double af[4], bf[4];
+      double af[MI], bf[NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[wm + 8 * i + g][kk + t];
+      for (int i = 0; i < MI; ++i) af[i] = As[wm + 8 * i + g][kk + t];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Bs[kk + t][wn + 8 * j + g];
+      for (int j = 0; j < NJ; ++j) bf[j] = Bs[kk + t][wn + 8 * j + g];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
     __syncthreads();
   }
   double* out = partial ? partial + (size_t)blockIdx.z * M * N : Cm;
   const int ld = partial ? N : ldc;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int m = m0 + wm + 8 * i + g, n = n0 + wn + 8 * j + 2 * t + c;
@@ -114,8 +126,13 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ partial, int sli
 
 static int dgemm(scb_ctx* ctx, int M, int N, int K, const double* A, int lda, int opA, const double* B, int ldb,
                  int opB, double* Cm, int ldc, cudaStream_t s, const int* done = nullptr) {
-  const int tiles = ((M + kGT - 1) / kGT) * ((N + kGT - 1) / kGT);
-  int slices = std::max(1, std::min((ctx->num_sms + tiles - 1) / tiles, K / 128));
+  // N = kB (every GEMM of the solver): 32 x 96 tiles, no padded columns; split-K sized so the
+  // grid is ~3 CTAs per SM.  Otherwise 64 x 64 tiles, ~1 CTA per SM.
+  const bool narrow = (N == 96);
+  const int TM = narrow ? 32 : kGT, TN = narrow ? 96 : kGT;
+  const int tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN);
+  const int want = narrow ? 3 * ctx->num_sms : ctx->num_sms;
+  int slices = std::max(1, std::min((want + tiles / 2) / tiles, K / 128));
   const int kps = ((K + slices - 1) / slices + kGK - 1) / kGK * kGK;
   slices = (K + kps - 1) / kps;
   double* partial = nullptr;
@@ -124,8 +141,11 @@ static int dgemm(scb_ctx* ctx, int M, int N, int K, const double* A, int lda, in
     SCB_TRY(ws_get(ctx, 3, (size_t)slices * M * N * sizeof(double), &ws, s));
     partial = (double*)ws;
   }
-  dim3 g((N + kGT - 1) / kGT, (M + kGT - 1) / kGT, slices);
-  dgemm_kernel<<<g, 128, 0, s>>>(M, N, K, A, lda, opA, B, ldb, opB, Cm, ldc, kps, partial, done);
+  dim3 g((N + TN - 1) / TN, (M + TM - 1) / TM, slices);
+  if (narrow)
+    dgemm_kernel<32, 96, 1, 4, 3><<<g, 128, 0, s>>>(M, N, K, A, lda, opA, B, ldb, opB, Cm, ldc, kps, partial, done);
+  else
+    dgemm_kernel<kGT, kGT, 2, 2, 1><<<g, 128, 0, s>>>(M, N, K, A, lda, opA, B, ldb, opB, Cm, ldc, kps, partial, done);
   SCB_LAUNCH_CHECK();
   if (slices > 1) {
     splitk_reduce_kernel<<<(unsigned)(((int64_t)M * N + 255) / 256), 256, 0, s>>>(partial, slices, M, N, Cm, ldc, done);
@@ -141,7 +161,10 @@ __global__ void __launch_bounds__(256) trsm_rows_kernel(const double* __restrict
   if (done && *done) return;
   extern __shared__ double rdyn[];
   double (*r)[kB + 1] = reinterpret_cast<double (*)[kB + 1]>(rdyn);
-  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) r[e / kB][e % kB] = R[e];
+  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
+    const int i = e / kB, j = e % kB;
+    r[i][j] = (i == j) ? 1.0 / R[e] : R[e];  // diagonal stored as its reciprocal
+  }
   __syncthreads();
   const int lane = lane_id();
   for (int row = blockIdx.x * 8 + warp_id(); row < h; row += gridDim.x * 8) {
@@ -153,7 +176,7 @@ __global__ void __launch_bounds__(256) trsm_rows_kernel(const double* __restrict
       double mj = 0.0;
 #pragma unroll
       for (int t = 0; t < 3; ++t) if (t == slot) mj = m[t];
-      const double xj = __shfl_sync(0xffffffffu, mj, owner) / r[j][j];
+      const double xj = __shfl_sync(0xffffffffu, mj, owner) * r[j][j];
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         const int c = lane + 32 * t;
@@ -276,42 +299,52 @@ __global__ void init_block_kernel(double* __restrict__ Q, int h) {
 
 // ------------------------------------------------------------------ Cholesky QR
 // In place Cholesky of the kB x kB Gram S = Q^T Q (one CTA), S -> R (upper, row-major).
+// Unscaled right-looking form, one barrier per step: step k subtracts a_ki a_kj / a_kk from the
+// trailing upper triangle (row k itself is final); the thread that updates a_{k+1,k+1} also
+// stores its reciprocal for the next step.  Rows are scaled by 1/sqrt(pivot) on the way out.
 constexpr int kCholThreads = 1024;  // 32 x 32 thread grid over the trailing matrix
 __global__ void __launch_bounds__(kCholThreads) chol_kernel(double* __restrict__ S, int* __restrict__ fail,
                                                              int* __restrict__ done) {
   if (*done) return;
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
+  __shared__ double invd[kB];
+  __shared__ int bad;
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) a[e / kB][e % kB] = S[e];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double d = a[0][0];
+    bad = 0;
+    if (!(d > 0.0)) { bad = 1; d = 1e-300; a[0][0] = d; }
+    invd[0] = 1.0 / d;
+  }
   __syncthreads();
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int k = 0; k < kB; ++k) {
-    // every thread derives the pivot itself (no extra barrier): row k of R = a[k][j] / sqrt(a_kk)
-    double d = a[k][k];
-    if (!(d > 0.0)) d = 1e-300;
-    const double r = sqrt(d), inv = 1.0 / r;
-    __syncthreads();  // all pivots read before row k is rescaled
-    if (threadIdx.x == 0) {
-      if (!(a[k][k] > 0.0)) {
-        *fail = 1;
-        *done = 1;  // stop the enqueued outer steps; the host redoes the solve with CGS2
-      }
-      a[k][k] = r;
-    }
-    for (int j = k + 1 + threadIdx.x; j < kB; j += blockDim.x) a[k][j] *= inv;
-    __syncthreads();
+    const double iv = invd[k];
     for (int i = k + 1 + ty; i < kB; i += 32) {
-      const double aki = a[k][i];
-      for (int j = i + tx; j < kB; j += 32) a[i][j] -= aki * a[k][j];
+      const double aki = a[k][i] * iv;
+      for (int j = i + tx; j < kB; j += 32) {
+        double v = a[i][j] - aki * a[k][j];
+        if (j == k + 1) {  // (i == j == k + 1): the next pivot
+          if (!(v > 0.0)) { bad = 1; v = 1e-300; }
+          invd[k + 1] = 1.0 / v;
+        }
+        a[i][j] = v;
+      }
     }
     __syncthreads();
   }
   for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
     const int i = e / kB, j = e % kB;
-    S[e] = (j >= i) ? a[i][j] : 0.0;
+    const double r = sqrt(a[i][i]);
+    S[e] = (j > i) ? a[i][j] / r : (j == i ? r : 0.0);
+  }
+  if (threadIdx.x == 0 && bad) {
+    *fail = 1;
+    *done = 1;  // stop the enqueued outer steps; the host redoes the solve with CGS2
   }
 }
-
 
 // ------------------------------------------------------------------ Jacobi (one CTA)
 // Cyclic two-sided Jacobi on the symmetric kB x kB matrix T; W accumulates rotations.
@@ -325,8 +358,8 @@ __device__ int g_jacobi_sweeps;  // debug: sweeps used by the last call
 
 // One round applies kB/2 disjoint rotations J_k at once: A := J^T A J, W := W J.  Every
 // element of A belongs to exactly one 2x2 block (rows of pair k, columns of pair l), updated
-// in a single pass as R_k^T B R_l by one thread (the k > l block is the mirror), so a round
-// is two barriers and one read + one write of A and W.
+// in a single pass as R_k^T B R_l by one thread (the k > l block is the mirror); the next
+// round's rotations are computed while W is updated, so a round is two barriers.
 // device-side solver state (no host round trip per outer step)
 struct EigState {
   double cheb_b;      // top of the damped interval of the Chebyshev filter (smallest Ritz value)
@@ -345,8 +378,10 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
   extern __shared__ double dyn[];
   double (*a)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);
   double (*w)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn + kB * kLd);
-  __shared__ double cs[kPairs], sn[kPairs];
-  __shared__ int pp[kPairs], qq[kPairs];
+  // rotations double-buffered by round parity: phase A applies round r's rotations to T;
+  // phase B computes round r+1's (warps 0-1) while the other warps apply round r's to W
+  __shared__ double cs[2][kPairs], sn[2][kPairs];
+  __shared__ int pp[2][kPairs], qq[2][kPairs];
   __shared__ short2 blk[kBlocks];
   __shared__ double red[2][kJacThreads / 32];
   __shared__ int wanted[kB];  // 1: row among the n_wanted largest diagonal entries
@@ -359,34 +394,36 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
     for (int k = 0; k < kPairs; ++k)
       for (int l = k; l < kPairs; ++l) blk[b++] = make_short2((short)k, (short)l);
   }
-  __syncthreads();
   constexpr int M = kB - 1;
+  auto rotations = [&](int rd, int buf) {  // threads 0 .. kPairs-1
+    const int i = threadIdx.x;
+    int p, q;
+    if (i == 0) { p = rd; q = M; }
+    else { p = (rd + i) % M; q = (rd - i + M) % M; }
+    if (p > q) { const int t = p; p = q; q = t; }
+    pp[buf][i] = p;
+    qq[buf][i] = q;
+    const double apq = a[p][q];
+    double c = 1.0, s = 0.0;
+    if (apq != 0.0) {
+      const double tau = (a[q][q] - a[p][p]) / (2.0 * apq);
+      const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+      c = rsqrt(1.0 + t * t);
+      s = t * c;
+    }
+    cs[buf][i] = c;
+    sn[buf][i] = s;
+  };
+  __syncthreads();
+  if (threadIdx.x < kPairs) rotations(0, 0);
+  __syncthreads();
+  int cur = 0;
   for (int sw = 0; sw < sweeps; ++sw) {
-    for (int rd = 0; rd < M; ++rd) {
-      if (threadIdx.x < kPairs) {
-        const int i = threadIdx.x;
-        int p, q;
-        if (i == 0) { p = rd; q = M; }
-        else { p = (rd + i) % M; q = (rd - i + M) % M; }
-        if (p > q) { const int t = p; p = q; q = t; }
-        pp[i] = p;
-        qq[i] = q;
-        const double apq = a[p][q];
-        double c = 1.0, s = 0.0;
-        if (apq != 0.0) {
-          const double tau = (a[q][q] - a[p][p]) / (2.0 * apq);
-          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = rsqrt(1.0 + t * t);
-          s = t * c;
-        }
-        cs[i] = c;
-        sn[i] = s;
-      }
-      __syncthreads();
-      for (int b = threadIdx.x; b < kBlocks; b += blockDim.x) {
+    for (int rd = 0; rd < M; ++rd, cur ^= 1) {
+      for (int b = threadIdx.x; b < kBlocks; b += blockDim.x) {  // phase A: T := J^T T J
         const short2 kl = blk[b];
-        const int pk = pp[kl.x], qk = qq[kl.x], pl = pp[kl.y], ql = qq[kl.y];
-        const double ck = cs[kl.x], sk = sn[kl.x], cl = cs[kl.y], sl = sn[kl.y];
+        const int pk = pp[cur][kl.x], qk = qq[cur][kl.x], pl = pp[cur][kl.y], ql = qq[cur][kl.y];
+        const double ck = cs[cur][kl.x], sk = sn[cur][kl.x], cl = cs[cur][kl.y], sl = sn[cur][kl.y];
         const double x00 = a[pk][pl], x01 = a[pk][ql], x10 = a[qk][pl], x11 = a[qk][ql];
         const double y00 = ck * x00 - sk * x10, y01 = ck * x01 - sk * x11;  // rows: R_k^T
         const double y10 = sk * x00 + ck * x10, y11 = sk * x01 + ck * x11;
@@ -403,13 +440,18 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
           a[ql][qk] = z11;
         }
       }
-      for (int e = threadIdx.x; e < kB * kPairs; e += blockDim.x) {  // W := W J
-        const int i = e / kPairs, l = e % kPairs;
-        const int p = pp[l], q = qq[l];
-        const double c = cs[l], s = sn[l];
-        const double wp = w[i][p], wq = w[i][q];
-        w[i][p] = c * wp - s * wq;
-        w[i][q] = s * wp + c * wq;
+      __syncthreads();
+      if (threadIdx.x < 64) {  // phase B
+        if (threadIdx.x < kPairs) rotations(rd + 1 < M ? rd + 1 : 0, cur ^ 1);
+      } else {
+        for (int e = threadIdx.x - 64; e < kB * kPairs; e += blockDim.x - 64) {  // W := W J
+          const int i = e / kPairs, l = e % kPairs;
+          const int p = pp[cur][l], q = qq[cur][l];
+          const double c = cs[cur][l], s = sn[cur][l];
+          const double wp = w[i][p], wq = w[i][q];
+          w[i][p] = c * wp - s * wq;
+          w[i][q] = s * wp + c * wq;
+        }
       }
       __syncthreads();
     }
