@@ -18,6 +18,7 @@ namespace scb {
 
 constexpr int kRowThreads = 512;          // threads per CTA of the row-streaming kernels
 constexpr int kQcThreads = 1024;          // QC: one CTA per SM (gene histogram fills smem)
+constexpr int kQcFlushRows = 4095;        // rows per CTA between flushes of the packed gene words
 constexpr int kHvgThreads = 1024;         // HVG sums: one CTA per SM (gene tile fills smem)
 constexpr int kMaxSplit = 3;              // gene tiles of the HVG pass: up to 4 (G <= ~58k)
 constexpr int kHvgTileW = (int)(227 * 1024 / 16);  // genes per HVG tile (4 u32 words each)
@@ -89,7 +90,11 @@ __device__ __forceinline__ void red_shared_add(uint32_t a, uint32_t v) {
 }
 
 // ============================================================================ QC
-// smem: n_cells u32[W], total_lo u32[W] for a gene tile [g0, g0+W), mt flag byte per gene.  The tile-0
+// smem: one packed u32 per gene of a tile [g0, g0+W) -- bits [20,32) cells with a nonzero count,
+// bits [0,20) the sum of the counts' low 8 bits -- and an mt flag byte per gene.  One shared
+// atomic per nonzero; count bits >= 8 go straight to the global u64 totals (0.1 % of C3's
+// nonzeros).  Every kQcFlushRows rows a CTA adds its words into the global counters and clears
+// them, so neither field can overflow (4095 rows x 255 < 2^20).  The tile-0
 // CTAs also write the per-cell metrics and, for the HVG pass, the per-row positions where
 // the original gene index crosses each HVG tile boundary (splits[r][t-1] = #entries with
 // gene < t*split_w, relative to the row start).
@@ -106,24 +111,43 @@ qc_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
   const int tile = blockIdx.y;
   const int g0 = tile * tile_w;
   const int w = min(tile_w, n_cols - g0);
-  uint32_t* s_cells = sm;
-  uint32_t* s_tot = sm + tile_w;
-  uint8_t* s_mt = reinterpret_cast<uint8_t*>(sm + 2 * tile_w);  // 0/1 per gene, ALL genes
-  for (int i = threadIdx.x; i < 2 * tile_w; i += blockDim.x) sm[i] = 0;
+  uint32_t* s_pack = sm;
+  uint8_t* s_mt = reinterpret_cast<uint8_t*>(sm + tile_w);  // 0/1 per gene, ALL genes
+  for (int i = threadIdx.x; i < tile_w; i += blockDim.x) sm[i] = 0;
   for (int i = threadIdx.x; i < n_cols; i += blockDim.x) s_mt[i] = mt_mask[i] ? 1 : 0;
   __syncthreads();
   const bool row_owner = (tile == 0);
   const int lane = lane_id();
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int wpc = blockDim.x >> 5;
+  const int64_t warps = (int64_t)gridDim.x * wpc;
+  const int flush_every = kQcFlushRows / wpc;  // loop iterations (each: one row per warp)
   // shared-window addresses biased by the tile origin: gene g lives at a + 4g
-  const uint32_t a_cells = smem_addr(s_cells) - 4u * (uint32_t)g0;
-  const uint32_t a_tot = smem_addr(s_tot) - 4u * (uint32_t)g0;
+  const uint32_t a_pack = smem_addr(s_pack) - 4u * (uint32_t)g0;
   const uint32_t a_mt = smem_addr(s_mt);
+  auto flush = [&]() {
+    __syncthreads();
+    for (int i = threadIdx.x; i < w; i += blockDim.x) {
+      const uint32_t v = s_pack[i];
+      if (v) {
+        if (v >> 20) atomicAdd(&g_cells[g0 + i], v >> 20);
+        if (v & 0xFFFFFu) atomicAdd(&g_total[g0 + i], (unsigned long long)(v & 0xFFFFFu));
+        s_pack[i] = 0u;
+      }
+    }
+    __syncthreads();
+  };
   // per-lane dummy gene of the tile for masked elements' zero adds (distinct lanes -> distinct
   // banks; a shared dummy would serialise the warp's atomics on one address)
   const int gd = g0 + lane % max(w, 1);
   bool bad = false;
-  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+  int since_flush = 0;
+  for (int64_t r0 = (int64_t)blockIdx.x * wpc; r0 < n_rows; r0 += warps) {  // CTA-uniform trip count
+    if (++since_flush > flush_every) {
+      flush();
+      since_flush = 1;
+    }
+    const int64_t r = r0 + warp_id();
+    if (r >= n_rows) continue;
     const int64_t b = indptr[r], e = indptr[r + 1];
     uint32_t cnt = 0;
     unsigned long long sum = 0, summt = 0;
@@ -175,20 +199,19 @@ qc_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
         cnt += (xv[k] != 0u) ? 1u : 0u;
         qsum += xv[k];
         qmt += lds_u8(a_mt + (uint32_t)g[k]) * xv[k];
-        // low 12 bits in smem (fire-and-forget: <= 2^20 rows per CTA keep the word below
-        // 2^32); zero increments land on the tile's first gene
-        // one tile covering every gene (G <= ~28k): every validated gene index is in it
+        // packed word: +1 cell in bits [20,32) for a nonzero, + low 8 bits of the count
+        // (fire-and-forget); masked elements add 0 to the lane's dummy gene.  One tile covering
+        // every gene (G <= ~50k): every validated gene index is in it
         const bool in_tile = SINGLE_TILE || (unsigned)(g[k] - g0) < (unsigned)w;
         const uint32_t ga = 4u * (uint32_t)(in_tile ? g[k] : gd);
-        red_shared_add(a_cells + ga, (in_tile & (xv[k] != 0u)) ? 1u : 0u);
-        red_shared_add(a_tot + ga, in_tile ? (xv[k] & 0xFFFu) : 0u);
+        red_shared_add(a_pack + ga, in_tile ? (((xv[k] != 0u) ? (1u << 20) : 0u) | (xv[k] & 0xFFu)) : 0u);
         hi_any |= in_tile ? xv[k] : 0u;
       }
-      if (hi_any > 0xFFFu) {  // rare: higher parts straight into the global u64 totals
+      if (hi_any > 0xFFu) {  // rare: higher parts straight into the global u64 totals
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if ((SINGLE_TILE || (unsigned)(g[k] - g0) < (unsigned)w) & (xv[k] > 0xFFFu))
-            atomicAdd(&g_total[g[k]], (unsigned long long)(xv[k] & ~0xFFFu));
+          if ((SINGLE_TILE || (unsigned)(g[k] - g0) < (unsigned)w) & (xv[k] > 0xFFu))
+            atomicAdd(&g_total[g[k]], (unsigned long long)(xv[k] & ~0xFFu));
       }
       sum += qsum;
       summt += qmt;
@@ -218,11 +241,7 @@ qc_kernel(const int64_t* __restrict__ indptr, const IT* __restrict__ indices,
     }
   }
   if (bad) atomicOr(flag, 1);
-  __syncthreads();
-  for (int i = threadIdx.x; i < w; i += blockDim.x) {
-    if (s_cells[i]) atomicAdd(&g_cells[g0 + i], s_cells[i]);
-    if (s_tot[i]) atomicAdd(&g_total[g0 + i], (unsigned long long)s_tot[i]);
-  }
+  flush();
 }
 
 __global__ void zero_if_flag_kernel(unsigned long long* __restrict__ a, int64_t n, const int* __restrict__ flag) {
@@ -1186,7 +1205,7 @@ static int qc_metrics_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indice
   cudaStream_t s = (cudaStream_t)stream;
   const size_t mt_bytes = ((size_t)n_cols + 15) & ~(size_t)15;
   SCB_REQUIRE(mt_bytes + 8 * 1024 <= kSmemLimit, SCB_ERR_UNSUPPORTED, "scb_qc_metrics: too many genes");
-  const int max_w = (int)((kSmemLimit - mt_bytes) / 8);
+  const int max_w = (int)((kSmemLimit - mt_bytes) / 4);
   const int n_tiles = ceil_div(n_cols, max_w);
   const int tile_w = ceil_div(n_cols, n_tiles);
   void* ws;
@@ -1196,11 +1215,10 @@ static int qc_metrics_impl(scb_ctx* ctx, const int64_t* indptr, const IT* indice
   unsigned long long* g_total = (unsigned long long*)((char*)ws + ((size_t)n_cols * 4 + 7) / 8 * 8);
   SCB_CUDA(cudaMemsetAsync(ws, 0, ws_bytes + 8, s));
   SCB_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), s));
-  const size_t smem = (size_t)tile_w * 8 + mt_bytes;
+  const size_t smem = (size_t)tile_w * 4 + mt_bytes;
   const int n_split = hvg_row_splits ? n_tiles_hvg - 1 : 0;
   if (n_rows > 0) {
-    // each CTA sees at most 2^20 rows, so its 12-bit partial gene totals cannot overflow a u32
-    dim3 grid((unsigned)std::max<int64_t>(grid_for(ctx, 1), (n_rows + (1 << 20) - 1) >> 20), n_tiles);
+    dim3 grid((unsigned)grid_for(ctx, 1), n_tiles);
     auto launch = [&](auto kern) {
       SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<grid, kQcThreads, smem, s>>>(indptr, indices, data, n_rows, n_cols, mt_mask, tile_w, n_split, kHvgTileW,
