@@ -489,20 +489,78 @@ subset_fill_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict
   extern __shared__ int32_t dyn_tab[];
   int32_t* tab = dyn_tab;
   uint32_t* ss = reinterpret_cast<uint32_t*>(dyn_tab + ((n_cols + 3) & ~3));
+  bool ident = true;  // every gene kept in place (the all-genes path): no compaction within rows
   for (int g = threadIdx.x; g < n_cols; g += blockDim.x) {
     const int r = remap[g];
+    ident &= (r == g);
     // kept: (slot + 1) << 16 | new index (both < 2^15, so the word stays non-negative); dropped: -1
     tab[g] = r < 0 ? -1 : (int32_t)((uint32_t)r | ((uint32_t)(slot_new[r] + 1) << 16));
   }
   for (int i = threadIdx.x; i < 4 * n_slots; i += blockDim.x) ss[i] = 0;
-  __syncthreads();
+  ident = __syncthreads_and(ident);
   const uint32_t a1lo = smem_addr(ss), a1hi = a1lo + 4u * n_slots, a2lo = a1lo + 8u * n_slots,
                  a2hi = a1lo + 12u * n_slots;
   const int64_t nnz = indptr[n_rows];
   const int lane = lane_id(), w = warp_id();
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t r1 = min(n_rows, r0 + rows_per_block);
-  for (int64_t r = r0 + w; r < r1; r += (blockDim.x >> 5)) {
+  // HVG column: scale sums (same integers as scale_sums_kernel)
+  auto add_sums = [&](float l, int sl) {
+    const uint64_t v1 = (uint64_t)__float2ull_rn(__fmul_rn(l, 268435456.0f));
+    const double l12 = (double)__fmul_rn(l, 4096.0f);
+    const uint64_t v2 = (uint64_t)__double2ull_rn(__dmul_rn(l12, l12));
+    const uint32_t ja = 4u * (uint32_t)sl;
+    if ((v1 | v2) < (1ull << 43)) {
+      red_shared_add(a1lo + ja, (uint32_t)(v1 & 0x3FFFFFu));
+      red_shared_add(a1hi + ja, (uint32_t)(v1 >> 22));
+      red_shared_add(a2lo + ja, (uint32_t)(v2 & 0x3FFFFFu));
+      red_shared_add(a2hi + ja, (uint32_t)(v2 >> 22));
+    } else {  // rare (not log-normalized scale): straight into the global limbs
+      atomicAdd(&sums[sl], v1 & 0xFFFFFFFFull);
+      atomicAdd(&sums[n_slots + sl], v1 >> 32);
+      atomicAdd(&sums[2 * n_slots + sl], v2 & 0xFFFFFFFFull);
+      atomicAdd(&sums[3 * n_slots + sl], v2 >> 32);
+    }
+  };
+  if (ident) {
+    // element p of row r lands at p + (new_indptr[kr] - indptr[r]): no scan, no staging;
+    // 16-byte stores when the shift keeps quads aligned
+    for (int64_t r = r0 + w; r < r1; r += (blockDim.x >> 5)) {
+      if (!cmask[r]) continue;
+      const int64_t kr = row_pos[r];
+      const float s = row_scale[kr];
+      const int64_t b = indptr[r], e = indptr[r + 1];
+      const int64_t delta = new_indptr[kr] - b;
+      const bool vec = (delta & 3) == 0;
+      stream_row_pipe<1>(indices, data, b, e, nnz, [&](const Quad& q) {
+        float l[4];
+        int sl[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int g = q.g[k];
+          const int32_t t = (((q.valid >> k) & 1u) && (unsigned)g < (unsigned)n_cols) ? tab[g] : -1;
+          sl[k] = t < 0 ? -1 : (int)((uint32_t)t >> 16) - 1;
+          l[k] = log1p_count(__fmul_rn(q.x[k], s));
+        }
+        const int64_t o = q.p + delta;
+        if (vec && q.valid == 0xFu) {
+          *reinterpret_cast<int4*>(out_idx + o) = make_int4(q.g[0], q.g[1], q.g[2], q.g[3]);
+          *reinterpret_cast<float4*>(out_val + o) = make_float4(l[0], l[1], l[2], l[3]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if ((q.valid >> k) & 1u) {
+              out_idx[o + k] = q.g[k];
+              out_val[o + k] = l[k];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (sl[k] >= 0) add_sums(l[k], sl[k]);
+      }, esc);
+    }
+  }
+  for (int64_t r = r0 + w; r < r1 && !ident; r += (blockDim.x >> 5)) {
     if (!cmask[r]) continue;
     const int64_t kr = row_pos[r];
     const float s = row_scale[kr];
@@ -534,23 +592,7 @@ subset_fill_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict
           s_idx[w][pos] = ng[k];
           s_val[w][pos] = l;
           ++pos;
-          if (sl[k] >= 0) {  // HVG column: scale sums (same integers as scale_sums_kernel)
-            const uint64_t v1 = (uint64_t)__float2ull_rn(__fmul_rn(l, 268435456.0f));
-            const double l12 = (double)__fmul_rn(l, 4096.0f);
-            const uint64_t v2 = (uint64_t)__double2ull_rn(__dmul_rn(l12, l12));
-            const uint32_t ja = 4u * (uint32_t)sl[k];
-            if ((v1 | v2) < (1ull << 43)) {
-              red_shared_add(a1lo + ja, (uint32_t)(v1 & 0x3FFFFFu));
-              red_shared_add(a1hi + ja, (uint32_t)(v1 >> 22));
-              red_shared_add(a2lo + ja, (uint32_t)(v2 & 0x3FFFFFu));
-              red_shared_add(a2hi + ja, (uint32_t)(v2 >> 22));
-            } else {  // rare (not log-normalized scale): straight into the global limbs
-              atomicAdd(&sums[sl[k]], v1 & 0xFFFFFFFFull);
-              atomicAdd(&sums[n_slots + sl[k]], v1 >> 32);
-              atomicAdd(&sums[2 * n_slots + sl[k]], v2 & 0xFFFFFFFFull);
-              atomicAdd(&sums[3 * n_slots + sl[k]], v2 >> 32);
-            }
-          }
+          if (sl[k] >= 0) add_sums(l, sl[k]);
         }
       __syncwarp();
       for (int j = lane; j < tot; j += 32) {
