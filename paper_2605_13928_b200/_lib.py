@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libscb_b200.so")
+LIB_PATH = os.environ.get("SCB_LIB_PATH") or os.path.join(_HERE, "libscb_b200.so")  # override: A/B experiments
 
 c_i32, c_i64, c_u64, c_dbl, c_ptr = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
 

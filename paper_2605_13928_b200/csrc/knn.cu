@@ -233,6 +233,17 @@ __device__ __forceinline__ int outward_tile(int start, int j, int n_kt) {
   return above > below ? start + (j - below) : start - (j - above);
 }
 
+// inverse of outward_tile: scan position of key tile kt
+__device__ __forceinline__ int outward_pos(int start, int kt, int n_kt) {
+  const int below = start, above = n_kt - 1 - start;
+  const int m = min(below, above);
+  const int d = kt - start;
+  if (d == 0) return 0;
+  if (d > 0 && d <= m) return 2 * d - 1;
+  if (d < 0 && -d <= m) return -2 * d;
+  return d > 0 ? d + below : -d + above;
+}
+
 // Work units of the persistent candidate kernel: query pairs, except that the pairs of a final
 // partial round (r <= gridDim/2 pairs) are split into two halves of their outward key scan, so
 // that round takes half as long; the two halves' lists go to a separate buffer (2 x KCT
@@ -380,10 +391,19 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
     // tcgen05.commit stalls its issuing thread until the tensor pipe drains, so a single issuer
     // leaves the pipe idle ~45% of the time; two issuers interleave.  Each qtile's MMA -> epilogue
     // ring is then independent of the other qtile's epilogue progress.
+    // The whole warp runs the issue loop and one elected lane issues each MMA / commit: the
+    // loop state stays warp-converged (a lane-0-only loop moves every descriptor through
+    // per-thread registers), which took the MMA+TMA-only time of this kernel from ~104 to ~76 ms
+    // at 1M cells.  A's four K-slice descriptors are fixed; B's advance by the stage stride.
     const int t = warp - 1;
-    if (lane == 0) {
+    {
       PROF_T0(tot);
       const uint32_t ab = tc::smem_u32(a_base + t * C::TILE);
+      const uint64_t ad0 = tc::smem_desc_sw128(ab, 16, 1024);
+      const uint64_t bd0 = tc::smem_desc_sw128(tc::smem_u32(b_base), 16, 1024);
+      const uint32_t bar_tf = tc::smem_u32(&t_full[t]), bar_be = tc::smem_u32(&b_empty[0]);
+      const uint32_t bar_bf = tc::smem_u32(&b_full[0]), bar_te = tc::smem_u32(&t_empty[t]);
+      const uint32_t bar_ae = tc::smem_u32(a_empty);
       int it = 0, pc = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++pc) {
         const KnnUnit U = knn_unit(u, n_full, n_kt);
@@ -392,22 +412,21 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
           const int s = it % C::STAGES;
           const int buf = it & 1;
           PROF_T0(w0);
-          tc::mbar_wait(&b_full[s], (it / C::STAGES) & 1);
+          tc::mbar_wait_a(bar_bf + 8 * s, (it / C::STAGES) & 1);
           PROF_ADD(3, w0);
-          const uint32_t bb = tc::smem_u32(b_base + s * C::B_BYTES);
           PROF_T0(w1);
-          tc::mbar_wait(&t_empty[buf * 2 + t], ((it >> 1) & 1) ^ 1);
+          tc::mbar_wait_a(bar_te + 16 * buf, ((it >> 1) & 1) ^ 1);
           PROF_ADD(2, w1);
           tc::tc_fence_after();
           const uint32_t d = tmem + buf * (2 * C::BN) + t * C::BN;
+          const uint64_t bd = bd0 + (uint64_t)((s * C::B_BYTES) >> 4);
 #pragma unroll
           for (int kk = 0; kk < kD / 16; ++kk)  // K = 16 fp16 = 32 bytes per MMA
-            mma_f16(d, tc::smem_desc_sw128(ab + kk * 32, 16, 1024), tc::smem_desc_sw128(bb + kk * 32, 16, 1024),
-                    C::IDESC, kk > 0 ? 1u : 0u);
-          tc::mma_commit(&t_full[buf * 2 + t]);
-          tc::mma_commit(&b_empty[s]);
+            tc::mma_f16_elect(d, ad0 + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), C::IDESC, kk > 0 ? 1u : 0u);
+          tc::mma_commit_elect(bar_tf + 16 * buf);
+          tc::mma_commit_elect(bar_be + 8 * s);
         }
-        tc::mma_commit(a_empty);
+        tc::mma_commit_elect(bar_ae);
       }
       PROF_ADD(4, tot);
     }
@@ -419,6 +438,9 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
     const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + t * C::BN + hf * C::COLS;
     const uint32_t tf_bar = tc::smem_u32(&t_full[t]), te_bar = tc::smem_u32(&t_empty[t]);  // + buf * 16
     const int n_k32 = (int)n_k;
+#ifdef SCB_KNN_LAZY
+    const int last_valid = n_k32 - (n_kt - 1) * C::BN - hf * C::COLS;  // valid keys of the last tile's slice
+#endif
     int it = 0;
     PROF_T0(tot);
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -441,16 +463,26 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         Qi[j] = -1;
       }
       const int64_t row = (int64_t)(pair * 2 + t) * C::BM + 32 * q + lane;
+#ifdef SCB_KNN_LAZY
+      const int jl = last_valid < C::COLS ? outward_pos(st, n_kt - 1, n_kt) : -1;
+#endif
       for (int i = U.i0; i < U.i1; ++i, ++it) {
+#ifndef SCB_KNN_LAZY
         const int kt = outward_tile(st, i, n_kt);
+#endif
         const int buf = it & 1;
         PROF_T0(w0);
         tc::mbar_wait_a(tf_bar + buf * 16, (it >> 1) & 1);
         PROF_ADD(0, w0);
         tc::tc_fence_after();
+#ifndef SCB_KNN_LAZY
         const int key0 = kt * C::BN + hf * C::COLS;
         const int valid = n_k32 - key0;  // < COLS only in the last tile (padding keys)
+#endif
         const uint32_t tb = tl + buf * (2 * C::BN);
+#ifdef SCB_KNN_MMA_ONLY  // experiment: no epilogue work (tensor pipe + TMA bound)
+        if (buf > 1)
+#endif
 #pragma unroll 1
         for (int c = 0; c < C::COLS / 32; ++c) {
           const uint32_t ta = tb + c * 32;
@@ -462,8 +494,13 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+#ifdef SCB_KNN_LAZY
+          if (i == jl) {  // padding keys of the last tile
+            const int lim = last_valid - c * 32;
+#else
           const int lim = valid - c * 32;
           if (lim < 32) {
+#endif
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (j >= lim) v[j] = INFINITY;
@@ -474,6 +511,9 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
             // column per lane) and goes to the lane's small queue; a full queue on ANY lane
             // merges every lane's queue at once.
             PROF_T0(w3);
+#ifdef SCB_KNN_LAZY
+            const int key0 = outward_tile(st, i, n_kt) * C::BN + hf * C::COLS;
+#endif
             uint32_t mask = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) mask |= (v[j] < thr) ? (1u << j) : 0u;

@@ -26,6 +26,26 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+#ifdef SCB_MBAR_WATCHDOG
+// debug builds: bounded waits that report the stuck barrier and trap
+__device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_wd(uint32_t a, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!mbar_try(a, parity))
+    if (clock64() - t0 > (4ll << 30)) {  // ~2 s
+      printf("mbar watchdog: block %d thread %d barrier smem 0x%x parity %u\n", blockIdx.x, threadIdx.x, a, parity);
+      __trap();
+    }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_wd(smem_u32(bar), parity); }
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) { mbar_wait_wd(a, parity); }
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   asm volatile(
@@ -39,6 +59,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 // variants on a precomputed shared-window address (hot loops: no generic->shared conversion)
+#ifdef SCB_MBAR_HINT
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {  // suspend up to ~SCB_MBAR_HINT ns per try
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity), "n"(SCB_MBAR_HINT)
+      : "memory");
+}
+#else
 __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -50,6 +83,8 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
+#endif
 __device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
@@ -137,6 +172,28 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn_major, bool b_mn_major) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// Warp-converged issue: every lane runs the issuing loop (so descriptors and addresses stay in
+// the uniform datapath) and elect.sync picks the one lane that issues the MMA / commit.
+__device__ __forceinline__ void mma_f16_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_elect(uint32_t bar_smem) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(bar_smem)
+      : "memory");
 }
 // arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
