@@ -435,12 +435,15 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int t = (e >> 2) & 1;        // query tile of the pair
     const int hf = e >> 3;             // key-column slice of each tile (HALVES == 2)
-    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + t * C::BN + hf * C::COLS;
-    const uint32_t tf_bar = tc::smem_u32(&t_full[t]), te_bar = tc::smem_u32(&t_empty[t]);  // + buf * 16
+    // Opaque copies (asm moves): the compiler must keep these in registers instead of
+    // rematerialising the shared-window / TMEM address arithmetic every tile -- at 96 registers
+    // it otherwise recomputes them on the ALU pipe, which the min filter already saturates.
+    uint32_t tl, tf_bar, te_bar;  // + buf * 2 * BN / + buf * 16
+    asm volatile("mov.b32 %0, %1;" : "=r"(tl) : "r"(tmem + ((uint32_t)(32 * q) << 16) + t * C::BN + hf * C::COLS));
+    asm volatile("mov.b32 %0, %1;" : "=r"(tf_bar) : "r"(tc::smem_u32(&t_full[t])));
+    asm volatile("mov.b32 %0, %1;" : "=r"(te_bar) : "r"(tc::smem_u32(&t_empty[t])));
     const int n_k32 = (int)n_k;
-#ifdef SCB_KNN_LAZY
     const int last_valid = n_k32 - (n_kt - 1) * C::BN - hf * C::COLS;  // valid keys of the last tile's slice
-#endif
     int it = 0;
     PROF_T0(tot);
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -463,27 +466,18 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         Qi[j] = -1;
       }
       const int64_t row = (int64_t)(pair * 2 + t) * C::BM + 32 * q + lane;
-#ifdef SCB_KNN_LAZY
       const int jl = last_valid < C::COLS ? outward_pos(st, n_kt - 1, n_kt) : -1;
-#endif
       for (int i = U.i0; i < U.i1; ++i, ++it) {
-#ifndef SCB_KNN_LAZY
-        const int kt = outward_tile(st, i, n_kt);
-#endif
         const int buf = it & 1;
         PROF_T0(w0);
         tc::mbar_wait_a(tf_bar + buf * 16, (it >> 1) & 1);
         PROF_ADD(0, w0);
         tc::tc_fence_after();
-#ifndef SCB_KNN_LAZY
-        const int key0 = kt * C::BN + hf * C::COLS;
-        const int valid = n_k32 - key0;  // < COLS only in the last tile (padding keys)
-#endif
         const uint32_t tb = tl + buf * (2 * C::BN);
 #ifdef SCB_KNN_MMA_ONLY  // experiment: no epilogue work (tensor pipe + TMA bound)
         if (buf > 1)
 #endif
-#pragma unroll 1
+#pragma unroll
         for (int c = 0; c < C::COLS / 32; ++c) {
           const uint32_t ta = tb + c * 32;
           uint32_t r[32];
@@ -494,13 +488,8 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-#ifdef SCB_KNN_LAZY
           if (i == jl) {  // padding keys of the last tile
             const int lim = last_valid - c * 32;
-#else
-          const int lim = valid - c * 32;
-          if (lim < 32) {
-#endif
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (j >= lim) v[j] = INFINITY;
@@ -511,9 +500,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
             // column per lane) and goes to the lane's small queue; a full queue on ANY lane
             // merges every lane's queue at once.
             PROF_T0(w3);
-#ifdef SCB_KNN_LAZY
             const int key0 = outward_tile(st, i, n_kt) * C::BN + hf * C::COLS;
-#endif
             uint32_t mask = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) mask |= (v[j] < thr) ? (1u << j) : 0u;
@@ -540,7 +527,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         }
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive_a(te_bar + buf * 16);
+        tc::mbar_arrive_elect(te_bar + buf * 16);
       }
       queue_merge<KC>(L, I, Qv, Qi, qn);
       if (row < n_q) {

@@ -85,6 +85,10 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
 }
 #endif
 #endif
+__device__ __forceinline__ void mbar_arrive_elect(uint32_t a) {  // one elected lane of a converged warp
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(a)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
