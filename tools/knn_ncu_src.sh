@@ -13,8 +13,8 @@ E = r.pca.X_pca.contiguous(); del X, r; torch.cuda.empty_cache()
 idx, dist = pp.neighbors(E, 15, n_comps=50); torch.cuda.synchronize(); print("ok")
 PY
 timeout 900 ncu --section SourceCounters --section WarpStateStats --section InstructionStats --section ComputeWorkloadAnalysis \
-  --import-source on --clock-control none -k regex:knn_candidates -c 1 -o gpurun_out/s3/knn_src3 -f python /tmp/knn_lists_once.py > gpurun_out/s3/knn_src.log 2>&1
+  --import-source on --clock-control none -k regex:knn_candidates -c 1 -o gpurun_out/s3/knn_src4 -f python /tmp/knn_lists_once.py > gpurun_out/s3/knn_src.log 2>&1
 echo "ncu rc $?"; tail -3 gpurun_out/s3/knn_src.log
-ncu -i gpurun_out/s3/knn_src3.ncu-rep --page details --csv > gpurun_out/s3/knn_src3_details.csv 2>&1
-ncu -i gpurun_out/s3/knn_src3.ncu-rep --page source --csv --print-source sass > gpurun_out/s3/knn_src3_sass.csv 2>&1
+ncu -i gpurun_out/s3/knn_src4.ncu-rep --page details --csv > gpurun_out/s3/knn_src4_details.csv 2>&1
+ncu -i gpurun_out/s3/knn_src4.ncu-rep --page source --csv --print-source sass > gpurun_out/s3/knn_src4_sass.csv 2>&1
 ls -la gpurun_out/s3/
