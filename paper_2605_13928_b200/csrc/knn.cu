@@ -504,9 +504,11 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
             // merges every lane's queue at once.
             PROF_T0(w3);
             const int key0 = outward_tile(st, i, n_kt) * C::BN + hf * C::COLS;
+            // bit j = sign of v[j] - thr (FADD on the FMA pipe, one funnel shift per column);
+            // v == thr gives +0 (bit clear), as v < thr requires
             uint32_t mask = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) mask |= (v[j] < thr) ? (1u << j) : 0u;
+            for (int j = 31; j >= 0; --j) mask = __funnelshift_l(__float_as_uint(v[j] - thr), mask, 1);
             uint32_t cm = __reduce_or_sync(0xffffffffu, mask);
             while (cm) {
               const int j = __ffs(cm) - 1;
