@@ -480,7 +480,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
 #ifdef SCB_KNN_MMA_ONLY  // experiment: no epilogue work (tensor pipe + TMA bound)
         if (buf > 1)
 #endif
-#pragma unroll
+#pragma unroll(C::COLS / 32 <= 2 ? C::COLS / 32 : 1)  // k > 16 (128-column lists): 4 chunks, not unrolled
         for (int c = 0; c < C::COLS / 32; ++c) {
           const uint32_t ta = tb + c * 32;
           uint32_t r[32];

@@ -17,7 +17,7 @@ sig = torch.linspace(4.0, 0.6, 50, device="cuda")
 centers = torch.randn(30, 50, device="cuda", generator=g) * sig * 1.5
 lab = torch.randint(0, 30, (n,), device="cuda", generator=g)
 X = (centers[lab] + torch.randn(n, 50, device="cuda", generator=g) * sig * 0.6).contiguous()
-for k in (15, 30):
+for k in [int(v) for v in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["15", "30"])]:
     for rep in range(2):
         t = (torch.cuda.Event(True), torch.cuda.Event(True))
         a, b = torch.cuda.Event(True), torch.cuda.Event(True)
