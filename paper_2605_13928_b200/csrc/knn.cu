@@ -10,17 +10,21 @@
 //    with s = max|X|/16 so everything fits FP16; one K=64 dot product gives the
 //    query-invariant score (d^2 - |q|^2)/s^2 with the 11-bit significands of TF32.
 // 3. candidates (tcgen05.mma.kind::f16, FP32 accumulate in TMEM): a persistent CTA owns a
-//    PAIR of 128-query tiles (smem-resident) and streams 128-key tiles through an 8-stage TMA
-//    pipeline.  Two MMA-issuing threads alternate key tiles (a tcgen05.commit stalls its
-//    issuer until the pipe drains, so one issuer leaves the tensor pipe idle ~45% of the
-//    time); each issues 2 x 4 MMAs (128x128x16) per key tile into its own half of a
-//    double-buffered accumulator (512 TMEM columns).  Epilogue warps own one query row per
+//    PAIR of 128-query tiles (smem-resident) and streams 128-key tiles through a 12-stage TMA
+//    pipeline.  Two MMA-issuing warps, one per query tile (a tcgen05.commit stalls its issuer
+//    until the pipe drains, so one issuer leaves the tensor pipe idle ~45% of the time), run
+//    warp-converged loops and let one elected lane issue each of the 4 MMAs (128x128x16) per
+//    key tile into the query tile's double-buffered accumulator (2 x 2 x 128 = 512 TMEM
+//    columns); producer and issuers sit on the highest warp ids.  Epilogue warps own one query row per
 //    lane and COLS = 128/HALVES key columns of every tile, keep a register-resident sorted
 //    top-KC list behind a 32-wide min filter, and re-read the few passing columns straight
 //    from TMEM (tcgen05.ld x1) instead of staging scores through shared memory.  With
 //    HALVES = 2 (k_cand 32) sixteen epilogue warps, four per SM sub-partition, hide the
 //    TMEM-load and vote latencies; the two half-lists of a row are concatenated (the top-k
-//    of the union is contained in the union of the per-half top-KC for k <= KC).
+//    of the union is contained in the union of the per-half top-KC for k <= KC).  The fast
+//    path per 32-column chunk is LDTM + 16 FMNMX3 + vote on the ALU pipe, which bounds the
+//    epilogue: addresses live in opaque registers (no per-tile rematerialisation) and key ids
+//    are only computed on the rare path.
 // 4. rerank: one warp per query recomputes exact FP32 squared distances of the k_cand
 //    candidates, sorts by (distance, original index) and keeps k (self included).
 #include <cstdlib>
