@@ -5,7 +5,7 @@ set -u
 O=${OUT:-gpurun_out/r02/final}
 mkdir -p $O
 make -C paper_2605_13928_b200/csrc -j16 > $O/build.log 2>&1 && make -C oracle >> $O/build.log 2>&1 || { tail -30 $O/build.log; exit 1; }
-timeout 1200 python bench.py --steps 10 --warmup 3 > $O/bench.json 2> $O/bench.err; echo "bench rc $?" >> $O/bench.err
+timeout 1200 python bench.py --steps ${STEPS:-10} --warmup ${WARMUP:-3} > $O/bench.json 2> $O/bench.err; echo "bench rc $?" >> $O/bench.err
 timeout 1200 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc $?" >> $O/bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
   python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_launches.log 2>&1; echo "ncu1 rc $?" >> $O/ncu_launches.log
