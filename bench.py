@@ -153,11 +153,17 @@ def cpu_c3_estimate(host_csr, mt, n_cells: int, keys, queries, args, workers: in
 
 def _cpu_line(est, cores, n_cells, G, k, n_keys):
     return {"value": est["value"], "unit": "cells/s", "cores": cores, "kind": "port",
-            "sample": (f"extrapolated to C3: oracle stages QC..PCA on {est['rows']} cells x {G} genes "
+            "sample": (f"{'extrapolated to' if max(n_cells / est['rows'], n_cells / est['queries']) > 1.01 else 'full run of'} "
+                       f"{_cfg_name(n_cells, G)}: oracle stages QC..PCA on {est['rows']} cells x {G} genes "
                        f"({est['t_stages_s']:.2f} s, x{n_cells / est['rows']:.0f}) + exact fp64 kNN (k={k}) of "
                        f"{est['queries']} queries against {n_keys} keys ({est['t_knn_s']:.2f} s, "
-                       f"x{n_cells / est['queries']:.0f}) = {est['t_c3_s']:.0f} s per C3 step; oracle/chunked.py "
+                       f"x{n_cells / est['queries']:.0f}) = {est['t_c3_s']:.0f} s per {_cfg_name(n_cells, G)} step; oracle/chunked.py "
                        f"on {cores} host cores")}
+
+
+def _cfg_name(N, G):
+    """BASELINE.json config label of a (cells, genes) workload."""
+    return {(1_000_000, 25_000): "C3", (100_000, 20_000): "C2", (10_000, 2_000): "C1"}.get((N, G), "custom")
 
 
 def bench_reference(args, rank, world):
@@ -208,7 +214,7 @@ def bench_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (numpy)",
         "data": "synthetic NB counts (oracle/synth.py model, CPU generator oracle/csynth.c, seed %d)" % args.seed,
-        "config": {"workload": f"C3: {N} cells x {G} genes, full QC->normalize->log1p->HVG(seurat,{args.hvg})->scale->"
+        "config": {"workload": f"{_cfg_name(N, G)}: {N} cells x {G} genes, full QC->normalize->log1p->HVG(seurat,{args.hvg})->scale->"
                                f"PCA(50)->kNN(k={args.k}, exact fp64) -- extrapolated from a bounded sample per step",
                    "cells": N, "genes": G, "sample_cells": args.ref_sample, "queries_per_step": args.ref_queries,
                    "gen_seconds": round(gen_s, 1)},
@@ -487,7 +493,7 @@ def main():
                                   "sums, fp64 slice sums", "eig": "f64", "projection": "3xTF32 tcgen05",
                           "knn": "FP16 tcgen05 candidate scores + FP32 exact re-rank"},
             "data": "synthetic NB counts generated on device (oracle/synth.py model, seed %d)" % args.seed,
-            "config": {"workload": f"C3: {N} cells x {G} genes (~{Z_total / N / G:.1%} dense), full QC->normalize->"
+            "config": {"workload": f"{_cfg_name(N, G)}: {N} cells x {G} genes (~{Z_total / N / G:.1%} dense), full QC->normalize->"
                                    f"log1p->HVG(seurat,{args.hvg})->{'regress_out+' if args.regress_out else ''}scale->PCA(50)->"
                                    f"kNN(k={args.k}, {KNN_LABEL}){'+umap graph' if args.graph or args.umap or args.cluster or args.de else ''}{'+umap layout' if args.umap else ''}{'+leiden' if args.cluster or args.de else ''}{'+rank_genes_groups' if args.de else ''}",
                        "cells": N, "genes": G, "nnz": int(Z_total), "kept_cells": int(n_keys), "hvg": H,
