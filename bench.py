@@ -241,8 +241,9 @@ def main():
     ap.add_argument("--ref-queries", type=int, default=1000, help="kNN queries per reference-arm step")
     ap.add_argument("--input", default="f32", choices=["u16", "f32"],
                     help="device-resident CSR layout of the timed step: int32/float32 or the compact u16 form")
-    ap.add_argument("--wire", default="u16", choices=["u16", "f32"],
-                    help="host->device layout of the e2e leg: compact u16 (decoded on the device) or int32/float32")
+    ap.add_argument("--wire", default="delta8", choices=["delta8", "u16", "f32"],
+                    help="host->device layout of the e2e leg: byte-delta (2 B/nnz) or compact u16 (4 B/nnz), both "
+                         "decoded on the device, or int32/float32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", action="store_true",
@@ -265,7 +266,7 @@ def main():
     import torch.distributed as td
     from paper_2605_13928_b200 import _lib, pipeline, synth
     from paper_2605_13928_b200.dist import Comm, row_shards_from_counts
-    from paper_2605_13928_b200.pp import DeviceCSR
+    from paper_2605_13928_b200.pp import DeltaCSR, DeviceCSR
 
     local = local % max(1, torch.cuda.device_count())  # (functional multi-rank check on one GPU)
     torch.cuda.set_device(local)
@@ -401,8 +402,13 @@ def main():
     e2e = None
     if not args.no_e2e:
         wire_u16 = args.wire == "u16"
-        Xw = X.to_u16() if wire_u16 else X.to_f32()
-        arrs = [Xw.indptr, Xw.indices, Xw.data] + ([Xw.esc_pos, Xw.esc_val] if wire_u16 else [])
+        wire_d8 = args.wire == "delta8"
+        if wire_d8:
+            Xw = DeltaCSR.from_csr(X)
+            arrs = Xw.tensors()
+        else:
+            Xw = X.to_u16() if wire_u16 else X.to_f32()
+            arrs = [Xw.indptr, Xw.indices, Xw.data] + ([Xw.esc_pos, Xw.esc_val] if wire_u16 else [])
         h_arrs = [torch.empty_like(t, device="cpu").pin_memory() for t in arrs]
         for h, t in zip(h_arrs, arrs):
             h.copy_(t)
@@ -414,9 +420,9 @@ def main():
         o_d = torch.empty((N_sub_loc, k), dtype=torch.float32).pin_memory()
         # decode targets (32-bit CSR in HBM), one per step in flight: the decode of step i+1 runs on
         # the copy stream right after its H2D, overlapping the compute of step i
-        Xds = [DeviceCSR(Xw.indptr, torch.empty(Xw.nnz, dtype=torch.int32, device=Xw.indices.device),
-                         torch.empty(Xw.nnz, dtype=torch.float32, device=Xw.indices.device), G)
-               for _ in range(2)] if wire_u16 else None
+        Xds = [DeviceCSR(Xw.indptr, torch.empty(Xw.nnz, dtype=torch.int32, device=arrs[1].device),
+                         torch.empty(Xw.nnz, dtype=torch.float32, device=arrs[1].device), G)
+               for _ in range(2)] if (wire_u16 or wire_d8) else None
         del X, Xw, arrs
         torch.cuda.empty_cache()
         comp = torch.cuda.current_stream()
@@ -434,7 +440,9 @@ def main():
                     cs.wait_event(consumed[j])  # step i-2 is done with buffer set j
                 for dst, src in zip(b, h_arrs):
                     dst.copy_(src, non_blocking=True)
-                if wire_u16:
+                if wire_d8:
+                    inputs[j] = DeltaCSR.from_tensors(b, G).to_f32(out=Xds[j])
+                elif wire_u16:
                     inputs[j] = DeviceCSR(b[0], b[1], b[2], G, esc_pos=b[3], esc_val=b[4]).to_f32(out=Xds[j])
                 else:
                     inputs[j] = DeviceCSR(b[0], b[1], b[2], G)
@@ -475,7 +483,10 @@ def main():
         e2e = {"value": N / (e_ms / 1e3), "unit": "cells/s", "ms_per_step": round(e_ms, 3),
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
                "h2d_GBps_measured": round(h2d_bytes / (first_copy_ms / 1e3) / 1e9, 1),  # (incl. the first decode)
-               "wire_format": ("compact u16 CSR (uint16 gene indices + uint16 counts + escape table), decoded on "
+               "wire_format": ("byte-delta CSR (1-byte gene-index delta + 1-byte count per nonzero, escape tables), "
+                               "decoded on the device each step (scb_csr_delta8_decode, inside the timed region)")
+                              if wire_d8 else
+                              ("compact u16 CSR (uint16 gene indices + uint16 counts + escape table), decoded on "
                                "the device each step (scb_csr_u16_decode, inside the timed region)") if wire_u16
                               else "int32/float32 CSR",
                "overlap": "pinned H2D (+ device decode) of step i+1 on a copy stream and the D2H of step i-1's graph "

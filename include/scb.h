@@ -220,6 +220,17 @@ SCB_API int scb_csr_u16_decode(scb_ctx* ctx, const uint16_t* indices16, const ui
                                const int64_t* esc_pos, const float* esc_val, int64_t n_esc, int32_t* indices,
                                float* data, void* stream);
 
+/* ---- f1 wire decode: byte-delta CSR -> int32 indices + float32 counts in HBM.  Per nonzero one
+ * byte dgene = g - g_prev - 1 (g_prev = -1 at a row start; 255 = escape: the delta is
+ * gesc_val at the sorted position gesc_pos) and one byte dcount = the count (255 = escape:
+ * cesc_val at cesc_pos); rows as indptr (sorted, unique gene indices within a row).  2 B on the
+ * wire per nonzero instead of 4 (u16) or 8 (int32 + float32); lossless (pp.DeltaCSR). */
+SCB_API int scb_csr_delta8_decode(scb_ctx* ctx, const int64_t* indptr, int64_t n_rows, const uint8_t* dgene,
+                                  const uint8_t* dcount, int64_t nnz, const int64_t* gesc_pos,
+                                  const int32_t* gesc_val, int64_t n_gesc, const int64_t* cesc_pos,
+                                  const float* cesc_val, int64_t n_cesc, int32_t* indices, float* data,
+                                  void* stream);
+
 /* ---- a5: sc.pp.highly_variable_genes(flavor="seurat", n_top_genes, n_bins) from the
  * (all-reduced) gene sums.  Outputs per gene: means, variances, dispersions (log),
  * dispersions_norm, mean_bin; hvg_mask; hvg_index = sorted selected genes (int32[n_cols]

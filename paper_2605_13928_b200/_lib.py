@@ -86,6 +86,8 @@ SIGNATURES = {
     "scb_hvg_gene_sums_u16": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr,
                               c_i64, c_ptr],
     "scb_csr_u16_decode": [c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_ptr],
+    "scb_csr_delta8_decode": [c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64,
+                              c_ptr, c_ptr, c_ptr],
     "scb_scale_dense_planes": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_dbl, c_dbl,
                                c_ptr, c_ptr, c_i64, c_i32, c_ptr],
     "scb_project_planes": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_i32, c_ptr],

@@ -452,3 +452,69 @@ extern "C" int scb_csr_u16_decode(scb_ctx* ctx, const uint16_t* indices16, const
   }
   return SCB_OK;
 }
+
+// ------------------------------------------------------------------ f1 wire decode: byte-delta CSR
+namespace scb {
+// index of position k in a sorted escape-position table (k is known to be present)
+__device__ __forceinline__ int64_t esc_find(const int64_t* __restrict__ pos, int64_t n, int64_t k) {
+  int64_t lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (pos[m] < k) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
+// warp per row: gene index = previous + 1 + byte delta (255: the delta is in the gene escape
+// table), count = byte (255: value in the count escape table); a warp scan carries the gene
+// index across each 32-element window (coalesced byte loads, 128-byte stores)
+__global__ void delta8_decode_kernel(const int64_t* __restrict__ indptr, int64_t n_rows,
+                                     const uint8_t* __restrict__ dgene, const uint8_t* __restrict__ dcount,
+                                     const int64_t* __restrict__ gpos, const int32_t* __restrict__ gval, int64_t n_g,
+                                     const int64_t* __restrict__ cpos, const float* __restrict__ cval, int64_t n_c,
+                                     int32_t* __restrict__ indices, float* __restrict__ data) {
+  const int lane = lane_id();
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    int carry = -1;
+    for (int64_t base = b; base < e; base += 32) {
+      const int64_t k = base + lane;
+      const bool ok = k < e;
+      const int dc = ok ? (int)__ldg(dgene + k) : 0;
+      const int cc = ok ? (int)__ldg(dcount + k) : 0;
+      int inc = ok ? dc + 1 : 0;
+      if (ok && dc == 255) inc = gval[esc_find(gpos, n_g, k)] + 1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      const int g = carry + inc;
+      carry = __shfl_sync(0xffffffffu, g, 31);
+      if (ok) {
+        indices[k] = g;
+        data[k] = cc == 255 ? cval[esc_find(cpos, n_c, k)] : (float)cc;
+      }
+    }
+  }
+}
+}  // namespace scb
+
+extern "C" int scb_csr_delta8_decode(scb_ctx* ctx, const int64_t* indptr, int64_t n_rows, const uint8_t* dgene,
+                                     const uint8_t* dcount, int64_t nnz, const int64_t* gesc_pos,
+                                     const int32_t* gesc_val, int64_t n_gesc, const int64_t* cesc_pos,
+                                     const float* cesc_val, int64_t n_cesc, int32_t* indices, float* data,
+                                     void* stream) {
+  using namespace scb;
+  SCB_REQUIRE(ctx && indptr && (nnz == 0 || (dgene && dcount && indices && data)), SCB_ERR_ARG,
+              "scb_csr_delta8_decode: null argument");
+  SCB_REQUIRE((n_gesc == 0 || (gesc_pos && gesc_val)) && (n_cesc == 0 || (cesc_pos && cesc_val)), SCB_ERR_ARG,
+              "scb_csr_delta8_decode: escape table missing");
+  if (n_rows == 0 || nnz == 0) return SCB_OK;
+  const int g = (int)std::min<int64_t>((int64_t)ctx->num_sms * 8, (n_rows + 7) / 8);
+  delta8_decode_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(indptr, n_rows, dgene, dcount, gesc_pos, gesc_val, n_gesc,
+                                                            cesc_pos, cesc_val, n_cesc, indices, data);
+  SCB_LAUNCH_CHECK();
+  return SCB_OK;
+}

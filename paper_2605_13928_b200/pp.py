@@ -135,6 +135,91 @@ class DeviceCSR:
         return DeviceCSR(self.indptr, ind, dat, self.n_cols)
 
 
+@dataclasses.dataclass
+class DeltaCSR:
+    """Byte-delta CSR, the densest lossless host->device wire form: per nonzero one byte ``dgene``
+    = g - g_prev - 1 (g_prev = -1 at a row start) and one byte ``dcount`` = the count, each 255
+    meaning "escaped" with the true delta / count in a sorted (position, value) table.  2 B per
+    nonzero (u16: 4 B, int32 + float32: 8 B); ``to_f32`` decodes it in HBM (scb_csr_delta8_decode)."""
+
+    indptr: torch.Tensor
+    dgene: torch.Tensor
+    dcount: torch.Tensor
+    gesc_pos: torch.Tensor
+    gesc_val: torch.Tensor
+    cesc_pos: torch.Tensor
+    cesc_val: torch.Tensor
+    n_cols: int
+
+    @property
+    def n_rows(self) -> int:
+        return self.indptr.numel() - 1
+
+    @property
+    def nnz(self) -> int:
+        return self.dgene.numel()
+
+    def tensors(self):
+        return [self.indptr, self.dgene, self.dcount, self.gesc_pos, self.gesc_val, self.cesc_pos, self.cesc_val]
+
+    @staticmethod
+    def from_tensors(ts, n_cols: int) -> "DeltaCSR":
+        return DeltaCSR(*ts, n_cols=n_cols)
+
+    @staticmethod
+    def from_csr(X: "DeviceCSR", chunk: int = 1 << 28) -> "DeltaCSR":
+        """Encode a 32-bit (or u16) CSR (any device; torch ops).  Needs sorted, unique gene indices
+        within each row and non-negative integer counts < 2^24 (ValueError otherwise)."""
+        if X.is_u16:
+            X = X.to_f32()
+        dev, Z = X.indices.device, X.nnz
+        ip = X.indptr
+        row_start = torch.zeros(Z + 1, dtype=torch.bool, device=dev)
+        row_start[ip[:-1]] = True  # (empty rows point at the next row's start: also a start)
+        dg = torch.empty(Z, dtype=torch.uint8, device=dev)
+        dc = torch.empty(Z, dtype=torch.uint8, device=dev)
+        gpos, gval, cpos, cval = [], [], [], []
+        for a in range(0, Z, chunk):
+            b = min(Z, a + chunk)
+            g = X.indices[a:b].to(torch.int32)
+            prev = torch.empty_like(g)
+            prev[1:] = g[:-1]
+            prev[0] = X.indices[a - 1] if a > 0 else -1
+            prev = torch.where(row_start[a:b], torch.full_like(g, -1), prev)
+            delta = g - prev - 1
+            if bool((delta < 0).any()):
+                raise ValueError("delta CSR needs sorted, unique gene indices within each row")
+            esc = delta > 254
+            dg[a:b] = torch.where(esc, torch.full_like(delta, 255), delta).to(torch.uint8)
+            idx = torch.nonzero(esc).view(-1)
+            gpos.append(idx.to(torch.int64) + a)
+            gval.append(delta[idx].to(torch.int32))
+            d = X.data[a:b]
+            bad = torch.stack([(d < 0).any(), (d >= 16777216).any(), (d != torch.round(d)).any()])
+            if bool(bad.any()):
+                raise ValueError("delta CSR needs non-negative integer counts < 2^24")
+            cesc = d >= 255
+            dc[a:b] = torch.clamp(d, max=255.0).to(torch.int32).to(torch.uint8)
+            idx = torch.nonzero(cesc).view(-1)
+            cpos.append(idx.to(torch.int64) + a)
+            cval.append(d[idx].to(torch.float32))
+        cat = lambda xs, dt: torch.cat(xs) if xs else torch.empty(0, dtype=dt, device=dev)  # noqa: E731
+        return DeltaCSR(ip, dg, dc, cat(gpos, torch.int64), cat(gval, torch.int32), cat(cpos, torch.int64),
+                        cat(cval, torch.float32), X.n_cols)
+
+    def to_f32(self, out: Optional["DeviceCSR"] = None) -> "DeviceCSR":
+        """The 32-bit CSR in HBM (one pass: 2 B read + 8 B written per nonzero); ``out`` =
+        preallocated 32-bit arrays to decode into."""
+        nnz = self.nnz
+        dev = self.dgene.device
+        ind = out.indices if out is not None else torch.empty(nnz, dtype=torch.int32, device=dev)
+        dat = out.data if out is not None else torch.empty(nnz, dtype=torch.float32, device=dev)
+        _lib.call("scb_csr_delta8_decode", _ctx(self.dgene), _p(self.indptr), self.n_rows, _p(self.dgene),
+                  _p(self.dcount), nnz, _p(self.gesc_pos), _p(self.gesc_val), int(self.gesc_pos.numel()),
+                  _p(self.cesc_pos), _p(self.cesc_val), int(self.cesc_pos.numel()), _p(ind), _p(dat), _stream(dev))
+        return DeviceCSR(self.indptr, ind, dat, self.n_cols)
+
+
 # ----------------------------------------------------------------------------- qc
 def calculate_qc_metrics(X: DeviceCSR, mt_mask: torch.Tensor, row_splits: bool = False, defer_check: bool = False):
     """sc.pp.calculate_qc_metrics(qc_vars=['mt'], percent_top=None, log1p=False).
