@@ -18,15 +18,19 @@ else:
     torch.save(E.cpu(), cache)
 torch.cuda.empty_cache()
 Ep = torch.zeros((E.shape[0], 64), device="cuda"); Ep[:, :50] = E
-ms = []
+ms, tot = [], []
 for _ in range(reps):
     t = (torch.cuda.Event(True), torch.cuda.Event(True))
+    a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+    a.record()
     idx, dist = pp.neighbors(Ep, 15, n_comps=50, timer=t)
+    b.record()
     torch.cuda.synchronize()
     ms.append(round(t[0].elapsed_time(t[1]), 2))
+    tot.append(round(a.elapsed_time(b) - t[0].elapsed_time(t[1]), 2))
 ref = "/tmp/knn_ref_idx.pt"
 if os.path.exists(ref):
     agree = (torch.load(ref).cuda() == idx).float().mean().item()
 else:
     torch.save(idx.cpu(), ref); agree = 1.0
-print(f"[knn time] {label} {method}: cand ms {ms} agree_with_first {agree:.6f}", flush=True)
+print(f"[knn time] {label} {method}: cand ms {ms} rest ms {tot} agree_with_first {agree:.6f}", flush=True)
