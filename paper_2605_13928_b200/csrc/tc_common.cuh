@@ -59,19 +59,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 // variants on a precomputed shared-window address (hot loops: no generic->shared conversion)
-#ifdef SCB_MBAR_HINT
-__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {  // suspend up to ~SCB_MBAR_HINT ns per try
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(parity), "n"(SCB_MBAR_HINT)
-      : "memory");
-}
-#else
 __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -83,7 +70,6 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-#endif
 #endif
 __device__ __forceinline__ void mbar_arrive_elect(uint32_t a) {  // one elected lane of a converged warp
   asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(a)
