@@ -276,7 +276,10 @@ __device__ __forceinline__ void list_insert(float (&L)[KC], int (&I)[KC], float 
   }
 }
 
-constexpr int kQ = 4;  // per-lane pending queue in front of the sorted list
+#ifndef SCB_KNN_QUEUE
+#define SCB_KNN_QUEUE 2  // A/B at C3: 1 / 2 / 3 / 4 / 6 entries -> 127.9 / 115.6 / 117.1 / 119.0 / 122.3 ms
+#endif
+constexpr int kQ = SCB_KNN_QUEUE;  // per-lane pending queue in front of the sorted list
 
 // merge the pending queue into the sorted list (executed by the whole warp at once, so the
 // O(KC) insertions of different lanes share the same issue slots)

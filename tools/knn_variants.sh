@@ -10,9 +10,7 @@ for v in "$@"; do
   cp paper_2605_13928_b200/libscb_b200.so /tmp/scb_variants/$label.so
 done
 (cd paper_2605_13928_b200/csrc && rm -f build/knn.o && make -j16 > /dev/null 2>&1)
-cp paper_2605_13928_b200/libscb_headknn.so /tmp/scb_variants/head.so 2>/dev/null
 for r in $(seq 1 $rounds); do
-  [ -f /tmp/scb_variants/head.so ] && SCB_LIB_PATH=/tmp/scb_variants/head.so timeout 300 python tools/knn_time.py "head r$r" lists 3 2>&1 | grep "knn time\|Error" | tail -1
   for v in "$@"; do
     label="${v%%:*}"
     SCB_LIB_PATH=/tmp/scb_variants/$label.so timeout 300 python tools/knn_time.py "$label r$r" lists 3 2>&1 | grep "knn time\|Error" | tail -1
