@@ -71,7 +71,7 @@ __device__ __forceinline__ float o2f(int i) { return __int_as_float(i >= 0 ? i :
 #define SCB_KNN_ORDER_DIMS 4  // A/B at C3: PC1-2 / 1-3 / 1-4 -> 115.9 / 115.1 / 113.1 ms
 #endif
 constexpr int kOrderDims = SCB_KNN_ORDER_DIMS;  // Morton curve over PC1..PC<kOrderDims> (<= 4)
-static_assert(kOrderDims >= 1 && kOrderDims <= 4, "order dims");
+static_assert(kOrderDims >= 1 && kOrderDims <= 8, "order dims");
 
 __global__ void range_kernel(const float* __restrict__ X, int64_t n, int d, int ld, unsigned* __restrict__ amax,
                              int* __restrict__ omin, int* __restrict__ omax) {
@@ -696,8 +696,8 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   SCB_TRY(ws_get(ctx, 0, total, &ws, s));
   char* p = (char*)ws;
   unsigned* amax = (unsigned*)p;
-  int* omin = (int*)(p + 16);
-  int* omax = (int*)(p + 32);
+  int* omin = (int*)(p + 64);   // [kOrderDims] (<= 8)
+  int* omax = (int*)(p + 128);  // [kOrderDims]
   p += up(sz[0]);
   int* hist = (int*)p; p += up(sz[1]);
   int* perm_q = (int*)p; p += up(sz[2]);
@@ -710,8 +710,11 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   int* cand = (int*)p; p += up(sz[9]);
   int* cand_tail = (int*)p;
   // FP16 scale and the PC1 range come from the KEYS (queries are rows of the same embedding)
-  const int init[12] = {0, 0, 0, 0, 0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff, (int)0x80000000, (int)0x80000000,
-                        (int)0x80000000, (int)0x80000000};
+  int init[48] = {0};  // amax (+ pad) | omin[8] at +64 B | omax[8] at +128 B
+  for (int c = 0; c < 8; ++c) {
+    init[16 + c] = 0x7fffffff;
+    init[32 + c] = (int)0x80000000;
+  }
   SCB_CUDA(cudaMemcpyAsync(amax, init, sizeof(init), cudaMemcpyHostToDevice, s));
   const int g = std::max(1, std::min(1184, ceil_div(n_k, 256)));
   range_kernel<<<g, 256, 0, s>>>(Kx, n_k, d, ld, amax, omin, omax);
