@@ -11,7 +11,8 @@
 //    query-invariant score (d^2 - |q|^2)/s^2 with the 11-bit significands of TF32.
 // 3. candidates (tcgen05.mma.kind::f16, FP32 accumulate in TMEM): a persistent CTA owns a
 //    PAIR of 128-query tiles (smem-resident) and streams 128-key tiles through a 12-stage TMA
-//    pipeline.  Two MMA-issuing warps, one per query tile (a tcgen05.commit stalls its issuer
+//    pipeline; two CTAs of a cluster (adjacent pairs, one shared scan order) each load half of
+//    every key tile and multicast it into both rings.  Two MMA-issuing warps, one per query tile (a tcgen05.commit stalls its issuer
 //    until the pipe drains, so one issuer leaves the tensor pipe idle ~45% of the time), run
 //    warp-converged loops and let one elected lane issue each of the 4 MMAs (128x128x16) per
 //    key tile into the query tile's double-buffered accumulator (2 x 2 x 128 = 512 TMEM
@@ -337,12 +338,19 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
   return r;
 }
 
-template <int KC, int HALVES>
+// CL = 2: 2-CTA clusters.  The CTAs of a cluster own adjacent query pairs (2v, 2v+1) of cluster
+// unit v and share one outward scan order (from pair 2v's start); each CTA loads one half (64
+// keys) of every key tile and multicasts it into both CTAs' rings, and every MMA issuer releases
+// a stage in both CTAs (multicast commit), so each key byte leaves L2 once per cluster.
+template <int KC, int HALVES, int CL = 1>
 __global__ void __launch_bounds__(KnnCfg<KC, HALVES>::THREADS, 1)
 knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, int64_t n_q,
                       int64_t n_k, const int* __restrict__ start_tile, int* __restrict__ cand, int n_full,
                       int n_units, int* __restrict__ cand_tail) {
   using C = KnnCfg<KC, HALVES>;
+  static_assert(CL == 1 || CL == 2, "cluster size");
+  const int crank = CL == 2 ? (int)tc::cluster_rank() : 0;
+  const int unit0 = blockIdx.x / CL, unit_step = gridDim.x / CL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* a_base = smem;                          // [qtile][128 rows x 128 B]
@@ -367,7 +375,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       tc::mbar_init(a_empty, 2);  // one commit per MMA issuer
       for (int s = 0; s < C::STAGES; ++s) {
         tc::mbar_init(&b_full[s], 1);
-        tc::mbar_init(&b_empty[s], 2);  // both issuers read every stage
+        tc::mbar_init(&b_empty[s], 2 * CL);  // both issuers (of every CTA of the cluster) read every stage
       }
       for (int b = 0; b < 2 * C::NBUF; ++b) {
         tc::mbar_init(&t_full[b], 1);
@@ -380,6 +388,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   }
   tc::tc_fence_before();
   __syncthreads();
+  if (CL == 2) tc::cluster_sync();  // both CTAs' barriers initialised before any remote arrive / multicast
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   PROF_DECL;
@@ -390,10 +399,10 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   if (rw == 0) {
     if (lane == 0) {
       int it = 0, pc = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++pc) {
+      for (int u = unit0; u < n_units; u += unit_step, ++pc) {
         const KnnUnit U = knn_unit(u, n_full, n_kt);
-        const int pair = U.pair;
-        const int st = start_tile[pair];
+        const int pair = CL * U.pair + crank;
+        const int st = start_tile[CL * U.pair];
         tc::mbar_wait(a_empty, (pc & 1) ^ 1);
         tc::mbar_arrive_expect_tx(a_full, C::A_BYTES);
         for (int t = 0; t < 2; ++t) tc::tma_load_2d(a_base + t * C::TILE, &tq, a_full, 0, (pair * 2 + t) * C::BM);
@@ -402,7 +411,11 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
           const int s = it % C::STAGES;
           tc::mbar_wait(&b_empty[s], ((it / C::STAGES) & 1) ^ 1);
           tc::mbar_arrive_expect_tx(&b_full[s], C::B_BYTES);
-          tc::tma_load_2d(b_base + s * C::B_BYTES, &tk, &b_full[s], 0, kt * C::BN);
+          if (CL == 2)  // my half of the tile, into both CTAs (tk's box is 64 rows)
+            tc::tma_load_2d_mc(b_base + s * C::B_BYTES + crank * (C::B_BYTES / 2), &tk, &b_full[s], 0,
+                               kt * C::BN + crank * (C::BN / 2), (uint16_t)0x3);
+          else
+            tc::tma_load_2d(b_base + s * C::B_BYTES, &tk, &b_full[s], 0, kt * C::BN);
           ++it;
         }
       }
@@ -426,7 +439,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       const uint32_t bar_bf = tc::smem_u32(&b_full[0]), bar_te = tc::smem_u32(&t_empty[t]);
       const uint32_t bar_ae = tc::smem_u32(a_empty);
       int it = 0, pc = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++pc) {
+      for (int u = unit0; u < n_units; u += unit_step, ++pc) {
         const KnnUnit U = knn_unit(u, n_full, n_kt);
         tc::mbar_wait(a_full, pc & 1);
         for (int i = U.i0; i < U.i1; ++i, ++it) {
@@ -445,7 +458,10 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
           for (int kk = 0; kk < kD / 16; ++kk)  // K = 16 fp16 = 32 bytes per MMA
             tc::mma_f16_elect(d, ad0 + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), C::IDESC, kk > 0 ? 1u : 0u);
           tc::mma_commit_elect(bar_tf + 16 * buf);
-          tc::mma_commit_elect(bar_be + 8 * s);
+          if (CL == 2)
+            tc::mma_commit_mc_elect(bar_be + 8 * s, (uint16_t)0x3);  // release the stage in both CTAs
+          else
+            tc::mma_commit_elect(bar_be + 8 * s);
         }
         tc::mma_commit_elect(bar_ae);
       }
@@ -467,10 +483,10 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
     const int last_valid = n_k32 - (n_kt - 1) * C::BN - hf * C::COLS;  // valid keys of the last tile's slice
     int it = 0;
     PROF_T0(tot);
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    for (int u = unit0; u < n_units; u += unit_step) {
       const KnnUnit U = knn_unit(u, n_full, n_kt);
-      const int pair = U.pair;
-      const int st = start_tile[pair];
+      const int pair = CL * U.pair + crank;
+      const int st = start_tile[CL * U.pair];
       float L[KC];
       int I[KC];
       float Qv[kQ];
@@ -554,7 +570,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       }
       queue_merge<KC>(L, I, Qv, Qi, qn);
       if (row < n_q) {
-        const int64_t tail_row0 = (int64_t)n_full * 2 * C::BM;
+        const int64_t tail_row0 = (int64_t)n_full * CL * 2 * C::BM;
         int* o = U.tail ? cand_tail + (row - tail_row0) * (2 * C::KCT) + U.half * C::KCT + hf * KC
                         : cand + row * C::KCT + hf * KC;
 #pragma unroll
@@ -566,6 +582,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   PROF_FLUSH;
   tc::tc_fence_before();
   __syncthreads();
+  if (CL == 2) tc::cluster_sync();  // no CTA leaves while the other may still multicast into it
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
@@ -679,13 +696,40 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   const bool same = (Qx == Kx && n_q == n_k);
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
   const int64_t n_pairs = (n_q + 2 * Cfg::BM - 1) / (2 * Cfg::BM);
-  // final partial round: split its pairs' key scans in two when that fits one round (§ KnnUnit)
-  const int64_t G = std::min<int64_t>(n_pairs, ctx->num_sms);
-  const int64_t r = n_pairs % G;
-  const bool split = r > 0 && 2 * r <= G && 2 * KCT <= 64;
-  const int64_t n_full = split ? n_pairs - r : n_pairs;
-  const int64_t n_units = split ? n_full + 2 * r : n_pairs;
-  const int64_t tail_row0 = std::min<int64_t>(n_q, n_full * 2 * Cfg::BM);
+  // cluster mode (CL = 2): units are pairs of adjacent query pairs, one per 2-CTA cluster
+#ifndef SCB_KNN_CL
+#define SCB_KNN_CL 2  // A/B at C3: 117.5 vs 119.4 ms, DRAM reads 8.6 vs 17.8 GB (ncu)
+#endif
+  constexpr int CL = (SCB_KNN_CL == 2 && HALVES == 2) ? 2 : 1;
+  const int64_t n_sp = (n_pairs + CL - 1) / CL;  // cluster units
+  // final partial round: split its units' key scans in two when that fits one round (§ KnnUnit)
+  int max_clusters = ctx->num_sms / CL;
+  if (CL == 2) {  // co-resident 2-CTA clusters (GPCs with an odd SM count leave SMs idle)
+    cudaLaunchConfig_t oc = {};
+    oc.gridDim = dim3((unsigned)(2 * (ctx->num_sms / 2)));
+    oc.blockDim = dim3(Cfg::THREADS);
+    oc.dynamicSmemBytes = Cfg::SMEM;
+    cudaLaunchAttribute oa[1];
+    oa[0].id = cudaLaunchAttributeClusterDimension;
+    oa[0].val.clusterDim.x = 2;
+    oa[0].val.clusterDim.y = 1;
+    oa[0].val.clusterDim.z = 1;
+    oc.attrs = oa;
+    oc.numAttrs = 1;
+    SCB_CUDA(cudaFuncSetAttribute(knn_candidates_kernel<KC, HALVES, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Cfg::SMEM));
+    int nc = 0;
+    SCB_CUDA(cudaOccupancyMaxActiveClusters(&nc, knn_candidates_kernel<KC, HALVES, CL>, &oc));
+    if (nc > 0) max_clusters = std::min(max_clusters, nc);
+    if (getenv("SCB_KNN_DEBUG")) fprintf(stderr, "[knn] co-resident 2-CTA clusters: %d\n", nc);
+  }
+  const int64_t Gc = std::min<int64_t>(n_sp, max_clusters);
+  const int64_t G = Gc * CL;
+  const int64_t r = n_sp % Gc;
+  const bool split = r > 0 && 2 * r <= Gc && 2 * KCT <= 64;
+  const int64_t n_full = split ? n_sp - r : n_sp;
+  const int64_t n_units = split ? n_full + 2 * r : n_sp;
+  const int64_t tail_row0 = std::min<int64_t>(n_q, n_full * CL * 2 * Cfg::BM);
   const int64_t tail_rows = n_q - tail_row0;
   const size_t sz[] = {256, sizeof(int) * kBuckets, 4 * (size_t)n_q, 4 * (size_t)n_k, 4 * (size_t)n_q,
                        4 * (size_t)n_k, 4 * (size_t)n_pairs, (size_t)n_q * kD * 2, (size_t)n_k * kD * 2,
@@ -734,11 +778,28 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
   SCB_LAUNCH_CHECK();
   CUtensorMap tq, tk;
   SCB_TRY(make_tmap_2d(&tq, Qa, (uint64_t)n_q, kD, kD, 2, 64, Cfg::BM));
-  SCB_TRY(make_tmap_2d(&tk, Ka, (uint64_t)n_k, kD, kD, 2, 64, Cfg::BN));
-  auto kern = knn_candidates_kernel<KC, HALVES>;
+  SCB_TRY(make_tmap_2d(&tk, Ka, (uint64_t)n_k, kD, kD, 2, 64, Cfg::BN / CL));
+  auto kern = knn_candidates_kernel<KC, HALVES, CL>;
   SCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   if (ev0) SCB_CUDA(cudaEventRecord(ev0, s));
-  kern<<<(int)G, Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, n_q, n_k, start, cand, (int)n_full, (int)n_units, cand_tail);
+  if (CL == 1) {
+    kern<<<(int)G, Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, n_q, n_k, start, cand, (int)n_full, (int)n_units, cand_tail);
+  } else {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)G);
+    lc.blockDim = dim3(Cfg::THREADS);
+    lc.dynamicSmemBytes = Cfg::SMEM;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    SCB_CUDA(cudaLaunchKernelEx(&lc, kern, tq, tk, n_q, n_k, (const int*)start, cand, (int)n_full, (int)n_units,
+                                cand_tail));
+  }
   SCB_LAUNCH_CHECK();
   if (ev1) SCB_CUDA(cudaEventRecord(ev1, s));
 #ifdef SCB_KNN_PROF
