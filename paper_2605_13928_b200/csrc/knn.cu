@@ -348,8 +348,8 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
                       int64_t n_k, const int* __restrict__ start_tile, int* __restrict__ cand, int n_full,
                       int n_units, int* __restrict__ cand_tail) {
   using C = KnnCfg<KC, HALVES>;
-  static_assert(CL == 1 || CL == 2, "cluster size");
-  const int crank = CL == 2 ? (int)tc::cluster_rank() : 0;
+  static_assert(CL == 1 || CL == 2 || CL == 4, "cluster size");
+  const int crank = CL > 1 ? (int)tc::cluster_rank() : 0;
   const int unit0 = blockIdx.x / CL, unit_step = gridDim.x / CL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -388,7 +388,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (CL == 2) tc::cluster_sync();  // both CTAs' barriers initialised before any remote arrive / multicast
+  if (CL > 1) tc::cluster_sync();  // every CTA's barriers initialised before any remote arrive / multicast
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   PROF_DECL;
@@ -411,9 +411,9 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
           const int s = it % C::STAGES;
           tc::mbar_wait(&b_empty[s], ((it / C::STAGES) & 1) ^ 1);
           tc::mbar_arrive_expect_tx(&b_full[s], C::B_BYTES);
-          if (CL == 2)  // my half of the tile, into both CTAs (tk's box is 64 rows)
-            tc::tma_load_2d_mc(b_base + s * C::B_BYTES + crank * (C::B_BYTES / 2), &tk, &b_full[s], 0,
-                               kt * C::BN + crank * (C::BN / 2), (uint16_t)0x3);
+          if (CL > 1)  // my 1/CL of the tile, into every CTA of the cluster (tk's box is BN/CL rows)
+            tc::tma_load_2d_mc(b_base + s * C::B_BYTES + crank * (C::B_BYTES / CL), &tk, &b_full[s], 0,
+                               kt * C::BN + crank * (C::BN / CL), (uint16_t)((1u << CL) - 1u));
           else
             tc::tma_load_2d(b_base + s * C::B_BYTES, &tk, &b_full[s], 0, kt * C::BN);
           ++it;
@@ -458,8 +458,8 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
           for (int kk = 0; kk < kD / 16; ++kk)  // K = 16 fp16 = 32 bytes per MMA
             tc::mma_f16_elect(d, ad0 + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), C::IDESC, kk > 0 ? 1u : 0u);
           tc::mma_commit_elect(bar_tf + 16 * buf);
-          if (CL == 2)
-            tc::mma_commit_mc_elect(bar_be + 8 * s, (uint16_t)0x3);  // release the stage in both CTAs
+          if (CL > 1)
+            tc::mma_commit_mc_elect(bar_be + 8 * s, (uint16_t)((1u << CL) - 1u));  // release the stage in every CTA
           else
             tc::mma_commit_elect(bar_be + 8 * s);
         }
@@ -582,7 +582,7 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
   PROF_FLUSH;
   tc::tc_fence_before();
   __syncthreads();
-  if (CL == 2) tc::cluster_sync();  // no CTA leaves while the other may still multicast into it
+  if (CL > 1) tc::cluster_sync();  // no CTA leaves while another may still multicast into it
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
@@ -700,18 +700,18 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
 #ifndef SCB_KNN_CL
 #define SCB_KNN_CL 2  // A/B at C3: 117.5 vs 119.4 ms, DRAM reads 8.6 vs 17.8 GB (ncu)
 #endif
-  constexpr int CL = (SCB_KNN_CL == 2 && HALVES == 2) ? 2 : 1;
+  constexpr int CL = HALVES == 2 ? SCB_KNN_CL : 1;
   const int64_t n_sp = (n_pairs + CL - 1) / CL;  // cluster units
   // final partial round: split its units' key scans in two when that fits one round (§ KnnUnit)
   int max_clusters = ctx->num_sms / CL;
-  if (CL == 2) {  // co-resident 2-CTA clusters (GPCs with an odd SM count leave SMs idle)
+  if (CL > 1) {  // co-resident clusters (GPCs whose SM count is not a multiple of CL leave SMs idle)
     cudaLaunchConfig_t oc = {};
-    oc.gridDim = dim3((unsigned)(2 * (ctx->num_sms / 2)));
+    oc.gridDim = dim3((unsigned)(CL * (ctx->num_sms / CL)));
     oc.blockDim = dim3(Cfg::THREADS);
     oc.dynamicSmemBytes = Cfg::SMEM;
     cudaLaunchAttribute oa[1];
     oa[0].id = cudaLaunchAttributeClusterDimension;
-    oa[0].val.clusterDim.x = 2;
+    oa[0].val.clusterDim.x = CL;
     oa[0].val.clusterDim.y = 1;
     oa[0].val.clusterDim.z = 1;
     oc.attrs = oa;
@@ -721,7 +721,7 @@ static int launch_knn(scb_ctx* ctx, const float* Qx, int64_t n_q, const float* K
     int nc = 0;
     SCB_CUDA(cudaOccupancyMaxActiveClusters(&nc, knn_candidates_kernel<KC, HALVES, CL>, &oc));
     if (nc > 0) max_clusters = std::min(max_clusters, nc);
-    if (getenv("SCB_KNN_DEBUG")) fprintf(stderr, "[knn] co-resident 2-CTA clusters: %d\n", nc);
+    if (getenv("SCB_KNN_DEBUG")) fprintf(stderr, "[knn] co-resident %d-CTA clusters: %d\n", CL, nc);
   }
   const int64_t Gc = std::min<int64_t>(n_sp, max_clusters);
   const int64_t G = Gc * CL;
