@@ -86,14 +86,17 @@ def test_knn_tile_boundaries_and_widths(n, d, k):
     np.testing.assert_allclose(dist, ref_d, rtol=1e-4, atol=1e-4)
 
 
-def test_knn_tail_split_units_and_ragged_last_tile():
-    """158 query pairs on 148 SMs: the final partial round (10 pairs) is split into 20 half-scan
-    units whose two lists per row are re-ranked together; the last key tile is ragged (padding
-    keys in the second column half only).  Checked against the float64 oracle on every row of
-    the split pairs and on random rows of the full rounds."""
+@pytest.mark.parametrize("n", [256 * 158 - 37, 256 * 149 + 5, 256 * 147 - 3])
+def test_knn_tail_split_units_and_ragged_last_tile(n):
+    """Query pairs beyond one grid round: 158 pairs = 79 two-CTA cluster units on 74 co-resident
+    clusters (the final partial round is split into half-scan units whose two lists per row are
+    re-ranked together), 150 pairs = 75 units (one split unit), 147 pairs (odd: the last
+    cluster's second CTA has no queries but still loads and releases its half of every key
+    tile); the last key tile is ragged (padding keys in the second column half only).  Checked
+    against the float64 oracle on random rows."""
     import torch
     from paper_2605_13928_b200 import pp
-    n, d, k = 256 * 158 - 37, 50, 15
+    d, k = 50, 15
     rng = np.random.default_rng(11)
     centers = rng.standard_normal((40, d)) * np.linspace(3.0, 0.5, d)
     X = (centers[rng.integers(0, 40, n)] + rng.standard_normal((n, d)) * np.linspace(1.0, 0.2, d)).astype(np.float32)
