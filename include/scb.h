@@ -159,7 +159,9 @@ SCB_API int scb_subset_fill(scb_ctx* ctx, const int64_t* indptr, const int32_t* 
 /* ---- a2 pass 2 fused with a6's statistics: as scb_subset_fill with row_scale (log1p values),
  * and sums u64[2][2][n_slots] += the fixed-point Σl, Σl² of the HVG columns (slot: int32 per
  * OUTPUT gene, -1 = not an HVG) -- the numbers scb_scale_gene_sums would compute from the
- * written matrix, without re-reading it.  Requires n_cols <= 32767 (else SCB_ERR_UNSUPPORTED). */
+ * written matrix, without re-reading it.  Requires n_cols <= 32767 (else SCB_ERR_UNSUPPORTED).
+ * new_indices may be NULL when every row and every gene is kept: the output then shares the
+ * input's indices (no copy; a kernel trap if a row or gene turns out to be dropped). */
 SCB_API int scb_subset_fill_scale_sums(scb_ctx* ctx, const int64_t* indptr, const int32_t* indices, const float* data,
                                int64_t n_rows, int32_t n_cols, const uint8_t* cell_mask, const int32_t* gene_remap,
                                const int64_t* new_indptr, const float* row_scale, const int32_t* slot,

@@ -522,15 +522,21 @@ subset_fill_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict
       atomicAdd(&sums[3 * n_slots + sl], v2 >> 32);
     }
   };
+  // out_idx == nullptr: every row and gene is kept, the output shares the input's indices
+  if (out_idx == nullptr && !ident) __trap();  // C-ABI contract violated
   if (ident) {
     // element p of row r lands at p + (new_indptr[kr] - indptr[r]): no scan, no staging;
     // 16-byte stores when the shift keeps quads aligned
     for (int64_t r = r0 + w; r < r1; r += (blockDim.x >> 5)) {
-      if (!cmask[r]) continue;
+      if (!cmask[r]) {
+        if (out_idx == nullptr) __trap();
+        continue;
+      }
       const int64_t kr = row_pos[r];
       const float s = row_scale[kr];
       const int64_t b = indptr[r], e = indptr[r + 1];
       const int64_t delta = new_indptr[kr] - b;
+      if (out_idx == nullptr && delta != 0) __trap();
       const bool vec = (delta & 3) == 0;
       stream_row_pipe<1>(indices, data, b, e, nnz, [&](const Quad& q) {
         float l[4];
@@ -544,13 +550,13 @@ subset_fill_sums_kernel(const int64_t* __restrict__ indptr, const IT* __restrict
         }
         const int64_t o = q.p + delta;
         if (vec && q.valid == 0xFu) {
-          *reinterpret_cast<int4*>(out_idx + o) = make_int4(q.g[0], q.g[1], q.g[2], q.g[3]);
+          if (out_idx) *reinterpret_cast<int4*>(out_idx + o) = make_int4(q.g[0], q.g[1], q.g[2], q.g[3]);
           *reinterpret_cast<float4*>(out_val + o) = make_float4(l[0], l[1], l[2], l[3]);
         } else {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if ((q.valid >> k) & 1u) {
-              out_idx[o + k] = q.g[k];
+              if (out_idx) out_idx[o + k] = q.g[k];
               out_val[o + k] = l[k];
             }
         }
@@ -1456,8 +1462,8 @@ static int subset_fill_scale_sums_impl(scb_ctx* ctx, const int64_t* indptr, cons
                                           const int32_t* slot, int32_t n_slots, int32_t* new_indices,
                                           float* new_data, uint64_t* sums, const int64_t* esc_pos, const float* esc_val, int64_t n_esc, void* stream) {
   const U16Esc esc{esc_pos, esc_val, n_esc};
-  SCB_REQUIRE(ctx && indptr && indices && data && cmask && remap && new_indptr && row_scale && slot && new_indices &&
-                  new_data && sums,
+  SCB_REQUIRE(ctx && indptr && indices && data && cmask && remap && new_indptr && row_scale && slot &&
+                  (new_indices || std::is_same<IT, int32_t>::value) && new_data && sums,
               SCB_ERR_ARG, "scb_subset_fill_scale_sums: null argument");
   SCB_REQUIRE(aligned16(indices) && aligned16(data), SCB_ERR_ARG, "scb_subset_fill_scale_sums: 16-byte alignment");
   SCB_REQUIRE(n_cols <= 32767 && n_slots > 0 && n_slots < 32767, SCB_ERR_UNSUPPORTED,

@@ -147,7 +147,8 @@ def run(X: pp.DeviceCSR, mt_mask: torch.Tensor, params: Params = Params(), *, co
     if p.regress_out:
         X_log = pp.subset_fill_log(X, cm, remap, new_indptr, row_scale, nnz, gk)
     else:
-        X_log, ssum = pp.subset_fill_log_scale_sums(X, cm, remap, new_indptr, row_scale, nnz, gk, slot, H)
+        X_log, ssum = pp.subset_fill_log_scale_sums(X, cm, remap, new_indptr, row_scale, nnz, gk, slot, H,
+                                                    all_kept=(nk_local == X.n_rows and gk == X.n_cols))
 
     # ------------------------------------------------------------------ regress (scale)
     tm.step("regress")

@@ -380,20 +380,23 @@ def subset_normalize(X: DeviceCSR, cell_mask, gene_mask, n_kept, target_sum: flo
 
 
 def subset_fill_log_scale_sums(X: DeviceCSR, cell_mask, remap, new_indptr, row_scale, nnz: int, n_genes_kept: int,
-                               slot: torch.Tensor, H: int, sums=None):
+                               slot: torch.Tensor, H: int, sums=None, all_kept: bool = False):
     """subset_fill_log fused with the scale step's gene sums of the HVG columns (``slot``: int32
     per kept gene, -1 = not an HVG).  Returns (X_log, sums u64[2][2][H]) or (X_log, None) when
-    the fused kernel does not apply (more than 32767 input genes) -- then use scale_gene_sums."""
+    the fused kernel does not apply (more than 32767 input genes) -- then use scale_gene_sums.
+    ``all_kept``: every row and gene of X is kept (the caller's QC counts say so): X_log shares
+    X's int32 indices instead of copying them (the kernel traps if that is not true)."""
     if X.n_cols > 32767:
         return subset_fill_log(X, cell_mask, remap, new_indptr, row_scale, nnz, n_genes_kept), None
     dev = X.device
-    ind = torch.empty(nnz, dtype=torch.int32, device=dev)
+    share = all_kept and X.indices.dtype == torch.int32 and nnz == X.nnz
+    ind = X.indices if share else torch.empty(nnz, dtype=torch.int32, device=dev)
     logv = torch.empty(nnz, dtype=torch.float32, device=dev)
     if sums is None:
         sums = torch.zeros((2, 2, H), dtype=torch.int64, device=dev)
     _lib.call("scb_subset_fill_scale_sums" + _fmt(X.indices, X.data), _ctx(X.data), _p(X.indptr), _p(X.indices),
               _p(X.data), X.n_rows, X.n_cols, _p(cell_mask), _p(remap), _p(new_indptr), _p(row_scale), _p(slot), H,
-              _p(ind), _p(logv), _p(sums), *_esc(X), _stream(dev))
+              _p(None if share else ind), _p(logv), _p(sums), *_esc(X), _stream(dev))
     return DeviceCSR(new_indptr, ind, logv, n_genes_kept, row_scale=row_scale), sums
 
 

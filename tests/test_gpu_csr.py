@@ -279,3 +279,24 @@ def test_scale_clip_modes_gpu(dev_state, clip):
         assert Z.min() >= -1.0
     else:
         assert Z.min() < -1.0
+
+def test_fused_fill_all_kept_shares_indices():
+    """Every row and gene kept: the fill pass writes only the log values and the kept matrix
+    shares the input's indices; values and fused sums equal the copying path's."""
+    import torch
+    import paper_2605_13928_b200 as scb
+    from paper_2605_13928_b200 import pp
+    X, mt = c1_inputs()
+    Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, X.n_cols)
+    qc = scb.calculate_qc_metrics(Xd, torch.as_tensor(mt))
+    cm, gm, kept = scb.filter_masks(qc, min_genes=0, max_genes=None, max_pct_mt=101.0, min_cells=0)
+    assert (int(kept[0]), int(kept[1])) == (Xd.n_rows, Xd.n_cols)
+    remap, nip, rs, rso, nnz = pp.subset_count_scale(Xd, cm, gm, kept, 1e4)
+    H = 300
+    slot = pp.gene_slots(torch.arange(0, 3 * H, 3, dtype=torch.int32, device=Xd.indices.device), kept[1])
+    ref, s_ref = pp.subset_fill_log_scale_sums(Xd, cm, remap, nip, rs, nnz, kept[1], slot, H)
+    got, s_got = pp.subset_fill_log_scale_sums(Xd, cm, remap, nip, rs, nnz, kept[1], slot, H, all_kept=True)
+    assert got.indices.data_ptr() == Xd.indices.data_ptr() and ref.indices.data_ptr() != Xd.indices.data_ptr()
+    assert torch.equal(got.indices, ref.indices) and torch.equal(got.data, ref.data)
+    assert torch.equal(got.indptr, Xd.indptr)
+    assert torch.equal(s_got, s_ref)
