@@ -81,7 +81,7 @@ def subset_fill_log(X, cm, remap, new_indptr, row_scale, nnz, n_genes_kept):
     return _PASS.pop(id(X))
 
 
-def subset_fill_log_scale_sums(X, cm, remap, new_indptr, row_scale, nnz, n_genes_kept, slot, H, sums=None):
+def subset_fill_log_scale_sums(X, cm, remap, new_indptr, row_scale, nnz, n_genes_kept, slot, H, sums=None, all_kept=False):
     Xl = subset_fill_log(X, cm, remap, new_indptr, row_scale, nnz, n_genes_kept)
     return Xl, scale_gene_sums(Xl, slot, H)
 
