@@ -466,35 +466,113 @@ __device__ __forceinline__ int64_t esc_find(const int64_t* __restrict__ pos, int
 }
 
 // warp per row: gene index = previous + 1 + byte delta (255: the delta is in the gene escape
-// table), count = byte (255: value in the count escape table); a warp scan carries the gene
-// index across each 32-element window (coalesced byte loads, 128-byte stores)
-__global__ void delta8_decode_kernel(const int64_t* __restrict__ indptr, int64_t n_rows,
+// table), count = byte (255: value in the count escape table).  Windows of 256 elements aligned
+// to 4 (elements of neighbouring rows masked) as two 128-element halves; in each half lane L owns
+// elements 4L..4L+3 (4-byte loads of both byte streams, one 16-byte store per array, so a warp
+// store instruction writes 512 contiguous bytes), a per-lane running sum + a warp scan carries
+// the gene index.  The next row's bounds are loaded while the current row is decoded.
+#ifndef SCB_D8_HALVES
+#define SCB_D8_HALVES 2
+#endif
+#ifndef SCB_D8_MINB
+#define SCB_D8_MINB 1
+#endif
+__global__ void __launch_bounds__(256, SCB_D8_MINB) delta8_decode_kernel(const int64_t* __restrict__ indptr, int64_t n_rows,
                                      const uint8_t* __restrict__ dgene, const uint8_t* __restrict__ dcount,
                                      const int64_t* __restrict__ gpos, const int32_t* __restrict__ gval, int64_t n_g,
                                      const int64_t* __restrict__ cpos, const float* __restrict__ cval, int64_t n_c,
-                                     int32_t* __restrict__ indices, float* __restrict__ data) {
+                                     int64_t nnz, int32_t* __restrict__ indices, float* __restrict__ data) {
+  constexpr int HALVES = SCB_D8_HALVES;
   const int lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); r < n_rows; r += warps) {
-    const int64_t b = indptr[r], e = indptr[r + 1];
+  int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  int64_t nb = 0, ne = 0;
+  if (r < n_rows) {
+    nb = indptr[r];
+    ne = indptr[r + 1];
+  }
+  for (; r < n_rows; r += warps) {
+    const int64_t b = nb, e = ne;
+    if (r + warps < n_rows) {
+      nb = indptr[r + warps];
+      ne = indptr[r + warps + 1];
+    }
     int carry = -1;
-    for (int64_t base = b; base < e; base += 32) {
-      const int64_t k = base + lane;
-      const bool ok = k < e;
-      const int dc = ok ? (int)__ldg(dgene + k) : 0;
-      const int cc = ok ? (int)__ldg(dcount + k) : 0;
-      int inc = ok ? dc + 1 : 0;
-      if (ok && dc == 255) inc = gval[esc_find(gpos, n_g, k)] + 1;
+    for (int64_t w0 = b & ~(int64_t)3; w0 < e; w0 += HALVES * 128) {
+      uint32_t gw[HALVES], cw[HALVES];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
+      for (int h = 0; h < HALVES; ++h) {
+        const int64_t k0 = w0 + 128 * h + 4 * lane;
+        gw[h] = 0u;
+        cw[h] = 0u;
+        if (k0 < e) {
+          if (k0 + 4 <= nnz) {
+            gw[h] = __ldg(reinterpret_cast<const uint32_t*>(dgene + k0));
+            cw[h] = __ldg(reinterpret_cast<const uint32_t*>(dcount + k0));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (k0 + j < nnz) {
+                gw[h] |= (uint32_t)dgene[k0 + j] << (8 * j);
+                cw[h] |= (uint32_t)dcount[k0 + j] << (8 * j);
+              }
+          }
+        }
       }
-      const int g = carry + inc;
-      carry = __shfl_sync(0xffffffffu, g, 31);
-      if (ok) {
-        indices[k] = g;
-        data[k] = cc == 255 ? cval[esc_find(cpos, n_c, k)] : (float)cc;
+#pragma unroll
+      for (int h = 0; h < HALVES; ++h) {
+        const int64_t k0 = w0 + 128 * h + 4 * lane;
+        // fast lanes: all 4 elements in the row and no escape byte (0xFF) in either word
+        const bool full = k0 >= b && k0 + 4 <= e;
+        const uint32_t ff = ((~gw[h] - 0x01010101u) & gw[h]) | ((~cw[h] - 0x01010101u) & cw[h]);
+        const bool fast = full && (ff & 0x80808080u) == 0u;
+        int incl[4];
+        float v[4];
+        if (fast) {
+          const uint32_t d = gw[h];
+          incl[0] = (int)(d & 0xFFu) + 1;
+          incl[1] = incl[0] + (int)((d >> 8) & 0xFFu) + 1;
+          incl[2] = incl[1] + (int)((d >> 16) & 0xFFu) + 1;
+          incl[3] = incl[2] + (int)(d >> 24) + 1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)  // 2^23 + byte as a float bit pattern, minus 2^23: exact
+            v[j] = __uint_as_float(__byte_perm(cw[h], 0x4B000000u, (unsigned)j | 0x7540u)) - 8388608.0f;
+        } else {
+          int sum = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int64_t k = k0 + j;
+            const bool ok = k >= b && k < e;
+            const int dg = (int)((gw[h] >> (8 * j)) & 0xFFu);
+            int inc = ok ? dg + 1 : 0;
+            if (ok && dg == 255) inc = gval[esc_find(gpos, n_g, k)] + 1;
+            sum += inc;
+            incl[j] = sum;
+            const uint32_t c = (cw[h] >> (8 * j)) & 0xFFu;
+            v[j] = (float)c;
+            if (c == 255u && ok) v[j] = cval[esc_find(cpos, n_c, k)];
+          }
+        }
+        const int sum = incl[3];
+        int x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += t;
+        }
+        const int g0 = carry + x - sum;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+        if (full) {
+          *reinterpret_cast<int4*>(indices + k0) = make_int4(g0 + incl[0], g0 + incl[1], g0 + incl[2], g0 + incl[3]);
+          *reinterpret_cast<float4*>(data + k0) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (k0 + j >= b && k0 + j < e) {
+              indices[k0 + j] = g0 + incl[j];
+              data[k0 + j] = v[j];
+            }
+        }
       }
     }
   }
@@ -511,10 +589,15 @@ extern "C" int scb_csr_delta8_decode(scb_ctx* ctx, const int64_t* indptr, int64_
               "scb_csr_delta8_decode: null argument");
   SCB_REQUIRE((n_gesc == 0 || (gesc_pos && gesc_val)) && (n_cesc == 0 || (cesc_pos && cesc_val)), SCB_ERR_ARG,
               "scb_csr_delta8_decode: escape table missing");
+  SCB_REQUIRE(((uintptr_t)dgene & 3) == 0 && ((uintptr_t)dcount & 3) == 0 && ((uintptr_t)indices & 15) == 0 &&
+                  ((uintptr_t)data & 15) == 0,
+              SCB_ERR_ARG, "scb_csr_delta8_decode: 4-byte aligned byte streams, 16-byte aligned outputs required");
   if (n_rows == 0 || nnz == 0) return SCB_OK;
-  const int g = (int)std::min<int64_t>((int64_t)ctx->num_sms * 8, (n_rows + 7) / 8);
+  int per_sm = 0;  // one resident wave (the grid-stride loop gives every warp the same share of rows)
+  SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, delta8_decode_kernel, 256, 0));
+  const int g = (int)std::min<int64_t>((int64_t)ctx->num_sms * std::max(per_sm, 1), (n_rows + 7) / 8);
   delta8_decode_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(indptr, n_rows, dgene, dcount, gesc_pos, gesc_val, n_gesc,
-                                                            cesc_pos, cesc_val, n_cesc, indices, data);
+                                                            cesc_pos, cesc_val, n_cesc, nnz, indices, data);
   SCB_LAUNCH_CHECK();
   return SCB_OK;
 }
