@@ -573,8 +573,13 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         const int64_t tail_row0 = (int64_t)n_full * CL * 2 * C::BM;
         int* o = U.tail ? cand_tail + (row - tail_row0) * (2 * C::KCT) + U.half * C::KCT + hf * KC
                         : cand + row * C::KCT + hf * KC;
+        if constexpr (KC % 4 == 0) {  // 16-byte stores (rows are 16-byte aligned: KCT, KC multiples of 4)
 #pragma unroll
-        for (int j = 0; j < KC; ++j) o[j] = I[j];
+          for (int j = 0; j < KC; j += 4) *reinterpret_cast<int4*>(o + j) = make_int4(I[j], I[j + 1], I[j + 2], I[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < KC; ++j) o[j] = I[j];
+        }
       }
     }
     PROF_ADD(1, tot);
