@@ -38,6 +38,19 @@ namespace scb {
 constexpr int kD = 64;            // padded augmented width (one 128-byte FP16 row)
 constexpr int kBuckets = 1 << 16; // PC1 counting-sort buckets
 
+// nanosleep back-off (ns) of the producer's / MMA issuers' / epilogue's barrier polls (0: plain
+// spin).  A spinning warp issues 3 instructions per poll on the sub-partition the epilogue warps
+// need (ncu: 15 % of all issued instructions were polls); A/B at C3 (4 rounds): 114.9 -> 112.9 ms
+#ifndef SCB_KNN_SLEEP_P
+#define SCB_KNN_SLEEP_P 64
+#endif
+#ifndef SCB_KNN_SLEEP_M
+#define SCB_KNN_SLEEP_M 32
+#endif
+#ifndef SCB_KNN_SLEEP_E
+#define SCB_KNN_SLEEP_E 0
+#endif
+
 // KC = per-warp list length, HALVES = epilogue warps per (query tile, TMEM lane quarter)
 template <int KC, int HALVES>
 struct KnnCfg {
@@ -409,7 +422,11 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
         for (int i = U.i0; i < U.i1; ++i) {
           const int kt = outward_tile(st, i, n_kt);
           const int s = it % C::STAGES;
+#if SCB_KNN_SLEEP_P > 0
+          tc::mbar_wait_sleep(tc::smem_u32(&b_empty[s]), ((it / C::STAGES) & 1) ^ 1, SCB_KNN_SLEEP_P);
+#else
           tc::mbar_wait(&b_empty[s], ((it / C::STAGES) & 1) ^ 1);
+#endif
           tc::mbar_arrive_expect_tx(&b_full[s], C::B_BYTES);
           if (CL > 1)  // my 1/CL of the tile, into every CTA of the cluster (tk's box is BN/CL rows)
             tc::tma_load_2d_mc(b_base + s * C::B_BYTES + crank * (C::B_BYTES / CL), &tk, &b_full[s], 0,
@@ -446,10 +463,18 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
           const int s = it % C::STAGES;
           const int buf = it & 1;
           PROF_T0(w0);
+#if SCB_KNN_SLEEP_M > 0
+          tc::mbar_wait_sleep(bar_bf + 8 * s, (it / C::STAGES) & 1, SCB_KNN_SLEEP_M);
+#else
           tc::mbar_wait_a(bar_bf + 8 * s, (it / C::STAGES) & 1);
+#endif
           PROF_ADD(3, w0);
           PROF_T0(w1);
+#if SCB_KNN_SLEEP_M > 0
+          tc::mbar_wait_sleep(bar_te + 16 * buf, ((it >> 1) & 1) ^ 1, SCB_KNN_SLEEP_M);
+#else
           tc::mbar_wait_a(bar_te + 16 * buf, ((it >> 1) & 1) ^ 1);
+#endif
           PROF_ADD(2, w1);
           tc::tc_fence_after();
           const uint32_t d = tmem + buf * (2 * C::BN) + t * C::BN;
@@ -507,7 +532,11 @@ knn_candidates_kernel(const __grid_constant__ CUtensorMap tq, const __grid_const
       for (int i = U.i0; i < U.i1; ++i, ++it) {
         const int buf = it & 1;
         PROF_T0(w0);
+#if SCB_KNN_SLEEP_E > 0
+        tc::mbar_wait_sleep(tf_bar + buf * 16, (it >> 1) & 1, SCB_KNN_SLEEP_E);
+#else
         tc::mbar_wait_a(tf_bar + buf * 16, (it >> 1) & 1);
+#endif
         PROF_ADD(0, w0);
         tc::tc_fence_after();
         const uint32_t tb = tl + buf * (2 * C::BN);

@@ -71,6 +71,18 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
       : "memory");
 }
 #endif
+// wait with a nanosleep back-off between polls: a waiting warp stops competing for issue slots
+// with the working warps of its sub-partition (each failed poll of the plain loop costs 3 issues)
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t a, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  for (;;) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+  }
+}
 __device__ __forceinline__ void mbar_arrive_elect(uint32_t a) {  // one elected lane of a converged warp
   asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(a)
                : "memory");
