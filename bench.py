@@ -47,9 +47,9 @@ def _peaks():
 
 
 def _tensor_pipe():
-    """ncu tensor-pipe utilisation of the tcgen05 kernels (profiles/r02h/tensor_pipe.json, one
+    """ncu tensor-pipe utilisation of the tcgen05 kernels (profiles/r02i/tensor_pipe.json, one
     ncu --metrics capture of a C3 bench step), or None."""
-    path = os.path.join(ROOT, "profiles", "r02h", "tensor_pipe.json")
+    path = os.path.join(ROOT, "profiles", "r02i", "tensor_pipe.json")
     try:
         with open(path) as f:
             return json.load(f)
@@ -368,7 +368,7 @@ def main():
             stages[kk] = {"ms": round(step_ms[kk], 4)}
     stages["knn"]["candidates_kernel_ms"] = round(knn_ms, 4)
     traffic = None  # dram bytes per launch of the kNN kernel from the committed ncu --set full capture
-    tpath = next((p for p in (os.path.join(ROOT, "profiles", r, "knn_traffic.json") for r in ("r02h", "r02g", "r02f", "r02d", "r02c", "r02", "r01"))
+    tpath = next((p for p in (os.path.join(ROOT, "profiles", r, "knn_traffic.json") for r in ("r02i", "r02h", "r02g", "r02f", "r02d", "r02c", "r02", "r01"))
                   if os.path.exists(p)), "")
     if os.path.exists(tpath) and world == 1:
         tj = json.load(open(tpath))

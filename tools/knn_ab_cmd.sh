@@ -1,1 +1,1 @@
-bash tools/knn_variants.sh 4 "base:" "pm64_32:-DSCB_KNN_SLEEP_P=64 -DSCB_KNN_SLEEP_M=32" "pm128_64:-DSCB_KNN_SLEEP_P=128 -DSCB_KNN_SLEEP_M=64" "p128:-DSCB_KNN_SLEEP_P=128"
+KNN_REPS=16 bash tools/knn_variants.sh 3 "base:" "e32:-DSCB_KNN_SLEEP_E=32" "e64:-DSCB_KNN_SLEEP_E=64" "spin:-DSCB_KNN_SLEEP_P=0 -DSCB_KNN_SLEEP_M=0"
