@@ -38,3 +38,34 @@ def test_delta8_c3_window_and_pipeline_input():
     assert wire < 2.2 * X.nnz + 8 * (X.n_rows + 1) + 64
     print(f"C3 window: {X.nnz} nonzeros, {D.gesc_pos.numel()} gene-gap and {D.cesc_pos.numel()} count escapes, "
           f"{wire / X.nnz:.3f} B per nonzero on the wire")
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_delta8_decode_tiny_rows_and_edge_escapes(seed):
+    """Rows of 0-9 entries (every window partial, row starts at every offset mod 4), gene gaps
+    > 254 at a row's first entry and across its last entries, counts >= 255 on first and last
+    entries, total nnz not a multiple of 4 (the byte-load tail at the end of the streams)."""
+    import torch
+    from paper_2605_13928_b200.pp import DeltaCSR, DeviceCSR
+    rng = np.random.default_rng(seed)
+    G, n = 40000, 5001
+    lens = rng.integers(0, 10, n)
+    rows = [np.sort(rng.choice(G, m, replace=False)) for m in lens]
+    ip = np.zeros(n + 1, np.int64)
+    ip[1:] = np.cumsum(lens)
+    if ip[-1] % 4 == 0:  # make the stream length ragged
+        rows[-1] = np.sort(np.append(rows[-1][:0], rng.choice(G, 1)))
+        lens[-1] = 1
+        ip[1:] = np.cumsum(lens)
+    ind = np.concatenate(rows).astype(np.int32)
+    data = rng.integers(1, 5, ip[-1]).astype(np.float32)
+    first, last = ip[:-1][lens > 0], ip[1:][lens > 0] - 1
+    data[first[::3]] = rng.integers(255, 1 << 20, len(first[::3]))
+    data[last[1::3]] = rng.integers(255, 1 << 20, len(last[1::3]))
+    X = DeviceCSR.from_host(ip, ind, data, G)
+    D = DeltaCSR.from_csr(X)
+    assert D.gesc_pos.numel() > 0 and D.cesc_pos.numel() > 0
+    Y = D.to_f32()
+    torch.cuda.synchronize()
+    assert torch.equal(Y.indices, X.indices)
+    assert torch.equal(Y.data, X.data)
