@@ -226,7 +226,8 @@ SCB_API int scb_csr_u16_decode(scb_ctx* ctx, const uint16_t* indices16, const ui
  * byte dgene = g - g_prev - 1 (g_prev = -1 at a row start; 255 = escape: the delta is
  * gesc_val at the sorted position gesc_pos) and one byte dcount = the count (255 = escape:
  * cesc_val at cesc_pos); rows as indptr (sorted, unique gene indices within a row).  2 B on the
- * wire per nonzero instead of 4 (u16) or 8 (int32 + float32); lossless (pp.DeltaCSR). */
+ * wire per nonzero instead of 4 (u16) or 8 (int32 + float32); lossless (pp.DeltaCSR).
+ * dgene / dcount 4-byte aligned, indices / data 16-byte aligned (else SCB_ERR_ARG). */
 SCB_API int scb_csr_delta8_decode(scb_ctx* ctx, const int64_t* indptr, int64_t n_rows, const uint8_t* dgene,
                                   const uint8_t* dcount, int64_t nnz, const int64_t* gesc_pos,
                                   const int32_t* gesc_val, int64_t n_gesc, const int64_t* cesc_pos,
