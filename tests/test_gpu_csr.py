@@ -300,3 +300,29 @@ def test_fused_fill_all_kept_shares_indices():
     assert torch.equal(got.indices, ref.indices) and torch.equal(got.data, ref.data)
     assert torch.equal(got.indptr, Xd.indptr)
     assert torch.equal(s_got, s_ref)
+
+
+def test_pipeline_all_kept_shared_indices_matches_copy(monkeypatch):
+    """Whole pipeline with filters that keep every cell and gene: the shared-indices fill path
+    gives bit-identical HVG set, scale statistics, PCA and kNN to the copying path, and leaves
+    the input matrix untouched."""
+    import torch
+    import paper_2605_13928_b200 as scb
+    from paper_2605_13928_b200 import pipeline, pp
+    X, mt = c1_inputs()
+    Xd = scb.DeviceCSR.from_host(X.indptr, X.indices, X.data, X.n_cols)
+    ind0, dat0 = Xd.indices.clone(), Xd.data.clone()
+    prm = pipeline.Params(min_genes=0, max_pct_mt=101.0, min_cells=0, n_top_genes=500, n_neighbors=10)
+    mtd = torch.as_tensor(mt, device="cuda")
+    shared = pipeline.run(Xd, mtd, prm, timing=False)
+    assert shared.X_log.indices.data_ptr() == Xd.indices.data_ptr()
+    orig = pp.subset_fill_log_scale_sums
+    monkeypatch.setattr(pp, "subset_fill_log_scale_sums",
+                        lambda *a, **k: orig(*a, **{**k, "all_kept": False}))
+    copied = pipeline.run(Xd, mtd, prm, timing=False)
+    assert copied.X_log.indices.data_ptr() != Xd.indices.data_ptr()
+    assert torch.equal(shared.hvg_index, copied.hvg_index)
+    assert torch.equal(shared.X_log.data, copied.X_log.data)
+    assert torch.equal(shared.pca.X_pca, copied.pca.X_pca)
+    assert torch.equal(shared.knn_index, copied.knn_index)
+    assert torch.equal(Xd.indices, ind0) and torch.equal(Xd.data, dat0)
