@@ -9,6 +9,7 @@
 // Integer sums are exact and order independent, so results are deterministic and
 // identical across 1/2/4/8-way cell sharding.
 #include <cuda_bf16.h>
+#include "planes_fmt.cuh"
 #include <type_traits>
 #include "common.cuh"
 #include "scan.cuh"

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <vector>
 #include <cuda_bf16.h>
+#include "planes_fmt.cuh"
 #include "tc_common.cuh"
 
 namespace scb {
@@ -47,7 +48,7 @@ struct GramCfg {
   static constexpr int C_BYTES = 2 * PLANE;           // hi + lo
   static constexpr int NF = 2, NC = 2;                // ring depths
   static constexpr int SMEM = NF * F_BYTES + NC * C_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr uint32_t IDESC = tc::idesc_bf16(BM, BN, true, true);
+  static constexpr uint32_t IDESC = tc::SCB_PLANES_IDESC(BM, BN, true, true);
 };
 
 template <int BN>
@@ -251,7 +252,7 @@ struct GramSplitCfg {
   static constexpr int STAGE = 2 * PLANE;
   static constexpr int STAGES = 4;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
-  static constexpr uint32_t IDESC = tc::idesc_bf16(BM, BN, true, true);
+  static constexpr uint32_t IDESC = tc::SCB_PLANES_IDESC(BM, BN, true, true);
   static constexpr int EPI_WARPS = 8;                 // 2 per TMEM lane quarter, BN/2 columns each
   static constexpr int COLS = BN / 2;
 };
@@ -352,8 +353,10 @@ gram_split_kernel(const __grid_constant__ CUtensorMap thi, const __grid_constant
           const uint64_t dal = tc::smem_desc_sw128(al + ko, C::BOX, 1024);
           const uint64_t dbl = tc::smem_desc_sw128(bl + ko, C::BOX, 1024);
           tc::mma_f16(acc, dah, dbh, C::IDESC, (first && kk == 0) ? 0u : 1u);
+#ifndef SCB_GRAM_1X  // experiment: hi x hi only (one product per output)
           tc::mma_f16(acc, dah, dbl, C::IDESC, 1u);
           tc::mma_f16(acc, dal, dbh, C::IDESC, 1u);
+#endif
         }
         tc::mma_commit(&empty[s]);
         if (last) tc::mma_commit(&acc_full[p]);

@@ -8,6 +8,7 @@
 // subtract the centring shift s = m V, and store the embedding rows.
 #include <vector>
 #include <cuda_bf16.h>
+#include "planes_fmt.cuh"
 #include "tc_common.cuh"
 
 namespace scb {
@@ -231,7 +232,7 @@ struct ProjPCfg {
   static constexpr int B_BYTES = NP * KB * 2;   // per plane
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // Ahi | Alo | Bhi | Blo
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
-  static constexpr uint32_t IDESC = tc::idesc_bf16(BM, NP, false, false);
+  static constexpr uint32_t IDESC = tc::SCB_PLANES_IDESC(BM, NP, false, false);
   static constexpr int TMEM_COLS = 2 * NP < 32 ? 32 : 2 * NP;
 };
 
