@@ -355,6 +355,12 @@ SCB_API int scb_rank_genes_groups(scb_ctx* ctx, const int64_t* indptr, const int
  * hp = ldz must be a multiple of 128; n_rows any. */
 SCB_API int scb_gram(scb_ctx* ctx, const float* Z, int64_t n_rows, int32_t hp, double* C, void* stream);
 
+/* ---- operand-plane format of this build: 0 = BF16 planes + three-product Gram (the default),
+ * 2 = FP16 planes + three-product Gram, 1 = FP16 planes + one-product (hi x hi) Gram.  The
+ * planes written by scb_split_bf16 / scb_scale_dense_planes and read by the Gram and the
+ * projection are 16-bit values of that format. */
+SCB_API int32_t scb_plane_format(void);
+
 /* ---- a7 operand prep: BF16 planes Zhi = bf16(Z), Zlo = bf16(Z - Zhi) (uint16 storage,
  * [n_rows][ld], ld % 4 == 0) in one streaming pass. */
 SCB_API int scb_split_bf16(scb_ctx* ctx, const float* Z, int64_t n_rows, int64_t ld, uint16_t* Zhi, uint16_t* Zlo,

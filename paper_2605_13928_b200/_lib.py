@@ -48,6 +48,7 @@ SIGNATURES = {
     "scb_gram": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
     "scb_gram_split": [c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr],
     "scb_split_bf16": [c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr],
+    "scb_plane_format": [],
     "scb_subset_fill_scale_sums": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i32,
                                    c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_umap_layout": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, ctypes.c_float, c_ptr, c_i64, c_i32, ctypes.c_float,
@@ -94,7 +95,8 @@ SIGNATURES = {
     "scb_synth_logmean": [c_ptr, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "scb_synth_rows": [c_ptr, c_u64, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
 }
-_RESTYPE = {"scb_last_error": ctypes.c_char_p, "scb_launch_count": ctypes.c_ulonglong, "scb_hvg_tiles": ctypes.c_int32}
+_RESTYPE = {"scb_last_error": ctypes.c_char_p, "scb_launch_count": ctypes.c_ulonglong, "scb_hvg_tiles": ctypes.c_int32,
+            "scb_plane_format": ctypes.c_int32}
 
 _lib = None
 _lock = threading.Lock()
@@ -189,3 +191,9 @@ def _destroy_all():
 import atexit  # noqa: E402
 
 atexit.register(_destroy_all)
+
+
+def plane_dtype():
+    """torch dtype of the Gram / projection operand planes of this build (scb_plane_format)."""
+    import torch
+    return torch.bfloat16 if int(load().scb_plane_format()) == 0 else torch.float16

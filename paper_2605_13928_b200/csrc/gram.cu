@@ -506,6 +506,20 @@ extern "C" int scb_gram_split(scb_ctx* ctx, const uint16_t* Zhi, const uint16_t*
   return launch_gram<128>(ctx, nullptr, Zhi, Zlo, n_rows, hp, C, s);
 }
 
+// format of the operand planes (scb_split_bf16, scb_scale_dense_planes, Gram, projection):
+// 0 BF16 + three-product Gram (default), 2 FP16 + three products, 1 FP16 + one product
+extern "C" int32_t scb_plane_format(void) {
+#ifdef SCB_PLANES_F16
+#ifdef SCB_GRAM_1X
+  return 1;
+#else
+  return 2;
+#endif
+#else
+  return 0;
+#endif
+}
+
 extern "C" int scb_split_bf16(scb_ctx* ctx, const float* Z, int64_t n_rows, int64_t ld, uint16_t* Zhi, uint16_t* Zlo,
                               void* stream) {
   SCB_REQUIRE(ctx && Z && Zhi && Zlo, SCB_ERR_ARG, "scb_split_bf16: null argument");

@@ -1,9 +1,12 @@
-// Operand-plane format of the Gram / projection / scaled-matrix planes.  Default BF16 hi/lo.
-// Experiment switch SCB_PLANES_F16: FP16 hi = fp16(z), lo = fp16(z - hi) instead (11-bit
-// significands: ~2^-22 per 3-product term, the 3xTF32 figure, at the same kind::f16 rate;
-// needs |z| < 65504, true for scaled and clipped data).  Included after <cuda_bf16.h> in the
-// files that write or read the planes; it renames the BF16 intrinsics used there.
+// Operand-plane format of the Gram / projection / scaled-matrix planes: BF16 hi/lo, or FP16
+// hi = fp16(z), lo = fp16(z - hi) (11-bit significands, the TF32 rounding at the full kind::f16
+// rate; needs |z| < 65504, true for scaled data).  Included after <cuda_bf16.h> in the files
+// that write or read the planes; under SCB_PLANES_F16 it renames the BF16 intrinsics used there.
 #pragma once
+// Default: BF16 planes and the three-product Gram.  Build switches (measured):
+// -DSCB_PLANES_F16 FP16 planes (no accuracy gain: the FP32 accumulation dominates), plus
+// -DSCB_GRAM_1X the one-product (hi x hi) Gram (PCA 15.0 -> 12.8 ms at C3, but subspace angles
+// of 1.0-1.7e-3 on the small C1 / edge configurations, over the 1e-3 bar).
 #ifdef SCB_PLANES_F16
 #include <cuda_fp16.h>
 #define __nv_bfloat16 __half

@@ -550,8 +550,8 @@ def scale_dense(X_log: DeviceCSR, slot, H, mean, inv, max_value=10.0, out=None, 
     ld = padded_width(H)
     dev = X_log.device
     if planes:
-        hi = torch.empty((X_log.n_rows, ld), dtype=torch.bfloat16, device=dev)
-        lo = torch.empty((X_log.n_rows, ld), dtype=torch.bfloat16, device=dev)
+        hi = torch.empty((X_log.n_rows, ld), dtype=_lib.plane_dtype(), device=dev)
+        lo = torch.empty((X_log.n_rows, ld), dtype=_lib.plane_dtype(), device=dev)
         _lib.call("scb_scale_dense_planes", _ctx(X_log.data), _p(X_log.indptr), _p(X_log.indices), _p(X_log.data),
                   X_log.n_rows, X_log.n_cols, _p(slot), H, _p(mean), _p(inv), float(max_value),
                   clip_min(max_value, clip), _p(hi), _p(lo), ld, H, _stream(dev))
@@ -666,8 +666,8 @@ def split_planes(sc: Scaled) -> Scaled:
         return sc
     n, ld = sc.Z.shape
     if sc.Z_hi is None:
-        sc.Z_hi = torch.empty((n, ld), dtype=torch.bfloat16, device=sc.Z.device)
-        sc.Z_lo = torch.empty((n, ld), dtype=torch.bfloat16, device=sc.Z.device)
+        sc.Z_hi = torch.empty((n, ld), dtype=_lib.plane_dtype(), device=sc.Z.device)
+        sc.Z_lo = torch.empty((n, ld), dtype=_lib.plane_dtype(), device=sc.Z.device)
     _lib.call("scb_split_bf16", _ctx(sc.Z), _p(sc.Z), n, ld, _p(sc.Z_hi), _p(sc.Z_lo), _stream(sc.Z.device))
     return sc
 

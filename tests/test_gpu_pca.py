@@ -84,8 +84,10 @@ def test_gram_split_planes_match_converter_path(n, h):
     sc = _scaled_from_host(Z, h)
     C1 = pp.gram(sc, planes=False).cpu().numpy()
     C2 = pp.gram(sc, keep_planes=True).cpu().numpy()
-    hi = sc.Z.to(torch.bfloat16)
-    lo = (sc.Z - hi.float()).to(torch.bfloat16)
+    from paper_2605_13928_b200 import _lib
+    dt = _lib.plane_dtype()
+    hi = sc.Z.to(dt)
+    lo = (sc.Z - hi.float()).to(dt)
     assert torch.equal(sc.Z_hi.view(torch.int16), hi.view(torch.int16))
     assert torch.equal(sc.Z_lo.view(torch.int16), lo.view(torch.int16))
     scale = np.sqrt(np.outer(np.diag(C1), np.diag(C1)))
@@ -93,9 +95,15 @@ def test_gram_split_planes_match_converter_path(n, h):
     C64 = Z64.T @ Z64
     e1 = (np.abs(C1[:h, :h] - C64) / np.maximum(scale[:h, :h], 1e-30)).max()
     e2 = (np.abs(C2[:h, :h] - C64) / np.maximum(scale[:h, :h], 1e-30)).max()
-    assert e2 <= e1 * 1.01 + 1e-7, (e1, e2)
-    assert e2 < 1e-5, e2
-    assert (np.abs(C1 - C2) / np.maximum(scale, 1e-30)).max() < 2e-5
+    if int(_lib.load().scb_plane_format()) == 1:
+        # one-product (hi x hi) planes Gram: fp16 operand rounding (2^-12 per operand, unbiased),
+        # against the converter path's three products
+        assert e2 < 2e-4, e2
+        assert (np.abs(C1 - C2) / np.maximum(scale, 1e-30)).max() < 2e-4
+    else:
+        assert e2 <= e1 * 1.01 + 1e-7, (e1, e2)
+        assert e2 < 1e-5, e2
+        assert (np.abs(C1 - C2) / np.maximum(scale, 1e-30)).max() < 2e-5
 
 
 def test_pca_rank_deficient_uses_cgs2_fallback():
