@@ -1,1 +1,1 @@
-KNN_REPS=16 bash tools/knn_variants.sh 3 "base:" "e32:-DSCB_KNN_SLEEP_E=32" "pm128_64:-DSCB_KNN_SLEEP_P=128 -DSCB_KNN_SLEEP_M=64" "e32pm128_64:-DSCB_KNN_SLEEP_E=32 -DSCB_KNN_SLEEP_P=128 -DSCB_KNN_SLEEP_M=64"
+KNN_REPS=16 bash tools/knn_variants.sh 3 "base:" "hint2k:-DSCB_KNN_HINT_E=2000" "hint200:-DSCB_KNN_HINT_E=200"
